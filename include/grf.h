@@ -1,0 +1,184 @@
+/*
+ * grf.h -- C ABI of the B200-native fractional-SPDE Gaussian-random-field sampler
+ * on metric graphs (arxiv 2605.02670, Kovacs / Molnar / Szaraz).  Implementation:
+ * libgrf.so (paper_2605_02670_b200/csrc, CUDA sm_100a, fp64).
+ *
+ * What one grf_sample call computes (PAPER.md = "P<line>"):
+ *
+ *     u_s = sum_{l=-K^-}^{K^+} (c_I^{(l)} M_L + c_L^{(l)} (kappa^2 M_L + G))^{-1} W_s,
+ *     W_s = M_L^{1/2} z_s,                                  s = 0 .. n_samples-1
+ *
+ *   P1 FEM on the metric graph with mesh size h (P122-123), lumped mass M_L
+ *   (P106-109, P137-145), stiffness G (P152-160), sinc-quadrature coefficients
+ *   c_I, c_L and limits K^-, K^+ (P60-67 [eq:coefficients], P335), kappa^2 M_L in
+ *   the operator per SURVEY §8c Q3.  Each node's system is solved by
+ *   Neumann-Neumann domain decomposition (P162-311): per-edge Thomas condensation
+ *   to the vertex Schur complement, matrix-free NN-preconditioned CG on it, and a
+ *   Thomas interior recovery; the node solutions are summed (P313-324).  The sum
+ *   over l equals (2k sin(pi beta)/pi) sum_l e^{2 beta y_l} (M + e^{2 y_l} K)^{-1} W
+ *   (the north_star weights) exactly.
+ *
+ * DOF order (SPEC.md S97; P150): interior nodes of edge 0 by ascending local x,
+ * then edge 1, ..., then the vertices 0..V-1.  Edge e = (edge_u[e], edge_v[e]) has
+ * local x = 0 at edge_u and x = length[e] at edge_v.
+ *
+ * Noise stream: sample j of a call with
+ * base seed sigma uses Philox4x32-10 key (lo32(sigma+j), hi32(sigma+j)) and for
+ * DOF i the counter (lo32(i), hi32(i), 0, 0); Box-Muller with the fixed ln / cos
+ * operation sequences of DESIGN.md; W_i = sqrt(M_L,ii) z_i.  Hence
+ * grf_sample(seed=s0, n=1) reproduces sample s0 of grf_sample(seed=0, n > s0).
+ *
+ * Conventions for every call:
+ *   - status codes, never exceptions / aborts across the ABI; grf_last_error()
+ *     returns a thread-local message for the last failing call on this thread;
+ *   - "device" pointers are CUDA device (or managed) memory on the current device,
+ *     "host" pointers are host memory; arrays are C-contiguous;
+ *   - the caller owns every buffer it passes; the library copies host inputs;
+ *   - stream arguments are cudaStream_t passed as void* (NULL = legacy default
+ *     stream); device work is enqueued asynchronously on that stream unless a
+ *     call says it synchronises.
+ *   - thread safety: distinct graph handles are independent; calls on one
+ *     handle must be externally serialised (the plan cache is mutated).
+ */
+#ifndef GRF_H_
+#define GRF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GRF_ABI_VERSION 1
+
+typedef enum grf_status {
+    GRF_OK = 0,
+    GRF_EINVAL = 1,        /* invalid argument (message says which) */
+    GRF_ENOMEM = 2,        /* allocation failed / workspace too small */
+    GRF_ECUDA = 3,         /* CUDA runtime error (message carries cudaGetErrorString) */
+    GRF_ENCCL = 4,         /* NCCL error */
+    GRF_ENOCONV = 5,       /* some (node, sample) PCG missed rtol in max_iter; output still written */
+    GRF_EUNSUPPORTED = 6   /* configuration outside what this build's kernels handle */
+} grf_status;
+
+/* Thread-local text of the last error on this thread ("" if none). */
+const char* grf_last_error(void);
+/* Build string, e.g. "grf 1 sm_100a". */
+const char* grf_version(void);
+
+/* Device-memory allocator used for the graph handle's persistent device data
+ * (mesh arrays, cached per-plan tables).  alloc returns NULL on failure.
+ * Pass NULL to grf_graph_create to use cudaMalloc / cudaFree. */
+typedef struct grf_allocator {
+    void* (*alloc)(size_t bytes, void* ctx, void* stream);
+    void (*free)(void* ptr, size_t bytes, void* ctx, void* stream);
+    void* ctx;
+} grf_allocator;
+
+typedef struct grf_graph grf_graph;
+
+/* Create a metric graph + its P1 mesh (P122-123: n_e = ceil(l_e/h) in fp64,
+ * h_e = l_e/n_e).  Host arrays of length n_edges, copied.  Self-loops and
+ * multi-edges are accepted.  GRF_EINVAL when: n_vertices < 1,
+ * n_edges < 1, an endpoint is out of range, a length is <= 0 or not finite, h <= 0
+ * or not finite, or a vertex has no incident edge (zero lumped mass).
+ * Device data is allocated through `alloc` (NULL: cudaMalloc) on the current
+ * device and uploaded synchronously.  *out receives the handle. */
+grf_status grf_graph_create(int64_t n_vertices, int64_t n_edges, const int64_t* edge_u,
+                            const int64_t* edge_v, const double* length, double h,
+                            const grf_allocator* alloc, grf_graph** out);
+/* Frees the handle and everything it allocated (synchronises the device first). */
+void grf_graph_destroy(grf_graph* g);
+
+/* N (all DOFs) and the number of edge-interior DOFs N_I = N - |V|. */
+grf_status grf_graph_num_dofs(const grf_graph* g, int64_t* n_dofs, int64_t* n_interior);
+/* Per-edge mesh layout into caller host arrays of length E (any may be NULL):
+ * n_el[e] = n_e, h_e[e], offset[e] = global index of the first interior DOF. */
+grf_status grf_graph_edge_layout(const grf_graph* g, int64_t* n_el, double* h_e, int64_t* offset);
+/* Lumped mass diagonal (P137-145) into a host array of length N; vertex sums in
+ * ascending edge id, edge_u end before edge_v end. */
+grf_status grf_graph_lumped_mass(const grf_graph* g, double* ml_host);
+
+/* Sinc-quadrature plan (P335, P60-65): K^- = ceil(pi^2/(4 k^2 beta)),
+ * K^+ = ceil(pi^2/(4 k^2 (1-beta))), L = K^- + K^+ + 1 nodes l = -K^-..K^+.
+ * c_I / c_L: optional host arrays of length L.  GRF_EINVAL unless 1/4 < beta < 1, k > 0. */
+grf_status grf_plan_info(double beta, double k, int64_t* k_minus, int64_t* k_plus,
+                         double* c_I, double* c_L);
+
+enum { GRF_PRECOND_NN = 0, GRF_PRECOND_JACOBI = 1, GRF_PRECOND_NONE = 2 };
+
+typedef struct grf_options {
+    double rtol;          /* PCG stop: ||r||_2 <= rtol ||g||_2 (recursive residual), default 1e-13 */
+    int32_t max_iter;     /* default |V| + 10 */
+    int32_t precond;      /* GRF_PRECOND_*, default NN (P260-298) */
+    int64_t node_begin;   /* sum only over quadrature nodes [node_begin, node_end) of 0..L-1 */
+    int64_t node_end;     /* (node sharding across GPUs); default 0 and -1 = all L nodes */
+} grf_options;
+void grf_options_default(grf_options* opt);
+
+typedef struct grf_stats {
+    int64_t n_nodes;           /* nodes summed by this call */
+    int64_t k_minus, k_plus;
+    int64_t n_systems;         /* (node, sample) vertex systems solved */
+    int64_t n_unconverged;     /* systems that hit max_iter */
+    int32_t iter_min, iter_max;
+    double iter_mean;
+    double worst_rel_residual; /* max over systems of the final ||r||_2/||g||_2 */
+    int64_t gpu_launches;      /* kernels this call launched */
+} grf_stats;
+
+/* Workspace bytes grf_sample / grf_apply need for these arguments. */
+grf_status grf_workspace_size(const grf_graph* g, double kappa, double beta, double k,
+                              int64_t n_samples, const grf_options* opt, size_t* bytes);
+
+/* White noise only: W_out[j*N + i] = W_i of sample j (device, n_samples x N). */
+grf_status grf_noise(grf_graph* g, uint64_t seed, int64_t n_samples, double* W_out, void* stream);
+
+/* GRF samples (see top of file).  u_out: device array n_samples x N, written.
+ * workspace: device, >= grf_workspace_size bytes (NULL/0 -> allocated and freed
+ * internally through the graph's allocator).  EINVAL unless kappa > 0,
+ * 1/4 < beta < 1, k > 0, n_samples >= 1.  The first call for a new
+ * (kappa, beta, k, node range) builds the per-(node, edge) plan tables (cached
+ * in the handle).  stats (nullable) is filled after synchronising the stream;
+ * GRF_ENOCONV is reported only when stats != NULL (it needs the sync).
+ * With stats == NULL the call is fully asynchronous. */
+grf_status grf_sample(grf_graph* g, double kappa, double beta, double k, uint64_t seed,
+                      int64_t n_samples, const grf_options* opt, double* u_out,
+                      void* workspace, size_t ws_bytes, void* stream, grf_stats* stats);
+
+/* Same as grf_sample with HOST output u_host (n_samples x N): device staging,
+ * device->host copy and a stream synchronisation happen inside the call. */
+grf_status grf_sample_host(grf_graph* g, double kappa, double beta, double k, uint64_t seed,
+                           int64_t n_samples, const grf_options* opt, double* u_host,
+                           void* stream, grf_stats* stats);
+
+/* Apply sum_l (A^{(l)})^{-1} to caller right-hand sides (no noise): rhs and
+ * u_out are device arrays n_rhs x N (may alias: in-place is allowed). */
+grf_status grf_apply(grf_graph* g, double kappa, double beta, double k, int64_t n_rhs,
+                     const double* rhs, const grf_options* opt, double* u_out,
+                     void* workspace, size_t ws_bytes, void* stream, grf_stats* stats);
+
+/* Stage entry point (tests, diagnostics): the local Schur blocks
+ * S^{(l,e)} = [[s_d, s_o], [s_o, s_d]] (P204-213 [eq:local_reduced_schur]) for the
+ * nodes of opt's range, into host array sigma[(l*E + e)*2 + {0,1}].  Synchronises. */
+grf_status grf_edge_schur(grf_graph* g, double kappa, double beta, double k,
+                          const grf_options* opt, double* sigma_host);
+
+/* ---- multi-GPU (one process per GPU, NCCL over NVLink/NVSwitch) ---------------
+ * grf_comm_get_unique_id on rank 0, broadcast the 128 bytes with any process
+ * group, then grf_comm_init on every rank (binds the current device). */
+typedef struct grf_comm grf_comm;
+grf_status grf_comm_get_unique_id(void* id128);
+grf_status grf_comm_init(const void* id128, int rank, int nranks, grf_comm** out);
+void grf_comm_destroy(grf_comm* c);
+
+/* Sum-reduce a device fp64 buffer of `count` elements to `root` over NCCL on
+ * `stream` (the l-shard reduction of partial quadrature sums). */
+grf_status grf_reduce_sum(grf_comm* c, const double* send, double* recv, int64_t count,
+                          int root, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRF_H_ */

@@ -16,6 +16,8 @@ index, mesh.py):
 ln_fixed / cos2pi_fixed are the fixed operation sequences below, built only
 from correctly rounded IEEE +, -, *, /, sqrt, floor and frexp, with NO fused
 multiply-add -- numpy evaluates each ufunc separately, so nothing contracts.
+Series constants are the correctly rounded doubles 1.0/n (n a small integer),
+so the only data-dependent division is s = (m-1)/(m+1) in ln_fixed.
 """
 from __future__ import annotations
 
@@ -83,16 +85,18 @@ def ln_fixed(x):
 
 
 def _cos_poly(t2):
+    """cos = 1 - t2/(2*1) (1 - t2/(4*3) (1 - ...)): Horner with reciprocal constants 1/((2j)(2j-1))."""
     p = np.ones_like(t2)
     for j in range(TRIG_TERMS, 0, -1):
-        p = 1.0 - (t2 / float((2 * j) * (2 * j - 1))) * p
+        p = 1.0 - (t2 * (1.0 / float((2 * j) * (2 * j - 1)))) * p
     return p
 
 
 def _sin_poly(t, t2):
+    """sin = t (1 - t2/(3*2) (1 - t2/(5*4) (1 - ...))), reciprocal constants 1/((2j+1)(2j))."""
     p = np.ones_like(t2)
     for j in range(TRIG_TERMS, 0, -1):
-        p = 1.0 - (t2 / float((2 * j + 1) * (2 * j))) * p
+        p = 1.0 - (t2 * (1.0 / float((2 * j + 1) * (2 * j)))) * p
     return t * p
 
 

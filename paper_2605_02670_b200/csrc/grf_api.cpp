@@ -1,0 +1,672 @@
+// C-ABI implementation (include/grf.h): graph/mesh setup on the host (PAPER.md P122-160),
+// quadrature plan (P60-67, P335), plan cache, workspace carving and the per-call launch
+// sequence K1 noise -> K3 condense -> K4 PCG -> K5 recover (K2 on a plan-cache miss).
+#include "grf.h"
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <list>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "grf_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+grf_status fail(grf_status st, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+#define CUDA_TRY(expr)                                                                          \
+    do {                                                                                        \
+        cudaError_t e_ = (expr);                                                                \
+        if (e_ != cudaSuccess) return fail(GRF_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+    } while (0)
+
+struct Alloc {
+    grf_allocator a{};
+    bool custom = false;
+    void* get(size_t bytes, cudaStream_t st) {
+        if (bytes == 0) bytes = 8;
+        if (custom) return a.alloc(bytes, a.ctx, st);
+        void* p = nullptr;
+        if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+        return p;
+    }
+    void put(void* p, size_t bytes, cudaStream_t st) {
+        if (!p) return;
+        if (bytes == 0) bytes = 8;
+        if (custom)
+            a.free(p, bytes, a.ctx, st);
+        else
+            cudaFree(p);
+    }
+};
+
+struct Block {
+    void* p;
+    size_t bytes;
+};
+
+struct PlanKey {
+    double kappa, beta, k;
+    int64_t nb, ne;
+    bool operator==(const PlanKey& o) const {
+        return std::memcmp(this, &o, sizeof(PlanKey)) == 0;
+    }
+};
+
+struct Plan {
+    PlanKey key{};
+    int64_t Km = 0, Kp = 0;
+    grf::DevPlan dev;
+    std::vector<Block> blocks;
+};
+
+}  // namespace
+
+struct grf_graph {
+    int device = 0;
+    Alloc alloc;
+    int64_t V = 0, E = 0, N = 0, NI = 0;
+    double h = 0.0;
+    std::vector<int64_t> eu, ev, n_el, off;
+    std::vector<double> len, he, ml;
+    grf::DevGraph dev;
+    std::vector<Block> blocks;  // graph-lifetime device allocations
+    std::list<std::unique_ptr<Plan>> plans;  // most recent first
+
+    template <class T>
+    T* upload(const std::vector<T>& v, grf_status* st) {
+        const size_t bytes = v.size() * sizeof(T);
+        void* p = alloc.get(bytes, nullptr);
+        if (!p) {
+            *st = fail(GRF_ENOMEM, "device allocation of %zu bytes failed", bytes);
+            return nullptr;
+        }
+        blocks.push_back({p, bytes});
+        if (bytes && cudaMemcpy(p, v.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+            *st = fail(GRF_ECUDA, "upload failed");
+            return nullptr;
+        }
+        return static_cast<T*>(p);
+    }
+};
+
+namespace {
+
+grf_status plan_limits(double beta, double k, int64_t* Km, int64_t* Kp) {
+    if (!(beta > 0.25 && beta < 1.0)) return fail(GRF_EINVAL, "beta must lie in (1/4, 1), got %g", beta);
+    if (!(k > 0.0) || !std::isfinite(k)) return fail(GRF_EINVAL, "k must be positive, got %g", k);
+    const double a = std::ceil((M_PI * M_PI) / (4.0 * k * k * beta));
+    const double b = std::ceil((M_PI * M_PI) / (4.0 * k * k * (1.0 - beta)));
+    if (!(a < 1e7 && b < 1e7)) return fail(GRF_EINVAL, "quadrature too large (k too small)");
+    *Km = (int64_t)a;
+    *Kp = (int64_t)b;
+    return GRF_OK;
+}
+
+// c_const = pi / (2 k sin(pi beta)); c_I = c_const e^{-2 beta y_l}; c_L = c_I e^{2 y_l}; y_l = l k  (P61-65)
+void plan_coefficients(double beta, double k, int64_t Km, int64_t lo, int64_t hi, double* cI, double* cL) {
+    const double c_const = M_PI / (2.0 * k * std::sin(M_PI * beta));
+    for (int64_t t = lo; t < hi; ++t) {
+        const double y = (double)(t - Km) * k;
+        const double ci = c_const * std::exp(-2.0 * beta * y);
+        cI[t - lo] = ci;
+        cL[t - lo] = ci * std::exp(2.0 * y);
+    }
+}
+
+grf_status resolve_range(const grf_options* opt, int64_t L, int64_t* nb, int64_t* ne) {
+    int64_t b = 0, e = L;
+    if (opt) {
+        b = opt->node_begin;
+        e = opt->node_end < 0 ? L : opt->node_end;
+    }
+    if (b < 0 || e > L || b >= e) return fail(GRF_EINVAL, "node range [%lld, %lld) invalid for L=%lld",
+                                              (long long)b, (long long)e, (long long)L);
+    *nb = b;
+    *ne = e;
+    return GRF_OK;
+}
+
+grf_status check_params(const grf_graph* g, double kappa, double beta, double k, int64_t n) {
+    if (!g) return fail(GRF_EINVAL, "graph is NULL");
+    if (!(kappa > 0.0) || !std::isfinite(kappa)) return fail(GRF_EINVAL, "kappa must be positive, got %g", kappa);
+    int64_t a, b;
+    grf_status st = plan_limits(beta, k, &a, &b);
+    if (st) return st;
+    if (n < 1) return fail(GRF_EINVAL, "n_samples must be >= 1");
+    if (n > 65535) return fail(GRF_EUNSUPPORTED, "n_samples > 65535 per call; split the call");
+    return GRF_OK;
+}
+
+grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf_options* opt, cudaStream_t st,
+                    Plan** out) {
+    int64_t Km, Kp;
+    grf_status s = plan_limits(beta, k, &Km, &Kp);
+    if (s) return s;
+    const int64_t Lfull = Km + Kp + 1;
+    int64_t nb, ne;
+    s = resolve_range(opt, Lfull, &nb, &ne);
+    if (s) return s;
+    PlanKey key{kappa, beta, k, nb, ne};
+    for (auto it = g->plans.begin(); it != g->plans.end(); ++it) {
+        if ((*it)->key == key) {
+            g->plans.splice(g->plans.begin(), g->plans, it);
+            *out = g->plans.front().get();
+            return GRF_OK;
+        }
+    }
+    const int64_t L = ne - nb;
+    if (L > grf::max_nodes_per_block())
+        return fail(GRF_EUNSUPPORTED, "%lld quadrature nodes in one call (max %d); shard the node range",
+                    (long long)L, grf::max_nodes_per_block());
+    auto p = std::make_unique<Plan>();
+    p->key = key;
+    p->Km = Km;
+    p->Kp = Kp;
+    std::vector<double> cI(L), cL(L);
+    plan_coefficients(beta, k, Km, nb, ne, cI.data(), cL.data());
+    auto grab = [&](size_t bytes) -> void* {
+        void* q = g->alloc.get(bytes, st);
+        if (q) p->blocks.push_back({q, bytes});
+        return q;
+    };
+    double* dcI = (double*)grab(L * sizeof(double));
+    double* dcL = (double*)grab(L * sizeof(double));
+    double* invd = (double*)grab((size_t)std::max<int64_t>(g->NI, 1) * L * sizeof(double));
+    double* sig = (double*)grab((size_t)L * g->E * 4 * sizeof(double));
+    if (!dcI || !dcL || !invd || !sig) {
+        for (auto& b : p->blocks) g->alloc.put(b.p, b.bytes, st);
+        return fail(GRF_ENOMEM, "plan tables (%.1f MB) could not be allocated",
+                    (double)((size_t)g->NI * L * 8 + (size_t)L * g->E * 32) / 1e6);
+    }
+    CUDA_TRY(cudaMemcpyAsync(dcI, cI.data(), L * sizeof(double), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dcL, cL.data(), L * sizeof(double), cudaMemcpyHostToDevice, st));
+    p->dev.L = (int32_t)L;
+    p->dev.kappa = kappa;
+    p->dev.cI = dcI;
+    p->dev.cL = dcL;
+    p->dev.invd = invd;
+    p->dev.sig = sig;
+    grf::launch_edge_setup(g->dev, p->dev, st);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(st));  // host vectors cI/cL die at return
+    // keep at most 4 plans
+    while (g->plans.size() >= 4) {
+        CUDA_TRY(cudaStreamSynchronize(st));
+        for (auto& b : g->plans.back()->blocks) g->alloc.put(b.p, b.bytes, st);
+        g->plans.pop_back();
+    }
+    g->plans.push_front(std::move(p));
+    *out = g->plans.front().get();
+    return GRF_OK;
+}
+
+size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct WsLayout {
+    size_t gu = 0, iters = 0, relres = 0, total = 0;
+};
+
+WsLayout ws_layout(const grf_graph* g, int64_t L, int64_t S) {
+    WsLayout w;
+    w.gu = 0;
+    size_t o = align_up((size_t)S * g->V * L * sizeof(double));
+    w.iters = o;
+    o += align_up((size_t)S * L * sizeof(int32_t));
+    w.relres = o;
+    o += align_up((size_t)S * L * sizeof(double));
+    w.total = o;
+    return w;
+}
+
+grf_status check_kernel_limits(const grf_graph* g) {
+    if (g->V > grf::pcg_max_vertices())
+        return fail(GRF_EUNSUPPORTED, "graph has %lld vertices; this build's shared-memory PCG handles <= %d",
+                    (long long)g->V, grf::pcg_max_vertices());
+    if (g->dev.max_m > grf::recover_max_interior())
+        return fail(GRF_EUNSUPPORTED, "an edge has %d interior nodes; recovery kernel handles <= %d",
+                    g->dev.max_m, grf::recover_max_interior());
+    return GRF_OK;
+}
+
+// Shared tail of grf_sample / grf_apply: u (holding W on entry) -> u.
+grf_status solve_inplace(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, double* u, void* ws,
+                         size_t ws_bytes, cudaStream_t st, grf_stats* stats, int64_t launches_so_far) {
+    const int64_t L = p->dev.L;
+    WsLayout w = ws_layout(g, L, S);
+    void* own = nullptr;
+    if (!ws) {
+        own = g->alloc.get(w.total, st);
+        if (!own) return fail(GRF_ENOMEM, "workspace of %zu bytes could not be allocated", w.total);
+        ws = own;
+    } else if (ws_bytes < w.total) {
+        return fail(GRF_ENOMEM, "workspace too small: %zu < %zu bytes", ws_bytes, w.total);
+    }
+    char* base = static_cast<char*>(ws);
+    double* gu = reinterpret_cast<double*>(base + w.gu);
+    int32_t* iters = reinterpret_cast<int32_t*>(base + w.iters);
+    double* relres = reinterpret_cast<double*>(base + w.relres);
+    grf::PcgParams prm;
+    prm.rtol = opt ? opt->rtol : 1e-13;
+    prm.max_iter = (opt && opt->max_iter > 0) ? opt->max_iter : (int32_t)(g->V + 10);
+    prm.precond = opt ? opt->precond : GRF_PRECOND_NN;
+    grf_status rc = GRF_OK;
+    grf::launch_condense(g->dev, p->dev, S, u, gu, st);
+    cudaError_t ce = cudaGetLastError();
+    if (ce == cudaSuccess) {
+        grf::launch_pcg(g->dev, p->dev, S, prm, gu, iters, relres, st);
+        ce = cudaGetLastError();
+    }
+    if (ce == cudaSuccess) ce = grf::launch_recover(g->dev, p->dev, S, u, gu, st);
+    if (ce != cudaSuccess) rc = fail(GRF_ECUDA, "kernel launch failed: %s", cudaGetErrorString(ce));
+    if (rc == GRF_OK && stats) {
+        std::vector<int32_t> it(S * L);
+        std::vector<double> rr(S * L);
+        ce = cudaMemcpyAsync(it.data(), iters, it.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+        if (ce == cudaSuccess)
+            ce = cudaMemcpyAsync(rr.data(), relres, rr.size() * sizeof(double), cudaMemcpyDeviceToHost, st);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+        if (ce != cudaSuccess) {
+            rc = fail(GRF_ECUDA, "stats readback: %s", cudaGetErrorString(ce));
+        } else {
+            std::memset(stats, 0, sizeof(*stats));
+            stats->n_nodes = L;
+            stats->k_minus = p->Km;
+            stats->k_plus = p->Kp;
+            stats->n_systems = S * L;
+            stats->iter_min = it.empty() ? 0 : *std::min_element(it.begin(), it.end());
+            stats->iter_max = it.empty() ? 0 : *std::max_element(it.begin(), it.end());
+            double sum = 0.0, worst = 0.0;
+            int64_t bad = 0;
+            for (size_t i = 0; i < it.size(); ++i) {
+                sum += it[i];
+                worst = std::max(worst, rr[i]);
+                if (!(rr[i] <= prm.rtol)) ++bad;
+            }
+            stats->iter_mean = it.empty() ? 0.0 : sum / it.size();
+            stats->worst_rel_residual = worst;
+            stats->n_unconverged = bad;
+            stats->gpu_launches = launches_so_far + 3;
+            if (bad) rc = fail(GRF_ENOCONV, "%lld of %lld PCG systems missed rtol %g (worst %g)", (long long)bad,
+                               (long long)(S * L), prm.rtol, worst);
+        }
+    }
+    if (own) {
+        cudaStreamSynchronize(st);
+        g->alloc.put(own, w.total, st);
+    }
+    return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* grf_last_error(void) { return g_err.c_str(); }
+const char* grf_version(void) { return "grf 1 sm_100a fp64"; }
+
+void grf_options_default(grf_options* opt) {
+    if (!opt) return;
+    opt->rtol = 1e-13;
+    opt->max_iter = 0;
+    opt->precond = GRF_PRECOND_NN;
+    opt->node_begin = 0;
+    opt->node_end = -1;
+}
+
+grf_status grf_graph_create(int64_t n_vertices, int64_t n_edges, const int64_t* edge_u, const int64_t* edge_v,
+                            const double* length, double h, const grf_allocator* alloc, grf_graph** out) {
+    if (!out) return fail(GRF_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (n_vertices < 1) return fail(GRF_EINVAL, "n_vertices must be >= 1");
+    if (n_edges < 1) return fail(GRF_EINVAL, "n_edges must be >= 1");
+    if (n_vertices > (1LL << 30) || n_edges > (1LL << 29)) return fail(GRF_EUNSUPPORTED, "graph too large");
+    if (!edge_u || !edge_v || !length) return fail(GRF_EINVAL, "edge arrays must not be NULL");
+    if (!(h > 0.0) || !std::isfinite(h)) return fail(GRF_EINVAL, "h must be positive and finite, got %g", h);
+    if (alloc && (!alloc->alloc || !alloc->free)) return fail(GRF_EINVAL, "allocator callbacks must be non-NULL");
+    auto g = std::make_unique<grf_graph>();
+    if (alloc) {
+        g->alloc.a = *alloc;
+        g->alloc.custom = true;
+    }
+    cudaGetDevice(&g->device);
+    const int64_t V = n_vertices, E = n_edges;
+    g->V = V;
+    g->E = E;
+    g->h = h;
+    g->eu.assign(edge_u, edge_u + E);
+    g->ev.assign(edge_v, edge_v + E);
+    g->len.assign(length, length + E);
+    std::vector<int64_t> deg(V, 0);
+    for (int64_t e = 0; e < E; ++e) {
+        if (g->eu[e] < 0 || g->eu[e] >= V || g->ev[e] < 0 || g->ev[e] >= V)
+            return fail(GRF_EINVAL, "edge %lld has an endpoint out of range", (long long)e);
+        if (!(g->len[e] > 0.0) || !std::isfinite(g->len[e]))
+            return fail(GRF_EINVAL, "edge %lld has non-positive or non-finite length", (long long)e);
+        deg[g->eu[e]]++;
+        deg[g->ev[e]]++;
+    }
+    for (int64_t v = 0; v < V; ++v)
+        if (deg[v] == 0) return fail(GRF_EINVAL, "vertex %lld is isolated (zero lumped mass)", (long long)v);
+    // Phase 1 mesh (P123): n_e = ceil(l_e / h), h_e = l_e / n_e
+    g->n_el.resize(E);
+    g->he.resize(E);
+    g->off.resize(E);
+    int64_t NI = 0;
+    int32_t max_m = 0;
+    std::vector<int32_t> mm(E);
+    for (int64_t e = 0; e < E; ++e) {
+        const double q = std::ceil(g->len[e] / h);
+        if (!(q < 1e9)) return fail(GRF_EUNSUPPORTED, "edge %lld needs %g elements", (long long)e, q);
+        int64_t n = std::max<int64_t>(1, (int64_t)q);
+        g->n_el[e] = n;
+        g->he[e] = g->len[e] / (double)n;
+        g->off[e] = NI;
+        mm[e] = (int32_t)(n - 1);
+        max_m = std::max(max_m, mm[e]);
+        NI += n - 1;
+    }
+    g->NI = NI;
+    g->N = NI + V;
+    // lumped mass (P137-145): interior h_e/2 + h_e/2; vertices sum h_e/2 in ascending edge, u end then v end
+    g->ml.assign(g->N, 0.0);
+    for (int64_t e = 0; e < E; ++e) {
+        const double half = g->he[e] / 2;
+        for (int64_t i = 0; i < g->n_el[e] - 1; ++i) g->ml[g->off[e] + i] = half + half;
+    }
+    for (int64_t e = 0; e < E; ++e) {
+        const double half = g->he[e] / 2;
+        g->ml[NI + g->eu[e]] += half;
+        g->ml[NI + g->ev[e]] += half;
+    }
+    std::vector<double> sq(g->N);
+    for (int64_t i = 0; i < g->N; ++i) sq[i] = std::sqrt(g->ml[i]);
+    // incidence CSR in (edge, end) order, owner = first incidence, 1/d_v
+    std::vector<int32_t> ptr(V + 1, 0), inc(2 * E), other(2 * E), owner(V, -1);
+    for (int64_t v = 0; v < V; ++v) ptr[v + 1] = ptr[v] + (int32_t)deg[v];
+    std::vector<int32_t> fill(ptr.begin(), ptr.end() - 1);
+    for (int64_t e = 0; e < E; ++e) {
+        const int64_t a = g->eu[e], b = g->ev[e];
+        inc[fill[a]] = (int32_t)(2 * e);
+        other[fill[a]++] = (int32_t)b;
+        inc[fill[b]] = (int32_t)(2 * e + 1);
+        other[fill[b]++] = (int32_t)a;
+    }
+    std::vector<double> inv_deg(V);
+    for (int64_t v = 0; v < V; ++v) {
+        owner[v] = inc[ptr[v]];
+        inv_deg[v] = 1.0 / (double)deg[v];
+    }
+    std::vector<int32_t> eu32(E), ev32(E);
+    for (int64_t e = 0; e < E; ++e) {
+        eu32[e] = (int32_t)g->eu[e];
+        ev32[e] = (int32_t)g->ev[e];
+    }
+    grf_status st = GRF_OK;
+    grf::DevGraph& d = g->dev;
+    d.V = (int32_t)V;
+    d.E = (int32_t)E;
+    d.N = g->N;
+    d.NI = NI;
+    d.max_m = max_m;
+    d.eu = g->upload(eu32, &st);
+    if (!st) d.ev = g->upload(ev32, &st);
+    if (!st) d.m = g->upload(mm, &st);
+    if (!st) d.off = g->upload(g->off, &st);
+    if (!st) d.h = g->upload(g->he, &st);
+    if (!st) d.inc_ptr = g->upload(ptr, &st);
+    if (!st) d.inc = g->upload(inc, &st);
+    if (!st) d.inc_other = g->upload(other, &st);
+    if (!st) d.inv_deg = g->upload(inv_deg, &st);
+    if (!st) d.owner = g->upload(owner, &st);
+    if (!st) d.sqrt_ml = g->upload(sq, &st);
+    if (st) {
+        grf_graph_destroy(g.release());
+        return st;
+    }
+    *out = g.release();
+    return GRF_OK;
+}
+
+void grf_graph_destroy(grf_graph* g) {
+    if (!g) return;
+    cudaDeviceSynchronize();
+    for (auto& p : g->plans)
+        for (auto& b : p->blocks) g->alloc.put(b.p, b.bytes, nullptr);
+    for (auto& b : g->blocks) g->alloc.put(b.p, b.bytes, nullptr);
+    delete g;
+}
+
+grf_status grf_graph_num_dofs(const grf_graph* g, int64_t* n_dofs, int64_t* n_interior) {
+    if (!g) return fail(GRF_EINVAL, "graph is NULL");
+    if (n_dofs) *n_dofs = g->N;
+    if (n_interior) *n_interior = g->NI;
+    return GRF_OK;
+}
+
+grf_status grf_graph_edge_layout(const grf_graph* g, int64_t* n_el, double* h_e, int64_t* offset) {
+    if (!g) return fail(GRF_EINVAL, "graph is NULL");
+    if (n_el) std::copy(g->n_el.begin(), g->n_el.end(), n_el);
+    if (h_e) std::copy(g->he.begin(), g->he.end(), h_e);
+    if (offset) std::copy(g->off.begin(), g->off.end(), offset);
+    return GRF_OK;
+}
+
+grf_status grf_graph_lumped_mass(const grf_graph* g, double* ml_host) {
+    if (!g || !ml_host) return fail(GRF_EINVAL, "NULL argument");
+    std::copy(g->ml.begin(), g->ml.end(), ml_host);
+    return GRF_OK;
+}
+
+grf_status grf_plan_info(double beta, double k, int64_t* k_minus, int64_t* k_plus, double* c_I, double* c_L) {
+    int64_t Km, Kp;
+    grf_status st = plan_limits(beta, k, &Km, &Kp);
+    if (st) return st;
+    if (k_minus) *k_minus = Km;
+    if (k_plus) *k_plus = Kp;
+    if (c_I || c_L) {
+        const int64_t L = Km + Kp + 1;
+        std::vector<double> a(L), b(L);
+        plan_coefficients(beta, k, Km, 0, L, a.data(), b.data());
+        if (c_I) std::copy(a.begin(), a.end(), c_I);
+        if (c_L) std::copy(b.begin(), b.end(), c_L);
+    }
+    return GRF_OK;
+}
+
+grf_status grf_workspace_size(const grf_graph* g, double kappa, double beta, double k, int64_t n_samples,
+                              const grf_options* opt, size_t* bytes) {
+    grf_status st = check_params(g, kappa, beta, k, n_samples);
+    if (st) return st;
+    if (!bytes) return fail(GRF_EINVAL, "bytes is NULL");
+    int64_t Km, Kp, nb, ne;
+    plan_limits(beta, k, &Km, &Kp);
+    st = resolve_range(opt, Km + Kp + 1, &nb, &ne);
+    if (st) return st;
+    *bytes = ws_layout(g, ne - nb, n_samples).total;
+    return GRF_OK;
+}
+
+grf_status grf_noise(grf_graph* g, uint64_t seed, int64_t n_samples, double* W_out, void* stream) {
+    if (!g || !W_out) return fail(GRF_EINVAL, "NULL argument");
+    if (n_samples < 1) return fail(GRF_EINVAL, "n_samples must be >= 1");
+    grf::launch_noise(g->dev, seed, n_samples, W_out, (cudaStream_t)stream);
+    CUDA_TRY(cudaGetLastError());
+    return GRF_OK;
+}
+
+grf_status grf_sample(grf_graph* g, double kappa, double beta, double k, uint64_t seed, int64_t n_samples,
+                      const grf_options* opt, double* u_out, void* workspace, size_t ws_bytes, void* stream,
+                      grf_stats* stats) {
+    grf_status st = check_params(g, kappa, beta, k, n_samples);
+    if (st) return st;
+    if (!u_out) return fail(GRF_EINVAL, "u_out is NULL");
+    st = check_kernel_limits(g);
+    if (st) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t nplans = g->plans.size();
+    Plan* p = nullptr;
+    st = get_plan(g, kappa, beta, k, opt, s, &p);
+    if (st) return st;
+    (void)nplans;
+    grf::launch_noise(g->dev, seed, n_samples, u_out, s);
+    CUDA_TRY(cudaGetLastError());
+    return solve_inplace(g, p, n_samples, opt, u_out, workspace, ws_bytes, s, stats, 1);
+}
+
+grf_status grf_apply(grf_graph* g, double kappa, double beta, double k, int64_t n_rhs, const double* rhs,
+                     const grf_options* opt, double* u_out, void* workspace, size_t ws_bytes, void* stream,
+                     grf_stats* stats) {
+    grf_status st = check_params(g, kappa, beta, k, n_rhs);
+    if (st) return st;
+    if (!u_out || !rhs) return fail(GRF_EINVAL, "NULL argument");
+    st = check_kernel_limits(g);
+    if (st) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    Plan* p = nullptr;
+    st = get_plan(g, kappa, beta, k, opt, s, &p);
+    if (st) return st;
+    if (rhs != u_out)
+        CUDA_TRY(cudaMemcpyAsync(u_out, rhs, (size_t)n_rhs * g->N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    return solve_inplace(g, p, n_rhs, opt, u_out, workspace, ws_bytes, s, stats, 0);
+}
+
+grf_status grf_sample_host(grf_graph* g, double kappa, double beta, double k, uint64_t seed, int64_t n_samples,
+                           const grf_options* opt, double* u_host, void* stream, grf_stats* stats) {
+    grf_status st = check_params(g, kappa, beta, k, n_samples);
+    if (st) return st;
+    if (!u_host) return fail(GRF_EINVAL, "u_host is NULL");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t ubytes = (size_t)n_samples * g->N * sizeof(double);
+    void* du = g->alloc.get(ubytes, s);
+    if (!du) return fail(GRF_ENOMEM, "staging buffer of %zu bytes could not be allocated", ubytes);
+    st = grf_sample(g, kappa, beta, k, seed, n_samples, opt, (double*)du, nullptr, 0, s, stats);
+    if (st == GRF_OK || st == GRF_ENOCONV) {
+        cudaError_t ce = cudaMemcpyAsync(u_host, du, ubytes, cudaMemcpyDeviceToHost, s);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+        if (ce != cudaSuccess) st = fail(GRF_ECUDA, "device->host copy: %s", cudaGetErrorString(ce));
+    }
+    cudaStreamSynchronize(s);
+    g->alloc.put(du, ubytes, s);
+    return st;
+}
+
+grf_status grf_edge_schur(grf_graph* g, double kappa, double beta, double k, const grf_options* opt,
+                          double* sigma_host) {
+    grf_status st = check_params(g, kappa, beta, k, 1);
+    if (st) return st;
+    if (!sigma_host) return fail(GRF_EINVAL, "sigma_host is NULL");
+    Plan* p = nullptr;
+    st = get_plan(g, kappa, beta, k, opt, nullptr, &p);
+    if (st) return st;
+    const int64_t n = (int64_t)p->dev.L * g->E;
+    std::vector<double> buf(n * 4);
+    CUDA_TRY(cudaMemcpy(buf.data(), p->dev.sig, n * 4 * sizeof(double), cudaMemcpyDeviceToHost));
+    for (int64_t t = 0; t < n; ++t) {
+        sigma_host[2 * t] = buf[4 * t];
+        sigma_host[2 * t + 1] = buf[4 * t + 1];
+    }
+    return GRF_OK;
+}
+
+// ---------------------------------------------------------------- NCCL (dlopen'ed)
+typedef int (*nccl_get_id_fn)(void*);
+typedef int (*nccl_init_fn)(void**, int, const void*, int);  // ncclComm_t*, nranks, ncclUniqueId (by value 128B), rank
+typedef int (*nccl_reduce_fn)(const void*, void*, size_t, int, int, int, void*, cudaStream_t);
+typedef int (*nccl_destroy_fn)(void*);
+typedef const char* (*nccl_err_fn)(int);
+
+}  // extern "C"
+
+namespace {
+struct NcclApi {
+    void* h = nullptr;
+    nccl_get_id_fn get_id = nullptr;
+    void* init = nullptr;
+    nccl_reduce_fn reduce = nullptr;
+    nccl_destroy_fn destroy = nullptr;
+    nccl_err_fn err = nullptr;
+    bool load() {
+        if (h) return true;
+        const char* names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char* n : names) {
+            h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+            if (h) break;
+        }
+        if (!h) return false;
+        get_id = (nccl_get_id_fn)dlsym(h, "ncclGetUniqueId");
+        init = dlsym(h, "ncclCommInitRank");
+        reduce = (nccl_reduce_fn)dlsym(h, "ncclReduce");
+        destroy = (nccl_destroy_fn)dlsym(h, "ncclCommDestroy");
+        err = (nccl_err_fn)dlsym(h, "ncclGetErrorString");
+        return get_id && init && reduce && destroy;
+    }
+};
+NcclApi g_nccl;
+struct UniqueId {
+    char internal[128];
+};
+typedef int (*nccl_init_real_fn)(void**, int, UniqueId, int);
+}  // namespace
+
+struct grf_comm {
+    void* comm = nullptr;
+    int rank = 0, nranks = 1;
+};
+
+extern "C" {
+
+grf_status grf_comm_get_unique_id(void* id128) {
+    if (!id128) return fail(GRF_EINVAL, "id is NULL");
+    if (!g_nccl.load()) return fail(GRF_ENCCL, "libnccl.so.2 could not be loaded");
+    int r = g_nccl.get_id(id128);
+    if (r) return fail(GRF_ENCCL, "ncclGetUniqueId: %s", g_nccl.err ? g_nccl.err(r) : "error");
+    return GRF_OK;
+}
+
+grf_status grf_comm_init(const void* id128, int rank, int nranks, grf_comm** out) {
+    if (!id128 || !out || nranks < 1 || rank < 0 || rank >= nranks) return fail(GRF_EINVAL, "bad comm arguments");
+    if (!g_nccl.load()) return fail(GRF_ENCCL, "libnccl.so.2 could not be loaded");
+    UniqueId uid;
+    std::memcpy(uid.internal, id128, 128);
+    auto c = std::make_unique<grf_comm>();
+    int r = ((nccl_init_real_fn)g_nccl.init)(&c->comm, nranks, uid, rank);
+    if (r) return fail(GRF_ENCCL, "ncclCommInitRank: %s", g_nccl.err ? g_nccl.err(r) : "error");
+    c->rank = rank;
+    c->nranks = nranks;
+    *out = c.release();
+    return GRF_OK;
+}
+
+void grf_comm_destroy(grf_comm* c) {
+    if (!c) return;
+    if (c->comm && g_nccl.destroy) g_nccl.destroy(c->comm);
+    delete c;
+}
+
+grf_status grf_reduce_sum(grf_comm* c, const double* send, double* recv, int64_t count, int root, void* stream) {
+    if (!c || !send || count < 0 || root < 0 || root >= c->nranks) return fail(GRF_EINVAL, "bad reduce arguments");
+    // ncclDouble = 8, ncclSum = 0
+    int r = g_nccl.reduce(send, recv, (size_t)count, 8, 0, root, c->comm, (cudaStream_t)stream);
+    if (r) return fail(GRF_ENCCL, "ncclReduce: %s", g_nccl.err ? g_nccl.err(r) : "error");
+    return GRF_OK;
+}
+
+}  // extern "C"

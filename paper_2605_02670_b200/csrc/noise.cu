@@ -1,0 +1,111 @@
+// K1: lumped-mass white noise W = M_L^{1/2} z  (PAPER.md P99-109 [eq:wh_def], P150).
+//
+// Canonical stream:
+//   key = (lo32(seed+s), hi32(seed+s)), counter = (lo32(i), hi32(i), 0, 0)
+//   (x0..x3) = Philox4x32-10, u1 = ((x0<<21 | x1>>11) + 1) 2^-53, u2 = (x2<<21 | x3>>11) 2^-53
+//   z = sqrt(-2 ln(u1)) cos(2 pi u2) with the FIXED ln / cos operation sequences below,
+//   W_i = sqrt(M_L,ii) z.
+// Bit-exactness with the CPU oracle needs every operation correctly rounded and
+// un-fused: this TU is compiled with --fmad=false AND uses the explicit
+// __d*_rn intrinsics (never contracted).
+//
+// Layout: W[s * N + i] (sample-major, the grf_sample output layout).  One thread
+// per (s, i), grid-stride; the write is a plain coalesced store -- the kernel is
+// bound by the fp64 polynomial work (~70 ops + 1 division per draw), not HBM.
+#include "grf_internal.h"
+
+namespace grf {
+namespace {
+
+__device__ __forceinline__ uint4 philox_round(uint4 c, uint2 k) {
+    const unsigned int M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    const unsigned int hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
+    const unsigned int hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
+    return make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+}
+
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        c = philox_round(c, k);
+        if (r < 9) {
+            k.x += 0x9E3779B9u;
+            k.y += 0xBB67AE85u;
+        }
+    }
+    return c;
+}
+
+// ln x for x in (0, 1]: x = m 2^e, m in [sqrt(1/2), sqrt(2)); s = (m-1)/(m+1);
+// ln m = 2 s sum_{j=0}^{12} s^{2j}/(2j+1) (Horner, constants 1.0/(2j+1)).
+__device__ __forceinline__ double ln_fixed(double x) {
+    const double LN2 = 0.6931471805599453;
+    const double SQRT_HALF = 0.7071067811865476;
+    int e;
+    double m = frexp(x, &e);
+    if (m < SQRT_HALF) {
+        m = __dmul_rn(m, 2.0);
+        e -= 1;
+    }
+    const double f = __dsub_rn(m, 1.0);
+    const double s = __ddiv_rn(f, __dadd_rn(m, 1.0));
+    const double s2 = __dmul_rn(s, s);
+    double p = 1.0 / 25.0;
+#pragma unroll
+    for (int j = 11; j >= 0; --j) p = __dadd_rn(1.0 / (double)(2 * j + 1), __dmul_rn(s2, p));
+    const double t = __dmul_rn(s, p);
+    return __dadd_rn(__dmul_rn((double)e, LN2), __dadd_rn(t, t));
+}
+
+// cos(2 pi u), u in [0,1) a multiple of 2^-53: t = 4u, q = floor(t + 1/2), f = t - q (exact),
+// theta = f pi/2 in [-pi/4, pi/4]; cos/sin by Taylor (10 Horner steps, constants 1.0/(n(n-1))).
+__device__ __forceinline__ double cos2pi_fixed(double u) {
+    const double HALF_PI = 1.5707963267948966;
+    const double t = __dmul_rn(4.0, u);
+    const double q = floor(__dadd_rn(t, 0.5));
+    const double f = __dsub_rn(t, q);
+    const double th = __dmul_rn(f, HALF_PI);
+    const double th2 = __dmul_rn(th, th);
+    double pc = 1.0, ps = 1.0;
+#pragma unroll
+    for (int j = 10; j >= 1; --j) {
+        pc = __dsub_rn(1.0, __dmul_rn(__dmul_rn(th2, 1.0 / (double)((2 * j) * (2 * j - 1))), pc));
+        ps = __dsub_rn(1.0, __dmul_rn(__dmul_rn(th2, 1.0 / (double)((2 * j + 1) * (2 * j))), ps));
+    }
+    const double c = pc;
+    const double sn = __dmul_rn(th, ps);
+    const int qi = ((int)q) & 3;
+    return qi == 0 ? c : (qi == 1 ? -sn : (qi == 2 ? -c : sn));
+}
+
+__global__ void __launch_bounds__(256) noise_kernel(const double* __restrict__ sqrt_ml, int64_t N,
+                                                    int64_t total, uint64_t seed, double* __restrict__ W) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = t / N;
+        const int64_t i = t - s * N;
+        const uint64_t key = seed + (uint64_t)s;
+        const uint4 x = philox4x32_10(make_uint4((unsigned)i, (unsigned)((uint64_t)i >> 32), 0u, 0u),
+                                      make_uint2((unsigned)key, (unsigned)(key >> 32)));
+        const uint64_t A = ((uint64_t)x.x << 21) | (uint64_t)(x.y >> 11);
+        const uint64_t B = ((uint64_t)x.z << 21) | (uint64_t)(x.w >> 11);
+        const double u1 = __dmul_rn((double)(A + 1ull), 0x1.0p-53);
+        const double u2 = __dmul_rn((double)B, 0x1.0p-53);
+        const double r = __dsqrt_rn(__dmul_rn(-2.0, ln_fixed(u1)));
+        const double z = __dmul_rn(r, cos2pi_fixed(u2));
+        W[t] = __dmul_rn(sqrt_ml[i], z);
+    }
+}
+
+}  // namespace
+
+void launch_noise(const DevGraph& g, uint64_t seed, int64_t n_samples, double* W, cudaStream_t st) {
+    const int64_t total = n_samples * g.N;
+    if (total == 0) return;
+    int64_t blocks = (total + 255) / 256;
+    const int64_t cap = 148 * 16;
+    if (blocks > cap) blocks = cap;
+    noise_kernel<<<(unsigned)blocks, 256, 0, st>>>(g.sqrt_ml, g.N, total, seed, W);
+}
+
+}  // namespace grf

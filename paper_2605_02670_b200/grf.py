@@ -1,0 +1,236 @@
+"""Thin Python binding of libgrf.so (include/grf.h) -- argument marshalling only.
+
+PyTorch provides device memory (its caching allocator is handed to the library
+as the grf_allocator), streams and process groups; every step of the sampler runs
+in the library's CUDA kernels.  Names follow the C ABI:
+
+    g = Graph(n_vertices, edge_u, edge_v, length, h)            # grf_graph_create
+    u = g.sample(kappa, beta, k, seed=0, n_samples=1)            # grf_sample  -> cuda fp64 [S, N]
+    W = g.noise(seed, n_samples)                                 # grf_noise
+    x = g.apply(kappa, beta, k, rhs)                             # grf_apply
+    S = g.edge_schur(kappa, beta, k)                             # grf_edge_schur (stage check)
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Tuple
+
+import numpy as np
+
+from ._lib import (ALLOC_FN, FREE_FN, GRF_ENOCONV, GRF_OK, GrfError, check, grf_allocator, grf_options,
+                   grf_stats, load)
+
+PRECOND = {"nn": 0, "neumann-neumann": 0, "jacobi": 1, "none": 2}
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2605_02670_b200 needs a CUDA device (B200); there is no CPU fallback")
+    return torch
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def plan_info(beta: float, k: float):
+    """(K^-, K^+, c_I[L], c_L[L]) of the sinc plan (P60-67, P335), via grf_plan_info."""
+    lib = load()
+    km, kp = C.c_int64(), C.c_int64()
+    check(lib.grf_plan_info(beta, k, C.byref(km), C.byref(kp), None, None))
+    L = km.value + kp.value + 1
+    cI = np.empty(L)
+    cL = np.empty(L)
+    check(lib.grf_plan_info(beta, k, C.byref(km), C.byref(kp), cI.ctypes.data_as(C.POINTER(C.c_double)),
+                            cL.ctypes.data_as(C.POINTER(C.c_double))))
+    return km.value, kp.value, cI, cL
+
+
+def make_options(rtol=1e-13, max_iter=0, precond="nn", node_range=None) -> grf_options:
+    o = grf_options()
+    load().grf_options_default(C.byref(o))
+    o.rtol = rtol
+    o.max_iter = max_iter
+    o.precond = PRECOND[precond] if isinstance(precond, str) else int(precond)
+    if node_range is not None:
+        o.node_begin, o.node_end = int(node_range[0]), int(node_range[1])
+    return o
+
+
+class Graph:
+    """A metric graph + its P1 mesh, resident on the current CUDA device."""
+
+    def __init__(self, n_vertices, edge_u, edge_v, length, h, use_torch_allocator: bool = True):
+        torch = _torch()
+        lib = load()
+        self._lib = lib
+        self.device = torch.cuda.current_device()
+        eu = np.ascontiguousarray(edge_u, dtype=np.int64)
+        ev = np.ascontiguousarray(edge_v, dtype=np.int64)
+        ln = np.ascontiguousarray(length, dtype=np.float64)
+        self.n_vertices = int(n_vertices)
+        self.n_edges = int(len(eu))
+        self.h = float(h)
+        self._alloc = None
+        if use_torch_allocator:
+            dev = self.device
+
+            def _a(nbytes, ctx, stream):
+                try:
+                    return torch.cuda.caching_allocator_alloc(int(nbytes), dev, int(stream or 0) or None)
+                except Exception:
+                    return None
+
+            def _f(ptr, nbytes, ctx, stream):
+                torch.cuda.caching_allocator_delete(int(ptr))
+
+            self._cb = (ALLOC_FN(_a), FREE_FN(_f))
+            self._alloc = grf_allocator(self._cb[0], self._cb[1], None)
+        h_ = C.c_void_p()
+        pi64 = C.POINTER(C.c_int64)
+        check(lib.grf_graph_create(self.n_vertices, self.n_edges, eu.ctypes.data_as(pi64), ev.ctypes.data_as(pi64),
+                                   ln.ctypes.data_as(C.POINTER(C.c_double)), self.h,
+                                   C.byref(self._alloc) if self._alloc is not None else None, C.byref(h_)))
+        self._h = h_
+        n, ni = C.c_int64(), C.c_int64()
+        check(lib.grf_graph_num_dofs(self._h, C.byref(n), C.byref(ni)))
+        self.n_dofs = n.value
+        self.n_interior = ni.value
+
+    @classmethod
+    def from_metric_graph(cls, g, h, **kw):
+        return cls(g.n_vertices, g.edge_u, g.edge_v, g.length, h, **kw)
+
+    # ------------------------------------------------------------------ queries
+    def edge_layout(self):
+        n_el = np.empty(self.n_edges, dtype=np.int64)
+        he = np.empty(self.n_edges)
+        off = np.empty(self.n_edges, dtype=np.int64)
+        check(self._lib.grf_graph_edge_layout(self._h, n_el.ctypes.data_as(C.POINTER(C.c_int64)),
+                                              he.ctypes.data_as(C.POINTER(C.c_double)),
+                                              off.ctypes.data_as(C.POINTER(C.c_int64))))
+        return n_el, he, off
+
+    def lumped_mass(self):
+        ml = np.empty(self.n_dofs)
+        check(self._lib.grf_graph_lumped_mass(self._h, ml.ctypes.data_as(C.POINTER(C.c_double))))
+        return ml
+
+    def workspace_size(self, kappa, beta, k, n_samples, **opts) -> int:
+        o = make_options(**opts)
+        b = C.c_size_t()
+        check(self._lib.grf_workspace_size(self._h, kappa, beta, k, n_samples, C.byref(o), C.byref(b)))
+        return b.value
+
+    # ------------------------------------------------------------------ compute
+    def noise(self, seed: int, n_samples: int, out=None, stream=None):
+        torch = _torch()
+        if out is None:
+            out = torch.empty((n_samples, self.n_dofs), dtype=torch.float64, device=f"cuda:{self.device}")
+        self._check_out(out, n_samples)
+        check(self._lib.grf_noise(self._h, C.c_uint64(seed & (2 ** 64 - 1)), n_samples, C.c_void_p(out.data_ptr()),
+                                  C.c_void_p(_stream_ptr(stream))))
+        return out
+
+    def _check_out(self, out, n):
+        torch = _torch()
+        if out.dtype != torch.float64 or not out.is_cuda or not out.is_contiguous() or out.numel() != n * self.n_dofs:
+            raise ValueError(f"out must be a contiguous cuda float64 tensor with {n}x{self.n_dofs} elements")
+
+    def sample(self, kappa, beta, k, seed=0, n_samples=1, out=None, workspace=None, stream=None,
+               return_stats=False, strict=True, **opts):
+        """GRF samples u [n_samples, N] (cuda fp64).  opts: rtol, max_iter, precond, node_range."""
+        torch = _torch()
+        o = make_options(**opts)
+        if out is None:
+            out = torch.empty((n_samples, self.n_dofs), dtype=torch.float64, device=f"cuda:{self.device}")
+        self._check_out(out, n_samples)
+        ws_ptr, ws_bytes = self._workspace(workspace, kappa, beta, k, n_samples, o)
+        st = grf_stats() if return_stats else None
+        rc = self._lib.grf_sample(self._h, kappa, beta, k, C.c_uint64(seed & (2 ** 64 - 1)), n_samples, C.byref(o),
+                                  C.c_void_p(out.data_ptr()), ws_ptr, ws_bytes, C.c_void_p(_stream_ptr(stream)),
+                                  C.byref(st) if st is not None else None)
+        self._keep = workspace
+        if rc == GRF_ENOCONV and not strict:
+            pass
+        else:
+            check(rc)
+        return (out, st.as_dict()) if return_stats else out
+
+    def sample_host(self, kappa, beta, k, seed=0, n_samples=1, stream=None, return_stats=False, **opts):
+        """grf_sample_host: the e2e call -- device staging + D2H copy + sync inside."""
+        o = make_options(**opts)
+        out = np.empty((n_samples, self.n_dofs))
+        st = grf_stats() if return_stats else None
+        check(self._lib.grf_sample_host(self._h, kappa, beta, k, C.c_uint64(seed & (2 ** 64 - 1)), n_samples,
+                                        C.byref(o), C.c_void_p(out.ctypes.data), C.c_void_p(_stream_ptr(stream)),
+                                        C.byref(st) if st is not None else None))
+        return (out, st.as_dict()) if return_stats else out
+
+    def sample_into_host(self, kappa, beta, k, seed, n_samples, host_out, stream=None, **opts):
+        """grf_sample_host into a caller (e.g. pinned) host buffer; returns host_out."""
+        o = make_options(**opts)
+        check(self._lib.grf_sample_host(self._h, kappa, beta, k, C.c_uint64(seed & (2 ** 64 - 1)), n_samples,
+                                        C.byref(o), C.c_void_p(host_out.data_ptr()), C.c_void_p(_stream_ptr(stream)),
+                                        None))
+        return host_out
+
+    def apply(self, kappa, beta, k, rhs, out=None, workspace=None, stream=None, return_stats=False, **opts):
+        torch = _torch()
+        o = make_options(**opts)
+        rhs = rhs.contiguous()
+        n = rhs.shape[0] if rhs.dim() == 2 else 1
+        if out is None:
+            out = torch.empty((n, self.n_dofs), dtype=torch.float64, device=rhs.device)
+        self._check_out(rhs, n)
+        self._check_out(out, n)
+        ws_ptr, ws_bytes = self._workspace(workspace, kappa, beta, k, n, o)
+        st = grf_stats() if return_stats else None
+        check(self._lib.grf_apply(self._h, kappa, beta, k, n, C.c_void_p(rhs.data_ptr()), C.byref(o),
+                                  C.c_void_p(out.data_ptr()), ws_ptr, ws_bytes, C.c_void_p(_stream_ptr(stream)),
+                                  C.byref(st) if st is not None else None))
+        self._keep = workspace
+        return (out, st.as_dict()) if return_stats else out
+
+    def edge_schur(self, kappa, beta, k, **opts):
+        """Local Schur blocks (s_d, s_o) per (node, edge): numpy [L, E, 2] (grf_edge_schur)."""
+        o = make_options(**opts)
+        km, kp, _, _ = plan_info(beta, k)
+        L = km + kp + 1
+        nb = o.node_begin
+        ne = L if o.node_end < 0 else o.node_end
+        buf = np.empty((ne - nb, self.n_edges, 2))
+        check(self._lib.grf_edge_schur(self._h, kappa, beta, k, C.byref(o), buf.ctypes.data_as(C.POINTER(C.c_double))))
+        return buf
+
+    def _workspace(self, workspace, kappa, beta, k, n, o):
+        torch = _torch()
+        b = C.c_size_t()
+        check(self._lib.grf_workspace_size(self._h, kappa, beta, k, n, C.byref(o), C.byref(b)))
+        if workspace is None:
+            workspace = torch.empty(b.value, dtype=torch.uint8, device=f"cuda:{self.device}")
+            self._ws_tmp = workspace
+        if workspace.numel() * workspace.element_size() < b.value:
+            raise ValueError(f"workspace needs {b.value} bytes")
+        return C.c_void_p(workspace.data_ptr()), C.c_size_t(workspace.numel() * workspace.element_size())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.grf_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def version() -> str:
+    return load().grf_version().decode()

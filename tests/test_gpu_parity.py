@@ -1,0 +1,236 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle (BASELINE north_star).
+
+Bars (north_star): noise bit-exact; fields <= 1e-9 relative L2 per sample with PCG at
+rtol 1e-13.  Intermediate stage: the local Schur blocks of K2 vs their dense definition
+(oracle/dd.py) to 1e-12.  Inputs are the seeded synthetic graphs of synth/.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle import dd, noise, solve  # noqa: E402
+from synth import CONFIGS, MetricGraph, config_graph, lattice, single_edge, star_of_lattices, tadpole  # noqa: E402
+
+FIELD_TOL = 1e-9
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _graph(g, h):
+    from paper_2605_02670_b200 import Graph
+    return Graph.from_metric_graph(g, h)
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b, axis=-1) / np.linalg.norm(b, axis=-1)
+
+
+def _bits(x):
+    return np.ascontiguousarray(x).view(np.uint64)
+
+
+# ----------------------------------------------------------------------------- noise
+def test_noise_bitexact_tadpole():
+    G = _graph(tadpole(), 0.01)
+    W = G.noise(5, 3).cpu().numpy()
+    prob = solve.setup(tadpole(), 0.01, 5.0, 0.75, 0.5)
+    ref = noise.white_noise(prob.ML, 5, 3)
+    assert np.array_equal(_bits(W), _bits(ref))
+    assert np.array_equal(G.lumped_mass(), prob.ML)
+
+
+def test_noise_bitexact_lattice_256_samples_sampled():
+    """Full config-3 noise call (256 x 198325); the oracle recomputes sampled rows / columns."""
+    cfg = CONFIGS["lattice256"]
+    g = config_graph("lattice256")
+    G = _graph(g, cfg["h"])
+    W = G.noise(cfg["seed"], cfg["n_samples"])
+    prob = solve.setup(g, cfg["h"], cfg["kappa"], cfg["beta"], cfg["k"])
+    rng = np.random.default_rng(0)
+    rows = [0, 1, 127, 255]
+    cols = np.unique(np.concatenate([rng.integers(0, G.n_dofs, 4000), [0, G.n_interior - 1, G.n_interior,
+                                                                       G.n_dofs - 1]]))
+    Wc = W[:, torch.as_tensor(cols, device=W.device)].cpu().numpy()
+    for s in range(0, 256, 15):
+        ref = noise.white_noise(prob.ML, cfg["seed"], 256, dofs=cols, samples=[s])[0]
+        assert np.array_equal(_bits(Wc[s]), _bits(ref)), f"sample {s}"
+    for s in rows:
+        ref = noise.white_noise(prob.ML, cfg["seed"], 256, samples=[s])[0]
+        assert np.array_equal(_bits(W[s].cpu().numpy()), _bits(ref)), f"row {s}"
+
+
+def test_noise_large_seed_wraps():
+    G = _graph(single_edge(1.0), 0.1)
+    seed = 2 ** 64 - 2
+    W = G.noise(seed, 4).cpu().numpy()
+    prob = solve.setup(single_edge(1.0), 0.1, 1.0, 0.6, 0.3)
+    ref = noise.white_noise(prob.ML, seed, 4)
+    assert np.array_equal(_bits(W), _bits(ref))
+
+
+# ----------------------------------------------------------------------------- K2 stage
+@pytest.mark.parametrize("gname,h,kappa,beta,k", [("tadpole", 0.01, 5.0, 0.75, 0.5),
+                                                  ("lattice4", 0.05, 10.0, 0.6, 0.3),
+                                                  ("short", 0.01, 2.0, 0.55, 0.3)])
+def test_edge_schur_vs_definition(gname, h, kappa, beta, k):
+    g = {"tadpole": tadpole(), "lattice4": lattice(4, seed=2),
+         "short": MetricGraph(3, np.array([0, 1, 1, 2]), np.array([1, 2, 2, 2]),
+                              np.array([0.004, 0.7, 0.015, 0.33]))}[gname]
+    G = _graph(g, h)
+    sig = G.edge_schur(kappa, beta, k)
+    prob = solve.setup(g, h, kappa, beta, k)
+    for li in range(0, prob.plan.n_nodes, max(1, prob.plan.n_nodes // 12)):
+        for e in range(g.n_edges):
+            S = dd.local_schur(prob, li, e)
+            scale = abs(S[0, 0])
+            assert abs(sig[li, e, 0] - S[0, 0]) <= 1e-12 * scale
+            assert abs(sig[li, e, 1] - S[0, 1]) <= 1e-12 * scale
+
+
+# ----------------------------------------------------------------------------- fields
+def test_config1_tadpole():
+    cfg = CONFIGS["tadpole"]
+    g = tadpole()
+    G = _graph(g, cfg["h"])
+    u, st = G.sample(cfg["kappa"], cfg["beta"], cfg["k"], seed=cfg["seed"], n_samples=1, return_stats=True)
+    ref, _, _ = solve.sample(g, cfg["h"], cfg["kappa"], cfg["beta"], cfg["k"], cfg["seed"], 1)
+    assert _rel(u.cpu().numpy(), ref).max() <= FIELD_TOL
+    assert st["n_unconverged"] == 0 and st["iter_max"] <= 2 and st["n_nodes"] == 55
+
+
+@pytest.mark.parametrize("gname", ["lattice4", "star2", "multi_loop_short", "single"])
+def test_per_node_solves(gname):
+    """node_range = [l, l+1) returns the single node solve x_l = A_l^{-1} W (c-form, P76)."""
+    g, h = {"lattice4": (lattice(4, seed=1), 0.05), "star2": (star_of_lattices(2, 3), 0.125),
+            "multi_loop_short": (MetricGraph(3, np.array([0, 0, 1, 1, 2]), np.array([1, 1, 2, 1, 2]),
+                                             np.array([0.5, 0.8, 0.004, 0.3, 0.21])), 0.01),
+            "single": (single_edge(0.77), 0.01)}[gname]
+    kappa, beta, k = 3.0, 0.65, 0.3
+    G = _graph(g, h)
+    prob = solve.setup(g, h, kappa, beta, k)
+    W = noise.white_noise(prob.ML, 9, 2)
+    for li in sorted({0, 1, prob.plan.n_nodes // 2, prob.plan.n_nodes - 1}):
+        u = G.sample(kappa, beta, k, seed=9, n_samples=2, node_range=(li, li + 1)).cpu().numpy()
+        ref = solve.node_solve(prob, li, W)
+        assert _rel(u, ref).max() <= 1e-10, f"node {li}"
+
+
+@pytest.mark.parametrize("precond", ["nn", "jacobi", "none"])
+def test_small_graph_all_preconditioners(precond):
+    g = lattice(5, seed=3)
+    h, kappa, beta, k = 0.02, 2.0, 0.7, 0.35
+    G = _graph(g, h)
+    u, st = G.sample(kappa, beta, k, seed=1, n_samples=5, precond=precond, return_stats=True)
+    ref, _, _ = solve.sample(g, h, kappa, beta, k, 1, 5)
+    assert _rel(u.cpu().numpy(), ref).max() <= FIELD_TOL
+    assert st["n_unconverged"] == 0
+
+
+def test_ragged_and_degenerate_edges():
+    """Edges with 0, 1, 2 interior nodes, a loop with n_e = 1, multi-edges; odd sample count."""
+    g = MetricGraph(4, np.array([0, 0, 1, 1, 2, 3, 2, 0]), np.array([1, 1, 2, 1, 3, 3, 0, 3]),
+                    np.array([0.01, 0.019, 0.031, 0.005, 0.9, 0.008, 0.43, 1.37]))
+    h, kappa, beta, k = 0.01, 4.0, 0.8, 0.3
+    G = _graph(g, h)
+    u = G.sample(kappa, beta, k, seed=4, n_samples=3).cpu().numpy()
+    ref, _, _ = solve.sample(g, h, kappa, beta, k, 4, 3)
+    assert _rel(u, ref).max() <= FIELD_TOL
+
+
+def test_single_edge_one_pcg_iteration():
+    G = _graph(single_edge(1.0), 0.01)
+    _, st = G.sample(3.0, 0.7, 0.4, seed=0, n_samples=2, return_stats=True)
+    assert st["iter_max"] <= 2 and st["iter_min"] >= 1
+    assert st["n_unconverged"] == 0
+
+
+def test_seed_convention_and_determinism():
+    g = lattice(4, seed=5)
+    G = _graph(g, 0.05)
+    a = G.sample(5.0, 0.6, 0.3, seed=0, n_samples=6).cpu().numpy()
+    b = G.sample(5.0, 0.6, 0.3, seed=3, n_samples=1).cpu().numpy()
+    c = G.sample(5.0, 0.6, 0.3, seed=0, n_samples=6).cpu().numpy()
+    assert np.array_equal(_bits(a[3]), _bits(b[0]))
+    assert np.array_equal(_bits(a), _bits(c))
+
+
+def test_apply_equals_sample_on_noise():
+    g = lattice(3, seed=6)
+    G = _graph(g, 0.05)
+    W = G.noise(2, 3)
+    u1 = G.sample(2.0, 0.6, 0.3, seed=2, n_samples=3)
+    u2 = G.apply(2.0, 0.6, 0.3, W)
+    assert torch.equal(u1, u2)
+    u3 = G.apply(2.0, 0.6, 0.3, W.clone(), out=None)
+    assert torch.equal(u1, u3)
+
+
+def test_node_range_partial_sums_add_up():
+    """sum over node shards == full sum (the multi-GPU l-sharding identity)."""
+    g = lattice(4, seed=7)
+    G = _graph(g, 0.05)
+    kappa, beta, k = 3.0, 0.7, 0.4
+    full = G.sample(kappa, beta, k, seed=1, n_samples=2).cpu().numpy()
+    L = solve.setup(g, 0.05, kappa, beta, k).plan.n_nodes
+    cuts = [0, L // 3, L // 2, L]
+    parts = sum(G.sample(kappa, beta, k, seed=1, n_samples=2, node_range=(a, b)).cpu().numpy()
+                for a, b in zip(cuts[:-1], cuts[1:]))
+    assert _rel(parts, full).max() <= 1e-13
+
+
+def test_host_output_matches_device():
+    g = lattice(3, seed=8)
+    G = _graph(g, 0.05)
+    a = G.sample(2.0, 0.6, 0.3, seed=0, n_samples=2).cpu().numpy()
+    b = G.sample_host(2.0, 0.6, 0.3, seed=0, n_samples=2)
+    assert np.array_equal(_bits(a), _bits(b))
+
+
+def test_invalid_arguments():
+    from paper_2605_02670_b200 import GrfError
+    G = _graph(single_edge(1.0), 0.1)
+    for kw in (dict(kappa=0.0, beta=0.6, k=0.3), dict(kappa=1.0, beta=0.2, k=0.3),
+               dict(kappa=1.0, beta=0.6, k=-1.0)):
+        with pytest.raises(GrfError):
+            G.sample(kw["kappa"], kw["beta"], kw["k"], n_samples=1)
+    with pytest.raises(GrfError):
+        G.sample(1.0, 0.6, 0.3, n_samples=1, node_range=(5, 2))
+
+
+# ----------------------------------------------------------------------------- BASELINE configs
+def test_config2_lattice_one_sample():
+    """configs[1] at full size: N = 198325, L = 259 (oracle ~45 s on CPU)."""
+    cfg = CONFIGS["lattice1"]
+    g = config_graph("lattice1")
+    G = _graph(g, cfg["h"])
+    u, st = G.sample(cfg["kappa"], cfg["beta"], cfg["k"], seed=cfg["seed"], n_samples=1, return_stats=True)
+    ref, _, _ = solve.sample(g, cfg["h"], cfg["kappa"], cfg["beta"], cfg["k"], cfg["seed"], 1)
+    assert _rel(u.cpu().numpy(), ref).max() <= FIELD_TOL
+    assert st["n_nodes"] == 259 and st["n_unconverged"] == 0
+
+
+def test_config3_lattice_256_samples_sampled():
+    """configs[2] at full size in the bench launch configuration (256 samples in one call);
+    the oracle recomputes samples 0, 101, 255 (all 212 nodes)."""
+    cfg = CONFIGS["lattice256"]
+    g = config_graph("lattice256")
+    G = _graph(g, cfg["h"])
+    u, st = G.sample(cfg["kappa"], cfg["beta"], cfg["k"], seed=cfg["seed"], n_samples=cfg["n_samples"],
+                     return_stats=True)
+    assert st["n_nodes"] == 212 and st["n_unconverged"] == 0
+    picks = [0, 101, 255]
+    ref, _, _ = solve.sample(g, cfg["h"], cfg["kappa"], cfg["beta"], cfg["k"], cfg["seed"], cfg["n_samples"],
+                             samples=picks)
+    got = u[picks].cpu().numpy()
+    assert _rel(got, ref).max() <= FIELD_TOL
+    # property at any size: every sample is finite and has the Matern-scale variance
+    uu = u.cpu().numpy()
+    assert np.isfinite(uu).all()
