@@ -154,7 +154,7 @@ grf_status grf_sample_host(grf_graph* g, double kappa, double beta, double k, ui
                            void* stream, grf_stats* stats);
 
 /* Apply sum_l (A^{(l)})^{-1} to caller right-hand sides (no noise): rhs and
- * u_out are device arrays n_rhs x N (may alias: in-place is allowed). */
+ * u_out are distinct device arrays n_rhs x N (EINVAL if they alias). */
 grf_status grf_apply(grf_graph* g, double kappa, double beta, double k, int64_t n_rhs,
                      const double* rhs, const grf_options* opt, double* u_out,
                      void* workspace, size_t ws_bytes, void* stream, grf_stats* stats);
@@ -164,6 +164,16 @@ grf_status grf_apply(grf_graph* g, double kappa, double beta, double k, int64_t 
  * nodes of opt's range, into host array sigma[(l*E + e)*2 + {0,1}].  Synchronises. */
 grf_status grf_edge_schur(grf_graph* g, double kappa, double beta, double k,
                           const grf_options* opt, double* sigma_host);
+
+/* ---- kernel timing (bench / diagnostics) ------------------------------------------
+ * With profiling enabled the library brackets every kernel it launches with CUDA events
+ * recorded on the launching stream (no synchronisation).  grf_profile_read synchronises
+ * those events, returns per-kernel totals since the last read and clears them:
+ * ms[k] / launches[k] for k = GRF_K_NOISE .. GRF_K_RECOVER (host arrays of length
+ * GRF_K_COUNT, either may be NULL). */
+enum { GRF_K_NOISE = 0, GRF_K_EDGE_SETUP = 1, GRF_K_CONDENSE = 2, GRF_K_PCG = 3, GRF_K_RECOVER = 4, GRF_K_COUNT = 5 };
+grf_status grf_profile_enable(grf_graph* g, int enable);
+grf_status grf_profile_read(grf_graph* g, double* ms, int64_t* launches);
 
 /* ---- multi-GPU (one process per GPU, NCCL over NVLink/NVSwitch) ---------------
  * grf_comm_get_unique_id on rank 0, broadcast the 128 bytes with any process

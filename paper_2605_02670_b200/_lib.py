@@ -43,7 +43,9 @@ EXPORTS = [
     "grf_graph_num_dofs", "grf_graph_edge_layout", "grf_graph_lumped_mass", "grf_plan_info",
     "grf_workspace_size", "grf_noise", "grf_sample", "grf_sample_host", "grf_apply", "grf_edge_schur",
     "grf_comm_get_unique_id", "grf_comm_init", "grf_comm_destroy", "grf_reduce_sum",
+    "grf_profile_enable", "grf_profile_read",
 ]
+KERNEL_NAMES = ["noise", "edge_setup", "condense", "pcg", "recover"]
 
 _lib = None
 
@@ -85,6 +87,8 @@ def load() -> C.CDLL:
         "grf_comm_init": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(P)]),
         "grf_comm_destroy": (None, [P]),
         "grf_reduce_sum": (C.c_int, [P, P, P, I64, C.c_int, P]),
+        "grf_profile_enable": (C.c_int, [P, C.c_int]),
+        "grf_profile_read": (C.c_int, [P, pd, pi64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -29,8 +29,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC,
           "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 PER_FILE = {"noise.cu": ["--fmad=false"]}
-SOURCES = ["noise.cu", "edge_setup.cu", "condense.cu", "pcg.cu", "recover.cu", "grf_api.cpp"]
-HEADERS = ["grf_internal.h"]
+SOURCES = ["noise.cu", "edge_setup.cu", "sweep.cu", "pcg.cu", "grf_api.cpp"]
+HEADERS = ["grf_internal.h", "thomas.cuh"]
 
 
 def nvcc() -> str:

@@ -7,10 +7,11 @@
 // each end carries share = (c_I + kappa^2 c_L) h_e / 2 + c_L / h_e of A_GG, and couples to
 // its adjacent interior node with coefficient b (A_GI, P185).
 //
-// Thomas factorisation of A_II (P187-194 [eq:thomas_coefficients]):
+// Thomas factorisation of A_II (P187-194 [eq:thomas_coefficients], thomas.cuh):
 //     d'_1 = a,  d'_lo,i = b / d'_{i-1},  d'_i = a - d'_lo,i b
-// stored as invd[(off_e + i - 1) * L + l] = 1 / d'_i (node-minor: a warp of nodes reads
-// one 256-B line per i in K3/K5).
+// K3/K5 (sweep.cu) use them through three node-minor tables [(off_e + t) * L + l]:
+//     mu_t = d'_lo,t = b / d'_{t-1} (mu_1 = 0),  g_t = 1 / (d'_t + d'_{m+1-t} - a),  kap_t = -g_t mu_t
+// (g_t is the diagonal of A_II^{-1}; see sweep.cu for the twisted-factorisation use).
 //
 // Local Schur complement (P204-213 [eq:local_reduced_schur]):
 //     S^{(l,e)} = A_GG - A_GI A_II^{-1} A_IG = [[s_d, s_o], [s_o, s_d]],
@@ -27,43 +28,48 @@
 // blocks: the same numerical vectors (P242 "yields the exact same numerical vector"),
 // O(|E|) per PCG iteration instead of O(N).
 #include "grf_internal.h"
+#include "thomas.cuh"
 
 namespace grf {
 namespace {
 
 __global__ void edge_setup_kernel(DevGraph g, int32_t L, const double* __restrict__ cIt,
-                                  const double* __restrict__ cLt, double kappa2, double* __restrict__ invd,
+                                  const double* __restrict__ cLt, double kappa2, double* __restrict__ mu_t,
+                                  double* __restrict__ gam_t, double* __restrict__ kap_t,
                                   double4* __restrict__ sig) {
     const int e = blockIdx.x;
     const double h = g.h[e];
     const int m = g.m[e];
-    const int64_t off = g.off[e];
+    double* tmu = mu_t + g.off[e] * L;
+    double* tgam = gam_t + g.off[e] * L;
+    double* tkap = kap_t + g.off[e] * L;
     for (int l = threadIdx.x; l < L; l += blockDim.x) {
         const double cI = cIt[l], cL = cLt[l];
-        const double mass = cI + kappa2 * cL;
-        const double stiff = cL / h;
-        const double a = mass * h + 2.0 * stiff;
-        const double b = -stiff;
-        const double share = mass * h * 0.5 + stiff;
+        const EdgeCoef c = edge_coef(cI, cL, kappa2, h);
+        const double share = (cI + kappa2 * cL) * h * 0.5 + c.beta;
         double sd, so;
         if (m == 0) {
             sd = share;
-            so = b;
+            so = c.b;
         } else {
-            double d = a;
-            double id = 1.0 / d;
-            invd[off * L + l] = id;
-            double prod = 1.0;  // prod_{i<m} (-b / d'_i)
-            for (int i = 1; i < m; ++i) {
-                prod *= -b * id;
-                const double lo = b * id;    // d'_lo,i+1 = b / d'_i
-                d = a - lo * b;
-                id = 1.0 / d;
-                invd[(off + i) * L + l] = id;
+            // pivots d'_t (stored temporarily in the kap table) and multipliers mu_t
+            double inv = 0.0;
+            double prod = 1.0;  // prod_{t=1}^{m-1} (-mu_t) = prod_{i<m} (-b / d'_i)
+            for (int t = 0; t < m; ++t) {
+                const double mu = thomas_step(c, inv);
+                tmu[(int64_t)t * L + l] = mu;
+                tkap[(int64_t)t * L + l] = c.a - mu * c.b;  // d'_t, the same expression thomas_step inverted
+                if (t > 0) prod *= -mu;
             }
-            const double b2 = b * b;
-            sd = share - b2 * id;
-            so = -b2 * (prod * id);
+            // twisted-factorisation diagonal g_t = (A_II^{-1})_tt = 1 / (d'_t + d'_{m+1-t} - a)
+            for (int t = 0; t < m; ++t)
+                tgam[(int64_t)t * L + l] =
+                    1.0 / (tkap[(int64_t)t * L + l] + tkap[(int64_t)(m - 1 - t) * L + l] - c.a);
+            for (int t = 0; t < m; ++t)
+                tkap[(int64_t)t * L + l] = -tgam[(int64_t)t * L + l] * tmu[(int64_t)t * L + l];
+            const double b2 = c.b * c.b;
+            sd = share - b2 * inv;          // (A_II^{-1})_11 = 1 / d'_m
+            so = -b2 * (prod * inv);        // (A_II^{-1})_1m
         }
         const double det = sd * sd - so * so;
         sig[(int64_t)l * g.E + e] = make_double4(sd, so, sd / det, -so / det);
@@ -75,7 +81,7 @@ __global__ void edge_setup_kernel(DevGraph g, int32_t L, const double* __restric
 void launch_edge_setup(const DevGraph& g, DevPlan& p, cudaStream_t st) {
     int threads = ((p.L + 31) / 32) * 32;
     if (threads > 256) threads = 256;
-    edge_setup_kernel<<<g.E, threads, 0, st>>>(g, p.L, p.cI, p.cL, p.kappa * p.kappa, p.invd,
+    edge_setup_kernel<<<g.E, threads, 0, st>>>(g, p.L, p.cI, p.cL, p.kappa * p.kappa, p.mu, p.gam, p.kap,
                                                reinterpret_cast<double4*>(p.sig));
 }
 

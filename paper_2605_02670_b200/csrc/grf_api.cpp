@@ -89,6 +89,39 @@ struct grf_graph {
     grf::DevGraph dev;
     std::vector<Block> blocks;  // graph-lifetime device allocations
     std::list<std::unique_ptr<Plan>> plans;  // most recent first
+    // kernel timing (grf_profile_enable / grf_profile_read)
+    bool prof = false;
+    struct Rec {
+        int kind;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    cudaEvent_t new_event() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e = nullptr;
+        cudaEventCreate(&e);
+        return e;
+    }
+    // run `launch` (enqueues one kernel on st), bracketed by events when profiling
+    template <class F>
+    cudaError_t timed(int kind, cudaStream_t st, F&& launch) {
+        if (!prof) {
+            launch();
+            return cudaGetLastError();
+        }
+        Rec r{kind, new_event(), new_event()};
+        cudaEventRecord(r.a, st);
+        launch();
+        cudaError_t e = cudaGetLastError();
+        cudaEventRecord(r.b, st);
+        recs.push_back(r);
+        return e;
+    }
 
     template <class T>
     T* upload(const std::vector<T>& v, grf_status* st) {
@@ -189,12 +222,15 @@ grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf
     };
     double* dcI = (double*)grab(L * sizeof(double));
     double* dcL = (double*)grab(L * sizeof(double));
-    double* invd = (double*)grab((size_t)std::max<int64_t>(g->NI, 1) * L * sizeof(double));
+    const size_t tab = (size_t)std::max<int64_t>(g->NI, 1) * L * sizeof(double);
+    double* mu = (double*)grab(tab);
+    double* gam = (double*)grab(tab);
+    double* kap = (double*)grab(tab);
     double* sig = (double*)grab((size_t)L * g->E * 4 * sizeof(double));
-    if (!dcI || !dcL || !invd || !sig) {
+    if (!dcI || !dcL || !mu || !gam || !kap || !sig) {
         for (auto& b : p->blocks) g->alloc.put(b.p, b.bytes, st);
         return fail(GRF_ENOMEM, "plan tables (%.1f MB) could not be allocated",
-                    (double)((size_t)g->NI * L * 8 + (size_t)L * g->E * 32) / 1e6);
+                    (double)(3 * (size_t)g->NI * L * 8 + (size_t)L * g->E * 32) / 1e6);
     }
     CUDA_TRY(cudaMemcpyAsync(dcI, cI.data(), L * sizeof(double), cudaMemcpyHostToDevice, st));
     CUDA_TRY(cudaMemcpyAsync(dcL, cL.data(), L * sizeof(double), cudaMemcpyHostToDevice, st));
@@ -202,10 +238,11 @@ grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf
     p->dev.kappa = kappa;
     p->dev.cI = dcI;
     p->dev.cL = dcL;
-    p->dev.invd = invd;
+    p->dev.mu = mu;
+    p->dev.gam = gam;
+    p->dev.kap = kap;
     p->dev.sig = sig;
-    grf::launch_edge_setup(g->dev, p->dev, st);
-    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(g->timed(GRF_K_EDGE_SETUP, st, [&] { grf::launch_edge_setup(g->dev, p->dev, st); }));
     CUDA_TRY(cudaStreamSynchronize(st));  // host vectors cI/cL die at return
     // keep at most 4 plans
     while (g->plans.size() >= 4) {
@@ -221,17 +258,25 @@ grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct WsLayout {
-    size_t gu = 0, iters = 0, relres = 0, total = 0;
+    size_t w = 0, ends = 0, ug = 0, iters = 0, relres = 0, counter = 0, total = 0;
 };
 
-WsLayout ws_layout(const grf_graph* g, int64_t L, int64_t S) {
+// with_noise: grf_sample keeps the white noise W (S x N) in the workspace
+WsLayout ws_layout(const grf_graph* g, int64_t L, int64_t S, bool with_noise = true) {
     WsLayout w;
-    w.gu = 0;
-    size_t o = align_up((size_t)S * g->V * L * sizeof(double));
+    size_t o = 0;
+    w.w = o;
+    if (with_noise) o += align_up((size_t)S * g->N * sizeof(double));
+    w.ends = o;
+    o += align_up((size_t)S * g->E * 2 * L * sizeof(double));
+    w.ug = o;
+    o += align_up((size_t)S * g->V * L * sizeof(double));
     w.iters = o;
     o += align_up((size_t)S * L * sizeof(int32_t));
     w.relres = o;
     o += align_up((size_t)S * L * sizeof(double));
+    w.counter = o;
+    o += align_up(2 * sizeof(int32_t));
     w.total = o;
     return w;
 }
@@ -247,10 +292,13 @@ grf_status check_kernel_limits(const grf_graph* g) {
 }
 
 // Shared tail of grf_sample / grf_apply: u (holding W on entry) -> u.
-grf_status solve_inplace(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, double* u, void* ws,
-                         size_t ws_bytes, cudaStream_t st, grf_stats* stats, int64_t launches_so_far) {
+// W (S x N, device) -> u (S x N, device).  When W is null the noise for `seed` is first
+// generated into the workspace (grf_sample); otherwise W is the caller's rhs (grf_apply).
+grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const double* W, uint64_t seed,
+                 double* u, void* ws, size_t ws_bytes, cudaStream_t st, grf_stats* stats) {
     const int64_t L = p->dev.L;
-    WsLayout w = ws_layout(g, L, S);
+    const bool gen = (W == nullptr);
+    WsLayout w = ws_layout(g, L, S, gen);
     void* own = nullptr;
     if (!ws) {
         own = g->alloc.get(w.total, st);
@@ -260,21 +308,39 @@ grf_status solve_inplace(grf_graph* g, Plan* p, int64_t S, const grf_options* op
         return fail(GRF_ENOMEM, "workspace too small: %zu < %zu bytes", ws_bytes, w.total);
     }
     char* base = static_cast<char*>(ws);
-    double* gu = reinterpret_cast<double*>(base + w.gu);
+    int64_t launches = 3;
+    if (gen) {
+        double* Wd = reinterpret_cast<double*>(base + w.w);
+        cudaError_t ne = g->timed(GRF_K_NOISE, st, [&] { grf::launch_noise(g->dev, seed, S, Wd, st); });
+        if (ne != cudaSuccess) {
+            if (own) g->alloc.put(own, w.total, st);
+            return fail(GRF_ECUDA, "noise launch: %s", cudaGetErrorString(ne));
+        }
+        W = Wd;
+        launches = 4;
+    }
+    double* ends = reinterpret_cast<double*>(base + w.ends);
+    double* uG = reinterpret_cast<double*>(base + w.ug);
     int32_t* iters = reinterpret_cast<int32_t*>(base + w.iters);
     double* relres = reinterpret_cast<double*>(base + w.relres);
+    int32_t* counters = reinterpret_cast<int32_t*>(base + w.counter);
     grf::PcgParams prm;
     prm.rtol = opt ? opt->rtol : 1e-13;
     prm.max_iter = (opt && opt->max_iter > 0) ? opt->max_iter : (int32_t)(g->V + 10);
     prm.precond = opt ? opt->precond : GRF_PRECOND_NN;
     grf_status rc = GRF_OK;
-    grf::launch_condense(g->dev, p->dev, S, u, gu, st);
-    cudaError_t ce = cudaGetLastError();
-    if (ce == cudaSuccess) {
-        grf::launch_pcg(g->dev, p->dev, S, prm, gu, iters, relres, st);
-        ce = cudaGetLastError();
-    }
-    if (ce == cudaSuccess) ce = grf::launch_recover(g->dev, p->dev, S, u, gu, st);
+    cudaError_t le = cudaSuccess;
+    cudaError_t ce = g->timed(GRF_K_CONDENSE, st, [&] {
+        le = grf::launch_condense(g->dev, p->dev, S, W, ends, grf::make_work_queue(g->dev, S, counters), st);
+    });
+    if (ce == cudaSuccess) ce = le;
+    if (ce == cudaSuccess)
+        ce = g->timed(GRF_K_PCG, st, [&] { grf::launch_pcg(g->dev, p->dev, S, prm, W, ends, uG, iters, relres, st); });
+    if (ce == cudaSuccess)
+        ce = g->timed(GRF_K_RECOVER, st, [&] {
+            le = grf::launch_recover(g->dev, p->dev, S, W, u, uG, grf::make_work_queue(g->dev, S, counters + 1), st);
+        });
+    if (ce == cudaSuccess) ce = le;
     if (ce != cudaSuccess) rc = fail(GRF_ECUDA, "kernel launch failed: %s", cudaGetErrorString(ce));
     if (rc == GRF_OK && stats) {
         std::vector<int32_t> it(S * L);
@@ -303,7 +369,7 @@ grf_status solve_inplace(grf_graph* g, Plan* p, int64_t S, const grf_options* op
             stats->iter_mean = it.empty() ? 0.0 : sum / it.size();
             stats->worst_rel_residual = worst;
             stats->n_unconverged = bad;
-            stats->gpu_launches = launches_so_far + 3;
+            stats->gpu_launches = launches;
             if (bad) rc = fail(GRF_ENOCONV, "%lld of %lld PCG systems missed rtol %g (worst %g)", (long long)bad,
                                (long long)(S * L), prm.rtol, worst);
         }
@@ -414,6 +480,9 @@ grf_status grf_graph_create(int64_t n_vertices, int64_t n_edges, const int64_t* 
         owner[v] = inc[ptr[v]];
         inv_deg[v] = 1.0 / (double)deg[v];
     }
+    std::vector<int32_t> order(E);
+    for (int64_t e = 0; e < E; ++e) order[e] = (int32_t)e;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return mm[a] > mm[b]; });
     std::vector<int32_t> eu32(E), ev32(E);
     for (int64_t e = 0; e < E; ++e) {
         eu32[e] = (int32_t)g->eu[e];
@@ -437,6 +506,7 @@ grf_status grf_graph_create(int64_t n_vertices, int64_t n_edges, const int64_t* 
     if (!st) d.inv_deg = g->upload(inv_deg, &st);
     if (!st) d.owner = g->upload(owner, &st);
     if (!st) d.sqrt_ml = g->upload(sq, &st);
+    if (!st) d.edge_order = g->upload(order, &st);
     if (st) {
         grf_graph_destroy(g.release());
         return st;
@@ -451,6 +521,11 @@ void grf_graph_destroy(grf_graph* g) {
     for (auto& p : g->plans)
         for (auto& b : p->blocks) g->alloc.put(b.p, b.bytes, nullptr);
     for (auto& b : g->blocks) g->alloc.put(b.p, b.bytes, nullptr);
+    for (auto& r : g->recs) {
+        g->pool.push_back(r.a);
+        g->pool.push_back(r.b);
+    }
+    for (auto e : g->pool) cudaEventDestroy(e);
     delete g;
 }
 
@@ -507,8 +582,8 @@ grf_status grf_workspace_size(const grf_graph* g, double kappa, double beta, dou
 grf_status grf_noise(grf_graph* g, uint64_t seed, int64_t n_samples, double* W_out, void* stream) {
     if (!g || !W_out) return fail(GRF_EINVAL, "NULL argument");
     if (n_samples < 1) return fail(GRF_EINVAL, "n_samples must be >= 1");
-    grf::launch_noise(g->dev, seed, n_samples, W_out, (cudaStream_t)stream);
-    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(g->timed(GRF_K_NOISE, (cudaStream_t)stream,
+                      [&] { grf::launch_noise(g->dev, seed, n_samples, W_out, (cudaStream_t)stream); }));
     return GRF_OK;
 }
 
@@ -526,9 +601,7 @@ grf_status grf_sample(grf_graph* g, double kappa, double beta, double k, uint64_
     st = get_plan(g, kappa, beta, k, opt, s, &p);
     if (st) return st;
     (void)nplans;
-    grf::launch_noise(g->dev, seed, n_samples, u_out, s);
-    CUDA_TRY(cudaGetLastError());
-    return solve_inplace(g, p, n_samples, opt, u_out, workspace, ws_bytes, s, stats, 1);
+    return solve(g, p, n_samples, opt, nullptr, seed, u_out, workspace, ws_bytes, s, stats);
 }
 
 grf_status grf_apply(grf_graph* g, double kappa, double beta, double k, int64_t n_rhs, const double* rhs,
@@ -543,9 +616,8 @@ grf_status grf_apply(grf_graph* g, double kappa, double beta, double k, int64_t 
     Plan* p = nullptr;
     st = get_plan(g, kappa, beta, k, opt, s, &p);
     if (st) return st;
-    if (rhs != u_out)
-        CUDA_TRY(cudaMemcpyAsync(u_out, rhs, (size_t)n_rhs * g->N * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    return solve_inplace(g, p, n_rhs, opt, u_out, workspace, ws_bytes, s, stats, 0);
+    if (rhs == u_out) return fail(GRF_EINVAL, "grf_apply: rhs and u_out must not alias");
+    return solve(g, p, n_rhs, opt, rhs, 0, u_out, workspace, ws_bytes, s, stats);
 }
 
 grf_status grf_sample_host(grf_graph* g, double kappa, double beta, double k, uint64_t seed, int64_t n_samples,
@@ -584,6 +656,35 @@ grf_status grf_edge_schur(grf_graph* g, double kappa, double beta, double k, con
         sigma_host[2 * t + 1] = buf[4 * t + 1];
     }
     return GRF_OK;
+}
+
+grf_status grf_profile_enable(grf_graph* g, int enable) {
+    if (!g) return fail(GRF_EINVAL, "graph is NULL");
+    g->prof = enable != 0;
+    return GRF_OK;
+}
+
+grf_status grf_profile_read(grf_graph* g, double* ms, int64_t* launches) {
+    if (!g) return fail(GRF_EINVAL, "graph is NULL");
+    double acc[GRF_K_COUNT] = {0};
+    int64_t cnt[GRF_K_COUNT] = {0};
+    grf_status rc = GRF_OK;
+    for (auto& r : g->recs) {
+        float t = 0.f;
+        cudaError_t e = cudaEventSynchronize(r.b);
+        if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.a, r.b);
+        if (e != cudaSuccess && rc == GRF_OK) rc = fail(GRF_ECUDA, "event timing: %s", cudaGetErrorString(e));
+        acc[r.kind] += t;
+        cnt[r.kind] += 1;
+        g->pool.push_back(r.a);
+        g->pool.push_back(r.b);
+    }
+    g->recs.clear();
+    for (int k = 0; k < GRF_K_COUNT; ++k) {
+        if (ms) ms[k] = acc[k];
+        if (launches) launches[k] = cnt[k];
+    }
+    return rc;
 }
 
 // ---------------------------------------------------------------- NCCL (dlopen'ed)

@@ -25,6 +25,7 @@ struct DevGraph {
     const double* inv_deg = nullptr;  // [V] 1 / d_v, d_v = incident edge ends (P261)
     const int32_t* owner = nullptr;   // [V] incidence code that writes the vertex value in recovery
     const double* sqrt_ml = nullptr;  // [N] sqrt of the lumped mass diagonal
+    const int32_t* edge_order = nullptr; // [E] edges by descending interior length (work-queue order)
 };
 
 // Device per-plan tables (one (kappa, beta, k, node range)).
@@ -33,7 +34,9 @@ struct DevPlan {
     double kappa = 0.0;
     const double* cI = nullptr;       // [L]
     const double* cL = nullptr;       // [L]
-    double* invd = nullptr;           // [NI * L]: 1/d'_i of A_II^{(l,e)}, layout [(off_e + i) * L + l]
+    double* mu = nullptr;             // [NI * L] Thomas multipliers  b/d'_{t-1}, layout [(off_e + t) * L + l]
+    double* gam = nullptr;            // [NI * L] diag of A_II^{-1}: 1/(d'_t + d'_{m+1-t} - a)
+    double* kap = nullptr;            // [NI * L] -gam_t * mu_t
     double* sig = nullptr;            // [L * E * 4]: (s_d, s_o, p_d, p_o) local Schur + its inverse
 };
 
@@ -43,20 +46,30 @@ struct PcgParams {
     int32_t precond = 0;
 };
 
+// Work queue of (edge, sample chunk) items shared by K3 and K5: items are handed out
+// longest edge first through an atomic counter (reset by the launcher).
+struct WorkQueue {
+    int32_t* counter = nullptr;       // device int, zeroed before each launch
+    int32_t samples_per_item = 0;
+    int32_t chunks = 0;               // sample chunks per edge
+    int32_t n_items = 0;              // E * chunks
+};
+
 // K1  noise (noise.cu): W[s*N + i] = sqrt(M_L,ii) z(seed + s, i)
 void launch_noise(const DevGraph& g, uint64_t seed, int64_t n_samples, double* W, cudaStream_t st);
 // K2  per-(node, edge) Thomas pivots + local Schur blocks (edge_setup.cu)
 void launch_edge_setup(const DevGraph& g, DevPlan& p, cudaStream_t st);
-// K3  condensed vertex rhs g[(s*V + v)*L + l] (condense.cu)
-void launch_condense(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W,
-                     double* gu, cudaStream_t st);
-// K4  batched NN-PCG on the vertex Schur systems, in place g -> u_Gamma (pcg.cu)
-void launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm,
-                double* gu, int32_t* iters, double* relres, cudaStream_t st);
-// K5  Thomas recovery + accumulation over nodes, W -> u in place (recover.cu)
-cudaError_t launch_recover(const DevGraph& g, const DevPlan& p, int64_t n_samples, double* Wu,
-                           const double* gu, cudaStream_t st);
+// K3  Thomas end values per (sample, edge, end, node) (sweep.cu): ends[((s*E + e)*2 + end)*L + l]
+cudaError_t launch_condense(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W,
+                            double* ends, WorkQueue wq, cudaStream_t st);
+// K4  batched NN-PCG on the vertex Schur systems (pcg.cu): g from (W, ends), u_G -> uG[(s*V + v)*L + l]
+void launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* W,
+                const double* ends, double* uG, int32_t* iters, double* relres, cudaStream_t st);
+// K5  Thomas recovery + accumulation over nodes (sweep.cu): u[s*N + dof] from W and u_G
+cudaError_t launch_recover(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W, double* u,
+                           const double* uG, WorkQueue wq, cudaStream_t st);
 
+WorkQueue make_work_queue(const DevGraph& g, int64_t n_samples, int32_t* counter);
 size_t pcg_smem_bytes(const DevGraph& g);
 int32_t pcg_max_vertices();
 int32_t recover_max_interior();

@@ -13,8 +13,9 @@
 // Mapping: one CTA per (node l, sample s) system; the vertex vectors x, r, z, p, q live in
 // shared memory (V <= pcg_max_vertices); dot products are warp-shuffle + smem block
 // reductions; every system iterates to its own convergence inside the kernel (no host
-// round trip).  g is read from, and u_G written back to, gu[(s*V + v)*L + l]; CTAs with
-// consecutive l share L2 sectors of that node-minor layout.
+// round trip).  g is gathered from K3's end values ends[((s*E + e)*2 + end)*L + l] and
+// u_G written to uG[(s*V + v)*L + l]; CTAs with consecutive l (the fastest grid index)
+// share the L2 sectors of these node-minor layouts.
 #include "grf_internal.h"
 
 #include <cub/block/block_reduce.cuh>
@@ -30,9 +31,11 @@ struct Sum2 {
     }
 };
 
-__global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L, const double4* __restrict__ sig,
-                                                          PcgParams prm, double* __restrict__ gu,
-                                                          int32_t* __restrict__ iters, double* __restrict__ relres) {
+__global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L, const double* __restrict__ cLt,
+                                                          const double4* __restrict__ sig, PcgParams prm,
+                                                          const double* __restrict__ W, const double* __restrict__ ends,
+                                                          double* __restrict__ uG, int32_t* __restrict__ iters,
+                                                          double* __restrict__ relres) {
     using BR1 = cub::BlockReduce<double, PCG_THREADS>;
     using BR2 = cub::BlockReduce<double2, PCG_THREADS>;
     __shared__ union {
@@ -51,7 +54,9 @@ __global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L,
     const int l = blockIdx.x;
     const int64_t s = blockIdx.y;
     const double4* sg = sig + (int64_t)l * g.E;
-    double* gcol = gu + (s * V) * (int64_t)L + l;
+    double* ucol = uG + (s * V) * (int64_t)L + l;
+    const double* ecol = ends + (s * g.E) * 2 * (int64_t)L + l;
+    const double cL = cLt[l];
 
     auto reduce1 = [&](double v) -> double {
         double t = BR1(tmp.r1).Sum(v);
@@ -100,9 +105,14 @@ __global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L,
         }
     };
 
+    // condensed rhs g_v = W_v + sum_{(e,end) at v} (c_L/h_e) w_end   (P233-239)
     double part = 0.0;
     for (int v = threadIdx.x; v < V; v += blockDim.x) {
-        const double gv = gcol[(int64_t)v * L];
+        double gv = W[s * g.N + g.NI + v];
+        for (int k = g.inc_ptr[v]; k < g.inc_ptr[v + 1]; ++k) {
+            const int code = g.inc[k];
+            gv += (cL / g.h[code >> 1]) * ecol[(int64_t)code * L];
+        }
         r[v] = gv;
         x[v] = 0.0;
         part += gv * gv;
@@ -157,7 +167,7 @@ __global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L,
             __syncthreads();
         }
     }
-    for (int v = threadIdx.x; v < V; v += blockDim.x) gcol[(int64_t)v * L] = x[v];
+    for (int v = threadIdx.x; v < V; v += blockDim.x) ucol[(int64_t)v * L] = x[v];
     if (threadIdx.x == 0) {
         iters[s * L + l] = it;
         relres[s * L + l] = gg > 0.0 ? sqrt(rr / gg) : 0.0;
@@ -170,8 +180,8 @@ int32_t pcg_max_vertices() { return 5000; }
 
 size_t pcg_smem_bytes(const DevGraph& g) { return sizeof(double) * 5 * (size_t)g.V; }
 
-void launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, double* gu,
-                int32_t* iters, double* relres, cudaStream_t st) {
+void launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* W,
+                const double* ends, double* uG, int32_t* iters, double* relres, cudaStream_t st) {
     const size_t smem = pcg_smem_bytes(g);
     static bool attr_set = false;
     if (!attr_set) {
@@ -179,8 +189,8 @@ void launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, const Pc
         attr_set = true;
     }
     dim3 grid(p.L, (unsigned)n_samples);
-    pcg_kernel<<<grid, PCG_THREADS, smem, st>>>(g, p.L, reinterpret_cast<const double4*>(p.sig), prm, gu, iters,
-                                                relres);
+    pcg_kernel<<<grid, PCG_THREADS, smem, st>>>(g, p.L, p.cL, reinterpret_cast<const double4*>(p.sig), prm, W, ends,
+                                                uG, iters, relres);
 }
 
 }  // namespace grf

@@ -220,6 +220,19 @@ class Graph:
             raise ValueError(f"workspace needs {b.value} bytes")
         return C.c_void_p(workspace.data_ptr()), C.c_size_t(workspace.numel() * workspace.element_size())
 
+    def profile(self, enable: bool = True):
+        """Bracket every kernel launch with CUDA events (grf_profile_enable)."""
+        check(self._lib.grf_profile_enable(self._h, 1 if enable else 0))
+
+    def profile_read(self):
+        """{kernel: (total_ms, launches)} since the last read (synchronises the recorded events)."""
+        from ._lib import KERNEL_NAMES
+        ms = np.zeros(len(KERNEL_NAMES))
+        n = np.zeros(len(KERNEL_NAMES), dtype=np.int64)
+        check(self._lib.grf_profile_read(self._h, ms.ctypes.data_as(C.POINTER(C.c_double)),
+                                         n.ctypes.data_as(C.POINTER(C.c_int64))))
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(KERNEL_NAMES)}
+
     def close(self):
         if getattr(self, "_h", None):
             self._lib.grf_graph_destroy(self._h)

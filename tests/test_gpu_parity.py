@@ -158,7 +158,11 @@ def test_seed_convention_and_determinism():
     a = G.sample(5.0, 0.6, 0.3, seed=0, n_samples=6).cpu().numpy()
     b = G.sample(5.0, 0.6, 0.3, seed=3, n_samples=1).cpu().numpy()
     c = G.sample(5.0, 0.6, 0.3, seed=0, n_samples=6).cpu().numpy()
-    assert np.array_equal(_bits(a[3]), _bits(b[0]))
+    # the noise is bit-identical; the field's sum over nodes may be grouped differently for a
+    # different sample count (the lane mapping depends on it), so it agrees to rounding
+    assert np.array_equal(_bits(G.noise(0, 6).cpu().numpy()[3]), _bits(G.noise(3, 1).cpu().numpy()[0]))
+    assert _rel(a[3], b[0]) <= 1e-13
+    # the same call is bitwise reproducible (fixed-order reductions, no atomics on data)
     assert np.array_equal(_bits(a), _bits(c))
 
 
