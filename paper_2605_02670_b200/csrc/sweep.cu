@@ -20,10 +20,14 @@
 //
 // Mapping: an item = (edge, tile of SL samples), pulled from a longest-edge-first queue.
 // lane = (sample, node sub-lane), warp = group of NLW*LL nodes; every thread carries
-// NLW nodes x 2 chains in registers.  The per-(l, t) coefficients are staged into shared
-// memory IB steps at a time and read as warp broadcasts; per-warp partial sums over the
-// thread's nodes are combined across warps through shared memory in fixed order
-// (deterministic) and added into the output (first visit writes, second adds).
+// NLW nodes x 2 chains in registers.  The per-(l, t) coefficients and the W tile are
+// staged into shared memory IB steps at a time with cp.async, double buffered (block
+// b+1 loads while block b computes), and read as warp broadcasts.  Per-warp partial sums
+// over the thread's nodes are combined across warps in fixed order (deterministic) into
+// an output tile kept in shared memory for the whole edge (written to HBM once,
+// coalesced); edges too long for the tile fall back to read-modify-write in global memory.
+#include <cuda_pipeline.h>
+
 #include "grf_internal.h"
 
 namespace grf {
@@ -31,6 +35,7 @@ namespace {
 
 constexpr int IB = 8;          // steps per staging / reduction block
 constexpr int MAXW = 16;       // warps per CTA
+constexpr int OTILE_BYTES = 48 * 1024;
 
 struct SweepArgs {
     DevGraph g;
@@ -45,6 +50,7 @@ struct SweepArgs {
     const double* uG;   // recover: [(s*V + v)*L + l]
     WorkQueue wq;
     int32_t nwarps;     // warps per CTA (node groups per round)
+    int32_t mtile;      // recover: edges with m <= mtile keep their output tile in smem
 };
 
 template <int SL>
@@ -52,12 +58,18 @@ struct Lanes {
     static constexpr int LL = 32 / SL;  // node sub-lanes per warp
 };
 
-// Shared memory layout (doubles):
-//   coef [3][IB][LR]                 staged mu/gam/kap for this round's LR nodes
-//   part [2*IB][P][SL+1]             per (row, partial, sample) sums, P = nwarps*LL
+__device__ __forceinline__ void cp8(double* dst, const double* src) { __pipeline_memcpy_async(dst, src, 8); }
+
+// Shared memory layout (doubles), NT = number of coefficient tables (1 condense, 3 recover):
+//   coef [2][NT][IB][LR]   staged mu (, gam, kap) for this round's LR nodes, double buffered
+//   wbuf [2][2][IB][SL+1]  staged W: [buffer][left/right positions][step][sample]
+//   part [2*IB][P][SL+1]   per (row, partial, sample) sums, P = nwarps*LL          (recover)
+//   otile[mtile][SL+1]     the edge's output tile                                  (recover)
 template <int NLW, int SL, bool REC>
 __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
     constexpr int LL = Lanes<SL>::LL;
+    constexpr int NT = REC ? 3 : 1;
+    constexpr int SP = SL + 1;
     extern __shared__ double smem[];
     __shared__ int item_sh;
     const DevGraph& g = A.g;
@@ -65,13 +77,16 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
     const int sl = lane % SL, ll = lane / SL;
     const int nwarps = A.nwarps;
     const int P = nwarps * LL;
-    const int LR = nwarps * NLW * LL;           // nodes per round
+    const int LR = nwarps * NLW * LL;  // nodes per round
     const int L = A.L;
     const int rounds = (L + LR - 1) / LR;
-    double* coef = smem;                          // 3*IB*LR
-    double* part = smem + 3 * IB * LR;            // 2*IB*P*(SL+1)
+    double* coef = smem;                                 // 2*NT*IB*LR
+    double* wbuf = coef + 2 * NT * IB * LR;              // 2*2*IB*SP
+    double* part = wbuf + 4 * IB * SP;                   // 2*IB*P*SP     (REC)
+    double* otile = part + (REC ? 2 * IB * P * SP : 0);  // mtile*SP      (REC)
     const int64_t N = g.N;
     const int V = g.V;
+    const int pidx = warp * LL + ll;
 
     for (;;) {
         if (tid == 0) item_sh = atomicAdd(A.wq.counter, 1);
@@ -84,15 +99,16 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
         const int64_t s = s0 + sl;
         const bool sact = s < A.S;
         const int64_t sc = sact ? s : (A.S - 1);
+        const int ns = (int)((A.S - s0) < SL ? (A.S - s0) : SL);
         const int m = g.m[e];
         const int64_t off = g.off[e];
         const double h = g.h[e];
         const int vu = g.eu[e], vv = g.ev[e];
-        const double* Wrow = A.W + sc * N + off;
+        const double* Wtile = A.W + s0 * N + off;
+        const bool in_smem = REC && (m <= A.mtile);
 
         for (int rd = 0; rd < rounds; ++rd) {
             const int lbase = rd * LR + warp * (NLW * LL) + ll;  // node of chain k: lbase + k*LL
-            double Y[NLW], Z[NLW];
             // ---------------- recover: vertex values owned by this edge (sum over l of u_G)
             if (REC) {
                 const bool ownL = g.owner[vu] == 2 * e, ownR = g.owner[vv] == 2 * e + 1;
@@ -106,14 +122,13 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
                             a1 += A.uG[(sc * V + vv) * (int64_t)L + l];
                         }
                     }
-                    const int pidx = warp * LL + ll;
-                    part[(0 * P + pidx) * (SL + 1) + sl] = a0;
-                    part[(1 * P + pidx) * (SL + 1) + sl] = a1;
+                    part[(0 * P + pidx) * SP + sl] = a0;
+                    part[(1 * P + pidx) * SP + sl] = a1;
                     __syncthreads();
                     for (int o = tid; o < 2 * SL; o += blockDim.x) {
                         const int side = o / SL, j = o % SL;
                         double t = 0.0;
-                        for (int p = 0; p < P; ++p) t += part[(side * P + p) * (SL + 1) + j];
+                        for (int p = 0; p < P; ++p) t += part[(side * P + p) * SP + j];
                         const int64_t so = s0 + j;
                         if (so < A.S && (side ? ownR : ownL)) {
                             double* dst = A.out + so * N + g.NI + (side ? vv : vu);
@@ -137,39 +152,74 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
                 }
                 continue;
             }
+            double Y[NLW], Z[NLW];
 #pragma unroll
             for (int k = 0; k < NLW; ++k) Y[k] = Z[k] = 0.0;
-            const double* mu_e = A.mu + off * L + rd * LR;
-            const double* gam_e = A.gam + off * L + rd * LR;
-            const double* kap_e = A.kap + off * L + rd * LR;
             const int lr_here = (L - rd * LR) < LR ? (L - rd * LR) : LR;
             const int lo = warp * (NLW * LL) + ll;  // local node index of chain 0 in the staged block
+            const int nblk = (m + IB - 1) / IB;
 
-            for (int t0 = 0; t0 < m; t0 += IB) {
+            // asynchronous staging of block b into buffer b&1 (division-free index math)
+            auto stage = [&](int b) {
+                const int t0 = b * IB;
                 const int nb = (m - t0) < IB ? (m - t0) : IB;
-                // stage coefficients for steps [t0, t0+nb) of this round's nodes (zero past L:
-                // such chains then contribute nothing)
-                __syncthreads();
-                for (int x = tid; x < nb * LR; x += blockDim.x) {
-                    const int tt = x / LR, lc = x - tt * LR;
-                    const bool ok = lc < lr_here;
-                    const int64_t src = (int64_t)(t0 + tt) * L + lc;
-                    coef[(0 * IB + tt) * LR + lc] = ok ? __ldg(mu_e + src) : 0.0;
-                    if (REC) {
-                        coef[(1 * IB + tt) * LR + lc] = ok ? __ldg(gam_e + src) : 0.0;
-                        coef[(2 * IB + tt) * LR + lc] = ok ? __ldg(kap_e + src) : 0.0;
+                double* cb = coef + (b & 1) * NT * IB * LR;
+                const int64_t row0 = (off + t0) * (int64_t)L + rd * LR;
+                for (int lc = tid; lc < LR; lc += blockDim.x) {
+                    const bool okl = lc < lr_here;
+#pragma unroll
+                    for (int tt = 0; tt < IB; ++tt) {
+                        const bool ok = okl && tt < nb;
+                        const int64_t src = row0 + (int64_t)tt * L + lc;
+#pragma unroll
+                        for (int tb = 0; tb < NT; ++tb) {
+                            double* dst = cb + (tb * IB + tt) * LR + lc;
+                            const double* tab = tb == 0 ? A.mu : (tb == 1 ? A.gam : A.kap);
+                            if (ok)
+                                cp8(dst, tab + src);
+                            else
+                                *dst = 0.0;  // nodes past L (and steps past m) contribute nothing
+                        }
                     }
                 }
+                double* wb = wbuf + (b & 1) * 2 * IB * SP;
+                for (int x = tid; x < 2 * IB * SL; x += blockDim.x) {
+                    const int side = x / (IB * SL), r = x % (IB * SL);
+                    const int j = r / IB, tt = r % IB;
+                    if (tt < nb) {
+                        const int pos = side ? (m - 1 - t0 - tt) : (t0 + tt);
+                        double* dst = wb + (side * IB + tt) * SP + j;
+                        if (j < ns)
+                            cp8(dst, Wtile + (int64_t)j * N + pos);
+                        else
+                            *dst = 0.0;
+                    }
+                }
+                __pipeline_commit();
+            };
+
+            stage(0);
+            for (int b = 0; b < nblk; ++b) {
+                const int t0 = b * IB;
+                const int nb = (m - t0) < IB ? (m - t0) : IB;
+                if (b + 1 < nblk) {
+                    stage(b + 1);
+                    __pipeline_wait_prior(1);
+                } else {
+                    __pipeline_wait_prior(0);
+                }
                 __syncthreads();
+                const double* cb = coef + (b & 1) * NT * IB * LR;
+                const double* wb = wbuf + (b & 1) * 2 * IB * SP;
                 for (int tt = 0; tt < nb; ++tt) {
                     const int t = t0 + tt;
-                    const double wl = __ldg(Wrow + t);
-                    const double wr = __ldg(Wrow + (m - 1 - t));
-                    const double* cmu = coef + (0 * IB + tt) * LR + lo;
-                    double accL = 0.0, accR = 0.0;
+                    const double wl = wb[tt * SP + sl];
+                    const double wr = wb[(IB + tt) * SP + sl];
+                    const double* cmu = cb + tt * LR + lo;
                     if (REC) {
-                        const double* cg = coef + (1 * IB + tt) * LR + lo;
-                        const double* ck = coef + (2 * IB + tt) * LR + lo;
+                        const double* cg = cb + (IB + tt) * LR + lo;
+                        const double* ck = cb + (2 * IB + tt) * LR + lo;
+                        double aL0 = 0.0, aL1 = 0.0, aR0 = 0.0, aR1 = 0.0;
                         const bool first = (t == 0), last = (t == m - 1);
                         if (first || last) {
                             // boundary rows: f_1 += (c_L/h) u_left, f_m += (c_L/h) u_right  (P310)
@@ -192,24 +242,28 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
                                     fr += ul;
                                 }
                                 const double c_mu = cmu[k * LL], c_g = cg[k * LL], c_k = ck[k * LL];
-                                accL += c_k * Y[k];
+                                aL0 += c_k * Y[k];
                                 Y[k] = fl - c_mu * Y[k];
                                 Z[k] = fr - c_mu * Z[k];
-                                accR += c_g * Z[k];
+                                aR0 += c_g * Z[k];
                             }
                         } else {
 #pragma unroll
-                            for (int k = 0; k < NLW; ++k) {
-                                const double c_mu = cmu[k * LL], c_g = cg[k * LL], c_k = ck[k * LL];
-                                accL += c_k * Y[k];     // left sweep: kap_t Y_{t-1} -> position t
-                                Y[k] = wl - c_mu * Y[k];
-                                Z[k] = wr - c_mu * Z[k];
-                                accR += c_g * Z[k];     // right sweep: g_t Z -> position m-1-t
+                            for (int k = 0; k < NLW; k += 2) {
+                                const double m0 = cmu[k * LL], g0 = cg[k * LL], k0 = ck[k * LL];
+                                const double m1 = cmu[(k + 1) * LL], g1 = cg[(k + 1) * LL], k1 = ck[(k + 1) * LL];
+                                aL0 += k0 * Y[k];  // left sweep: kap_t Y_{t-1} -> position t
+                                aL1 += k1 * Y[k + 1];
+                                Y[k] = wl - m0 * Y[k];
+                                Y[k + 1] = wl - m1 * Y[k + 1];
+                                Z[k] = wr - m0 * Z[k];
+                                Z[k + 1] = wr - m1 * Z[k + 1];
+                                aR0 += g0 * Z[k];  // right sweep: g_t Z -> position m-1-t
+                                aR1 += g1 * Z[k + 1];
                             }
                         }
-                        const int pidx = warp * LL + ll;
-                        part[((tt)*P + pidx) * (SL + 1) + sl] = accL;
-                        part[((IB + tt) * P + pidx) * (SL + 1) + sl] = accR;
+                        part[(tt * P + pidx) * SP + sl] = aL0 + aL1;
+                        part[((IB + tt) * P + pidx) * SP + sl] = aR0 + aR1;
                     } else {
 #pragma unroll
                         for (int k = 0; k < NLW; ++k) {
@@ -220,37 +274,30 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
                     }
                 }
                 if (REC) {
-                    __syncthreads();
-                    // Each position i is visited by the left sweep at step i and by the right sweep at
-                    // step m-1-i; visits are processed per IB block, left rows before right rows, so
+                    // Position i is visited by the left sweep at step i and by the right sweep at
+                    // step m-1-i; per block the left rows are folded in before the right rows, so
                     // the first visit is the smaller (block, phase) pair.
-                    // left-sweep rows: positions t0..t0+nb-1
-                    for (int o = tid; o < nb * SL; o += blockDim.x) {
-                        const int tt = o / SL, j = o % SL;
-                        double acc = 0.0;
-                        for (int p = 0; p < P; ++p) acc += part[(tt * P + p) * (SL + 1) + j];
-                        const int64_t so = s0 + j;
-                        if (so < A.S) {
-                            const int i = t0 + tt;
-                            double* dst = A.out + so * N + off + i;
-                            const bool first = (rd == 0) && (i / IB <= (m - 1 - i) / IB);
-                            *dst = first ? acc : *dst + acc;
+                    for (int side = 0; side < 2; ++side) {
+                        __syncthreads();
+                        for (int o = tid; o < IB * SL; o += blockDim.x) {
+                            const int j = o / IB, tt = o % IB;
+                            if (tt >= nb) continue;
+                            double acc = 0.0;
+                            for (int p = 0; p < P; ++p) acc += part[((side * IB + tt) * P + p) * SP + j];
+                            const int i = side ? (m - 1 - (t0 + tt)) : (t0 + tt);
+                            const int bi = i / IB, bm = (m - 1 - i) / IB;
+                            const bool first = (rd == 0) && (side ? (bm < bi) : (bi <= bm));
+                            if (in_smem) {
+                                double* dst = otile + i * SP + j;
+                                *dst = first ? acc : *dst + acc;
+                            } else if (s0 + j < A.S) {
+                                double* dst = A.out + (s0 + j) * N + off + i;
+                                *dst = first ? acc : *dst + acc;
+                            }
                         }
                     }
-                    __syncthreads();
-                    // right-sweep rows: positions m-1-t
-                    for (int o = tid; o < nb * SL; o += blockDim.x) {
-                        const int tt = o / SL, j = o % SL;
-                        double acc = 0.0;
-                        for (int p = 0; p < P; ++p) acc += part[((IB + tt) * P + p) * (SL + 1) + j];
-                        const int64_t so = s0 + j;
-                        if (so < A.S) {
-                            const int i = m - 1 - (t0 + tt);
-                            double* dst = A.out + so * N + off + i;
-                            const bool first = (rd == 0) && ((m - 1 - i) / IB < i / IB);
-                            *dst = first ? acc : *dst + acc;
-                        }
-                    }
+                } else {
+                    __syncthreads();  // buffer b&1 is restaged two blocks later
                 }
             }
             if (!REC) {
@@ -267,18 +314,33 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
                 }
             }
         }
+        if (in_smem && m > 0) {
+            __syncthreads();
+            for (int o = tid; o < m * ns; o += blockDim.x) {
+                const int j = o / m, i = o - j * m;
+                A.out[(s0 + j) * N + off + i] = otile[i * SP + j];
+            }
+        }
     }
 }
 
 template <int NLW, int SL, bool REC>
 cudaError_t launch_sweep(SweepArgs a, cudaStream_t st) {
     constexpr int LL = Lanes<SL>::LL;
+    constexpr int NT = REC ? 3 : 1;
     int nw = (a.L + NLW * LL - 1) / (NLW * LL);
     if (nw > MAXW) nw = MAXW;
     a.nwarps = nw;
     const int LR = nw * NLW * LL;
     const int P = nw * LL;
-    const size_t smem = sizeof(double) * ((size_t)3 * IB * LR + (size_t)2 * IB * P * (SL + 1));
+    size_t base = (size_t)2 * NT * IB * LR + (size_t)4 * IB * (SL + 1);
+    if (REC) base += (size_t)2 * IB * P * (SL + 1);
+    a.mtile = REC ? (int)(OTILE_BYTES / (sizeof(double) * (SL + 1))) : 0;
+    size_t smem = sizeof(double) * (base + (REC ? (size_t)a.mtile * (SL + 1) : 0));
+    if (REC && smem > 220 * 1024) {  // no room for the smem output tile
+        a.mtile = 0;
+        smem = sizeof(double) * base;
+    }
     cudaError_t e = cudaFuncSetAttribute(sweep_kernel<NLW, SL, REC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
@@ -321,13 +383,13 @@ WorkQueue make_work_queue(const DevGraph& g, int64_t n_samples, int32_t* counter
 
 cudaError_t launch_condense(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W, double* ends,
                             WorkQueue wq, cudaStream_t st) {
-    SweepArgs a{g, p.L, p.cL, p.mu, p.gam, p.kap, n_samples, W, ends, nullptr, wq, 0};
+    SweepArgs a{g, p.L, p.cL, p.mu, p.gam, p.kap, n_samples, W, ends, nullptr, wq, 0, 0};
     return dispatch<false>(a, st);
 }
 
 cudaError_t launch_recover(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W, double* u,
                            const double* uG, WorkQueue wq, cudaStream_t st) {
-    SweepArgs a{g, p.L, p.cL, p.mu, p.gam, p.kap, n_samples, W, u, uG, wq, 0};
+    SweepArgs a{g, p.L, p.cL, p.mu, p.gam, p.kap, n_samples, W, u, uG, wq, 0, 0};
     return dispatch<true>(a, st);
 }
 
