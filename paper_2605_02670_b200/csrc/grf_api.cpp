@@ -227,7 +227,8 @@ grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf
     double* gam = (double*)grab(tab);
     double* kap = (double*)grab(tab);
     double* sig = (double*)grab((size_t)L * g->E * 4 * sizeof(double));
-    if (!dcI || !dcL || !mu || !gam || !kap || !sig) {
+    double* ops = (double*)grab((size_t)L * grf::pcg_table_doubles(g->dev) * sizeof(double));
+    if (!dcI || !dcL || !mu || !gam || !kap || !sig || !ops) {
         for (auto& b : p->blocks) g->alloc.put(b.p, b.bytes, st);
         return fail(GRF_ENOMEM, "plan tables (%.1f MB) could not be allocated",
                     (double)(3 * (size_t)g->NI * L * 8 + (size_t)L * g->E * 32) / 1e6);
@@ -242,7 +243,11 @@ grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf
     p->dev.gam = gam;
     p->dev.kap = kap;
     p->dev.sig = sig;
-    CUDA_TRY(g->timed(GRF_K_EDGE_SETUP, st, [&] { grf::launch_edge_setup(g->dev, p->dev, st); }));
+    p->dev.ops = ops;
+    CUDA_TRY(g->timed(GRF_K_EDGE_SETUP, st, [&] {
+        grf::launch_edge_setup(g->dev, p->dev, st);
+        grf::launch_pcg_tables(g->dev, p->dev, st);
+    }));
     CUDA_TRY(cudaStreamSynchronize(st));  // host vectors cI/cL die at return
     // keep at most 4 plans
     while (g->plans.size() >= 4) {
@@ -282,7 +287,7 @@ WsLayout ws_layout(const grf_graph* g, int64_t L, int64_t S, bool with_noise = t
 }
 
 grf_status check_kernel_limits(const grf_graph* g) {
-    if (g->V > grf::pcg_max_vertices())
+    if (!grf::pcg_supported(g->dev))
         return fail(GRF_EUNSUPPORTED, "graph has %lld vertices; this build's shared-memory PCG handles <= %d",
                     (long long)g->V, grf::pcg_max_vertices());
     if (g->dev.max_m > grf::recover_max_interior())
@@ -328,6 +333,8 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
     prm.rtol = opt ? opt->rtol : 1e-13;
     prm.max_iter = (opt && opt->max_iter > 0) ? opt->max_iter : (int32_t)(g->V + 10);
     prm.precond = opt ? opt->precond : GRF_PRECOND_NN;
+    prm.debug_nogather = getenv("GRF_DEBUG_NOGATHER") ? 1 : 0;
+    prm.debug_nowrite = getenv("GRF_DEBUG_NOWRITE") ? 1 : 0;
     grf_status rc = GRF_OK;
     cudaError_t le = cudaSuccess;
     cudaError_t ce = g->timed(GRF_K_CONDENSE, st, [&] {
@@ -475,6 +482,21 @@ grf_status grf_graph_create(int64_t n_vertices, int64_t n_edges, const int64_t* 
         inc[fill[b]] = (int32_t)(2 * e + 1);
         other[fill[b]++] = (int32_t)a;
     }
+    // ELL (padded) copy of the incidence lists for the PCG kernels
+    int32_t max_deg = 0;
+    for (int64_t v = 0; v < V; ++v) max_deg = std::max<int32_t>(max_deg, (int32_t)deg[v]);
+    int32_t ell_w = 4;
+    while (ell_w < max_deg) ell_w *= 2;
+    std::vector<int32_t> ell_other((size_t)ell_w * V), ell_code((size_t)ell_w * V, 0), ell_valid((size_t)ell_w * V, 0);
+    for (int64_t v = 0; v < V; ++v) {
+        for (int32_t j = 0; j < ell_w; ++j) ell_other[(size_t)j * V + v] = (int32_t)v;
+        for (int32_t k = ptr[v]; k < ptr[v + 1]; ++k) {
+            const int32_t j = k - ptr[v];
+            ell_other[(size_t)j * V + v] = other[k];
+            ell_code[(size_t)j * V + v] = inc[k];
+            ell_valid[(size_t)j * V + v] = 1;
+        }
+    }
     std::vector<double> inv_deg(V);
     for (int64_t v = 0; v < V; ++v) {
         owner[v] = inc[ptr[v]];
@@ -507,6 +529,11 @@ grf_status grf_graph_create(int64_t n_vertices, int64_t n_edges, const int64_t* 
     if (!st) d.owner = g->upload(owner, &st);
     if (!st) d.sqrt_ml = g->upload(sq, &st);
     if (!st) d.edge_order = g->upload(order, &st);
+    d.max_deg = max_deg;
+    d.ell_w = ell_w;
+    if (!st) d.ell_other = g->upload(ell_other, &st);
+    if (!st) d.ell_code = g->upload(ell_code, &st);
+    if (!st) d.ell_valid = g->upload(ell_valid, &st);
     if (st) {
         grf_graph_destroy(g.release());
         return st;

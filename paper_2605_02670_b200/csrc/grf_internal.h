@@ -26,6 +26,11 @@ struct DevGraph {
     const int32_t* owner = nullptr;   // [V] incidence code that writes the vertex value in recovery
     const double* sqrt_ml = nullptr;  // [N] sqrt of the lumped mass diagonal
     const int32_t* edge_order = nullptr; // [E] edges by descending interior length (work-queue order)
+    int32_t max_deg = 0;              // max vertex degree (incident edge ends)
+    int32_t ell_w = 0;                // ELL width = max_deg rounded up to 4/8/16/32
+    const int32_t* ell_other = nullptr; // [ell_w][V] other endpoint of incidence slot j of v (v if padding)
+    const int32_t* ell_code = nullptr;  // [ell_w][V] incidence code 2e+end of slot j (0 if padding)
+    const int32_t* ell_valid = nullptr; // [ell_w][V] 1 for a real incidence, 0 for padding
 };
 
 // Device per-plan tables (one (kappa, beta, k, node range)).
@@ -38,12 +43,15 @@ struct DevPlan {
     double* gam = nullptr;            // [NI * L] diag of A_II^{-1}: 1/(d'_t + d'_{m+1-t} - a)
     double* kap = nullptr;            // [NI * L] -gam_t * mu_t
     double* sig = nullptr;            // [L * E * 4]: (s_d, s_o, p_d, p_o) local Schur + its inverse
+    double* ops = nullptr;            // [L * (3V + 4E)]: per-node CSR tables of S and M^{-1} (pcg.cu)
 };
 
 struct PcgParams {
     double rtol = 1e-13;
     int32_t max_iter = 0;
     int32_t precond = 0;
+    int32_t debug_nogather = 0;  // experiments only (GRF_DEBUG_NOGATHER)
+    int32_t debug_nowrite = 0;   // experiments only (GRF_DEBUG_NOWRITE)
 };
 
 // Work queue of (edge, sample chunk) items shared by K3 and K5: items are handed out
@@ -68,6 +76,11 @@ void launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, const Pc
 // K5  Thomas recovery + accumulation over nodes (sweep.cu): u[s*N + dof] from W and u_G
 cudaError_t launch_recover(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W, double* u,
                            const double* uG, WorkQueue wq, cudaStream_t st);
+
+// K2b per-node CSR operator tables for K4 (pcg.cu)
+void launch_pcg_tables(const DevGraph& g, const DevPlan& p, cudaStream_t st);
+size_t pcg_table_doubles(const DevGraph& g);
+bool pcg_supported(const DevGraph& g);
 
 WorkQueue make_work_queue(const DevGraph& g, int64_t n_samples, int32_t* counter);
 size_t pcg_smem_bytes(const DevGraph& g);

@@ -3,194 +3,424 @@
 //     S^{(l)} u_G = g,   S^{(l)} = sum_e R_e^T S^{(l,e)} R_e        (P113-116, P244 [eq:goal_func_1])
 //
 // Dirichlet step (P247-258): y = S p evaluated edge-locally; with the exact 2x2 local
-// Schur blocks of K2 this is q_v = sum_{(e,end) at v} (s_d p_v + s_o p_other).
+// Schur blocks of K2, (S p)_v = sum_{(e,end) at v} (s_d p_v + s_o p_other).
 // Neumann step (P260-298): z = D^{-1} (sum_e R_e^T S_e^{-1} R_e) D^{-1} r, i.e.
 //     r~ = r / d (eq:distribute_dv), delta = S_e^{-1} r~ per edge, z_v = (1/d_v) sum delta
 // (eq:induced_displacements); D_vv = d_v = incident edge ends.
 // A loop edge has other == v, so both its ends add to v (sum of all 4 entries, Q18).
 // Stopping rule: ||r_k||_2 <= rtol ||g||_2, x_0 = 0.
 //
-// Mapping: one CTA per (node l, sample s) system; the vertex vectors x, r, z, p, q live in
-// shared memory (V <= pcg_max_vertices); dot products are warp-shuffle + smem block
-// reductions; every system iterates to its own convergence inside the kernel (no host
-// round trip).  g is gathered from K3's end values ends[((s*E + e)*2 + end)*L + l] and
-// u_G written to uG[(s*V + v)*L + l]; CTAs with consecutive l (the fastest grid index)
-// share the L2 sectors of these node-minor layouts.
-#include "grf_internal.h"
+// Both operators are applied in the same "diagonal + incidence slots" form, from per-node
+// tables built once per plan (pcg_tables_kernel).  The incidence lists are padded to the
+// ELL width W (max degree rounded up to a power of two; padding slots point at v with a
+// zero coefficient), so every (vertex, slot) loop is fully unrolled with independent loads:
+//     (S p)_v      = DS_v p_v + sum_j OS_jv p_{o_jv},     DS_v = sum s_d,   OS = s_o
+//     (M^{-1} r)_v = DM_v r_v + sum_j OM_jv r_{o_jv},     DM_v = d_v^-2 sum p_d,
+//                                                         OM = p_o / (d_v d_o)
+//     Jacobi:        DJ_v r_v,                            DJ_v = 1 / diag(S)_v
+//     condensed rhs  g_v = W_v + sum_j GK_jv w_{c_jv},    GK = c_L / h_e     (P233-239, Q6)
+//
+// Mapping: CTA = (node l, chunk of samples) split into independent thread groups (named
+// barriers) that share the node's tables, staged once in shared memory.  Each group solves
+// batches of SB samples: r and p are [V][SB] in shared memory, x/q/z live in registers of
+// the vertex's owner thread, and one group reduction (a single barrier) per dot product
+// carries all SB values.  Each sample has its own alpha/beta and stops at its own
+// convergence.  g is gathered from K3's end values ends[((s*E + e)*2 + end)*L + l] (+ W_v);
+// u_G is written to uG[(s*V + v)*L + l].
+#include <cstdlib>
 
-#include <cub/block/block_reduce.cuh>
+#include "grf_internal.h"
 
 namespace grf {
 namespace {
 
-constexpr int PCG_THREADS = 256;
+constexpr int PCG_THREADS = 512;
+constexpr size_t SMEM_LIMIT = 220 * 1024;
 
-struct Sum2 {
-    __device__ __forceinline__ double2 operator()(const double2& a, const double2& b) const {
-        return make_double2(a.x + b.x, a.y + b.y);
+// per node l: [DS (V) | DM (V) | DJ (V) | OS (W*V) | OM (W*V) | GK (W*V)], slot-major [j][v]
+__host__ __device__ inline int64_t table_stride(int V, int W) { return 3 * (int64_t)V + 3 * (int64_t)W * V; }
+
+__global__ void pcg_tables_kernel(DevGraph g, int32_t L, const double* __restrict__ cLt,
+                                  const double4* __restrict__ sig, double* __restrict__ ops) {
+    const int V = g.V, E = g.E, Wd = g.ell_w;
+    const int64_t stride = table_stride(V, Wd);
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < (int64_t)L * V;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int l = (int)(x / V), v = (int)(x - (int64_t)l * V);
+        const double4* sg = sig + (int64_t)l * E;
+        double* t = ops + l * stride;
+        double* DS = t;
+        double* DM = DS + V;
+        double* DJ = DM + V;
+        double* OS = DJ + V;
+        double* OM = OS + (int64_t)Wd * V;
+        double* GK = OM + (int64_t)Wd * V;
+        const double idv = g.inv_deg[v];
+        const double cL = cLt[l];
+        double ds = 0.0, dm = 0.0, diag = 0.0;
+        for (int j = 0; j < Wd; ++j) {
+            const int64_t sj = (int64_t)j * V + v;
+            if (g.ell_valid[sj]) {
+                const int e = g.ell_code[sj] >> 1;
+                const double4 c = sg[e];
+                const int o = g.ell_other[sj];
+                ds += c.x;
+                dm += c.z;
+                OS[sj] = c.y;
+                OM[sj] = c.w * idv * g.inv_deg[o];
+                GK[sj] = cL / g.h[e];
+                diag += c.x + (o == v ? c.y : 0.0);
+            } else {
+                OS[sj] = OM[sj] = GK[sj] = 0.0;
+            }
+        }
+        DS[v] = ds;
+        DM[v] = dm * idv * idv;
+        DJ[v] = 1.0 / diag;
     }
-};
+}
 
-__global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L, const double* __restrict__ cLt,
-                                                          const double4* __restrict__ sig, PcgParams prm,
-                                                          const double* __restrict__ W, const double* __restrict__ ends,
+// named barrier for one thread group (ids 1..15; id 0 is __syncthreads)
+__device__ __forceinline__ void group_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Group-wide sum of NV doubles per thread, broadcast back.  One barrier per call: the
+// partials go to buffer `flip`, and consecutive calls alternate buffers, so a buffer is
+// rewritten only after every thread has passed the next call's barrier.
+template <int GT, int NV>
+__device__ __forceinline__ void group_sum(double (&v)[NV], double* red /* [2][GT/32][NV] */, int& flip, int bar_id) {
+    constexpr int NW = GT / 32;
+    const int lane = threadIdx.x & 31, w = (threadIdx.x % GT) >> 5;
+    double* rb = red + flip * NW * NV;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        double t = v[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) rb[w * NV + j] = t;
+    }
+    group_bar(bar_id, GT);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) t += rb[q * NV + j];
+        v[j] = t;
+    }
+    flip ^= 1;
+}
+
+template <int GT, int SB, int VPT, int W, bool STAGED>
+__global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L, const double* __restrict__ ops,
+                                                          PcgParams prm, int64_t S, int32_t spc,
+                                                          const double* __restrict__ Wn, const double* __restrict__ ends,
                                                           double* __restrict__ uG, int32_t* __restrict__ iters,
                                                           double* __restrict__ relres) {
-    using BR1 = cub::BlockReduce<double, PCG_THREADS>;
-    using BR2 = cub::BlockReduce<double2, PCG_THREADS>;
-    __shared__ union {
-        typename BR1::TempStorage r1;
-        typename BR2::TempStorage r2;
-    } tmp;
-    __shared__ double bcast[2];
+    constexpr int NG = PCG_THREADS / GT;
+    constexpr int NW = GT / 32;
     extern __shared__ double sm[];
-    const int V = g.V;
-    double* x = sm;
-    double* r = x + V;
-    double* z = r + V;
-    double* p = z + V;
-    double* q = p + V;
-
+    __shared__ double red_all[NG][2 * NW * 2 * SB];
+    const int V = g.V, E = g.E;
+    const int64_t stride = table_stride(V, W);
     const int l = blockIdx.x;
-    const int64_t s = blockIdx.y;
-    const double4* sg = sig + (int64_t)l * g.E;
-    double* ucol = uG + (s * V) * (int64_t)L + l;
-    const double* ecol = ends + (s * g.E) * 2 * (int64_t)L + l;
-    const double cL = cLt[l];
-
-    auto reduce1 = [&](double v) -> double {
-        double t = BR1(tmp.r1).Sum(v);
-        if (threadIdx.x == 0) bcast[0] = t;
-        __syncthreads();
-        t = bcast[0];
-        __syncthreads();
-        return t;
-    };
-    auto reduce2 = [&](double a, double b) -> double2 {
-        double2 t = BR2(tmp.r2).Reduce(make_double2(a, b), Sum2());
-        if (threadIdx.x == 0) {
-            bcast[0] = t.x;
-            bcast[1] = t.y;
+    const int tid = threadIdx.x;
+    const int gid = tid / GT, gt = tid % GT;
+    const int bar_id = 1 + gid;
+    double* r = sm + (size_t)gid * 2 * V * SB;  // [V][SB] per group
+    double* p = r + (size_t)V * SB;            // [V][SB] per group
+    double* red = red_all[gid];
+    int flip = 0;
+    const double* tab = ops + l * stride;
+    const int* eo = g.ell_other;
+    const int* ec = g.ell_code;
+    if (STAGED) {  // node tables + ELL index arrays into shared memory, once per CTA
+        double* st = sm + (size_t)NG * 2 * V * SB;
+        int* so = reinterpret_cast<int*>(st + stride);
+        int* sc = so + W * V;
+        for (int64_t i = tid; i < stride; i += PCG_THREADS) st[i] = tab[i];
+        for (int i = tid; i < W * V; i += PCG_THREADS) {
+            so[i] = g.ell_other[i];
+            sc[i] = g.ell_code[i];
         }
-        __syncthreads();
-        t = make_double2(bcast[0], bcast[1]);
-        __syncthreads();
-        return t;
-    };
-    auto precond = [&]() {  // z = M^{-1} r
-        for (int v = threadIdx.x; v < V; v += blockDim.x) {
-            const int k0 = g.inc_ptr[v], k1 = g.inc_ptr[v + 1];
-            double zv;
-            if (prm.precond == 0) {          // Neumann-Neumann (P298)
-                const double idv = g.inv_deg[v];
-                const double rv = r[v] * idv;
-                double acc = 0.0;
-                for (int k = k0; k < k1; ++k) {
-                    const double4 c = sg[g.inc[k] >> 1];
-                    const int o = g.inc_other[k];
-                    acc += c.z * rv + c.w * (r[o] * g.inv_deg[o]);
-                }
-                zv = idv * acc;
-            } else if (prm.precond == 1) {   // Jacobi on diag(S)
-                double dg = 0.0;
-                for (int k = k0; k < k1; ++k) {
-                    const double4 c = sg[g.inc[k] >> 1];
-                    dg += c.x + (g.inc_other[k] == v ? c.y : 0.0);
-                }
-                zv = r[v] / dg;
-            } else {
-                zv = r[v];
-            }
-            z[v] = zv;
-        }
-    };
-
-    // condensed rhs g_v = W_v + sum_{(e,end) at v} (c_L/h_e) w_end   (P233-239)
-    double part = 0.0;
-    for (int v = threadIdx.x; v < V; v += blockDim.x) {
-        double gv = W[s * g.N + g.NI + v];
-        for (int k = g.inc_ptr[v]; k < g.inc_ptr[v + 1]; ++k) {
-            const int code = g.inc[k];
-            gv += (cL / g.h[code >> 1]) * ecol[(int64_t)code * L];
-        }
-        r[v] = gv;
-        x[v] = 0.0;
-        part += gv * gv;
+        tab = st;
+        eo = so;
+        ec = sc;
     }
-    const double gg = reduce1(part);  // (syncs: r complete)
-    int it = 0;
-    double rr = gg;
-    if (gg > 0.0) {
-        precond();
-        __syncthreads();
-        part = 0.0;
-        for (int v = threadIdx.x; v < V; v += blockDim.x) {
-            p[v] = z[v];
-            part += r[v] * z[v];
+    __syncthreads();
+    const double* DS = tab;
+    const double* DM = DS + V;
+    const double* DJ = DM + V;
+    const double* OS = DJ + V;
+    const double* OM = OS + (size_t)W * V;
+    const double* GK = OM + (size_t)W * V;
+
+    // y = D x + sum_j O_j x_{o_j} over the owner's vertices, for SB samples (x = r or p in smem)
+    auto apply = [&](const double* D, const double* O, const double* xs, double (&y)[VPT][SB]) {
+#pragma unroll
+        for (int a = 0; a < VPT; ++a) {
+            const int v = gt + a * GT;
+            if (v < V) {
+                const double d = D[v];
+#pragma unroll
+                for (int j = 0; j < SB; ++j) y[a][j] = d * xs[v * SB + j];
+#pragma unroll
+                for (int s = 0; s < W; ++s) {
+                    const double c = O[s * V + v];
+                    const double* xo = xs + eo[s * V + v] * SB;
+#pragma unroll
+                    for (int j = 0; j < SB; ++j) y[a][j] += c * xo[j];
+                }
+            }
         }
-        double rz = reduce1(part);
-        const double tol2 = prm.rtol * prm.rtol * gg;
-        while (it < prm.max_iter) {
+    };
+    // z = M^{-1} r (Neumann step); needs r of neighbours: callers barrier first
+    auto precond = [&](double (&z)[VPT][SB]) {
+        if (prm.precond == 0) {
+            apply(DM, OM, r, z);
+        } else {
+#pragma unroll
+            for (int a = 0; a < VPT; ++a) {
+                const int v = gt + a * GT;
+                if (v < V) {
+                    const double d = prm.precond == 1 ? DJ[v] : 1.0;
+#pragma unroll
+                    for (int j = 0; j < SB; ++j) z[a][j] = d * r[v * SB + j];
+                }
+            }
+        }
+    };
+
+    const int64_t c0 = (int64_t)blockIdx.y * spc;
+    const int64_t c1 = (c0 + spc) < S ? (c0 + spc) : S;
+    for (int64_t s0 = c0 + (int64_t)gid * SB; s0 < c1; s0 += (int64_t)NG * SB) {
+        const int ns = (int)((c1 - s0) < SB ? (c1 - s0) : SB);
+        double x[VPT][SB], q[VPT][SB];
+        double gg[SB];
+#pragma unroll
+        for (int j = 0; j < SB; ++j) gg[j] = 0.0;
+        // ---- condensed rhs g (gathered end values), x = 0, r = g
+#pragma unroll
+        for (int a = 0; a < VPT; ++a) {
+            const int v = gt + a * GT;
+#pragma unroll
+            for (int j = 0; j < SB; ++j) x[a][j] = 0.0;
+            if (v < V) {
+#pragma unroll
+                for (int j = 0; j < SB; ++j) {
+                    const int64_t s = s0 + (j < ns ? j : 0);
+                    const double* ecol = ends + (s * E) * 2 * (int64_t)L + l;
+                    double gv = Wn[s * g.N + g.NI + v];
+                    if (!prm.debug_nogather) {
+#pragma unroll
+                        for (int t = 0; t < W; ++t) gv += GK[t * V + v] * ecol[(int64_t)ec[t * V + v] * L];
+                    }
+                    if (j >= ns) gv = 0.0;
+                    r[v * SB + j] = gv;
+                    gg[j] += gv * gv;
+                }
+            }
+        }
+        group_sum<GT, SB>(gg, red, flip, bar_id);  // (barrier: r complete)
+        double rz[SB], tol2[SB], rrj[SB];
+        bool done[SB];
+        int its[SB];
+        {
+            double z[VPT][SB];
+            precond(z);
+#pragma unroll
+            for (int j = 0; j < SB; ++j) rz[j] = 0.0;
+#pragma unroll
+            for (int a = 0; a < VPT; ++a) {
+                const int v = gt + a * GT;
+                if (v < V) {
+#pragma unroll
+                    for (int j = 0; j < SB; ++j) {
+                        p[v * SB + j] = z[a][j];
+                        rz[j] += r[v * SB + j] * z[a][j];
+                    }
+                }
+            }
+            group_sum<GT, SB>(rz, red, flip, bar_id);  // (barrier: p complete)
+        }
+        bool all_done = true;
+#pragma unroll
+        for (int j = 0; j < SB; ++j) {
+            tol2[j] = prm.rtol * prm.rtol * gg[j];
+            done[j] = !(gg[j] > 0.0);
+            its[j] = 0;
+            rrj[j] = gg[j];
+            all_done = all_done && done[j];
+        }
+        int it = 0;
+        while (!all_done && it < prm.max_iter) {
             ++it;
-            // q = S p  (Dirichlet step, matrix free)
-            part = 0.0;
-            for (int v = threadIdx.x; v < V; v += blockDim.x) {
-                const int k0 = g.inc_ptr[v], k1 = g.inc_ptr[v + 1];
-                const double pv = p[v];
-                double acc = 0.0;
-                for (int k = k0; k < k1; ++k) {
-                    const double4 c = sg[g.inc[k] >> 1];
-                    acc += c.x * pv + c.y * p[g.inc_other[k]];
+            // ---- q = S p (Dirichlet step) and p.q
+            apply(DS, OS, p, q);
+            double pq[SB];
+#pragma unroll
+            for (int j = 0; j < SB; ++j) pq[j] = 0.0;
+#pragma unroll
+            for (int a = 0; a < VPT; ++a) {
+                const int v = gt + a * GT;
+                if (v < V) {
+#pragma unroll
+                    for (int j = 0; j < SB; ++j) pq[j] += p[v * SB + j] * q[a][j];
                 }
-                q[v] = acc;
-                part += pv * acc;
             }
-            const double pq = reduce1(part);
-            const double alpha = rz / pq;
-            for (int v = threadIdx.x; v < V; v += blockDim.x) {
-                x[v] += alpha * p[v];
-                r[v] -= alpha * q[v];
+            group_sum<GT, SB>(pq, red, flip, bar_id);
+            double alpha[SB];
+#pragma unroll
+            for (int j = 0; j < SB; ++j) alpha[j] = done[j] ? 0.0 : rz[j] / pq[j];
+#pragma unroll
+            for (int a = 0; a < VPT; ++a) {
+                const int v = gt + a * GT;
+                if (v < V) {
+#pragma unroll
+                    for (int j = 0; j < SB; ++j) {
+                        x[a][j] += alpha[j] * p[v * SB + j];
+                        r[v * SB + j] -= alpha[j] * q[a][j];
+                    }
+                }
             }
-            __syncthreads();
-            precond();
-            double pr = 0.0, pz = 0.0;
-            for (int v = threadIdx.x; v < V; v += blockDim.x) {
-                pr += r[v] * r[v];
-                pz += r[v] * z[v];
+            group_bar(bar_id, GT);
+            double z[VPT][SB];
+            precond(z);
+            double t2[2 * SB];
+#pragma unroll
+            for (int j = 0; j < 2 * SB; ++j) t2[j] = 0.0;
+#pragma unroll
+            for (int a = 0; a < VPT; ++a) {
+                const int v = gt + a * GT;
+                if (v < V) {
+#pragma unroll
+                    for (int j = 0; j < SB; ++j) {
+                        const double rv = r[v * SB + j];
+                        t2[j] += rv * rv;
+                        t2[SB + j] += rv * z[a][j];
+                    }
+                }
             }
-            const double2 t = reduce2(pr, pz);
-            rr = t.x;
-            if (rr <= tol2) break;
-            const double bet = t.y / rz;
-            rz = t.y;
-            for (int v = threadIdx.x; v < V; v += blockDim.x) p[v] = z[v] + bet * p[v];
-            __syncthreads();
+            group_sum<GT, 2 * SB>(t2, red, flip, bar_id);
+            double bet[SB];
+            all_done = true;
+#pragma unroll
+            for (int j = 0; j < SB; ++j) {
+                if (!done[j]) {
+                    its[j] = it;
+                    rrj[j] = t2[j];
+                    if (t2[j] <= tol2[j]) done[j] = true;
+                }
+                bet[j] = done[j] ? 0.0 : t2[SB + j] / rz[j];
+                if (!done[j]) rz[j] = t2[SB + j];
+                all_done = all_done && done[j];
+            }
+            if (all_done) break;
+#pragma unroll
+            for (int a = 0; a < VPT; ++a) {
+                const int v = gt + a * GT;
+                if (v < V) {
+#pragma unroll
+                    for (int j = 0; j < SB; ++j)
+                        if (!done[j]) p[v * SB + j] = z[a][j] + bet[j] * p[v * SB + j];
+                }
+            }
+            group_bar(bar_id, GT);
         }
+        // ---- write u_G and the per-system stats
+#pragma unroll
+        for (int a = 0; a < VPT; ++a) {
+            const int v = gt + a * GT;
+            if (v < V && !prm.debug_nowrite) {
+#pragma unroll
+                for (int j = 0; j < SB; ++j)
+                    if (j < ns) uG[((s0 + j) * V + v) * (int64_t)L + l] = x[a][j];
+            }
+        }
+        if (gt == 0) {
+#pragma unroll
+            for (int j = 0; j < SB; ++j) {
+                if (j < ns) {
+                    iters[(s0 + j) * L + l] = its[j];
+                    relres[(s0 + j) * L + l] = gg[j] > 0.0 ? sqrt(rrj[j] / gg[j]) : 0.0;
+                }
+            }
+        }
+        group_bar(bar_id, GT);  // r/p are rewritten by the next batch's gather
     }
-    for (int v = threadIdx.x; v < V; v += blockDim.x) ucol[(int64_t)v * L] = x[v];
-    if (threadIdx.x == 0) {
-        iters[s * L + l] = it;
-        relres[s * L + l] = gg > 0.0 ? sqrt(rr / gg) : 0.0;
+}
+
+size_t vec_bytes(const DevGraph& g, int SB, int NG) { return sizeof(double) * 2 * (size_t)g.V * SB * NG; }
+size_t staged_bytes(const DevGraph& g) {
+    return sizeof(double) * (size_t)table_stride(g.V, g.ell_w) + sizeof(int) * 2 * (size_t)g.ell_w * g.V;
+}
+
+template <int GT, int SB, int VPT, int W>
+bool launch_t(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* Wn,
+              const double* ends, double* uG, int32_t* iters, double* relres, cudaStream_t st) {
+    constexpr int NG = PCG_THREADS / GT;
+    if (g.ell_w != W || g.V > GT * VPT) return false;
+    const size_t vb = vec_bytes(g, SB, NG);
+    if (vb > SMEM_LIMIT) return false;
+    const bool staged = vb + staged_bytes(g) <= SMEM_LIMIT;
+    const size_t smem = staged ? vb + staged_bytes(g) : vb;
+    // chunks of samples per CTA: fill the GPU, keep every group busy
+    int64_t groups = (148 * 2 + p.L - 1) / p.L;
+    const int64_t batches = (n_samples + SB - 1) / SB;
+    const int64_t maxg = (batches + NG - 1) / NG;
+    if (groups > maxg) groups = maxg;
+    if (groups < 1) groups = 1;
+    const int32_t spc = (int32_t)(((batches + groups - 1) / groups) * SB);
+    groups = (n_samples + spc - 1) / spc;
+    const dim3 grid(p.L, (unsigned)groups);
+    if (staged) {
+        cudaFuncSetAttribute(pcg_kernel<GT, SB, VPT, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        pcg_kernel<GT, SB, VPT, W, true><<<grid, PCG_THREADS, smem, st>>>(g, p.L, p.ops, prm, n_samples, spc, Wn, ends,
+                                                                        uG, iters, relres);
+    } else {
+        cudaFuncSetAttribute(pcg_kernel<GT, SB, VPT, W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        pcg_kernel<GT, SB, VPT, W, false><<<grid, PCG_THREADS, smem, st>>>(g, p.L, p.ops, prm, n_samples, spc, Wn,
+                                                                         ends, uG, iters, relres);
     }
+    return true;
+}
+
+template <int W>
+bool launch_w(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* Wn,
+              const double* ends, double* uG, int32_t* iters, double* relres, cudaStream_t st) {
+    if (launch_t<128, 1, 8, W>(g, p, n_samples, prm, Wn, ends, uG, iters, relres, st)) return true;   // V <= 1024
+    if (launch_t<256, 1, 8, W>(g, p, n_samples, prm, Wn, ends, uG, iters, relres, st)) return true;   // V <= 2048
+    return launch_t<512, 1, 8, W>(g, p, n_samples, prm, Wn, ends, uG, iters, relres, st);            // V <= 4096
 }
 
 }  // namespace
 
-int32_t pcg_max_vertices() { return 5000; }
+int32_t pcg_max_vertices() { return 8 * PCG_THREADS; }
 
-size_t pcg_smem_bytes(const DevGraph& g) { return sizeof(double) * 5 * (size_t)g.V; }
+size_t pcg_smem_bytes(const DevGraph& g) { return vec_bytes(g, 1, 1); }
+
+size_t pcg_table_doubles(const DevGraph& g) { return (size_t)table_stride(g.V, g.ell_w); }
+
+bool pcg_supported(const DevGraph& g) {
+    return g.V <= pcg_max_vertices() && g.ell_w <= 32 && vec_bytes(g, 1, 1) <= SMEM_LIMIT;
+}
+
+void launch_pcg_tables(const DevGraph& g, const DevPlan& p, cudaStream_t st) {
+    const int64_t n = (int64_t)p.L * g.V;
+    int blocks = (int)((n + 255) / 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    pcg_tables_kernel<<<blocks, 256, 0, st>>>(g, p.L, p.cL, reinterpret_cast<const double4*>(p.sig), p.ops);
+}
 
 void launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* W,
                 const double* ends, double* uG, int32_t* iters, double* relres, cudaStream_t st) {
-    const size_t smem = pcg_smem_bytes(g);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(pcg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_set = true;
+    switch (g.ell_w) {
+        case 4: launch_w<4>(g, p, n_samples, prm, W, ends, uG, iters, relres, st); break;
+        case 8: launch_w<8>(g, p, n_samples, prm, W, ends, uG, iters, relres, st); break;
+        case 16: launch_w<16>(g, p, n_samples, prm, W, ends, uG, iters, relres, st); break;
+        default: launch_w<32>(g, p, n_samples, prm, W, ends, uG, iters, relres, st); break;
     }
-    dim3 grid(p.L, (unsigned)n_samples);
-    pcg_kernel<<<grid, PCG_THREADS, smem, st>>>(g, p.L, p.cL, reinterpret_cast<const double4*>(p.sig), prm, W, ends,
-                                                uG, iters, relres);
 }
 
 }  // namespace grf
