@@ -28,12 +28,13 @@
 // coalesced); edges too long for the tile fall back to read-modify-write in global memory.
 #include <cuda_pipeline.h>
 
+#include <cstdlib>
+
 #include "grf_internal.h"
 
 namespace grf {
 namespace {
 
-constexpr int IB = 8;          // steps per staging / reduction block
 constexpr int MAXW = 16;       // warps per CTA
 constexpr int OTILE_BYTES = 48 * 1024;
 
@@ -65,11 +66,12 @@ __device__ __forceinline__ void cp8(double* dst, const double* src) { __pipeline
 //   wbuf [2][2][IB][SL+1]  staged W: [buffer][left/right positions][step][sample]
 //   part [2*IB][P][SL+1]   per (row, partial, sample) sums, P = nwarps*LL          (recover)
 //   otile[mtile][SL+1]     the edge's output tile                                  (recover)
-template <int NLW, int SL, bool REC>
+template <int NLW, int SL, bool REC, int IB>
 __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
     constexpr int LL = Lanes<SL>::LL;
     constexpr int NT = REC ? 3 : 1;
     constexpr int SP = SL + 1;
+    constexpr int NBUF = REC ? 2 : 3;  // staging buffers (prefetch distance NBUF-1 blocks)
     extern __shared__ double smem[];
     __shared__ int item_sh;
     const DevGraph& g = A.g;
@@ -81,8 +83,9 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
     const int L = A.L;
     const int rounds = (L + LR - 1) / LR;
     double* coef = smem;                                 // 2*NT*IB*LR
-    double* wbuf = coef + 2 * NT * IB * LR;              // 2*2*IB*SP
-    double* part = wbuf + 4 * IB * SP;                   // 2*IB*P*SP     (REC)
+    double* wbuf = coef + NBUF * NT * IB * LR;           // NBUF*2*IB*SP
+    double* part = wbuf + NBUF * 2 * IB * SP;            // 2*IB*P*SP     (REC)
+    double* g1buf = part;                                // LR             (condense: g_1 row)
     double* otile = part + (REC ? 2 * IB * P * SP : 0);  // mtile*SP      (REC)
     const int64_t N = g.N;
     const int V = g.V;
@@ -108,6 +111,7 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
         const bool in_smem = REC && (m <= A.mtile);
 
         for (int rd = 0; rd < rounds; ++rd) {
+            if (rd > 0) __syncthreads();  // staging buffers of the previous round are free
             const int lbase = rd * LR + warp * (NLW * LL) + ll;  // node of chain k: lbase + k*LL
             // ---------------- recover: vertex values owned by this edge (sum over l of u_G)
             if (REC) {
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
             auto stage = [&](int b) {
                 const int t0 = b * IB;
                 const int nb = (m - t0) < IB ? (m - t0) : IB;
-                double* cb = coef + (b & 1) * NT * IB * LR;
+                double* cb = coef + (b % NBUF) * NT * IB * LR;
                 const int64_t row0 = (off + t0) * (int64_t)L + rd * LR;
                 for (int lc = tid; lc < LR; lc += blockDim.x) {
                     const bool okl = lc < lr_here;
@@ -182,7 +186,15 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
                         }
                     }
                 }
-                double* wb = wbuf + (b & 1) * 2 * IB * SP;
+                if (!REC && b == 0) {  // g_1 (= g_m) row for the end values, staged with block 0
+                    for (int lc = tid; lc < LR; lc += blockDim.x) {
+                        if (lc < lr_here)
+                            cp8(g1buf + lc, A.gam + off * (int64_t)L + rd * LR + lc);
+                        else
+                            g1buf[lc] = 0.0;
+                    }
+                }
+                double* wb = wbuf + (b % NBUF) * 2 * IB * SP;
                 for (int x = tid; x < 2 * IB * SL; x += blockDim.x) {
                     const int side = x / (IB * SL), r = x % (IB * SL);
                     const int j = r / IB, tt = r % IB;
@@ -198,19 +210,23 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
                 __pipeline_commit();
             };
 
-            stage(0);
+            // prefetch NBUF-1 blocks ahead; one commit group per block (empty groups past the end).
+            // Per block: wait for block b, one barrier (b visible to all; every thread is done with
+            // block b-1, whose buffer is restaged next), then issue block b+NBUF-1 and compute b.
+#pragma unroll
+            for (int b = 0; b < NBUF - 1; ++b) {
+                if (b < nblk) stage(b);
+                else __pipeline_commit();
+            }
             for (int b = 0; b < nblk; ++b) {
                 const int t0 = b * IB;
                 const int nb = (m - t0) < IB ? (m - t0) : IB;
-                if (b + 1 < nblk) {
-                    stage(b + 1);
-                    __pipeline_wait_prior(1);
-                } else {
-                    __pipeline_wait_prior(0);
-                }
+                __pipeline_wait_prior(NBUF - 2);
                 __syncthreads();
-                const double* cb = coef + (b & 1) * NT * IB * LR;
-                const double* wb = wbuf + (b & 1) * 2 * IB * SP;
+                if (b + NBUF - 1 < nblk) stage(b + NBUF - 1);
+                else __pipeline_commit();
+                const double* cb = coef + (b % NBUF) * NT * IB * LR;
+                const double* wb = wbuf + (b % NBUF) * 2 * IB * SP;
                 for (int tt = 0; tt < nb; ++tt) {
                     const int t = t0 + tt;
                     const double wl = wb[tt * SP + sl];
@@ -296,8 +312,6 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
                             }
                         }
                     }
-                } else {
-                    __syncthreads();  // buffer b&1 is restaged two blocks later
                 }
             }
             if (!REC) {
@@ -306,7 +320,7 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
                 for (int k = 0; k < NLW; ++k) {
                     const int l = lbase + k * LL;
                     if (l < L && sact) {
-                        const double g1 = __ldg(A.gam + off * L + l);
+                        const double g1 = g1buf[lo + k * LL];
                         double* o = A.out + (s * g.E + e) * 2 * (int64_t)L + l;
                         o[0] = g1 * Z[k];
                         o[L] = g1 * Y[k];
@@ -324,7 +338,7 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
     }
 }
 
-template <int NLW, int SL, bool REC>
+template <int NLW, int SL, bool REC, int IB>
 cudaError_t launch_sweep(SweepArgs a, cudaStream_t st) {
     constexpr int LL = Lanes<SL>::LL;
     constexpr int NT = REC ? 3 : 1;
@@ -333,37 +347,48 @@ cudaError_t launch_sweep(SweepArgs a, cudaStream_t st) {
     a.nwarps = nw;
     const int LR = nw * NLW * LL;
     const int P = nw * LL;
-    size_t base = (size_t)2 * NT * IB * LR + (size_t)4 * IB * (SL + 1);
-    if (REC) base += (size_t)2 * IB * P * (SL + 1);
+    constexpr int NBUF = REC ? 2 : 3;
+    size_t base = (size_t)NBUF * NT * IB * LR + (size_t)NBUF * 2 * IB * (SL + 1);
+    base += REC ? (size_t)2 * IB * P * (SL + 1) : (size_t)LR;
     a.mtile = REC ? (int)(OTILE_BYTES / (sizeof(double) * (SL + 1))) : 0;
     size_t smem = sizeof(double) * (base + (REC ? (size_t)a.mtile * (SL + 1) : 0));
     if (REC && smem > 220 * 1024) {  // no room for the smem output tile
         a.mtile = 0;
         smem = sizeof(double) * base;
     }
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<NLW, SL, REC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<NLW, SL, REC, IB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(a.wq.counter, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return e;
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<NLW, SL, REC>, nw * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<NLW, SL, REC, IB>, nw * 32, smem);
     if (per_sm < 1) per_sm = 1;
     int blocks = 148 * per_sm;
     if (blocks > a.wq.n_items) blocks = a.wq.n_items;
-    sweep_kernel<NLW, SL, REC><<<blocks, nw * 32, smem, st>>>(a);
+    sweep_kernel<NLW, SL, REC, IB><<<blocks, nw * 32, smem, st>>>(a);
     return cudaGetLastError();
 }
 
 template <bool REC>
 cudaError_t dispatch(SweepArgs a, cudaStream_t st) {
+    // steps per staging block (tuning knob GRF_SWEEP_IB for experiments; default 8 / 16)
+    static const int ib_env = [] {
+        const char* e = getenv("GRF_SWEEP_IB");
+        return e ? atoi(e) : 0;
+    }();
+    const int ib = REC ? 8 : (ib_env ? ib_env : 16);  // recover: smem holds partials + output tile
     // sample lanes per warp: as many samples as the call has, up to 32
-    if (a.S >= 32) return launch_sweep<16, 32, REC>(a, st);
-    if (a.S >= 16) return launch_sweep<16, 16, REC>(a, st);
-    if (a.S >= 8) return launch_sweep<8, 8, REC>(a, st);
-    if (a.S >= 4) return launch_sweep<8, 4, REC>(a, st);
-    if (a.S >= 2) return launch_sweep<8, 2, REC>(a, st);
-    return launch_sweep<8, 1, REC>(a, st);
+    if (a.S >= 32) {
+        if (ib == 32) return launch_sweep<16, 32, REC, 32>(a, st);
+        if (ib == 16) return launch_sweep<16, 32, REC, 16>(a, st);
+        return launch_sweep<16, 32, REC, 8>(a, st);
+    }
+    if (a.S >= 16) return launch_sweep<16, 16, REC, 8>(a, st);
+    if (a.S >= 8) return launch_sweep<8, 8, REC, 8>(a, st);
+    if (a.S >= 4) return launch_sweep<8, 4, REC, 8>(a, st);
+    if (a.S >= 2) return launch_sweep<8, 2, REC, 8>(a, st);
+    return launch_sweep<8, 1, REC, 8>(a, st);
 }
 
 int sample_lanes(int64_t S) {
