@@ -64,10 +64,10 @@ __device__ __forceinline__ void cp8(double* dst, const double* src) { __pipeline
 // Shared memory layout (doubles), NT = number of coefficient tables (1 condense, 3 recover):
 //   coef [2][NT][IB][LR]   staged mu (, gam, kap) for this round's LR nodes, double buffered
 //   wbuf [2][2][IB][SL+1]  staged W: [buffer][left/right positions][step][sample]
-//   part [2*IB][P][SL+1]   per (row, partial, sample) sums, P = nwarps*LL          (recover)
+//   part [2][2*IB][P][SL+1] per (row, partial, sample) sums, P = nwarps*LL, double buffered (recover)
 //   otile[mtile][SL+1]     the edge's output tile                                  (recover)
-template <int NLW, int SL, bool REC, int IB>
-__global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
+template <int NLW, int SL, bool REC, int IB, int MAXT>
+__global__ void __launch_bounds__(MAXT) sweep_kernel(SweepArgs A) {
     constexpr int LL = Lanes<SL>::LL;
     constexpr int NT = REC ? 3 : 1;
     constexpr int SP = SL + 1;
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
     double* wbuf = coef + NBUF * NT * IB * LR;           // NBUF*2*IB*SP
     double* part = wbuf + NBUF * 2 * IB * SP;            // 2*IB*P*SP     (REC)
     double* g1buf = part;                                // LR             (condense: g_1 row)
-    double* otile = part + (REC ? 2 * IB * P * SP : 0);  // mtile*SP      (REC)
+    double* otile = part + (REC ? 4 * IB * P * SP : 0);  // mtile*SP      (REC; part is double buffered)
     const int64_t N = g.N;
     const int V = g.V;
     const int pidx = warp * LL + ll;
@@ -109,6 +109,12 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
         const int vu = g.eu[e], vv = g.ev[e];
         const double* Wtile = A.W + s0 * N + off;
         const bool in_smem = REC && (m <= A.mtile);
+        if (REC && m > 0) {  // u_G at both ends is needed at the first and last step: warm L2 now
+            for (int l = 4 * (warp * LL + ll); l < L; l += 4 * nwarps * LL) {  // one 32-B sector each
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(A.uG + (sc * V + vu) * (int64_t)L + l));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(A.uG + (sc * V + vv) * (int64_t)L + l));
+            }
+        }
 
         for (int rd = 0; rd < rounds; ++rd) {
             if (rd > 0) __syncthreads();  // staging buffers of the previous round are free
@@ -218,6 +224,36 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
                 if (b < nblk) stage(b);
                 else __pipeline_commit();
             }
+            // fold the per-warp partial sums of block bp into the output (deferred by one block so
+            // that it needs no barrier of its own).  Position i is visited by the left sweep at
+            // step i and by the right sweep at step m-1-i; left rows are folded before right rows,
+            // so the first visit is the smaller (block, phase) pair.  Only near the edge midpoint
+            // can one block hold both visits of a position: then the two phases are separated.
+            auto fold = [&](int bp) {
+                const int t0p = bp * IB;
+                const int nbp = (m - t0p) < IB ? (m - t0p) : IB;
+                const double* pb = part + (bp & 1) * 2 * IB * P * SP;
+                const bool overlap = (t0p + nbp > m - t0p - nbp) && (m - 1 - t0p >= t0p);
+                for (int side = 0; side < 2; ++side) {
+                    if (side == 1 && overlap) __syncthreads();
+                    for (int o = tid; o < IB * SL; o += blockDim.x) {
+                        const int j = o / IB, tt = o % IB;
+                        if (tt >= nbp) continue;
+                        double acc = 0.0;
+                        for (int q = 0; q < P; ++q) acc += pb[((side * IB + tt) * P + q) * SP + j];
+                        const int i = side ? (m - 1 - (t0p + tt)) : (t0p + tt);
+                        const int bi = i / IB, bm = (m - 1 - i) / IB;
+                        const bool first = (rd == 0) && (side ? (bm < bi) : (bi <= bm));
+                        if (in_smem) {
+                            double* dst = otile + i * SP + j;
+                            *dst = first ? acc : *dst + acc;
+                        } else if (s0 + j < A.S) {
+                            double* dst = A.out + (s0 + j) * N + off + i;
+                            *dst = first ? acc : *dst + acc;
+                        }
+                    }
+                }
+            };
             for (int b = 0; b < nblk; ++b) {
                 const int t0 = b * IB;
                 const int nb = (m - t0) < IB ? (m - t0) : IB;
@@ -225,6 +261,8 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
                 __syncthreads();
                 if (b + NBUF - 1 < nblk) stage(b + NBUF - 1);
                 else __pipeline_commit();
+                if (REC && b > 0) fold(b - 1);
+                double* pw = part + (b & 1) * 2 * IB * P * SP;
                 const double* cb = coef + (b % NBUF) * NT * IB * LR;
                 const double* wb = wbuf + (b % NBUF) * 2 * IB * SP;
                 for (int tt = 0; tt < nb; ++tt) {
@@ -278,8 +316,8 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
                                 aR1 += g1 * Z[k + 1];
                             }
                         }
-                        part[(tt * P + pidx) * SP + sl] = aL0 + aL1;
-                        part[((IB + tt) * P + pidx) * SP + sl] = aR0 + aR1;
+                        pw[(tt * P + pidx) * SP + sl] = aL0 + aL1;
+                        pw[((IB + tt) * P + pidx) * SP + sl] = aR0 + aR1;
                     } else {
 #pragma unroll
                         for (int k = 0; k < NLW; ++k) {
@@ -289,30 +327,10 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
                         }
                     }
                 }
-                if (REC) {
-                    // Position i is visited by the left sweep at step i and by the right sweep at
-                    // step m-1-i; per block the left rows are folded in before the right rows, so
-                    // the first visit is the smaller (block, phase) pair.
-                    for (int side = 0; side < 2; ++side) {
-                        __syncthreads();
-                        for (int o = tid; o < IB * SL; o += blockDim.x) {
-                            const int j = o / IB, tt = o % IB;
-                            if (tt >= nb) continue;
-                            double acc = 0.0;
-                            for (int p = 0; p < P; ++p) acc += part[((side * IB + tt) * P + p) * SP + j];
-                            const int i = side ? (m - 1 - (t0 + tt)) : (t0 + tt);
-                            const int bi = i / IB, bm = (m - 1 - i) / IB;
-                            const bool first = (rd == 0) && (side ? (bm < bi) : (bi <= bm));
-                            if (in_smem) {
-                                double* dst = otile + i * SP + j;
-                                *dst = first ? acc : *dst + acc;
-                            } else if (s0 + j < A.S) {
-                                double* dst = A.out + (s0 + j) * N + off + i;
-                                *dst = first ? acc : *dst + acc;
-                            }
-                        }
-                    }
-                }
+            }
+            if (REC) {
+                __syncthreads();
+                fold(nblk - 1);
             }
             if (!REC) {
                 // w_m = g_m Y_m (left sweep end), w_1 = g_1 Z_1 (right sweep end); g_1 = g_m
@@ -338,35 +356,35 @@ __global__ void __launch_bounds__(MAXW * 32) sweep_kernel(SweepArgs A) {
     }
 }
 
-template <int NLW, int SL, bool REC, int IB>
+template <int NLW, int SL, bool REC, int IB, int MAXT = MAXW * 32>
 cudaError_t launch_sweep(SweepArgs a, cudaStream_t st) {
     constexpr int LL = Lanes<SL>::LL;
     constexpr int NT = REC ? 3 : 1;
     int nw = (a.L + NLW * LL - 1) / (NLW * LL);
-    if (nw > MAXW) nw = MAXW;
+    if (nw > MAXT / 32) nw = MAXT / 32;
     a.nwarps = nw;
     const int LR = nw * NLW * LL;
     const int P = nw * LL;
     constexpr int NBUF = REC ? 2 : 3;
     size_t base = (size_t)NBUF * NT * IB * LR + (size_t)NBUF * 2 * IB * (SL + 1);
-    base += REC ? (size_t)2 * IB * P * (SL + 1) : (size_t)LR;
+    base += REC ? (size_t)4 * IB * P * (SL + 1) : (size_t)LR;
     a.mtile = REC ? (int)(OTILE_BYTES / (sizeof(double) * (SL + 1))) : 0;
     size_t smem = sizeof(double) * (base + (REC ? (size_t)a.mtile * (SL + 1) : 0));
     if (REC && smem > 220 * 1024) {  // no room for the smem output tile
         a.mtile = 0;
         smem = sizeof(double) * base;
     }
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<NLW, SL, REC, IB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<NLW, SL, REC, IB, MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(a.wq.counter, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return e;
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<NLW, SL, REC, IB>, nw * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<NLW, SL, REC, IB, MAXT>, nw * 32, smem);
     if (per_sm < 1) per_sm = 1;
     int blocks = 148 * per_sm;
     if (blocks > a.wq.n_items) blocks = a.wq.n_items;
-    sweep_kernel<NLW, SL, REC, IB><<<blocks, nw * 32, smem, st>>>(a);
+    sweep_kernel<NLW, SL, REC, IB, MAXT><<<blocks, nw * 32, smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -380,6 +398,7 @@ cudaError_t dispatch(SweepArgs a, cudaStream_t st) {
     const int ib = REC ? 8 : (ib_env ? ib_env : 16);  // recover: smem holds partials + output tile
     // sample lanes per warp: as many samples as the call has, up to 32
     if (a.S >= 32) {
+        if (REC) return launch_sweep<32, 32, REC, 8, 256>(a, st);  // 32 nodes x 2 chains per thread
         if (ib == 32) return launch_sweep<16, 32, REC, 32>(a, st);
         if (ib == 16) return launch_sweep<16, 32, REC, 16>(a, st);
         return launch_sweep<16, 32, REC, 8>(a, st);
