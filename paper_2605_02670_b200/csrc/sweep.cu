@@ -18,14 +18,15 @@
 //   K5 recover  (f = W_I + (c_L/h_e)(u_left e_1 + u_right e_m), P306-311):
 //                                 u_i = sum_l g_i (Y_i + Z_i - f_i)  (+ vertex values sum_l u_G)
 //
-// Mapping: an item = (edge, tile of SL samples), pulled from a longest-edge-first queue.
-// lane = (sample, node sub-lane), warp = group of NLW*LL nodes; every thread carries
-// NLW nodes x 2 chains in registers.  The per-(l, t) coefficients and the W tile are
-// staged into shared memory IB steps at a time with cp.async, double buffered (block
-// b+1 loads while block b computes), and read as warp broadcasts.  Per-warp partial sums
-// over the thread's nodes are combined across warps in fixed order (deterministic) into
-// an output tile kept in shared memory for the whole edge (written to HBM once,
-// coalesced); edges too long for the tile fall back to read-modify-write in global memory.
+// Mapping: a warp owns one (edge, tile of SL samples) and ALL quadrature nodes: lane =
+// (sample sl, node sub-lane ll), LL = 32/SL sub-lanes, and each thread carries the NLW
+// consecutive nodes ll*NLW .. ll*NLW+NLW-1 (2 chains each) in registers.  The sum over l is
+// an in-thread sum over the thread's nodes plus log2(LL) warp shuffles -- no cross-warp
+// reduction, no partial-sum buffers.  The warps of a CTA work on the same edge (different
+// sample tiles), so the per-(l, t) coefficients are staged once per CTA in shared memory,
+// IB steps at a time with cp.async, double buffered, and read as (near-)broadcasts.  Each
+// warp keeps its edge's output tile in shared memory and writes it to HBM once, coalesced.
+// Edges are handed out longest first through an atomic work queue.
 #include <cuda_pipeline.h>
 
 #include <cstdlib>
@@ -35,8 +36,8 @@
 namespace grf {
 namespace {
 
-constexpr int MAXW = 16;       // warps per CTA
-constexpr int OTILE_BYTES = 48 * 1024;
+constexpr int NWARP = 8;     // warps per CTA
+constexpr int OTILE_DOUBLES_PER_WARP = 640;  // smem output tile per warp: m * SL <= 640
 
 struct SweepArgs {
     DevGraph g;
@@ -50,46 +51,51 @@ struct SweepArgs {
     double* out;        // condense: ends; recover: u [s*N + dof]
     const double* uG;   // recover: [(s*V + v)*L + l]
     WorkQueue wq;
-    int32_t nwarps;     // warps per CTA (node groups per round)
-    int32_t mtile;      // recover: edges with m <= mtile keep their output tile in smem
-};
-
-template <int SL>
-struct Lanes {
-    static constexpr int LL = 32 / SL;  // node sub-lanes per warp
+    int32_t rounds;     // node rounds (L > NLW*LL only)
 };
 
 __device__ __forceinline__ void cp8(double* dst, const double* src) { __pipeline_memcpy_async(dst, src, 8); }
 
-// Shared memory layout (doubles), NT = number of coefficient tables (1 condense, 3 recover):
-//   coef [2][NT][IB][LR]   staged mu (, gam, kap) for this round's LR nodes, double buffered
-//   wbuf [2][2][IB][SL+1]  staged W: [buffer][left/right positions][step][sample]
-//   part [2][2*IB][P][SL+1] per (row, partial, sample) sums, P = nwarps*LL, double buffered (recover)
-//   otile[mtile][SL+1]     the edge's output tile                                  (recover)
-template <int NLW, int SL, bool REC, int IB, int MAXT>
-__global__ void __launch_bounds__(MAXT) sweep_kernel(SweepArgs A) {
-    constexpr int LL = Lanes<SL>::LL;
+// smem node stride per sub-lane: NLW rounded so that the LL sub-lanes' LDS.128 hit
+// disjoint banks (stride in doubles = 2, 6, 10 or 14 mod 16) and stays 16-byte aligned
+template <int NLW>
+struct Stride {
+    static constexpr int e = (NLW + 1) / 2 * 2;
+    static constexpr int v = (e % 4 == 2) ? e : e + 2;
+};
+
+// Shared memory (doubles):
+//   coef [2][IB][NT][LP]      staged mu (, gam, kap); LP = LL * stride padded node slots
+//   wbuf [2][IB][2][NWARP*SL]  staged W (left position t, right position m-1-t) for the CTA's samples
+//   g1   [LP]                  condense: g_1 row
+//   otile[NWARP][m][SL]        recover: per-warp output tile (edges with m * SL <= OTILE_DOUBLES_PER_WARP)
+template <int NLW, int SL>
+struct Geo {
+    static constexpr int LL = 32 / SL;
+    static constexpr int LP = LL * Stride<NLW>::v;
+    static constexpr int IB = LP > 320 ? 4 : 8;  // steps per staging block (smem budget)
+};
+
+template <int NLW, int SL, bool REC>
+__global__ void __launch_bounds__(NWARP * 32) sweep_kernel(SweepArgs A) {
+    constexpr int LL = 32 / SL;
     constexpr int NT = REC ? 3 : 1;
-    constexpr int SP = SL + 1;
-    constexpr int NBUF = REC ? 2 : 3;  // staging buffers (prefetch distance NBUF-1 blocks)
+    constexpr int NS = Stride<NLW>::v;
+    constexpr int LP = LL * NS;
+    constexpr int IB = Geo<NLW, SL>::IB;
+    constexpr int CS = NWARP * SL;  // samples per CTA item
     extern __shared__ double smem[];
     __shared__ int item_sh;
     const DevGraph& g = A.g;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int sl = lane % SL, ll = lane / SL;
-    const int nwarps = A.nwarps;
-    const int P = nwarps * LL;
-    const int LR = nwarps * NLW * LL;  // nodes per round
     const int L = A.L;
-    const int rounds = (L + LR - 1) / LR;
-    double* coef = smem;                                 // 2*NT*IB*LR
-    double* wbuf = coef + NBUF * NT * IB * LR;           // NBUF*2*IB*SP
-    double* part = wbuf + NBUF * 2 * IB * SP;            // 2*IB*P*SP     (REC)
-    double* g1buf = part;                                // LR             (condense: g_1 row)
-    double* otile = part + (REC ? 4 * IB * P * SP : 0);  // mtile*SP      (REC; part is double buffered)
+    double* coef = smem;                        // 2*IB*NT*LP
+    double* wbuf = coef + 2 * IB * NT * LP;     // 2*IB*2*CS
+    double* g1b = wbuf + 2 * IB * 2 * CS;       // LP
+    double* otile = g1b + LP + warp * OTILE_DOUBLES_PER_WARP;
     const int64_t N = g.N;
     const int V = g.V;
-    const int pidx = warp * LL + ll;
 
     for (;;) {
         if (tid == 0) item_sh = atomicAdd(A.wq.counter, 1);
@@ -98,61 +104,66 @@ __global__ void __launch_bounds__(MAXT) sweep_kernel(SweepArgs A) {
         __syncthreads();
         if (it >= A.wq.n_items) break;
         const int e = g.edge_order[it / A.wq.chunks];
-        const int64_t s0 = (int64_t)(it % A.wq.chunks) * SL;
-        const int64_t s = s0 + sl;
+        const int64_t c0 = (int64_t)(it % A.wq.chunks) * CS;  // first sample of the CTA item
+        const int64_t s = c0 + warp * SL + sl;
         const bool sact = s < A.S;
         const int64_t sc = sact ? s : (A.S - 1);
-        const int ns = (int)((A.S - s0) < SL ? (A.S - s0) : SL);
         const int m = g.m[e];
         const int64_t off = g.off[e];
         const double h = g.h[e];
         const int vu = g.eu[e], vv = g.ev[e];
-        const double* Wtile = A.W + s0 * N + off;
-        const bool in_smem = REC && (m <= A.mtile);
-        if (REC && m > 0) {  // u_G at both ends is needed at the first and last step: warm L2 now
-            for (int l = 4 * (warp * LL + ll); l < L; l += 4 * nwarps * LL) {  // one 32-B sector each
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(A.uG + (sc * V + vu) * (int64_t)L + l));
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(A.uG + (sc * V + vv) * (int64_t)L + l));
-            }
-        }
+        const bool in_smem = REC && (m * SL <= OTILE_DOUBLES_PER_WARP);
+        const int ncs = (int)((A.S - c0) < CS ? (A.S - c0) : CS);  // live samples of the item
 
-        for (int rd = 0; rd < rounds; ++rd) {
-            if (rd > 0) __syncthreads();  // staging buffers of the previous round are free
-            const int lbase = rd * LR + warp * (NLW * LL) + ll;  // node of chain k: lbase + k*LL
-            // ---------------- recover: vertex values owned by this edge (sum over l of u_G)
+        for (int rd = 0; rd < A.rounds; ++rd) {
+            if (rd > 0) __syncthreads();
+            const int lbase = rd * LL * NLW + ll * NLW;  // node of chain k: lbase + k
+            const int lr0 = rd * LL * NLW;
+            const int lr_here = (L - lr0) < LL * NLW ? (L - lr0) : LL * NLW;
+            // ---------------- recover: vertex values owned by this edge (u_v = sum_l u_G)
             if (REC) {
                 const bool ownL = g.owner[vu] == 2 * e, ownR = g.owner[vv] == 2 * e + 1;
                 if (ownL || ownR) {
                     double a0 = 0.0, a1 = 0.0;
 #pragma unroll
                     for (int k = 0; k < NLW; ++k) {
-                        const int l = lbase + k * LL;
-                        if (l < L) {
+                        const int l = lbase + k;
+                        if (l < L && l < lr0 + lr_here) {
                             a0 += A.uG[(sc * V + vu) * (int64_t)L + l];
                             a1 += A.uG[(sc * V + vv) * (int64_t)L + l];
                         }
                     }
-                    part[(0 * P + pidx) * SP + sl] = a0;
-                    part[(1 * P + pidx) * SP + sl] = a1;
-                    __syncthreads();
-                    for (int o = tid; o < 2 * SL; o += blockDim.x) {
-                        const int side = o / SL, j = o % SL;
-                        double t = 0.0;
-                        for (int p = 0; p < P; ++p) t += part[(side * P + p) * SP + j];
-                        const int64_t so = s0 + j;
-                        if (so < A.S && (side ? ownR : ownL)) {
-                            double* dst = A.out + so * N + g.NI + (side ? vv : vu);
-                            *dst = rd == 0 ? t : *dst + t;
+#pragma unroll
+                    for (int o = SL; o < 32; o <<= 1) {
+                        a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+                        a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+                    }
+                    if (ll == 0 && sact) {
+                        if (ownL) {
+                            double* d = A.out + s * N + g.NI + vu;
+                            *d = rd == 0 ? a0 : *d + a0;
+                        }
+                        if (ownR) {
+                            double* d = A.out + s * N + g.NI + vv;
+                            *d = rd == 0 ? a1 : *d + a1;
                         }
                     }
-                    __syncthreads();
+                }
+                if (m > 0) {  // u_G at both ends is read at the first and the last step: warm L2
+                    for (int k = 0; k < NLW; k += 4) {
+                        const int l = lbase + k;
+                        if (l < L) {
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(A.uG + (sc * V + vu) * (int64_t)L + l));
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(A.uG + (sc * V + vv) * (int64_t)L + l));
+                        }
+                    }
                 }
             }
             if (m == 0) {
                 if (!REC) {
 #pragma unroll
                     for (int k = 0; k < NLW; ++k) {
-                        const int l = lbase + k * LL;
+                        const int l = lbase + k;
                         if (l < L && sact) {
                             double* o = A.out + (s * g.E + e) * 2 * (int64_t)L + l;
                             o[0] = 0.0;
@@ -165,50 +176,47 @@ __global__ void __launch_bounds__(MAXT) sweep_kernel(SweepArgs A) {
             double Y[NLW], Z[NLW];
 #pragma unroll
             for (int k = 0; k < NLW; ++k) Y[k] = Z[k] = 0.0;
-            const int lr_here = (L - rd * LR) < LR ? (L - rd * LR) : LR;
-            const int lo = warp * (NLW * LL) + ll;  // local node index of chain 0 in the staged block
             const int nblk = (m + IB - 1) / IB;
 
-            // asynchronous staging of block b into buffer b&1 (division-free index math)
+            // asynchronous staging of block b into buffer b&1: coefficients for the round's nodes
+            // (node lc of the round goes to sub-lane lc / NLW, slot lc % NLW), and W of the CTA's samples
             auto stage = [&](int b) {
                 const int t0 = b * IB;
                 const int nb = (m - t0) < IB ? (m - t0) : IB;
-                double* cb = coef + (b % NBUF) * NT * IB * LR;
-                const int64_t row0 = (off + t0) * (int64_t)L + rd * LR;
-                for (int lc = tid; lc < LR; lc += blockDim.x) {
-                    const bool okl = lc < lr_here;
+                double* cb = coef + (b & 1) * IB * NT * LP;
+                for (int x = tid; x < IB * LL * NLW; x += NWARP * 32) {
+                    const int tt = x / (LL * NLW), lc = x % (LL * NLW);
+                    const int slot = (lc / NLW) * NS + lc % NLW;
+                    const bool ok = tt < nb && lc < lr_here;
+                    const int64_t src = (off + t0 + tt) * (int64_t)L + lr0 + lc;
 #pragma unroll
-                    for (int tt = 0; tt < IB; ++tt) {
-                        const bool ok = okl && tt < nb;
-                        const int64_t src = row0 + (int64_t)tt * L + lc;
-#pragma unroll
-                        for (int tb = 0; tb < NT; ++tb) {
-                            double* dst = cb + (tb * IB + tt) * LR + lc;
-                            const double* tab = tb == 0 ? A.mu : (tb == 1 ? A.gam : A.kap);
-                            if (ok)
-                                cp8(dst, tab + src);
-                            else
-                                *dst = 0.0;  // nodes past L (and steps past m) contribute nothing
-                        }
-                    }
-                }
-                if (!REC && b == 0) {  // g_1 (= g_m) row for the end values, staged with block 0
-                    for (int lc = tid; lc < LR; lc += blockDim.x) {
-                        if (lc < lr_here)
-                            cp8(g1buf + lc, A.gam + off * (int64_t)L + rd * LR + lc);
+                    for (int tb = 0; tb < NT; ++tb) {
+                        double* dst = cb + (tt * NT + tb) * LP + slot;
+                        const double* tab = tb == 0 ? A.mu : (tb == 1 ? A.gam : A.kap);
+                        if (ok)
+                            cp8(dst, tab + src);
                         else
-                            g1buf[lc] = 0.0;
+                            *dst = 0.0;  // nodes past L (and steps past m) contribute nothing
                     }
                 }
-                double* wb = wbuf + (b % NBUF) * 2 * IB * SP;
-                for (int x = tid; x < 2 * IB * SL; x += blockDim.x) {
-                    const int side = x / (IB * SL), r = x % (IB * SL);
+                if (!REC && b == 0) {  // g_1 (= g_m) row for the end values
+                    for (int lc = tid; lc < LL * NLW; lc += NWARP * 32) {
+                        const int slot = (lc / NLW) * NS + lc % NLW;
+                        if (lc < lr_here)
+                            cp8(g1b + slot, A.gam + off * (int64_t)L + lr0 + lc);
+                        else
+                            g1b[slot] = 0.0;
+                    }
+                }
+                double* wb = wbuf + (b & 1) * IB * 2 * CS;
+                for (int x = tid; x < 2 * CS * IB; x += NWARP * 32) {
+                    const int side = x / (CS * IB), r = x % (CS * IB);
                     const int j = r / IB, tt = r % IB;
                     if (tt < nb) {
                         const int pos = side ? (m - 1 - t0 - tt) : (t0 + tt);
-                        double* dst = wb + (side * IB + tt) * SP + j;
-                        if (j < ns)
-                            cp8(dst, Wtile + (int64_t)j * N + pos);
+                        double* dst = wb + (tt * 2 + side) * CS + j;
+                        if (j < ncs)
+                            cp8(dst, A.W + (c0 + j) * N + off + pos);
                         else
                             *dst = 0.0;
                     }
@@ -216,129 +224,105 @@ __global__ void __launch_bounds__(MAXT) sweep_kernel(SweepArgs A) {
                 __pipeline_commit();
             };
 
-            // prefetch NBUF-1 blocks ahead; one commit group per block (empty groups past the end).
-            // Per block: wait for block b, one barrier (b visible to all; every thread is done with
-            // block b-1, whose buffer is restaged next), then issue block b+NBUF-1 and compute b.
-#pragma unroll
-            for (int b = 0; b < NBUF - 1; ++b) {
-                if (b < nblk) stage(b);
-                else __pipeline_commit();
-            }
-            // fold the per-warp partial sums of block bp into the output (deferred by one block so
-            // that it needs no barrier of its own).  Position i is visited by the left sweep at
-            // step i and by the right sweep at step m-1-i; left rows are folded before right rows,
-            // so the first visit is the smaller (block, phase) pair.  Only near the edge midpoint
-            // can one block hold both visits of a position: then the two phases are separated.
-            auto fold = [&](int bp) {
-                const int t0p = bp * IB;
-                const int nbp = (m - t0p) < IB ? (m - t0p) : IB;
-                const double* pb = part + (bp & 1) * 2 * IB * P * SP;
-                const bool overlap = (t0p + nbp > m - t0p - nbp) && (m - 1 - t0p >= t0p);
-                for (int side = 0; side < 2; ++side) {
-                    if (side == 1 && overlap) __syncthreads();
-                    for (int o = tid; o < IB * SL; o += blockDim.x) {
-                        const int j = o / IB, tt = o % IB;
-                        if (tt >= nbp) continue;
-                        double acc = 0.0;
-                        for (int q = 0; q < P; ++q) acc += pb[((side * IB + tt) * P + q) * SP + j];
-                        const int i = side ? (m - 1 - (t0p + tt)) : (t0p + tt);
-                        const int bi = i / IB, bm = (m - 1 - i) / IB;
-                        const bool first = (rd == 0) && (side ? (bm < bi) : (bi <= bm));
-                        if (in_smem) {
-                            double* dst = otile + i * SP + j;
-                            *dst = first ? acc : *dst + acc;
-                        } else if (s0 + j < A.S) {
-                            double* dst = A.out + (s0 + j) * N + off + i;
-                            *dst = first ? acc : *dst + acc;
-                        }
-                    }
+            // recovery boundary rows (P310): f_1 += (c_L/h) u_left, f_m += (c_L/h) u_right
+            auto bnd = [&](int k, double& ul, double& ur) {
+                const int l = lbase + k;
+                ul = ur = 0.0;
+                if (l < L && l < lr0 + lr_here) {
+                    const double beta = A.cL[l] / h;
+                    ul = beta * A.uG[(sc * V + vu) * (int64_t)L + l];
+                    ur = beta * A.uG[(sc * V + vv) * (int64_t)L + l];
                 }
             };
+
+            stage(0);
             for (int b = 0; b < nblk; ++b) {
                 const int t0 = b * IB;
                 const int nb = (m - t0) < IB ? (m - t0) : IB;
-                __pipeline_wait_prior(NBUF - 2);
-                __syncthreads();
-                if (b + NBUF - 1 < nblk) stage(b + NBUF - 1);
-                else __pipeline_commit();
-                if (REC && b > 0) fold(b - 1);
-                double* pw = part + (b & 1) * 2 * IB * P * SP;
-                const double* cb = coef + (b % NBUF) * NT * IB * LR;
-                const double* wb = wbuf + (b % NBUF) * 2 * IB * SP;
+                __pipeline_wait_prior(0);
+                __syncthreads();  // block b visible; everyone is done with block b-1's buffer
+                if (b + 1 < nblk) stage(b + 1);
+                const double* cb = coef + (b & 1) * IB * NT * LP + ll * NS;
+                const double* wb = wbuf + (b & 1) * IB * 2 * CS + warp * SL + sl;
                 for (int tt = 0; tt < nb; ++tt) {
                     const int t = t0 + tt;
-                    const double wl = wb[tt * SP + sl];
-                    const double wr = wb[(IB + tt) * SP + sl];
-                    const double* cmu = cb + tt * LR + lo;
+                    const double wl = wb[(tt * 2 + 0) * CS];
+                    const double wr = wb[(tt * 2 + 1) * CS];
+                    const double* cmu = cb + (tt * NT + 0) * LP;
                     if (REC) {
-                        const double* cg = cb + (IB + tt) * LR + lo;
-                        const double* ck = cb + (2 * IB + tt) * LR + lo;
-                        double aL0 = 0.0, aL1 = 0.0, aR0 = 0.0, aR1 = 0.0;
-                        const bool first = (t == 0), last = (t == m - 1);
-                        if (first || last) {
-                            // boundary rows: f_1 += (c_L/h) u_left, f_m += (c_L/h) u_right  (P310)
+                        const double* cg = cb + (tt * NT + 1) * LP;
+                        const double* ck = cb + (tt * NT + 2) * LP;
+                        double aL0 = 0.0, aL1 = 0.0, aL2 = 0.0, aR0 = 0.0, aR1 = 0.0, aR2 = 0.0;
+                        if (t == 0 || t == m - 1) {
 #pragma unroll
                             for (int k = 0; k < NLW; ++k) {
-                                const int l = lbase + k * LL;
-                                double ul = 0.0, ur = 0.0;
-                                if (l < L) {
-                                    const double beta = A.cL[l] / h;
-                                    ul = beta * A.uG[(sc * V + vu) * (int64_t)L + l];
-                                    ur = beta * A.uG[(sc * V + vv) * (int64_t)L + l];
-                                }
+                                double ul, ur;
+                                bnd(k, ul, ur);
                                 double fl = wl, fr = wr;
-                                if (first) {
+                                if (t == 0) {
                                     fl += ul;
                                     fr += ur;
                                 }
-                                if (last) {
+                                if (t == m - 1) {
                                     fl += ur;
                                     fr += ul;
                                 }
-                                const double c_mu = cmu[k * LL], c_g = cg[k * LL], c_k = ck[k * LL];
-                                aL0 += c_k * Y[k];
-                                Y[k] = fl - c_mu * Y[k];
-                                Z[k] = fr - c_mu * Z[k];
-                                aR0 += c_g * Z[k];
+                                aL0 += ck[k] * Y[k];
+                                Y[k] = fl - cmu[k] * Y[k];
+                                Z[k] = fr - cmu[k] * Z[k];
+                                aR0 += cg[k] * Z[k];
                             }
                         } else {
 #pragma unroll
-                            for (int k = 0; k < NLW; k += 2) {
-                                const double m0 = cmu[k * LL], g0 = cg[k * LL], k0 = ck[k * LL];
-                                const double m1 = cmu[(k + 1) * LL], g1 = cg[(k + 1) * LL], k1 = ck[(k + 1) * LL];
-                                aL0 += k0 * Y[k];  // left sweep: kap_t Y_{t-1} -> position t
-                                aL1 += k1 * Y[k + 1];
-                                Y[k] = wl - m0 * Y[k];
-                                Y[k + 1] = wl - m1 * Y[k + 1];
-                                Z[k] = wr - m0 * Z[k];
-                                Z[k + 1] = wr - m1 * Z[k + 1];
-                                aR0 += g0 * Z[k];  // right sweep: g_t Z -> position m-1-t
-                                aR1 += g1 * Z[k + 1];
+                            for (int k = 0; k < NLW; ++k) {
+                                double& aL = (k % 3 == 0) ? aL0 : (k % 3 == 1 ? aL1 : aL2);
+                                double& aR = (k % 3 == 0) ? aR0 : (k % 3 == 1 ? aR1 : aR2);
+                                aL += ck[k] * Y[k];  // left sweep: kap_t Y_{t-1} -> position t
+                                Y[k] = wl - cmu[k] * Y[k];
+                                Z[k] = wr - cmu[k] * Z[k];
+                                aR += cg[k] * Z[k];  // right sweep: g_t Z -> position m-1-t
                             }
                         }
-                        pw[(tt * P + pidx) * SP + sl] = aL0 + aL1;
-                        pw[((IB + tt) * P + pidx) * SP + sl] = aR0 + aR1;
+                        double cl = aL0 + aL1 + aL2, cr = aR0 + aR1 + aR2;
+#pragma unroll
+                        for (int o = SL; o < 32; o <<= 1) {  // sum over the node sub-lanes
+                            cl += __shfl_xor_sync(0xffffffffu, cl, o);
+                            cr += __shfl_xor_sync(0xffffffffu, cr, o);
+                        }
+                        // position i gets its left part at step i and its right part at step m-1-i;
+                        // the earlier visit writes, the later adds (the middle: left then right)
+                        if (ll == 0) {
+                            const int il = t, ir = m - 1 - t;
+                            const bool fl1 = rd == 0 && il <= m - 1 - il;
+                            const bool fr1 = rd == 0 && ir > m - 1 - ir;
+                            if (in_smem) {
+                                double* dl = otile + il * SL + sl;
+                                *dl = fl1 ? cl : *dl + cl;
+                                double* dr = otile + ir * SL + sl;
+                                *dr = fr1 ? cr : *dr + cr;
+                            } else if (sact) {
+                                double* dl = A.out + s * N + off + il;
+                                *dl = fl1 ? cl : *dl + cl;
+                                double* dr = A.out + s * N + off + ir;
+                                *dr = fr1 ? cr : *dr + cr;
+                            }
+                        }
                     } else {
 #pragma unroll
                         for (int k = 0; k < NLW; ++k) {
-                            const double c_mu = cmu[k * LL];
-                            Y[k] = wl - c_mu * Y[k];
-                            Z[k] = wr - c_mu * Z[k];
+                            Y[k] = wl - cmu[k] * Y[k];
+                            Z[k] = wr - cmu[k] * Z[k];
                         }
                     }
                 }
-            }
-            if (REC) {
-                __syncthreads();
-                fold(nblk - 1);
             }
             if (!REC) {
                 // w_m = g_m Y_m (left sweep end), w_1 = g_1 Z_1 (right sweep end); g_1 = g_m
 #pragma unroll
                 for (int k = 0; k < NLW; ++k) {
-                    const int l = lbase + k * LL;
-                    if (l < L && sact) {
-                        const double g1 = g1buf[lo + k * LL];
+                    const int l = lbase + k;
+                    if (l < L && l < lr0 + lr_here && sact) {
+                        const double g1 = g1b[ll * NS + k];
                         double* o = A.out + (s * g.E + e) * 2 * (int64_t)L + l;
                         o[0] = g1 * Z[k];
                         o[L] = g1 * Y[k];
@@ -347,93 +331,84 @@ __global__ void __launch_bounds__(MAXT) sweep_kernel(SweepArgs A) {
             }
         }
         if (in_smem && m > 0) {
-            __syncthreads();
-            for (int o = tid; o < m * ns; o += blockDim.x) {
+            __syncwarp();
+            // the warp's SL samples, positions contiguous per sample row
+            for (int o = lane; o < m * SL; o += 32) {
                 const int j = o / m, i = o - j * m;
-                A.out[(s0 + j) * N + off + i] = otile[i * SP + j];
+                const int64_t sj = c0 + warp * SL + j;
+                if (sj < A.S) A.out[sj * N + off + i] = otile[i * SL + j];
             }
         }
     }
 }
 
-template <int NLW, int SL, bool REC, int IB, int MAXT = MAXW * 32>
+template <int NLW, int SL, bool REC>
 cudaError_t launch_sweep(SweepArgs a, cudaStream_t st) {
-    constexpr int LL = Lanes<SL>::LL;
+    constexpr int LL = 32 / SL;
     constexpr int NT = REC ? 3 : 1;
-    int nw = (a.L + NLW * LL - 1) / (NLW * LL);
-    if (nw > MAXT / 32) nw = MAXT / 32;
-    a.nwarps = nw;
-    const int LR = nw * NLW * LL;
-    const int P = nw * LL;
-    constexpr int NBUF = REC ? 2 : 3;
-    size_t base = (size_t)NBUF * NT * IB * LR + (size_t)NBUF * 2 * IB * (SL + 1);
-    base += REC ? (size_t)4 * IB * P * (SL + 1) : (size_t)LR;
-    a.mtile = REC ? (int)(OTILE_BYTES / (sizeof(double) * (SL + 1))) : 0;
-    size_t smem = sizeof(double) * (base + (REC ? (size_t)a.mtile * (SL + 1) : 0));
-    if (REC && smem > 220 * 1024) {  // no room for the smem output tile
-        a.mtile = 0;
-        smem = sizeof(double) * base;
-    }
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<NLW, SL, REC, IB, MAXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    constexpr int LP = LL * Stride<NLW>::v;
+    constexpr int IB = Geo<NLW, SL>::IB;
+    constexpr int CS = NWARP * SL;
+    a.rounds = (a.L + LL * NLW - 1) / (LL * NLW);
+    a.wq.samples_per_item = CS;
+    a.wq.chunks = (int)((a.S + CS - 1) / CS);
+    a.wq.n_items = a.g.E * a.wq.chunks;
+    const size_t smem = sizeof(double) * ((size_t)2 * IB * NT * LP + (size_t)2 * IB * 2 * CS + LP +
+                                          (REC ? (size_t)NWARP * OTILE_DOUBLES_PER_WARP : 0));
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<NLW, SL, REC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(a.wq.counter, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return e;
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<NLW, SL, REC, IB, MAXT>, nw * 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<NLW, SL, REC>, NWARP * 32, smem);
     if (per_sm < 1) per_sm = 1;
     int blocks = 148 * per_sm;
     if (blocks > a.wq.n_items) blocks = a.wq.n_items;
-    sweep_kernel<NLW, SL, REC, IB, MAXT><<<blocks, nw * 32, smem, st>>>(a);
+    sweep_kernel<NLW, SL, REC><<<blocks, NWARP * 32, smem, st>>>(a);
     return cudaGetLastError();
 }
 
+// node sub-lanes LL (= 32/SL) and nodes per thread NLW for this (L, S): as few node
+// sub-lanes as keep NLW <= 28 (more samples per warp), but no more sample lanes than samples
 template <bool REC>
 cudaError_t dispatch(SweepArgs a, cudaStream_t st) {
-    // steps per staging block (tuning knob GRF_SWEEP_IB for experiments; default 8 / 16)
-    static const int ib_env = [] {
-        const char* e = getenv("GRF_SWEEP_IB");
-        return e ? atoi(e) : 0;
-    }();
-    const int ib = REC ? 8 : (ib_env ? ib_env : 16);  // recover: smem holds partials + output tile
-    // sample lanes per warp: as many samples as the call has, up to 32
-    if (a.S >= 32) {
-        if (REC) return launch_sweep<32, 32, REC, 8, 256>(a, st);  // 32 nodes x 2 chains per thread
-        if (ib == 32) return launch_sweep<16, 32, REC, 32>(a, st);
-        if (ib == 16) return launch_sweep<16, 32, REC, 16>(a, st);
-        return launch_sweep<16, 32, REC, 8>(a, st);
-    }
-    if (a.S >= 16) return launch_sweep<16, 16, REC, 8>(a, st);
-    if (a.S >= 8) return launch_sweep<8, 8, REC, 8>(a, st);
-    if (a.S >= 4) return launch_sweep<8, 4, REC, 8>(a, st);
-    if (a.S >= 2) return launch_sweep<8, 2, REC, 8>(a, st);
-    return launch_sweep<8, 1, REC, 8>(a, st);
-}
-
-int sample_lanes(int64_t S) {
-    return S >= 32 ? 32 : S >= 16 ? 16 : S >= 8 ? 8 : S >= 4 ? 4 : S >= 2 ? 2 : 1;
+    int ll = 1;
+    while (ll < 32 && (a.L + ll - 1) / ll > 28) ll *= 2;
+    while (ll < 32 && 32 / ll > a.S) ll *= 2;
+    const int need = (a.L + ll - 1) / ll;
+    const int nlw = need <= 8 ? 8 : (need <= 16 ? 16 : 28);
+#define GRF_SW(NL, SLV) \
+    if (nlw == NL && 32 / ll == SLV) return launch_sweep<NL, SLV, REC>(a, st);
+    GRF_SW(8, 32) GRF_SW(16, 32) GRF_SW(28, 32)
+    GRF_SW(8, 16) GRF_SW(16, 16) GRF_SW(28, 16)
+    GRF_SW(8, 8) GRF_SW(16, 8) GRF_SW(28, 8)
+    GRF_SW(8, 4) GRF_SW(16, 4) GRF_SW(28, 4)
+    GRF_SW(8, 2) GRF_SW(16, 2) GRF_SW(28, 2)
+    GRF_SW(8, 1) GRF_SW(16, 1) GRF_SW(28, 1)
+#undef GRF_SW
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace
 
 WorkQueue make_work_queue(const DevGraph& g, int64_t n_samples, int32_t* counter) {
-    WorkQueue q;
+    WorkQueue q;  // the item shape (edge, samples per CTA) is fixed by the launcher
     q.counter = counter;
-    q.samples_per_item = sample_lanes(n_samples);
-    q.chunks = (int)((n_samples + q.samples_per_item - 1) / q.samples_per_item);
-    q.n_items = g.E * q.chunks;
+    (void)g;
+    (void)n_samples;
     return q;
 }
 
 cudaError_t launch_condense(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W, double* ends,
                             WorkQueue wq, cudaStream_t st) {
-    SweepArgs a{g, p.L, p.cL, p.mu, p.gam, p.kap, n_samples, W, ends, nullptr, wq, 0, 0};
+    SweepArgs a{g, p.L, p.cL, p.mu, p.gam, p.kap, n_samples, W, ends, nullptr, wq, 1};
     return dispatch<false>(a, st);
 }
 
 cudaError_t launch_recover(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W, double* u,
                            const double* uG, WorkQueue wq, cudaStream_t st) {
-    SweepArgs a{g, p.L, p.cL, p.mu, p.gam, p.kap, n_samples, W, u, uG, wq, 0, 0};
+    SweepArgs a{g, p.L, p.cL, p.mu, p.gam, p.kap, n_samples, W, u, uG, wq, 1};
     return dispatch<true>(a, st);
 }
 
