@@ -29,8 +29,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC,
           "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 PER_FILE = {"noise.cu": ["--fmad=false"]}
-SOURCES = ["noise.cu", "edge_setup.cu", "sweep.cu", "pcg.cu", "grf_api.cpp"]
-HEADERS = ["grf_internal.h", "thomas.cuh"]
+SOURCES = ["noise.cu", "edge_setup.cu", "sweep.cu", "sweep_cond.cu", "sweep_rec_a.cu", "sweep_rec_b.cu", "pcg.cu", "grf_api.cpp"]
+HEADERS = ["grf_internal.h", "thomas.cuh", "sweep_impl.cuh"]
 
 
 def nvcc() -> str:

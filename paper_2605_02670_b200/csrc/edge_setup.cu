@@ -9,9 +9,10 @@
 //
 // Thomas factorisation of A_II (P187-194 [eq:thomas_coefficients], thomas.cuh):
 //     d'_1 = a,  d'_lo,i = b / d'_{i-1},  d'_i = a - d'_lo,i b
-// K3/K5 (sweep.cu) use them through three node-minor tables [(off_e + t) * L + l]:
-//     mu_t = d'_lo,t = b / d'_{t-1} (mu_1 = 0),  g_t = 1 / (d'_t + d'_{m+1-t} - a),  kap_t = -g_t mu_t
-// (g_t is the diagonal of A_II^{-1}; see sweep.cu for the twisted-factorisation use).
+// K3/K5 (sweep_impl.cuh) use them through two node-minor tables [(off_e + t) * Lp + l]
+// (row padded to the sweep tiling Lp >= L with zeros, which makes padded nodes inert):
+//     mu_t = d'_lo,t = b / d'_{t-1} (mu_1 = 0),  g_t = 1 / (d'_t + d'_{m+1-t} - a)
+// (g_t is the diagonal of A_II^{-1}; see sweep_impl.cuh for the twisted-factorisation use).
 //
 // Local Schur complement (P204-213 [eq:local_reduced_schur]):
 //     S^{(l,e)} = A_GG - A_GI A_II^{-1} A_IG = [[s_d, s_o], [s_o, s_d]],
@@ -33,16 +34,17 @@
 namespace grf {
 namespace {
 
-__global__ void edge_setup_kernel(DevGraph g, int32_t L, const double* __restrict__ cIt,
+__global__ void edge_setup_kernel(DevGraph g, int32_t L, int32_t Lp, const double* __restrict__ cIt,
                                   const double* __restrict__ cLt, double kappa2, double* __restrict__ mu_t,
-                                  double* __restrict__ gam_t, double* __restrict__ kap_t,
-                                  double4* __restrict__ sig) {
+                                  double* __restrict__ gam_t, double4* __restrict__ sig) {
     const int e = blockIdx.x;
     const double h = g.h[e];
     const int m = g.m[e];
-    double* tmu = mu_t + g.off[e] * L;
-    double* tgam = gam_t + g.off[e] * L;
-    double* tkap = kap_t + g.off[e] * L;
+    double* tmu = mu_t + g.off[e] * Lp;
+    double* tgam = gam_t + g.off[e] * Lp;
+    for (int l = L + threadIdx.x; l < Lp; l += blockDim.x) {  // padded nodes: inert zeros
+        for (int t = 0; t < m; ++t) tmu[(int64_t)t * Lp + l] = tgam[(int64_t)t * Lp + l] = 0.0;
+    }
     for (int l = threadIdx.x; l < L; l += blockDim.x) {
         const double cI = cIt[l], cL = cLt[l];
         const EdgeCoef c = edge_coef(cI, cL, kappa2, h);
@@ -52,21 +54,23 @@ __global__ void edge_setup_kernel(DevGraph g, int32_t L, const double* __restric
             sd = share;
             so = c.b;
         } else {
-            // pivots d'_t (stored temporarily in the kap table) and multipliers mu_t
+            // pivots d'_t (stored temporarily in the g table) and multipliers mu_t
             double inv = 0.0;
             double prod = 1.0;  // prod_{t=1}^{m-1} (-mu_t) = prod_{i<m} (-b / d'_i)
             for (int t = 0; t < m; ++t) {
                 const double mu = thomas_step(c, inv);
-                tmu[(int64_t)t * L + l] = mu;
-                tkap[(int64_t)t * L + l] = c.a - mu * c.b;  // d'_t, the same expression thomas_step inverted
+                tmu[(int64_t)t * Lp + l] = mu;
+                tgam[(int64_t)t * Lp + l] = c.a - mu * c.b;  // d'_t, the same expression thomas_step inverted
                 if (t > 0) prod *= -mu;
             }
-            // twisted-factorisation diagonal g_t = (A_II^{-1})_tt = 1 / (d'_t + d'_{m+1-t} - a)
-            for (int t = 0; t < m; ++t)
-                tgam[(int64_t)t * L + l] =
-                    1.0 / (tkap[(int64_t)t * L + l] + tkap[(int64_t)(m - 1 - t) * L + l] - c.a);
-            for (int t = 0; t < m; ++t)
-                tkap[(int64_t)t * L + l] = -tgam[(int64_t)t * L + l] * tmu[(int64_t)t * L + l];
+            // twisted-factorisation diagonal g_t = (A_II^{-1})_tt = 1 / (d'_t + d'_{m+1-t} - a), computed in
+            // mirrored pairs (t, m-1-t) so the in-place overwrite of the pivots is safe
+            for (int t = 0; t <= (m - 1) / 2; ++t) {
+                const int tm = m - 1 - t;
+                const double gv = 1.0 / (tgam[(int64_t)t * Lp + l] + tgam[(int64_t)tm * Lp + l] - c.a);
+                tgam[(int64_t)t * Lp + l] = gv;
+                tgam[(int64_t)tm * Lp + l] = gv;
+            }
             const double b2 = c.b * c.b;
             sd = share - b2 * inv;          // (A_II^{-1})_11 = 1 / d'_m
             so = -b2 * (prod * inv);        // (A_II^{-1})_1m
@@ -81,7 +85,7 @@ __global__ void edge_setup_kernel(DevGraph g, int32_t L, const double* __restric
 void launch_edge_setup(const DevGraph& g, DevPlan& p, cudaStream_t st) {
     int threads = ((p.L + 31) / 32) * 32;
     if (threads > 256) threads = 256;
-    edge_setup_kernel<<<g.E, threads, 0, st>>>(g, p.L, p.cI, p.cL, p.kappa * p.kappa, p.mu, p.gam, p.kap,
+    edge_setup_kernel<<<g.E, threads, 0, st>>>(g, p.L, p.Lp, p.cI, p.cL, p.kappa * p.kappa, p.mu, p.gam,
                                                reinterpret_cast<double4*>(p.sig));
 }
 

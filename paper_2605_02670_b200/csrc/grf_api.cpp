@@ -206,14 +206,13 @@ grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf
         }
     }
     const int64_t L = ne - nb;
-    if (L > grf::max_nodes_per_block())
-        return fail(GRF_EUNSUPPORTED, "%lld quadrature nodes in one call (max %d); shard the node range",
-                    (long long)L, grf::max_nodes_per_block());
+    int32_t Lp = 0, TL = 0, rounds = 0;
+    grf::plan_tiling((int32_t)L, &Lp, &TL, &rounds);
     auto p = std::make_unique<Plan>();
     p->key = key;
     p->Km = Km;
     p->Kp = Kp;
-    std::vector<double> cI(L), cL(L);
+    std::vector<double> cI(L), cL(Lp, 0.0);  // c_L zero padded to the table row Lp
     plan_coefficients(beta, k, Km, nb, ne, cI.data(), cL.data());
     auto grab = [&](size_t bytes) -> void* {
         void* q = g->alloc.get(bytes, st);
@@ -221,27 +220,28 @@ grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf
         return q;
     };
     double* dcI = (double*)grab(L * sizeof(double));
-    double* dcL = (double*)grab(L * sizeof(double));
-    const size_t tab = (size_t)std::max<int64_t>(g->NI, 1) * L * sizeof(double);
+    double* dcL = (double*)grab(Lp * sizeof(double));
+    const size_t tab = (size_t)std::max<int64_t>(g->NI, 1) * Lp * sizeof(double);
     double* mu = (double*)grab(tab);
     double* gam = (double*)grab(tab);
-    double* kap = (double*)grab(tab);
     double* sig = (double*)grab((size_t)L * g->E * 4 * sizeof(double));
     double* ops = (double*)grab((size_t)L * grf::pcg_table_doubles(g->dev) * sizeof(double));
-    if (!dcI || !dcL || !mu || !gam || !kap || !sig || !ops) {
+    if (!dcI || !dcL || !mu || !gam || !sig || !ops) {
         for (auto& b : p->blocks) g->alloc.put(b.p, b.bytes, st);
         return fail(GRF_ENOMEM, "plan tables (%.1f MB) could not be allocated",
-                    (double)(3 * (size_t)g->NI * L * 8 + (size_t)L * g->E * 32) / 1e6);
+                    (double)(2 * tab + (size_t)L * g->E * 32) / 1e6);
     }
     CUDA_TRY(cudaMemcpyAsync(dcI, cI.data(), L * sizeof(double), cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(dcL, cL.data(), L * sizeof(double), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dcL, cL.data(), Lp * sizeof(double), cudaMemcpyHostToDevice, st));
     p->dev.L = (int32_t)L;
+    p->dev.Lp = Lp;
+    p->dev.TL = TL;
+    p->dev.rounds = rounds;
     p->dev.kappa = kappa;
     p->dev.cI = dcI;
     p->dev.cL = dcL;
     p->dev.mu = mu;
     p->dev.gam = gam;
-    p->dev.kap = kap;
     p->dev.sig = sig;
     p->dev.ops = ops;
     CUDA_TRY(g->timed(GRF_K_EDGE_SETUP, st, [&] {
@@ -290,9 +290,6 @@ grf_status check_kernel_limits(const grf_graph* g) {
     if (!grf::pcg_supported(g->dev))
         return fail(GRF_EUNSUPPORTED, "graph has %lld vertices; this build's shared-memory PCG handles <= %d",
                     (long long)g->V, grf::pcg_max_vertices());
-    if (g->dev.max_m > grf::recover_max_interior())
-        return fail(GRF_EUNSUPPORTED, "an edge has %d interior nodes; recovery kernel handles <= %d",
-                    g->dev.max_m, grf::recover_max_interior());
     return GRF_OK;
 }
 
@@ -313,7 +310,7 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
         return fail(GRF_ENOMEM, "workspace too small: %zu < %zu bytes", ws_bytes, w.total);
     }
     char* base = static_cast<char*>(ws);
-    int64_t launches = 3;
+    int64_t launches = 4;
     if (gen) {
         double* Wd = reinterpret_cast<double*>(base + w.w);
         cudaError_t ne = g->timed(GRF_K_NOISE, st, [&] { grf::launch_noise(g->dev, seed, S, Wd, st); });
@@ -322,7 +319,7 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
             return fail(GRF_ECUDA, "noise launch: %s", cudaGetErrorString(ne));
         }
         W = Wd;
-        launches = 4;
+        launches = 5;
     }
     double* ends = reinterpret_cast<double*>(base + w.ends);
     double* uG = reinterpret_cast<double*>(base + w.ug);
@@ -338,14 +335,15 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
     grf_status rc = GRF_OK;
     cudaError_t le = cudaSuccess;
     cudaError_t ce = g->timed(GRF_K_CONDENSE, st, [&] {
-        le = grf::launch_condense(g->dev, p->dev, S, W, ends, grf::make_work_queue(g->dev, S, counters), st);
+        le = grf::launch_condense(g->dev, p->dev, S, W, ends, counters, st);
     });
     if (ce == cudaSuccess) ce = le;
     if (ce == cudaSuccess)
         ce = g->timed(GRF_K_PCG, st, [&] { grf::launch_pcg(g->dev, p->dev, S, prm, W, ends, uG, iters, relres, st); });
     if (ce == cudaSuccess)
         ce = g->timed(GRF_K_RECOVER, st, [&] {
-            le = grf::launch_recover(g->dev, p->dev, S, W, u, uG, grf::make_work_queue(g->dev, S, counters + 1), st);
+            le = grf::launch_recover(g->dev, p->dev, S, W, u, uG, counters + 1, st);
+            if (le == cudaSuccess) le = grf::launch_vertex_sum(g->dev, p->dev, S, uG, u, st);
         });
     if (ce == cudaSuccess) ce = le;
     if (ce != cudaSuccess) rc = fail(GRF_ECUDA, "kernel launch failed: %s", cudaGetErrorString(ce));

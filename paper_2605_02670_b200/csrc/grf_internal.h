@@ -38,10 +38,12 @@ struct DevPlan {
     int32_t L = 0;                    // nodes in this plan's range
     double kappa = 0.0;
     const double* cI = nullptr;       // [L]
-    const double* cL = nullptr;       // [L]
-    double* mu = nullptr;             // [NI * L] Thomas multipliers  b/d'_{t-1}, layout [(off_e + t) * L + l]
-    double* gam = nullptr;            // [NI * L] diag of A_II^{-1}: 1/(d'_t + d'_{m+1-t} - a)
-    double* kap = nullptr;            // [NI * L] -gam_t * mu_t
+    const double* cL = nullptr;       // [Lp] (zero for l >= L)
+    int32_t Lp = 0;                   // padded node row of the Thomas tables (sweep_impl.cuh tiling)
+    int32_t TL = 0;                   // nodes per thread of the sweep kernels
+    int32_t rounds = 0;               // node rounds: Lp = rounds * 32 * TL
+    double* mu = nullptr;             // [NI * Lp] Thomas multipliers  b/d'_{t-1}, layout [(off_e + t) * Lp + l]
+    double* gam = nullptr;            // [NI * Lp] diag of A_II^{-1}: 1/(d'_t + d'_{m+1-t} - a); 0 for l >= L
     double* sig = nullptr;            // [L * E * 4]: (s_d, s_o, p_d, p_o) local Schur + its inverse
     double* ops = nullptr;            // [L * (3V + 4E)]: per-node CSR tables of S and M^{-1} (pcg.cu)
 };
@@ -54,38 +56,32 @@ struct PcgParams {
     int32_t debug_nowrite = 0;   // experiments only (GRF_DEBUG_NOWRITE)
 };
 
-// Work queue of (edge, sample chunk) items shared by K3 and K5: items are handed out
-// longest edge first through an atomic counter (reset by the launcher).
-struct WorkQueue {
-    int32_t* counter = nullptr;       // device int, zeroed before each launch
-    int32_t samples_per_item = 0;
-    int32_t chunks = 0;               // sample chunks per edge
-    int32_t n_items = 0;              // E * chunks
-};
-
 // K1  noise (noise.cu): W[s*N + i] = sqrt(M_L,ii) z(seed + s, i)
 void launch_noise(const DevGraph& g, uint64_t seed, int64_t n_samples, double* W, cudaStream_t st);
 // K2  per-(node, edge) Thomas pivots + local Schur blocks (edge_setup.cu)
 void launch_edge_setup(const DevGraph& g, DevPlan& p, cudaStream_t st);
 // K3  Thomas end values per (sample, edge, end, node) (sweep.cu): ends[((s*E + e)*2 + end)*L + l]
+// (items = (edge, sample tile), handed out longest edge first through the device counter)
 cudaError_t launch_condense(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W,
-                            double* ends, WorkQueue wq, cudaStream_t st);
+                            double* ends, int32_t* counter, cudaStream_t st);
 // K4  batched NN-PCG on the vertex Schur systems (pcg.cu): g from (W, ends), u_G -> uG[(s*V + v)*L + l]
 void launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* W,
                 const double* ends, double* uG, int32_t* iters, double* relres, cudaStream_t st);
 // K5  Thomas recovery + accumulation over nodes (sweep.cu): u[s*N + dof] from W and u_G
 cudaError_t launch_recover(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W, double* u,
-                           const double* uG, WorkQueue wq, cudaStream_t st);
+                           const double* uG, int32_t* counter, cudaStream_t st);
+// K5b vertex values u_v = sum_l u_G^{(l)}(v) (sweep.cu)
+cudaError_t launch_vertex_sum(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* uG, double* u,
+                              cudaStream_t st);
+// node tiling of the Thomas tables for L nodes: Lp = rounds * 32 * TL (sweep.cu)
+void plan_tiling(int32_t L, int32_t* Lp, int32_t* tl, int32_t* rounds);
 
 // K2b per-node CSR operator tables for K4 (pcg.cu)
 void launch_pcg_tables(const DevGraph& g, const DevPlan& p, cudaStream_t st);
 size_t pcg_table_doubles(const DevGraph& g);
 bool pcg_supported(const DevGraph& g);
 
-WorkQueue make_work_queue(const DevGraph& g, int64_t n_samples, int32_t* counter);
 size_t pcg_smem_bytes(const DevGraph& g);
 int32_t pcg_max_vertices();
-int32_t recover_max_interior();
-int32_t max_nodes_per_block();
 
 }  // namespace grf

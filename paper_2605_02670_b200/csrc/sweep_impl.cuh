@@ -1,0 +1,534 @@
+// K3 (condense) and K5 (recover + quadrature sum): the per-edge Thomas work of PAPER.md
+// P187-239 and P300-324, batched over (quadrature node l) x (sample s) x (edge e).
+//
+// For one edge, node l and right-hand side f (length m), the interior block
+// A_II = tridiag(b, a, b) (Toeplitz) is eliminated from both ends with the
+// paper's Thomas multipliers (P187-221):
+//   left  sweep:  Y_0 = f_0,      Y_t = f_t - mu_t Y_{t-1},       mu_t = b / d'_{t-1}, mu_0 = 0
+//   right sweep:  Z_0 = f_{m-1},  Z_t = f_{m-1-t} - mu_t Z_{t-1}  (same pivots: A_II persymmetric)
+// and the Thomas solution is the twisted-factorisation combination of the two sweeps
+//   (A_II^{-1} f)_i = g_i (Y_i + Z_{m-1-i} - f_i),   g_i = 1 / (d'_i + d'_{m-1-i} - a)
+// (equal, up to rounding, to forward + back substitution P215-228: both are exact LU-type
+// eliminations of the same system).  Because Y_i - f_i = -mu_i Y_{i-1}, position i receives
+// -g_i mu_i Y_{i-1} from the left sweep (at step i) and g_i Z (from the right sweep, at step
+// m-1-i; g is symmetric, so step t uses g_t for both).  No intermediate vector is stored.
+//
+//   K3 condense (f = W_I):  w_1 = g_0 Z_{m-1},  w_m = g_0 Y_{m-1}   -> ends[((s*E+e)*2+end)*L + l]
+//   K5 recover  (f = W_I + (c_L/h_e)(u_left e_1 + u_right e_m), P306-311):
+//                           u_i = sum_l (A_II^{(l)})^{-1} f^{(l)}     -> u[s*N + off + i]
+//
+// Mapping (register tiles).  A CTA works on one item = (edge e, tile of CS samples) and on
+// all quadrature nodes, in `rounds` node rounds of 32*TL nodes.  Its threads form a
+// 32 (l-threads) x NST (s-threads) grid; each thread carries TL nodes x TS samples x
+// 2 chains in registers, so every staged coefficient feeds TS samples and every staged
+// noise value feeds TL nodes.  A warp is LW l-lanes x (32/LW) s-lanes (lane = sl*LW + ll);
+// there are NWL = 32/LW l-warps and NWS s-warps.  l-thread lt owns the node pairs
+// (2 lt + 64 q, +1), q < TL/2, and for odd TL the node 64 (TL/2) + lt, so a warp's
+// coefficient loads are conflict-free LDS.128 broadcasts over its s-lanes.
+//
+// Staging.  Per block of IB steps the node-minor tables mu, g [(off_e + t) * Lp + l] are
+// brought into shared memory by the bulk-copy engine (cp.async.bulk + mbarrier transaction
+// count; one thread issues), and the noise of the CTA's samples by per-lane cp.async;
+// both double buffered, one __syncthreads per block.
+//
+// Recover sum over l.  Per step each thread has 2*TS partial sums (left/right x samples)
+// over its TL nodes; a shuffle reduce-scatter over the warp's LW l-lanes leaves one value
+// per lane, which goes to a per-block partial buffer [IB][NWL][2][CS]; after the next
+// barrier the partials are folded over the NWL l-warps in fixed order into an output tile
+// [CS][m|1] kept in shared memory for the whole item (or, for edges too long for the tile,
+// straight into u with read-add-write).  Every sum has a fixed order: results are
+// bitwise reproducible for a given launch shape.
+#pragma once
+
+#include <cuda_pipeline.h>
+
+#include "grf_internal.h"
+
+namespace grf {
+namespace sweep {
+
+constexpr int IB = 8;          // steps per staging block
+constexpr int NLT = 32;        // l-threads per CTA: a node round is 32 * TL nodes
+constexpr size_t SMEM_MAX = 227 * 1024;
+
+struct Args {
+    DevGraph g;
+    int32_t L, Lp;          // nodes; padded table row (multiple of 32 * TL * rounds)
+    int32_t rounds;         // node rounds (Lp = rounds * 32 * TL)
+    const double* cL;       // [Lp] c_L per node (zero padded)
+    const double* mu;       // [(off + t) * Lp + l]
+    const double* gam;      // [(off + t) * Lp + l]
+    int64_t S;
+    const double* W;        // [s * N + dof]
+    double* out;            // condense: ends; recover: u [s * N + dof]
+    const double* uG;       // recover: [(s * V + v) * L + l]
+    int32_t* counter;       // work-queue counter (zeroed by the launcher)
+    int32_t chunks;         // sample tiles per edge
+    int32_t n_items;        // E * chunks
+    int32_t nws;            // s-warps per CTA (blockDim.x = 32 * NWL * nws)
+    int32_t tile_ms;        // recover: max (m | 1) the shared-memory output tile holds (0: none)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// global -> shared bulk copy (TMA engine, no tensor map); bytes multiple of 16, both 16B aligned
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int TL, int TS, int LW, bool REC>
+struct Cfg {
+    static constexpr int NWL = 32 / LW;      // l-warps
+    static constexpr int SLW = 32 / LW;      // s-lanes per warp
+    static constexpr int NV = 2 * TS;        // partial sums per thread per step (recover)
+    static constexpr int NTAB = REC ? 2 : 1; // mu (, g)
+    static constexpr int RN = NLT * TL;      // nodes per round
+    static_assert(LW >= NV || !REC, "the reduce-scatter needs LW >= 2 TS");
+    // shared memory layout (bytes), cs = samples per CTA item
+    static size_t coef_bytes() { return (size_t)2 * NTAB * IB * RN * sizeof(double); }
+    static size_t w_bytes(int cs) { return (size_t)2 * IB * 2 * cs * sizeof(double); }
+    static size_t part_bytes(int cs) { return REC ? (size_t)2 * IB * NWL * 2 * cs * sizeof(double) : 0; }
+    static size_t fixed_bytes(int cs) { return 64 + coef_bytes() + w_bytes(cs) + part_bytes(cs); }
+};
+
+template <int TL, int TS, int LW, bool REC>
+__global__ void __launch_bounds__(256) sweep_kernel(Args A) {
+    using C = Cfg<TL, TS, LW, REC>;
+    constexpr int NWL = C::NWL, SLW = C::SLW, NV = C::NV, NTAB = C::NTAB, RN = C::RN;
+    constexpr int NP = TL / 2;               // node pairs per thread
+    constexpr bool ODD = (TL & 1) != 0;
+    const int nthreads = blockDim.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ll = lane % LW, sl = lane / LW;
+    const int lw = warp % NWL, sw = warp / NWL;
+    const int lt = lw * LW + ll;             // l-thread 0..31
+    const int CS = A.nws * SLW * TS;         // samples per item
+    const int st0 = (sw * SLW + sl) * TS;    // this thread's first sample within the item
+    const DevGraph& g = A.g;
+    const int64_t N = g.N;
+    const int L = A.L, Lp = A.Lp;
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);           // [2]
+    int* item_sh = reinterpret_cast<int*>(smem_raw + 16);
+    double* coef = reinterpret_cast<double*>(smem_raw + 64);         // [2][NTAB][IB][RN]
+    double* wbuf = coef + 2 * NTAB * IB * RN;                        // [2][IB][2][CS]
+    double* part = wbuf + 2 * IB * 2 * CS;                           // [2][IB][NWL][2][CS] (REC)
+    double* otile = part + (REC ? 2 * IB * NWL * 2 * CS : 0);        // [CS][tile_ms] (REC)
+
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t phases = 0u;  // bit b: parity of the next completion of bar[b]
+
+    // node slot (within a round) of this thread's node n (0..TL-1)
+    auto slot = [&](int n) -> int { return (n < 2 * NP) ? (2 * lt + 64 * (n >> 1) + (n & 1)) : (64 * NP + lt); };
+
+    for (;;) {
+        if (tid == 0) *item_sh = atomicAdd(A.counter, 1);
+        __syncthreads();
+        const int it = *item_sh;
+        __syncthreads();
+        if (it >= A.n_items) break;
+        const int e = g.edge_order[it / A.chunks];
+        const int64_t c0 = (int64_t)(it % A.chunks) * CS;
+        const int m = g.m[e];
+        const int64_t off = g.off[e];
+        const double h = g.h[e];
+        const int vu = g.eu[e], vv = g.ev[e];
+        const int ms = m | 1;
+        const bool in_tile = REC && ms <= A.tile_ms;
+        // this thread's samples (clamped for loads; writes check s < S)
+        int64_t sidx[TS];
+#pragma unroll
+        for (int j = 0; j < TS; ++j) {
+            const int64_t s = c0 + st0 + j;
+            sidx[j] = s < A.S ? s : A.S - 1;
+        }
+
+        if (m == 0) {
+            if (!REC) {  // no interior: zero end values
+                for (int x = tid; x < CS * 2 * L; x += nthreads) {
+                    const int s = x / (2 * L), r = x % (2 * L);
+                    if (c0 + s < A.S) A.out[((c0 + s) * g.E + e) * 2 * (int64_t)L + r] = 0.0;
+                }
+            }
+            continue;
+        }
+        const int nblk = (m + IB - 1) / IB;
+
+        for (int rd = 0; rd < A.rounds; ++rd) {
+            const int rb = rd * RN;  // first node of the round
+            double Y[TL][TS], Z[TL][TS];
+            if (REC) {
+                // boundary rows (P310): f_0 += (c_L/h) u_left, f_{m-1} += (c_L/h) u_right; both
+                // enter the chains at step 0 (mu_0 = 0), so preload beta*u into the chain registers
+#pragma unroll
+                for (int n = 0; n < TL; ++n) {
+                    const int l = rb + slot(n);
+                    const bool ok = l < L;
+                    const double beta = ok ? A.cL[l] / h : 0.0;
+#pragma unroll
+                    for (int j = 0; j < TS; ++j) {
+                        const double ul = ok ? A.uG[(sidx[j] * g.V + vu) * (int64_t)L + l] : 0.0;
+                        const double ur = ok ? A.uG[(sidx[j] * g.V + vv) * (int64_t)L + l] : 0.0;
+                        Y[n][j] = beta * (m == 1 ? ul + ur : ul);
+                        Z[n][j] = beta * (m == 1 ? ul + ur : ur);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int n = 0; n < TL; ++n)
+#pragma unroll
+                    for (int j = 0; j < TS; ++j) Y[n][j] = Z[n][j] = 0.0;
+            }
+
+            auto stage = [&](int b) {
+                const int t0 = b * IB;
+                const int nb = (m - t0) < IB ? (m - t0) : IB;
+                const int buf = b & 1;
+                if (tid == 0) {
+                    fence_proxy_async();
+                    const uint32_t row = RN * sizeof(double);
+                    mbar_expect_tx(&bar[buf], (uint32_t)(NTAB * nb) * row);
+#pragma unroll
+                    for (int tb = 0; tb < NTAB; ++tb) {
+                        const double* tab = (tb == 0 ? A.mu : A.gam) + (off + t0) * (int64_t)Lp + rb;
+                        double* dst = coef + (buf * NTAB + tb) * IB * RN;
+                        if (A.rounds == 1) {
+                            bulk_g2s(dst, tab, (uint32_t)nb * row, &bar[buf]);
+                        } else {
+                            for (int tt = 0; tt < nb; ++tt) bulk_g2s(dst + tt * RN, tab + tt * (int64_t)Lp, row, &bar[buf]);
+                        }
+                    }
+                }
+                // noise of the item's samples at the left positions t0.. and right positions m-1-t0..
+                double* wb = wbuf + buf * IB * 2 * CS;
+                for (int x = tid; x < IB * 2 * CS; x += nthreads) {
+                    const int tt = x % IB, r = x / IB;
+                    const int s = r % CS, side = r / CS;
+                    if (tt < nb) {
+                        int64_t sg = c0 + s;
+                        if (sg >= A.S) sg = A.S - 1;
+                        const int pos = side ? (m - 1 - t0 - tt) : (t0 + tt);
+                        __pipeline_memcpy_async(wb + (tt * 2 + side) * CS + s, A.W + sg * N + off + pos, 8);
+                    }
+                }
+                __pipeline_commit();
+            };
+
+            // fold block b's partial sums (over the NWL l-warps, fixed order) into the output.
+            // Step t adds its left value to position t and its right value to position m-1-t;
+            // a thread takes step t together with its mirror step m-1-t when both lie in this
+            // block, so no two threads touch one position within a fold.
+            auto fold = [&](int b) {
+                const int t0 = b * IB;
+                const int nb = (m - t0) < IB ? (m - t0) : IB;
+                const double* pb = part + (b & 1) * IB * NWL * 2 * CS;
+                auto psum = [&](int tt, int side, int s) {
+                    double v = 0.0;
+#pragma unroll
+                    for (int q = 0; q < NWL; ++q) v += pb[((tt * NWL + q) * 2 + side) * CS + s];
+                    return v;
+                };
+                auto put = [&](int s, int p, double v, bool first) {
+                    if (in_tile) {
+                        double* d = otile + s * ms + p;
+                        *d = first ? v : *d + v;
+                    } else if (c0 + s < A.S) {
+                        double* d = A.out + (c0 + s) * N + off + p;
+                        *d = first ? v : *d + v;
+                    }
+                };
+                for (int x = tid; x < nb * CS; x += nthreads) {
+                    const int s = x % CS, tt = x / CS;
+                    const int t = t0 + tt, tm = m - 1 - t;
+                    const bool mirror_here = tm >= t0 && tm < t0 + nb;
+                    if (mirror_here && tm < t) continue;  // handled with the mirror step
+                    const double vl = psum(tt, 0, s), vr = psum(tt, 1, s);
+                    if (tm == t) {
+                        put(s, t, vl + vr, rd == 0);
+                    } else if (mirror_here) {  // both visits of positions t and tm are in this block
+                        const int ttm = tm - t0;
+                        put(s, t, vl + psum(ttm, 1, s), rd == 0);
+                        put(s, tm, vr + psum(ttm, 0, s), rd == 0);
+                    } else {
+                        const bool first = rd == 0 && t < tm;  // first visit of both t and tm is at min(t, tm)
+                        put(s, t, vl, first);
+                        put(s, tm, vr, first);
+                    }
+                }
+            };
+
+            stage(0);
+            for (int b = 0; b < nblk; ++b) {
+                const int t0 = b * IB;
+                const int nb = (m - t0) < IB ? (m - t0) : IB;
+                const int buf = b & 1;
+                mbar_wait(&bar[buf], (phases >> buf) & 1u);
+                phases ^= 1u << buf;
+                __pipeline_wait_prior(0);
+                __syncthreads();  // block b staged and visible; block b-1 buffers and partials free/complete
+                if (b + 1 < nblk) stage(b + 1);
+                if (REC && b > 0) fold(b - 1);
+                const double* cmu = coef + (buf * NTAB + 0) * IB * RN;
+                const double* cga = coef + (buf * NTAB + 1) * IB * RN;
+                const double* wb = wbuf + buf * IB * 2 * CS;
+                double* pb = part + buf * IB * NWL * 2 * CS;
+                for (int tt = 0; tt < nb; ++tt) {
+                    const int t = t0 + tt;
+                    double wl[TS], wr[TS];
+#pragma unroll
+                    for (int j = 0; j < TS; j += 2) {
+                        if (TS == 1) {
+                            wl[0] = wb[(tt * 2 + 0) * CS + st0];
+                            wr[0] = wb[(tt * 2 + 1) * CS + st0];
+                        } else {
+                            const double2 a = *reinterpret_cast<const double2*>(wb + (tt * 2 + 0) * CS + st0 + j);
+                            const double2 c = *reinterpret_cast<const double2*>(wb + (tt * 2 + 1) * CS + st0 + j);
+                            wl[j] = a.x;
+                            wl[j + 1] = a.y;
+                            wr[j] = c.x;
+                            wr[j + 1] = c.y;
+                        }
+                    }
+                    const double* rmu = cmu + tt * RN;
+                    const double* rga = cga + tt * RN;
+                    if (!REC) {
+#pragma unroll
+                        for (int q = 0; q < NP; ++q) {
+                            const double2 m2 = *reinterpret_cast<const double2*>(rmu + 2 * lt + 64 * q);
+#pragma unroll
+                            for (int j = 0; j < TS; ++j) {
+                                Y[2 * q][j] = fma(-m2.x, Y[2 * q][j], wl[j]);
+                                Z[2 * q][j] = fma(-m2.x, Z[2 * q][j], wr[j]);
+                                Y[2 * q + 1][j] = fma(-m2.y, Y[2 * q + 1][j], wl[j]);
+                                Z[2 * q + 1][j] = fma(-m2.y, Z[2 * q + 1][j], wr[j]);
+                            }
+                        }
+                        if (ODD) {
+                            const double mu = rmu[64 * NP + lt];
+#pragma unroll
+                            for (int j = 0; j < TS; ++j) {
+                                Y[TL - 1][j] = fma(-mu, Y[TL - 1][j], wl[j]);
+                                Z[TL - 1][j] = fma(-mu, Z[TL - 1][j], wr[j]);
+                            }
+                        }
+                    } else {
+                        double aL[TS], aR[TS];
+#pragma unroll
+                        for (int j = 0; j < TS; ++j) aL[j] = aR[j] = 0.0;
+                        if (t == 0) {
+                            // mu_0 = 0: Y_0 = f_0 (W + preloaded boundary term), no left contribution
+#pragma unroll
+                            for (int n = 0; n < TL; ++n) {
+                                const double gg = rga[slot(n)];
+#pragma unroll
+                                for (int j = 0; j < TS; ++j) {
+                                    Y[n][j] += wl[j];
+                                    Z[n][j] += wr[j];
+                                    aR[j] = fma(gg, Z[n][j], aR[j]);
+                                }
+                            }
+                        } else if (t == m - 1) {
+                            // last step: the left chain reaches position m-1 (f += beta u_right), the
+                            // right chain position 0 (f += beta u_left)
+#pragma unroll
+                            for (int n = 0; n < TL; ++n) {
+                                const int sn = slot(n);
+                                const int l = rb + sn;
+                                const bool ok = l < L;
+                                const double beta = ok ? A.cL[l] / h : 0.0;
+                                const double mu = rmu[sn], gg = rga[sn];
+                                const double nk = gg * mu;
+#pragma unroll
+                                for (int j = 0; j < TS; ++j) {
+                                    const double ul = ok ? A.uG[(sidx[j] * g.V + vu) * (int64_t)L + l] : 0.0;
+                                    const double ur = ok ? A.uG[(sidx[j] * g.V + vv) * (int64_t)L + l] : 0.0;
+                                    aL[j] = fma(-nk, Y[n][j], aL[j]);
+                                    Y[n][j] = fma(beta, ur, fma(-mu, Y[n][j], wl[j]));
+                                    Z[n][j] = fma(beta, ul, fma(-mu, Z[n][j], wr[j]));
+                                    aR[j] = fma(gg, Z[n][j], aR[j]);
+                                }
+                            }
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < NP; ++q) {
+                                const double2 m2 = *reinterpret_cast<const double2*>(rmu + 2 * lt + 64 * q);
+                                const double2 g2 = *reinterpret_cast<const double2*>(rga + 2 * lt + 64 * q);
+                                const double k0 = g2.x * m2.x, k1 = g2.y * m2.y;
+#pragma unroll
+                                for (int j = 0; j < TS; ++j) {
+                                    aL[j] = fma(-k0, Y[2 * q][j], aL[j]);
+                                    Y[2 * q][j] = fma(-m2.x, Y[2 * q][j], wl[j]);
+                                    Z[2 * q][j] = fma(-m2.x, Z[2 * q][j], wr[j]);
+                                    aR[j] = fma(g2.x, Z[2 * q][j], aR[j]);
+                                    aL[j] = fma(-k1, Y[2 * q + 1][j], aL[j]);
+                                    Y[2 * q + 1][j] = fma(-m2.y, Y[2 * q + 1][j], wl[j]);
+                                    Z[2 * q + 1][j] = fma(-m2.y, Z[2 * q + 1][j], wr[j]);
+                                    aR[j] = fma(g2.y, Z[2 * q + 1][j], aR[j]);
+                                }
+                            }
+                            if (ODD) {
+                                const double mu = rmu[64 * NP + lt], gg = rga[64 * NP + lt];
+                                const double nk = gg * mu;
+#pragma unroll
+                                for (int j = 0; j < TS; ++j) {
+                                    aL[j] = fma(-nk, Y[TL - 1][j], aL[j]);
+                                    Y[TL - 1][j] = fma(-mu, Y[TL - 1][j], wl[j]);
+                                    Z[TL - 1][j] = fma(-mu, Z[TL - 1][j], wr[j]);
+                                    aR[j] = fma(gg, Z[TL - 1][j], aR[j]);
+                                }
+                            }
+                        }
+                        // reduce-scatter of the NV = 2 TS partials over the warp's LW l-lanes:
+                        // the high l-lane bits split the values, the low ones all-reduce
+                        double v[NV];
+#pragma unroll
+                        for (int j = 0; j < TS; ++j) {
+                            v[j] = aL[j];
+                            v[TS + j] = aR[j];
+                        }
+                        int cnt = NV;
+#pragma unroll
+                        for (int o = LW / 2; o >= 1; o >>= 1) {
+                            if (cnt > 1) {
+                                const int half = cnt / 2;
+                                const bool up = (ll & o) != 0;
+#pragma unroll
+                                for (int i = 0; i < NV / 2; ++i) {
+                                    if (i < half) {
+                                        const double send = up ? v[i] : v[i + half];
+                                        const double keep = up ? v[i + half] : v[i];
+                                        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                                    }
+                                }
+                                cnt = half;
+                            } else {
+                                v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+                            }
+                        }
+                        constexpr int SH = (LW / NV) > 1 ? ((LW / NV) == 2 ? 1 : ((LW / NV) == 4 ? 2 : ((LW / NV) == 8 ? 3 : 4))) : 0;
+                        if ((ll & ((1 << SH) - 1)) == 0) {
+                            // lane keeps value index idx = bit-reverse-free order: the scatter levels
+                            // peel the index from its high bit down
+                            const int idx = ll >> SH;
+                            const int side = idx / TS, j = idx % TS;
+                            pb[((tt * NWL + lw) * 2 + side) * CS + st0 + j] = v[0];
+                        }
+                    }
+                }
+            }
+            if (REC) {
+                __syncthreads();
+                fold(nblk - 1);
+            } else {
+                // w_1 = g_0 Z (right sweep end, position 0), w_m = g_0 Y (left sweep end); g_0 = g_{m-1}
+#pragma unroll
+                for (int n = 0; n < TL; ++n) {
+                    const int l = rb + slot(n);
+                    if (l < L) {
+                        const double g0 = A.gam[off * (int64_t)Lp + l];
+#pragma unroll
+                        for (int j = 0; j < TS; ++j) {
+                            const int64_t s = c0 + st0 + j;
+                            if (s < A.S) {
+                                double* o = A.out + (s * g.E + e) * 2 * (int64_t)L + l;
+                                o[0] = g0 * Z[n][j];
+                                o[L] = g0 * Y[n][j];
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        if (in_tile) {
+            __syncthreads();
+            for (int x = tid; x < CS * m; x += nthreads) {
+                const int s = x / m, p = x - s * m;
+                if (c0 + s < A.S) A.out[(c0 + s) * N + off + p] = otile[s * ms + p];
+            }
+        }
+    }
+}
+
+// Launch shape for one instance: threads = 32 * NWL * nws; items = E * ceil(S / CS).
+template <int TL, int TS, int LW, bool REC>
+cudaError_t launch(Args a, cudaStream_t st) {
+    using C = Cfg<TL, TS, LW, REC>;
+    const int cs = a.nws * C::SLW * TS;
+    a.chunks = (int32_t)((a.S + cs - 1) / cs);
+    a.n_items = a.g.E * a.chunks;
+    const int threads = 32 * C::NWL * a.nws;
+    size_t smem = C::fixed_bytes(cs);
+    a.tile_ms = 0;
+    if (REC) {
+        // the output tile holds edges with (m | 1) <= tile_ms; size it for the longest edge if it fits
+        const int want = a.g.max_m | 1;
+        const size_t room = SMEM_MAX > smem ? SMEM_MAX - smem : 0;
+        const int fit = (int)(room / ((size_t)cs * sizeof(double)));
+        a.tile_ms = want <= fit ? want : ((fit - 1) | 1);
+        if (a.tile_ms < 1) a.tile_ms = 0;
+        smem += (size_t)cs * a.tile_ms * sizeof(double);
+    }
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<TL, TS, LW, REC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(a.counter, 0, sizeof(int32_t), st);
+    if (e != cudaSuccess) return e;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<TL, TS, LW, REC>, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    int blocks = 148 * per_sm;
+    if (blocks > a.n_items) blocks = a.n_items;
+    sweep_kernel<TL, TS, LW, REC><<<blocks, threads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+// Sample mapping of one launch (the node tile TL is fixed by the plan's Lp):
+//   variant 0: TS = 4, LW = 8  (warp = 8 l-lanes x 4 s-lanes = 16 samples), nws = 2 (CS = 32) or 1 (CS = 16)
+//   variant 1: TS = 1, LW = 32 (warp = 32 l-lanes x 1 sample), nws = 1 (CS = 1): few samples
+template <int TL, bool REC>
+cudaError_t launch_tl(Args a, cudaStream_t st) {
+    if (a.S >= 9) {
+        a.nws = a.S >= 17 ? 2 : 1;
+        return launch<TL, 4, 8, REC>(a, st);
+    }
+    a.nws = 1;
+    return launch<TL, 1, 32, REC>(a, st);
+}
+
+}  // namespace sweep
+}  // namespace grf
