@@ -5,9 +5,12 @@
 
 namespace grf {
 namespace sweep {
-cudaError_t condense_tl(int tl, Args a, cudaStream_t st);
-cudaError_t recover_tl_a(int tl, Args a, cudaStream_t st);
-cudaError_t recover_tl_b(int tl, Args a, cudaStream_t st);
+cudaError_t launch_c0(int tl, Args a, cudaStream_t st);
+cudaError_t launch_c1(int tl, Args a, cudaStream_t st);
+cudaError_t launch_c2(int tl, Args a, cudaStream_t st);
+cudaError_t launch_r0(int tl, Args a, cudaStream_t st);
+cudaError_t launch_r1(int tl, Args a, cudaStream_t st);
+cudaError_t launch_r2(int tl, Args a, cudaStream_t st);
 }  // namespace sweep
 
 namespace {
@@ -43,13 +46,22 @@ void plan_tiling(int32_t L, int32_t* Lp, int32_t* tl, int32_t* rounds) {
 
 cudaError_t launch_condense(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W, double* ends,
                             int32_t* counter, cudaStream_t st) {
-    return sweep::condense_tl(p.TL, make_args(g, p, n_samples, W, ends, nullptr, counter), st);
+    const sweep::Args a = make_args(g, p, n_samples, W, ends, nullptr, counter);
+    switch (sweep::variant_for(n_samples)) {
+        case sweep::V2: return sweep::launch_c2(p.TL, a, st);
+        case sweep::V1: return sweep::launch_c1(p.TL, a, st);
+        default: return sweep::launch_c0(p.TL, a, st);
+    }
 }
 
 cudaError_t launch_recover(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W, double* u,
                            const double* uG, int32_t* counter, cudaStream_t st) {
-    sweep::Args a = make_args(g, p, n_samples, W, u, uG, counter);
-    return p.TL <= 6 ? sweep::recover_tl_a(p.TL, a, st) : sweep::recover_tl_b(p.TL, a, st);
+    const sweep::Args a = make_args(g, p, n_samples, W, u, uG, counter);
+    switch (sweep::variant_for(n_samples)) {
+        case sweep::V2: return sweep::launch_r2(p.TL, a, st);
+        case sweep::V1: return sweep::launch_r1(p.TL, a, st);
+        default: return sweep::launch_r0(p.TL, a, st);
+    }
 }
 
 }  // namespace grf

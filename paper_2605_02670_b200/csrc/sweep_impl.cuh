@@ -105,34 +105,43 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-template <int TL, int TS, int LW, bool REC>
+// Compile-time shape of one kernel instance.
+template <int TL, int TS, int LW, int NWS, bool REC>
 struct Cfg {
-    static constexpr int NWL = 32 / LW;      // l-warps
-    static constexpr int SLW = 32 / LW;      // s-lanes per warp
-    static constexpr int NV = 2 * TS;        // partial sums per thread per step (recover)
-    static constexpr int NTAB = REC ? 2 : 1; // mu (, g)
-    static constexpr int RN = NLT * TL;      // nodes per round
-    static_assert(LW >= NV || !REC, "the reduce-scatter needs LW >= 2 TS");
-    // shared memory layout (bytes), cs = samples per CTA item
-    static size_t coef_bytes() { return (size_t)2 * NTAB * IB * RN * sizeof(double); }
-    static size_t w_bytes(int cs) { return (size_t)2 * IB * 2 * cs * sizeof(double); }
-    static size_t part_bytes(int cs) { return REC ? (size_t)2 * IB * NWL * 2 * cs * sizeof(double) : 0; }
-    static size_t fixed_bytes(int cs) { return 64 + coef_bytes() + w_bytes(cs) + part_bytes(cs); }
+    static constexpr int NWL = 32 / LW;             // l-warps
+    static constexpr int SLW = 32 / LW;             // s-lanes per warp
+    static constexpr int NT = 32 * NWL * NWS;       // threads per CTA
+    static constexpr int CS = NWS * SLW * TS;       // samples per item
+    static constexpr int NTAB = REC ? 2 : 1;        // staged tables: mu (, g)
+    static constexpr int RN = NLT * TL;             // nodes per round
+    static constexpr int IBK = REC ? 8 : 16;        // steps per staging block
+    // recover with TS = 4: sample slot j of a thread is sample (j ^ sig(lane)); this makes
+    // the reduce-scatter over the 8 l-lanes select-free (see reduce_store)
+    static constexpr bool PERM = REC && TS == 4;
+    static constexpr int NC = PERM ? 2 : 1;         // staged noise copies: natural, pair-swapped
+    static constexpr size_t COEF = (size_t)2 * NTAB * IBK * RN * sizeof(double);
+    static constexpr size_t WB = (size_t)2 * IBK * 2 * NC * CS * sizeof(double);
+    static constexpr size_t PART = REC ? (size_t)2 * IBK * NWL * 2 * CS * sizeof(double) : 0;
+    static constexpr size_t FIXED = 64 + COEF + WB + PART;
+    static constexpr int WEL = IBK * 2 * NC * CS;   // staged noise elements per block
+    static_assert(REC ? ((TS == 4 && LW == 8) || (TS == 1 && LW == 32)) : true, "recover reduce shapes");
+    static_assert((CS & (CS - 1)) == 0, "CS must be a power of two");
 };
 
-template <int TL, int TS, int LW, bool REC>
-__global__ void __launch_bounds__(256) sweep_kernel(Args A) {
-    using C = Cfg<TL, TS, LW, REC>;
-    constexpr int NWL = C::NWL, SLW = C::SLW, NV = C::NV, NTAB = C::NTAB, RN = C::RN;
+template <int TL, int TS, int LW, int NWS, bool REC>
+__global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Args A) {
+    using C = Cfg<TL, TS, LW, NWS, REC>;
+    constexpr int NWL = C::NWL, SLW = C::SLW, NT = C::NT, CS = C::CS, NTAB = C::NTAB, RN = C::RN;
+    constexpr int IBK = C::IBK, NC = C::NC;
+    constexpr bool PERM = C::PERM;
     constexpr int NP = TL / 2;               // node pairs per thread
     constexpr bool ODD = (TL & 1) != 0;
-    const int nthreads = blockDim.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ll = lane % LW, sl = lane / LW;
     const int lw = warp % NWL, sw = warp / NWL;
     const int lt = lw * LW + ll;             // l-thread 0..31
-    const int CS = A.nws * SLW * TS;         // samples per item
-    const int st0 = (sw * SLW + sl) * TS;    // this thread's first sample within the item
+    const int st0 = (sw * SLW + sl) * TS;    // first sample (within the item) of this thread
+    const int sig = PERM ? (((ll & 1) << 1) | ((ll >> 1) & 1)) : 0;
     const DevGraph& g = A.g;
     const int64_t N = g.N;
     const int L = A.L, Lp = A.Lp;
@@ -140,10 +149,10 @@ __global__ void __launch_bounds__(256) sweep_kernel(Args A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);           // [2]
     int* item_sh = reinterpret_cast<int*>(smem_raw + 16);
-    double* coef = reinterpret_cast<double*>(smem_raw + 64);         // [2][NTAB][IB][RN]
-    double* wbuf = coef + 2 * NTAB * IB * RN;                        // [2][IB][2][CS]
-    double* part = wbuf + 2 * IB * 2 * CS;                           // [2][IB][NWL][2][CS] (REC)
-    double* otile = part + (REC ? 2 * IB * NWL * 2 * CS : 0);        // [CS][tile_ms] (REC)
+    double* coef = reinterpret_cast<double*>(smem_raw + 64);         // [2][NTAB][IBK][RN]
+    double* wbuf = coef + 2 * NTAB * IBK * RN;                       // [2][IBK][2][NC][CS]
+    double* part = wbuf + 2 * IBK * 2 * NC * CS;                     // [2][IBK][NWL][2][CS] (REC)
+    double* otile = part + (REC ? 2 * IBK * NWL * 2 * CS : 0);       // [CS][tile_ms] (REC)
 
     if (tid == 0) {
         mbar_init(&bar[0], 1);
@@ -170,31 +179,31 @@ __global__ void __launch_bounds__(256) sweep_kernel(Args A) {
         const int vu = g.eu[e], vv = g.ev[e];
         const int ms = m | 1;
         const bool in_tile = REC && ms <= A.tile_ms;
-        // this thread's samples (clamped for loads; writes check s < S)
-        int64_t sidx[TS];
+        int64_t sidx[TS];  // sample of slot j (clamped for loads; writes check c0 + st0 + (j ^ sig) < S)
 #pragma unroll
         for (int j = 0; j < TS; ++j) {
-            const int64_t s = c0 + st0 + j;
+            const int64_t s = c0 + st0 + (j ^ sig);
             sidx[j] = s < A.S ? s : A.S - 1;
         }
 
         if (m == 0) {
             if (!REC) {  // no interior: zero end values
-                for (int x = tid; x < CS * 2 * L; x += nthreads) {
-                    const int s = x / (2 * L), r = x % (2 * L);
+                for (int x = tid; x < CS * 2 * L; x += NT) {
+                    const int s = x / (2 * L), r = x - s * 2 * L;
                     if (c0 + s < A.S) A.out[((c0 + s) * g.E + e) * 2 * (int64_t)L + r] = 0.0;
                 }
             }
             continue;
         }
-        const int nblk = (m + IB - 1) / IB;
+        const int nblk = (m + IBK - 1) / IBK;
 
         for (int rd = 0; rd < A.rounds; ++rd) {
             const int rb = rd * RN;  // first node of the round
             double Y[TL][TS], Z[TL][TS];
+            double g0[REC ? 1 : TL];
             if (REC) {
                 // boundary rows (P310): f_0 += (c_L/h) u_left, f_{m-1} += (c_L/h) u_right; both
-                // enter the chains at step 0 (mu_0 = 0), so preload beta*u into the chain registers
+                // enter the chains at step 0 (mu_0 = 0): preload beta*u into the chain registers
 #pragma unroll
                 for (int n = 0; n < TL; ++n) {
                     const int l = rb + slot(n);
@@ -210,23 +219,26 @@ __global__ void __launch_bounds__(256) sweep_kernel(Args A) {
                 }
             } else {
 #pragma unroll
-                for (int n = 0; n < TL; ++n)
+                for (int n = 0; n < TL; ++n) {
+                    const int l = rb + slot(n);
+                    g0[n] = l < L ? A.gam[off * (int64_t)Lp + l] : 0.0;  // g_0 = g_{m-1} for the end values
 #pragma unroll
                     for (int j = 0; j < TS; ++j) Y[n][j] = Z[n][j] = 0.0;
+                }
             }
 
             auto stage = [&](int b) {
-                const int t0 = b * IB;
-                const int nb = (m - t0) < IB ? (m - t0) : IB;
+                const int t0 = b * IBK;
+                const int nb = (m - t0) < IBK ? (m - t0) : IBK;
                 const int buf = b & 1;
                 if (tid == 0) {
                     fence_proxy_async();
-                    const uint32_t row = RN * sizeof(double);
+                    constexpr uint32_t row = RN * sizeof(double);
                     mbar_expect_tx(&bar[buf], (uint32_t)(NTAB * nb) * row);
 #pragma unroll
                     for (int tb = 0; tb < NTAB; ++tb) {
                         const double* tab = (tb == 0 ? A.mu : A.gam) + (off + t0) * (int64_t)Lp + rb;
-                        double* dst = coef + (buf * NTAB + tb) * IB * RN;
+                        double* dst = coef + (buf * NTAB + tb) * IBK * RN;
                         if (A.rounds == 1) {
                             bulk_g2s(dst, tab, (uint32_t)nb * row, &bar[buf]);
                         } else {
@@ -234,16 +246,23 @@ __global__ void __launch_bounds__(256) sweep_kernel(Args A) {
                         }
                     }
                 }
-                // noise of the item's samples at the left positions t0.. and right positions m-1-t0..
-                double* wb = wbuf + buf * IB * 2 * CS;
-                for (int x = tid; x < IB * 2 * CS; x += nthreads) {
-                    const int tt = x % IB, r = x / IB;
-                    const int s = r % CS, side = r / CS;
-                    if (tt < nb) {
-                        int64_t sg = c0 + s;
-                        if (sg >= A.S) sg = A.S - 1;
-                        const int pos = side ? (m - 1 - t0 - tt) : (t0 + tt);
-                        __pipeline_memcpy_async(wb + (tt * 2 + side) * CS + s, A.W + sg * N + off + pos, 8);
+                // noise of the item's samples at left positions t0+tt and right positions m-1-t0-tt;
+                // copy c = 1 holds the samples pair-swapped (sample s ^ 1 at index s)
+                double* wb = wbuf + buf * IBK * 2 * NC * CS;
+#pragma unroll
+                for (int k = 0; k < (C::WEL + NT - 1) / NT; ++k) {
+                    const int x = tid + k * NT;
+                    if (x < C::WEL) {
+                        const int tt = x % IBK, r = x / IBK;
+                        const int s = r % CS, r2 = r / CS;
+                        const int c = r2 % NC, side = r2 / NC;
+                        if (tt < nb) {
+                            int64_t sg = c0 + (c ? (s ^ 1) : s);
+                            if (sg >= A.S) sg = A.S - 1;
+                            const int pos = side ? (m - 1 - t0 - tt) : (t0 + tt);
+                            __pipeline_memcpy_async(wb + ((tt * 2 + side) * NC + c) * CS + s, A.W + sg * N + off + pos,
+                                                    8);
+                        }
                     }
                 }
                 __pipeline_commit();
@@ -254,9 +273,9 @@ __global__ void __launch_bounds__(256) sweep_kernel(Args A) {
             // a thread takes step t together with its mirror step m-1-t when both lie in this
             // block, so no two threads touch one position within a fold.
             auto fold = [&](int b) {
-                const int t0 = b * IB;
-                const int nb = (m - t0) < IB ? (m - t0) : IB;
-                const double* pb = part + (b & 1) * IB * NWL * 2 * CS;
+                const int t0 = b * IBK;
+                const int nb = (m - t0) < IBK ? (m - t0) : IBK;
+                const double* pb = part + (b & 1) * IBK * NWL * 2 * CS;
                 auto psum = [&](int tt, int side, int s) {
                     double v = 0.0;
 #pragma unroll
@@ -272,7 +291,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(Args A) {
                         *d = first ? v : *d + v;
                     }
                 };
-                for (int x = tid; x < nb * CS; x += nthreads) {
+                for (int x = tid; x < nb * CS; x += NT) {
                     const int s = x % CS, tt = x / CS;
                     const int t = t0 + tt, tm = m - 1 - t;
                     const bool mirror_here = tm >= t0 && tm < t0 + nb;
@@ -294,8 +313,8 @@ __global__ void __launch_bounds__(256) sweep_kernel(Args A) {
 
             stage(0);
             for (int b = 0; b < nblk; ++b) {
-                const int t0 = b * IB;
-                const int nb = (m - t0) < IB ? (m - t0) : IB;
+                const int t0 = b * IBK;
+                const int nb = (m - t0) < IBK ? (m - t0) : IBK;
                 const int buf = b & 1;
                 mbar_wait(&bar[buf], (phases >> buf) & 1u);
                 phases ^= 1u << buf;
@@ -303,30 +322,35 @@ __global__ void __launch_bounds__(256) sweep_kernel(Args A) {
                 __syncthreads();  // block b staged and visible; block b-1 buffers and partials free/complete
                 if (b + 1 < nblk) stage(b + 1);
                 if (REC && b > 0) fold(b - 1);
-                const double* cmu = coef + (buf * NTAB + 0) * IB * RN;
-                const double* cga = coef + (buf * NTAB + 1) * IB * RN;
-                const double* wb = wbuf + buf * IB * 2 * CS;
-                double* pb = part + buf * IB * NWL * 2 * CS;
-                for (int tt = 0; tt < nb; ++tt) {
-                    const int t = t0 + tt;
-                    double wl[TS], wr[TS];
+                const double* cmu = coef + (buf * NTAB + 0) * IBK * RN;
+                const double* cga = coef + (buf * NTAB + 1) * IBK * RN;
+                const double* wb = wbuf + buf * IBK * 2 * NC * CS;
+
+                // noise of this thread's slots at step tt (left and right positions)
+                auto load_w = [&](int tt, double (&wl)[TS], double (&wr)[TS]) {
+                    if (TS == 1) {
+                        wl[0] = wb[(tt * 2 + 0) * NC * CS + st0];
+                        wr[0] = wb[(tt * 2 + 1) * NC * CS + st0];
+                    } else {
+                        const int cp = PERM ? (sig & 1) : 0, px = PERM ? (sig >> 1) : 0;
 #pragma unroll
-                    for (int j = 0; j < TS; j += 2) {
-                        if (TS == 1) {
-                            wl[0] = wb[(tt * 2 + 0) * CS + st0];
-                            wr[0] = wb[(tt * 2 + 1) * CS + st0];
-                        } else {
-                            const double2 a = *reinterpret_cast<const double2*>(wb + (tt * 2 + 0) * CS + st0 + j);
-                            const double2 c = *reinterpret_cast<const double2*>(wb + (tt * 2 + 1) * CS + st0 + j);
-                            wl[j] = a.x;
-                            wl[j + 1] = a.y;
-                            wr[j] = c.x;
-                            wr[j + 1] = c.y;
+                        for (int q = 0; q < TS / 2; ++q) {
+                            const int o = st0 + 2 * (q ^ px);
+                            const double2 a = *reinterpret_cast<const double2*>(wb + ((tt * 2 + 0) * NC + cp) * CS + o);
+                            const double2 c = *reinterpret_cast<const double2*>(wb + ((tt * 2 + 1) * NC + cp) * CS + o);
+                            wl[2 * q] = a.x;
+                            wl[2 * q + 1] = a.y;
+                            wr[2 * q] = c.x;
+                            wr[2 * q + 1] = c.y;
                         }
                     }
-                    const double* rmu = cmu + tt * RN;
-                    const double* rga = cga + tt * RN;
-                    if (!REC) {
+                };
+
+                if (!REC) {
+                    for (int tt = 0; tt < nb; ++tt) {
+                        double wl[TS], wr[TS];
+                        load_w(tt, wl, wr);
+                        const double* rmu = cmu + tt * RN;
 #pragma unroll
                         for (int q = 0; q < NP; ++q) {
                             const double2 m2 = *reinterpret_cast<const double2*>(rmu + 2 * lt + 64 * q);
@@ -346,109 +370,159 @@ __global__ void __launch_bounds__(256) sweep_kernel(Args A) {
                                 Z[TL - 1][j] = fma(-mu, Z[TL - 1][j], wr[j]);
                             }
                         }
-                    } else {
-                        double aL[TS], aR[TS];
+                    }
+                } else {
+                    // generic step: left chain gives -g mu Y_{t-1} to position t, right chain g Z to m-1-t
+                    auto body_mid = [&](int tt, double (&aL)[TS], double (&aR)[TS]) {
+                        double wl[TS], wr[TS];
+                        load_w(tt, wl, wr);
+                        const double* rmu = cmu + tt * RN;
+                        const double* rga = cga + tt * RN;
 #pragma unroll
                         for (int j = 0; j < TS; ++j) aL[j] = aR[j] = 0.0;
-                        if (t == 0) {
-                            // mu_0 = 0: Y_0 = f_0 (W + preloaded boundary term), no left contribution
 #pragma unroll
-                            for (int n = 0; n < TL; ++n) {
-                                const double gg = rga[slot(n)];
+                        for (int q = 0; q < NP; ++q) {
+                            const double2 m2 = *reinterpret_cast<const double2*>(rmu + 2 * lt + 64 * q);
+                            const double2 g2 = *reinterpret_cast<const double2*>(rga + 2 * lt + 64 * q);
+                            const double k0 = g2.x * m2.x, k1 = g2.y * m2.y;
 #pragma unroll
-                                for (int j = 0; j < TS; ++j) {
-                                    Y[n][j] += wl[j];
-                                    Z[n][j] += wr[j];
-                                    aR[j] = fma(gg, Z[n][j], aR[j]);
-                                }
+                            for (int j = 0; j < TS; ++j) {
+                                aL[j] = fma(-k0, Y[2 * q][j], aL[j]);
+                                Y[2 * q][j] = fma(-m2.x, Y[2 * q][j], wl[j]);
+                                Z[2 * q][j] = fma(-m2.x, Z[2 * q][j], wr[j]);
+                                aR[j] = fma(g2.x, Z[2 * q][j], aR[j]);
+                                aL[j] = fma(-k1, Y[2 * q + 1][j], aL[j]);
+                                Y[2 * q + 1][j] = fma(-m2.y, Y[2 * q + 1][j], wl[j]);
+                                Z[2 * q + 1][j] = fma(-m2.y, Z[2 * q + 1][j], wr[j]);
+                                aR[j] = fma(g2.y, Z[2 * q + 1][j], aR[j]);
                             }
-                        } else if (t == m - 1) {
-                            // last step: the left chain reaches position m-1 (f += beta u_right), the
-                            // right chain position 0 (f += beta u_left)
+                        }
+                        if (ODD) {
+                            const double mu = rmu[64 * NP + lt], gg = rga[64 * NP + lt];
+                            const double nk = gg * mu;
 #pragma unroll
-                            for (int n = 0; n < TL; ++n) {
-                                const int sn = slot(n);
-                                const int l = rb + sn;
-                                const bool ok = l < L;
-                                const double beta = ok ? A.cL[l] / h : 0.0;
-                                const double mu = rmu[sn], gg = rga[sn];
-                                const double nk = gg * mu;
+                            for (int j = 0; j < TS; ++j) {
+                                aL[j] = fma(-nk, Y[TL - 1][j], aL[j]);
+                                Y[TL - 1][j] = fma(-mu, Y[TL - 1][j], wl[j]);
+                                Z[TL - 1][j] = fma(-mu, Z[TL - 1][j], wr[j]);
+                                aR[j] = fma(gg, Z[TL - 1][j], aR[j]);
+                            }
+                        }
+                    };
+                    // step 0: mu_0 = 0, Y_0 = f_0 (W + the preloaded boundary term), no left contribution
+                    auto body_first = [&](double (&aL)[TS], double (&aR)[TS]) {
+                        double wl[TS], wr[TS];
+                        load_w(0, wl, wr);
+                        const double* rga = cga;
 #pragma unroll
-                                for (int j = 0; j < TS; ++j) {
-                                    const double ul = ok ? A.uG[(sidx[j] * g.V + vu) * (int64_t)L + l] : 0.0;
-                                    const double ur = ok ? A.uG[(sidx[j] * g.V + vv) * (int64_t)L + l] : 0.0;
-                                    aL[j] = fma(-nk, Y[n][j], aL[j]);
-                                    Y[n][j] = fma(beta, ur, fma(-mu, Y[n][j], wl[j]));
-                                    Z[n][j] = fma(beta, ul, fma(-mu, Z[n][j], wr[j]));
-                                    aR[j] = fma(gg, Z[n][j], aR[j]);
-                                }
+                        for (int j = 0; j < TS; ++j) aL[j] = aR[j] = 0.0;
+#pragma unroll
+                        for (int n = 0; n < TL; ++n) {
+                            const double gg = rga[slot(n)];
+#pragma unroll
+                            for (int j = 0; j < TS; ++j) {
+                                Y[n][j] += wl[j];
+                                Z[n][j] += wr[j];
+                                aR[j] = fma(gg, Z[n][j], aR[j]);
+                            }
+                        }
+                    };
+                    // step m-1 (m >= 2): the left chain reaches position m-1 (f += beta u_right), the right
+                    // chain position 0 (f += beta u_left)
+                    auto body_last = [&](int tt, double (&aL)[TS], double (&aR)[TS]) {
+                        double wl[TS], wr[TS];
+                        load_w(tt, wl, wr);
+                        const double* rmu = cmu + tt * RN;
+                        const double* rga = cga + tt * RN;
+#pragma unroll
+                        for (int j = 0; j < TS; ++j) aL[j] = aR[j] = 0.0;
+#pragma unroll
+                        for (int n = 0; n < TL; ++n) {
+                            const int sn = slot(n);
+                            const int l = rb + sn;
+                            const bool ok = l < L;
+                            const double beta = ok ? A.cL[l] / h : 0.0;
+                            const double mu = rmu[sn], gg = rga[sn];
+                            const double nk = gg * mu;
+#pragma unroll
+                            for (int j = 0; j < TS; ++j) {
+                                const double ul = ok ? A.uG[(sidx[j] * g.V + vu) * (int64_t)L + l] : 0.0;
+                                const double ur = ok ? A.uG[(sidx[j] * g.V + vv) * (int64_t)L + l] : 0.0;
+                                aL[j] = fma(-nk, Y[n][j], aL[j]);
+                                Y[n][j] = fma(beta, ur, fma(-mu, Y[n][j], wl[j]));
+                                Z[n][j] = fma(beta, ul, fma(-mu, Z[n][j], wr[j]));
+                                aR[j] = fma(gg, Z[n][j], aR[j]);
+                            }
+                        }
+                    };
+                    // sum the step's partials over the warp's l-lanes and store them for the fold
+                    double* pb = part + buf * IBK * NWL * 2 * CS + lw * 2 * CS + st0 + sig;
+                    auto reduce_store = [&](double (&aL)[TS], double (&aR)[TS], int tt) {
+                        if (TS == 4) {
+                            // slot j holds sample j ^ sig; sig bit 1 = ll bit 0, sig bit 0 = ll bit 1, so the
+                            // partner's slots {2,3} (xor 1) and slot 1 (xor 2) are this lane's slots {0,1} / 0
+                            aL[0] += __shfl_xor_sync(0xffffffffu, aL[2 % TS], 1);
+                            aL[1 % TS] += __shfl_xor_sync(0xffffffffu, aL[3 % TS], 1);
+                            aR[0] += __shfl_xor_sync(0xffffffffu, aR[2 % TS], 1);
+                            aR[1 % TS] += __shfl_xor_sync(0xffffffffu, aR[3 % TS], 1);
+                            aL[0] += __shfl_xor_sync(0xffffffffu, aL[1 % TS], 2);
+                            aR[0] += __shfl_xor_sync(0xffffffffu, aR[1 % TS], 2);
+                            aL[0] += __shfl_xor_sync(0xffffffffu, aL[0], 4);
+                            aR[0] += __shfl_xor_sync(0xffffffffu, aR[0], 4);
+                            if ((ll & 4) == 0) {
+                                pb[tt * NWL * 2 * CS] = aL[0];
+                                pb[tt * NWL * 2 * CS + CS] = aR[0];
                             }
                         } else {
 #pragma unroll
-                            for (int q = 0; q < NP; ++q) {
-                                const double2 m2 = *reinterpret_cast<const double2*>(rmu + 2 * lt + 64 * q);
-                                const double2 g2 = *reinterpret_cast<const double2*>(rga + 2 * lt + 64 * q);
-                                const double k0 = g2.x * m2.x, k1 = g2.y * m2.y;
-#pragma unroll
-                                for (int j = 0; j < TS; ++j) {
-                                    aL[j] = fma(-k0, Y[2 * q][j], aL[j]);
-                                    Y[2 * q][j] = fma(-m2.x, Y[2 * q][j], wl[j]);
-                                    Z[2 * q][j] = fma(-m2.x, Z[2 * q][j], wr[j]);
-                                    aR[j] = fma(g2.x, Z[2 * q][j], aR[j]);
-                                    aL[j] = fma(-k1, Y[2 * q + 1][j], aL[j]);
-                                    Y[2 * q + 1][j] = fma(-m2.y, Y[2 * q + 1][j], wl[j]);
-                                    Z[2 * q + 1][j] = fma(-m2.y, Z[2 * q + 1][j], wr[j]);
-                                    aR[j] = fma(g2.y, Z[2 * q + 1][j], aR[j]);
-                                }
+                            for (int o = 16; o >= 1; o >>= 1) {
+                                aL[0] += __shfl_xor_sync(0xffffffffu, aL[0], o);
+                                aR[0] += __shfl_xor_sync(0xffffffffu, aR[0], o);
                             }
-                            if (ODD) {
-                                const double mu = rmu[64 * NP + lt], gg = rga[64 * NP + lt];
-                                const double nk = gg * mu;
-#pragma unroll
-                                for (int j = 0; j < TS; ++j) {
-                                    aL[j] = fma(-nk, Y[TL - 1][j], aL[j]);
-                                    Y[TL - 1][j] = fma(-mu, Y[TL - 1][j], wl[j]);
-                                    Z[TL - 1][j] = fma(-mu, Z[TL - 1][j], wr[j]);
-                                    aR[j] = fma(gg, Z[TL - 1][j], aR[j]);
-                                }
+                            if (ll == 0) {
+                                pb[tt * NWL * 2 * CS] = aL[0];
+                                pb[tt * NWL * 2 * CS + CS] = aR[0];
                             }
                         }
-                        // reduce-scatter of the NV = 2 TS partials over the warp's LW l-lanes:
-                        // the high l-lane bits split the values, the low ones all-reduce
-                        double v[NV];
+                    };
+                    // software pipeline: the reduction of step tt-1 is independent of step tt's FMAs, so
+                    // the scheduler overlaps the shuffle latency with them
+                    const bool last_here = (t0 + nb == m) && (m > 1);
+                    const int tend = last_here ? nb - 1 : nb;
+                    double pL[TS], pR[TS];
+                    bool pend = false;
+                    int tt = 0;
+                    if (t0 == 0) {
+                        body_first(pL, pR);
+                        tt = 1;
+                        pend = true;
+                    } else if (tend > 0) {
+                        body_mid(0, pL, pR);
+                        tt = 1;
+                        pend = true;
+                    }
+                    for (; tt < tend; ++tt) {
+                        double aL[TS], aR[TS];
+                        body_mid(tt, aL, aR);
+                        reduce_store(pL, pR, tt - 1);
 #pragma unroll
                         for (int j = 0; j < TS; ++j) {
-                            v[j] = aL[j];
-                            v[TS + j] = aR[j];
-                        }
-                        int cnt = NV;
-#pragma unroll
-                        for (int o = LW / 2; o >= 1; o >>= 1) {
-                            if (cnt > 1) {
-                                const int half = cnt / 2;
-                                const bool up = (ll & o) != 0;
-#pragma unroll
-                                for (int i = 0; i < NV / 2; ++i) {
-                                    if (i < half) {
-                                        const double send = up ? v[i] : v[i + half];
-                                        const double keep = up ? v[i + half] : v[i];
-                                        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-                                    }
-                                }
-                                cnt = half;
-                            } else {
-                                v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
-                            }
-                        }
-                        constexpr int SH = (LW / NV) > 1 ? ((LW / NV) == 2 ? 1 : ((LW / NV) == 4 ? 2 : ((LW / NV) == 8 ? 3 : 4))) : 0;
-                        if ((ll & ((1 << SH) - 1)) == 0) {
-                            // lane keeps value index idx = bit-reverse-free order: the scatter levels
-                            // peel the index from its high bit down
-                            const int idx = ll >> SH;
-                            const int side = idx / TS, j = idx % TS;
-                            pb[((tt * NWL + lw) * 2 + side) * CS + st0 + j] = v[0];
+                            pL[j] = aL[j];
+                            pR[j] = aR[j];
                         }
                     }
+                    if (last_here) {
+                        double aL[TS], aR[TS];
+                        body_last(nb - 1, aL, aR);
+                        if (pend) reduce_store(pL, pR, nb - 2);
+#pragma unroll
+                        for (int j = 0; j < TS; ++j) {
+                            pL[j] = aL[j];
+                            pR[j] = aR[j];
+                        }
+                        pend = true;
+                    }
+                    if (pend) reduce_store(pL, pR, nb - 1);
                 }
             }
             if (REC) {
@@ -457,17 +531,16 @@ __global__ void __launch_bounds__(256) sweep_kernel(Args A) {
             } else {
                 // w_1 = g_0 Z (right sweep end, position 0), w_m = g_0 Y (left sweep end); g_0 = g_{m-1}
 #pragma unroll
-                for (int n = 0; n < TL; ++n) {
-                    const int l = rb + slot(n);
-                    if (l < L) {
-                        const double g0 = A.gam[off * (int64_t)Lp + l];
+                for (int j = 0; j < TS; ++j) {
+                    const int64_t s = c0 + st0 + j;
+                    if (s < A.S) {
+                        double* o = A.out + (s * g.E + e) * 2 * (int64_t)L + rb;
 #pragma unroll
-                        for (int j = 0; j < TS; ++j) {
-                            const int64_t s = c0 + st0 + j;
-                            if (s < A.S) {
-                                double* o = A.out + (s * g.E + e) * 2 * (int64_t)L + l;
-                                o[0] = g0 * Z[n][j];
-                                o[L] = g0 * Y[n][j];
+                        for (int n = 0; n < TL; ++n) {
+                            const int sn = slot(n);
+                            if (rb + sn < L) {
+                                o[sn] = g0[n] * Z[n][j];
+                                o[L + sn] = g0[n] * Y[n][j];
                             }
                         }
                     }
@@ -476,7 +549,7 @@ __global__ void __launch_bounds__(256) sweep_kernel(Args A) {
         }
         if (in_tile) {
             __syncthreads();
-            for (int x = tid; x < CS * m; x += nthreads) {
+            for (int x = tid; x < CS * m; x += NT) {
                 const int s = x / m, p = x - s * m;
                 if (c0 + s < A.S) A.out[(c0 + s) * N + off + p] = otile[s * ms + p];
             }
@@ -484,50 +557,59 @@ __global__ void __launch_bounds__(256) sweep_kernel(Args A) {
     }
 }
 
-// Launch shape for one instance: threads = 32 * NWL * nws; items = E * ceil(S / CS).
-template <int TL, int TS, int LW, bool REC>
+// One instance: threads = NT, items = E * ceil(S / CS), persistent CTAs over an atomic queue.
+template <int TL, int TS, int LW, int NWS, bool REC>
 cudaError_t launch(Args a, cudaStream_t st) {
-    using C = Cfg<TL, TS, LW, REC>;
-    const int cs = a.nws * C::SLW * TS;
-    a.chunks = (int32_t)((a.S + cs - 1) / cs);
+    using C = Cfg<TL, TS, LW, NWS, REC>;
+    a.chunks = (int32_t)((a.S + C::CS - 1) / C::CS);
     a.n_items = a.g.E * a.chunks;
-    const int threads = 32 * C::NWL * a.nws;
-    size_t smem = C::fixed_bytes(cs);
+    size_t smem = C::FIXED;
     a.tile_ms = 0;
     if (REC) {
-        // the output tile holds edges with (m | 1) <= tile_ms; size it for the longest edge if it fits
+        // the output tile holds edges with (m | 1) <= tile_ms; sized for the longest edge if it fits
         const int want = a.g.max_m | 1;
         const size_t room = SMEM_MAX > smem ? SMEM_MAX - smem : 0;
-        const int fit = (int)(room / ((size_t)cs * sizeof(double)));
-        a.tile_ms = want <= fit ? want : ((fit - 1) | 1);
-        if (a.tile_ms < 1) a.tile_ms = 0;
-        smem += (size_t)cs * a.tile_ms * sizeof(double);
+        const int fit = (int)(room / ((size_t)C::CS * sizeof(double)));
+        a.tile_ms = want <= fit ? want : (fit >= 1 ? ((fit - 1) | 1) : 0);
+        smem += (size_t)C::CS * a.tile_ms * sizeof(double);
     }
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<TL, TS, LW, REC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<TL, TS, LW, NWS, REC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(a.counter, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return e;
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<TL, TS, LW, REC>, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<TL, TS, LW, NWS, REC>, C::NT, smem);
     if (per_sm < 1) per_sm = 1;
     int blocks = 148 * per_sm;
     if (blocks > a.n_items) blocks = a.n_items;
-    sweep_kernel<TL, TS, LW, REC><<<blocks, threads, smem, st>>>(a);
+    sweep_kernel<TL, TS, LW, NWS, REC><<<blocks, C::NT, smem, st>>>(a);
     return cudaGetLastError();
 }
 
-// Sample mapping of one launch (the node tile TL is fixed by the plan's Lp):
-//   variant 0: TS = 4, LW = 8  (warp = 8 l-lanes x 4 s-lanes = 16 samples), nws = 2 (CS = 32) or 1 (CS = 16)
-//   variant 1: TS = 1, LW = 32 (warp = 32 l-lanes x 1 sample), nws = 1 (CS = 1): few samples
-template <int TL, bool REC>
-cudaError_t launch_tl(Args a, cudaStream_t st) {
-    if (a.S >= 9) {
-        a.nws = a.S >= 17 ? 2 : 1;
-        return launch<TL, 4, 8, REC>(a, st);
+// Sample mapping (the node tile TL is fixed by the plan's Lp):
+//   V2: TS = 4, LW = 8, NWS = 2  (CTA = 4 l-warps x 2 s-warps, 32 samples per item)   S >= 17
+//   V1: TS = 4, LW = 8, NWS = 1  (CTA = 4 l-warps, 16 samples per item)               9 <= S <= 16
+//   V0: TS = 1, LW = 32, NWS = 1 (CTA = 1 warp, 1 sample per item)                    S <= 8
+enum Variant { V0 = 0, V1 = 1, V2 = 2 };
+inline Variant variant_for(int64_t S) { return S >= 17 ? V2 : (S >= 9 ? V1 : V0); }
+
+template <bool REC, int V>
+cudaError_t launch_v(int tl, Args a, cudaStream_t st) {
+    constexpr int TS = V == V0 ? 1 : 4, LW = V == V0 ? 32 : 8, NWS = V == V2 ? 2 : 1;
+    switch (tl) {
+        case 1: return launch<1, TS, LW, NWS, REC>(a, st);
+        case 2: return launch<2, TS, LW, NWS, REC>(a, st);
+        case 3: return launch<3, TS, LW, NWS, REC>(a, st);
+        case 4: return launch<4, TS, LW, NWS, REC>(a, st);
+        case 5: return launch<5, TS, LW, NWS, REC>(a, st);
+        case 6: return launch<6, TS, LW, NWS, REC>(a, st);
+        case 7: return launch<7, TS, LW, NWS, REC>(a, st);
+        case 8: return launch<8, TS, LW, NWS, REC>(a, st);
+        case 9: return launch<9, TS, LW, NWS, REC>(a, st);
+        case 10: return launch<10, TS, LW, NWS, REC>(a, st);
+        default: return cudaErrorInvalidValue;
     }
-    a.nws = 1;
-    return launch<TL, 1, 32, REC>(a, st);
 }
 
 }  // namespace sweep
