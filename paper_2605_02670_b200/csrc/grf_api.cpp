@@ -263,7 +263,7 @@ grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct WsLayout {
-    size_t w = 0, ends = 0, ug = 0, iters = 0, relres = 0, counter = 0, total = 0;
+    size_t w = 0, ends = 0, rhs = 0, ug = 0, iters = 0, relres = 0, counter = 0, total = 0;
 };
 
 // with_noise: grf_sample keeps the white noise W (S x N) in the workspace
@@ -272,10 +272,15 @@ WsLayout ws_layout(const grf_graph* g, int64_t L, int64_t S, bool with_noise = t
     size_t o = 0;
     w.w = o;
     if (with_noise) o += align_up((size_t)S * g->N * sizeof(double));
+    // ends / uG are sample-tiled (grf_internal.h): sized for whole tiles
+    const int64_t cs = (int64_t)1 << grf::sample_tile_log2(S);
+    const int64_t Sp = (S + cs - 1) / cs * cs;
     w.ends = o;
-    o += align_up((size_t)S * g->E * 2 * L * sizeof(double));
+    o += align_up((size_t)Sp * g->E * 2 * L * sizeof(double));
+    w.rhs = o;
+    o += align_up((size_t)Sp * g->V * L * sizeof(double));
     w.ug = o;
-    o += align_up((size_t)S * g->V * L * sizeof(double));
+    o += align_up((size_t)Sp * g->V * L * sizeof(double));
     w.iters = o;
     o += align_up((size_t)S * L * sizeof(int32_t));
     w.relres = o;
@@ -323,6 +328,7 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
     }
     double* ends = reinterpret_cast<double*>(base + w.ends);
     double* uG = reinterpret_cast<double*>(base + w.ug);
+    double* rhs = reinterpret_cast<double*>(base + w.rhs);
     int32_t* iters = reinterpret_cast<int32_t*>(base + w.iters);
     double* relres = reinterpret_cast<double*>(base + w.relres);
     int32_t* counters = reinterpret_cast<int32_t*>(base + w.counter);
@@ -330,8 +336,6 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
     prm.rtol = opt ? opt->rtol : 1e-13;
     prm.max_iter = (opt && opt->max_iter > 0) ? opt->max_iter : (int32_t)(g->V + 10);
     prm.precond = opt ? opt->precond : GRF_PRECOND_NN;
-    prm.debug_nogather = getenv("GRF_DEBUG_NOGATHER") ? 1 : 0;
-    prm.debug_nowrite = getenv("GRF_DEBUG_NOWRITE") ? 1 : 0;
     grf_status rc = GRF_OK;
     cudaError_t le = cudaSuccess;
     cudaError_t ce = g->timed(GRF_K_CONDENSE, st, [&] {
@@ -339,7 +343,7 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
     });
     if (ce == cudaSuccess) ce = le;
     if (ce == cudaSuccess)
-        ce = g->timed(GRF_K_PCG, st, [&] { grf::launch_pcg(g->dev, p->dev, S, prm, W, ends, uG, iters, relres, st); });
+        ce = g->timed(GRF_K_PCG, st, [&] { grf::launch_pcg(g->dev, p->dev, S, prm, W, ends, rhs, uG, iters, relres, st); });
     if (ce == cudaSuccess)
         ce = g->timed(GRF_K_RECOVER, st, [&] {
             le = grf::launch_recover(g->dev, p->dev, S, W, u, uG, counters + 1, st);

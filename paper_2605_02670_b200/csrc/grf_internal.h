@@ -52,9 +52,27 @@ struct PcgParams {
     double rtol = 1e-13;
     int32_t max_iter = 0;
     int32_t precond = 0;
-    int32_t debug_nogather = 0;  // experiments only (GRF_DEBUG_NOGATHER)
-    int32_t debug_nowrite = 0;   // experiments only (GRF_DEBUG_NOWRITE)
 };
+
+// Sample-tiled layouts of the per-call intermediates (shared by K3, K4, K5): samples are
+// grouped in tiles of cs = sample_tile(S) (the sweep kernels' samples per item, a power of
+// two), and within a tile the sample index is the fastest dimension, so a sweep item
+// (edge, sample tile) writes / reads contiguous runs and a PCG CTA (node, sample octet)
+// reads 64-byte runs.
+//   ends  (K3 -> K4): end values w^{(l,s)}_{code}, code = 2 e + end   [tile][l][code][cs]
+//   uG    (K4 -> K5): vertex solution u_G^{(l,s)}(v)                   [tile][v][l][cs]
+__host__ __device__ inline int64_t ends_index(int64_t s, int32_t l, int32_t code, int32_t L, int32_t E, int32_t cs_log2) {
+    return ((((s >> cs_log2) * L + l) * (int64_t)(2 * E) + code) << cs_log2) + (s & ((1 << cs_log2) - 1));
+}
+__host__ __device__ inline int64_t ug_index(int64_t s, int32_t v, int32_t l, int32_t L, int32_t V, int32_t cs_log2) {
+    return ((((s >> cs_log2) * V + v) * (int64_t)L + l) << cs_log2) + (s & ((1 << cs_log2) - 1));
+}
+//   rhs   (K4a -> K4): condensed right-hand side g^{(l,s)}(v)        [tile][l][cs][v]
+__host__ __device__ inline int64_t rhs_index(int64_t s, int32_t l, int32_t v, int32_t L, int32_t V, int32_t cs_log2) {
+    return (((((s >> cs_log2) * L + l) << cs_log2) + (s & ((1 << cs_log2) - 1))) * (int64_t)V) + v;
+}
+// log2 of the sample tile for S samples (sweep.cu)
+int32_t sample_tile_log2(int64_t S);
 
 // K1  noise (noise.cu): W[s*N + i] = sqrt(M_L,ii) z(seed + s, i)
 void launch_noise(const DevGraph& g, uint64_t seed, int64_t n_samples, double* W, cudaStream_t st);
@@ -65,8 +83,9 @@ void launch_edge_setup(const DevGraph& g, DevPlan& p, cudaStream_t st);
 cudaError_t launch_condense(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W,
                             double* ends, int32_t* counter, cudaStream_t st);
 // K4  batched NN-PCG on the vertex Schur systems (pcg.cu): g from (W, ends), u_G -> uG[(s*V + v)*L + l]
+// (K4a first assembles g = W_G + sum (c_L/h_e) w_end from the end values into rhs)
 void launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* W,
-                const double* ends, double* uG, int32_t* iters, double* relres, cudaStream_t st);
+                const double* ends, double* rhs, double* uG, int32_t* iters, double* relres, cudaStream_t st);
 // K5  Thomas recovery + accumulation over nodes (sweep.cu): u[s*N + dof] from W and u_G
 cudaError_t launch_recover(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W, double* u,
                            const double* uG, int32_t* counter, cudaStream_t st);
@@ -75,6 +94,10 @@ cudaError_t launch_vertex_sum(const DevGraph& g, const DevPlan& p, int64_t n_sam
                               cudaStream_t st);
 // node tiling of the Thomas tables for L nodes: Lp = rounds * 32 * TL (sweep.cu)
 void plan_tiling(int32_t L, int32_t* Lp, int32_t* tl, int32_t* rounds);
+
+// K4 warp-per-system variant (pcg_warp.cu); false if the graph is outside its range
+bool launch_pcg_warp(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* rhs,
+                     double* uG, int32_t* iters, double* relres, cudaStream_t st);
 
 // K2b per-node CSR operator tables for K4 (pcg.cu)
 void launch_pcg_tables(const DevGraph& g, const DevPlan& p, cudaStream_t st);

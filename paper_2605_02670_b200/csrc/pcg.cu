@@ -25,7 +25,7 @@
 // batches of SB samples: r and p are [V][SB] in shared memory, x/q/z live in registers of
 // the vertex's owner thread, and one group reduction (a single barrier) per dot product
 // carries all SB values.  Each sample has its own alpha/beta and stops at its own
-// convergence.  g is gathered from K3's end values ends[((s*E + e)*2 + end)*L + l] (+ W_v);
+// convergence.  g is read from the assembled rhs (K4a, assemble_rhs_kernel);
 // u_G is written to uG[(s*V + v)*L + l].
 #include <cstdlib>
 
@@ -113,9 +113,8 @@ __device__ __forceinline__ void group_sum(double (&v)[NV], double* red /* [2][GT
 
 template <int GT, int SB, int VPT, int W, bool STAGED>
 __global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L, const double* __restrict__ ops,
-                                                          PcgParams prm, int64_t S, int32_t spc,
-                                                          const double* __restrict__ Wn, const double* __restrict__ ends,
-                                                          double* __restrict__ uG, int32_t* __restrict__ iters,
+                                                          PcgParams prm, int64_t S, int32_t spc, int32_t csl,
+                                                          const double* __restrict__ rhs, double* __restrict__ uG, int32_t* __restrict__ iters,
                                                           double* __restrict__ relres) {
     constexpr int NG = PCG_THREADS / GT;
     constexpr int NW = GT / 32;
@@ -209,12 +208,7 @@ __global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L,
 #pragma unroll
                 for (int j = 0; j < SB; ++j) {
                     const int64_t s = s0 + (j < ns ? j : 0);
-                    const double* ecol = ends + (s * E) * 2 * (int64_t)L + l;
-                    double gv = Wn[s * g.N + g.NI + v];
-                    if (!prm.debug_nogather) {
-#pragma unroll
-                        for (int t = 0; t < W; ++t) gv += GK[t * V + v] * ecol[(int64_t)ec[t * V + v] * L];
-                    }
+                    double gv = rhs[rhs_index(s, l, v, L, V, csl)];
                     if (j >= ns) gv = 0.0;
                     r[v * SB + j] = gv;
                     gg[j] += gv * gv;
@@ -331,10 +325,10 @@ __global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L,
 #pragma unroll
         for (int a = 0; a < VPT; ++a) {
             const int v = gt + a * GT;
-            if (v < V && !prm.debug_nowrite) {
+            if (v < V) {
 #pragma unroll
                 for (int j = 0; j < SB; ++j)
-                    if (j < ns) uG[((s0 + j) * V + v) * (int64_t)L + l] = x[a][j];
+                    if (j < ns) uG[ug_index(s0 + j, v, l, L, V, csl)] = x[a][j];
             }
         }
         if (gt == 0) {
@@ -356,8 +350,8 @@ size_t staged_bytes(const DevGraph& g) {
 }
 
 template <int GT, int SB, int VPT, int W>
-bool launch_t(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* Wn,
-              const double* ends, double* uG, int32_t* iters, double* relres, cudaStream_t st) {
+bool launch_t(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* rhs,
+              double* uG, int32_t* iters, double* relres, cudaStream_t st) {
     constexpr int NG = PCG_THREADS / GT;
     if (g.ell_w != W || g.V > GT * VPT) return false;
     const size_t vb = vec_bytes(g, SB, NG);
@@ -373,25 +367,81 @@ bool launch_t(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgP
     const int32_t spc = (int32_t)(((batches + groups - 1) / groups) * SB);
     groups = (n_samples + spc - 1) / spc;
     const dim3 grid(p.L, (unsigned)groups);
+    const int32_t csl = sample_tile_log2(n_samples);
     if (staged) {
         cudaFuncSetAttribute(pcg_kernel<GT, SB, VPT, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        pcg_kernel<GT, SB, VPT, W, true><<<grid, PCG_THREADS, smem, st>>>(g, p.L, p.ops, prm, n_samples, spc, Wn, ends,
+        pcg_kernel<GT, SB, VPT, W, true><<<grid, PCG_THREADS, smem, st>>>(g, p.L, p.ops, prm, n_samples, spc, csl, rhs,
                                                                         uG, iters, relres);
     } else {
         cudaFuncSetAttribute(pcg_kernel<GT, SB, VPT, W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-        pcg_kernel<GT, SB, VPT, W, false><<<grid, PCG_THREADS, smem, st>>>(g, p.L, p.ops, prm, n_samples, spc, Wn,
-                                                                         ends, uG, iters, relres);
+        pcg_kernel<GT, SB, VPT, W, false><<<grid, PCG_THREADS, smem, st>>>(g, p.L, p.ops, prm, n_samples, spc, csl, rhs,
+                                                                         uG, iters, relres);
     }
     return true;
 }
 
+
 template <int W>
-bool launch_w(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* Wn,
-              const double* ends, double* uG, int32_t* iters, double* relres, cudaStream_t st) {
-    if (launch_t<128, 1, 8, W>(g, p, n_samples, prm, Wn, ends, uG, iters, relres, st)) return true;   // V <= 1024
-    if (launch_t<256, 1, 8, W>(g, p, n_samples, prm, Wn, ends, uG, iters, relres, st)) return true;   // V <= 2048
-    return launch_t<512, 1, 8, W>(g, p, n_samples, prm, Wn, ends, uG, iters, relres, st);            // V <= 4096
+bool launch_w(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* rhs,
+              double* uG, int32_t* iters, double* relres, cudaStream_t st) {
+    if (launch_pcg_warp(g, p, n_samples, prm, rhs, uG, iters, relres, st)) return true;  // V <= 1024, W <= 8
+    if (launch_t<128, 1, 8, W>(g, p, n_samples, prm, rhs, uG, iters, relres, st)) return true;   // V <= 1024
+    if (launch_t<256, 1, 8, W>(g, p, n_samples, prm, rhs, uG, iters, relres, st)) return true;   // V <= 2048
+    return launch_t<512, 1, 8, W>(g, p, n_samples, prm, rhs, uG, iters, relres, st);            // V <= 4096
+}
+
+// K4a: condensed right-hand side g_v = W_v + sum_j (c_L/h_e) w_{code_j(v)} (P233-239)
+// for every (node, sample), from the sample-tiled end values into rhs [tile][l][cs][v].
+// CTA per (tile, l, block of 32 vertices): phase 1 reads the incident end-value rows with the
+// sample index fastest (coalesced), phase 2 transposes through shared memory and writes
+// vertex-contiguous rows of rhs (coalesced), adding W_v read vertex-contiguous as well.
+constexpr int ASM_VB = 32;
+
+__global__ void __launch_bounds__(256) assemble_rhs_kernel(DevGraph g, int32_t L, const double* __restrict__ ops,
+                                                           int64_t S, int32_t csl, const double* __restrict__ Wn,
+                                                           const double* __restrict__ ends, double* __restrict__ rhs) {
+    __shared__ double acc[ASM_VB][33];
+    __shared__ double gks[32][ASM_VB];  // c_L/h_e of incidence slot j of the block's vertices (0: padding)
+    __shared__ int codes[32][ASM_VB];   // incidence code 2e+end of slot j (0 for padding: a valid row)
+    const int V = g.V, E = g.E, Wd = g.ell_w;
+    const int cs = 1 << csl;
+    const int vblocks = (V + ASM_VB - 1) / ASM_VB;
+    const int64_t tiles = (S + cs - 1) >> csl;
+    const int64_t stride = table_stride(V, Wd);
+    for (int64_t b = blockIdx.x; b < tiles * L * vblocks; b += gridDim.x) {
+        const int vb = (int)(b % vblocks);
+        const int64_t tl = b / vblocks;  // tile * L + l
+        const int l = (int)(tl % L);
+        const int64_t tile = tl / L;
+        const double* GK = ops + l * stride + 3 * (int64_t)V + 2 * (int64_t)Wd * V;
+        for (int x = threadIdx.x; x < Wd * ASM_VB; x += blockDim.x) {
+            const int j = x / ASM_VB, vl = x % ASM_VB;
+            const int v = vb * ASM_VB + vl;
+            const bool ok = v < V && g.ell_valid[j * V + v];
+            codes[j][vl] = ok ? g.ell_code[j * V + v] : 0;
+            gks[j][vl] = ok ? GK[j * V + v] : 0.0;
+        }
+        __syncthreads();
+        const double* slab = ends + ((tl * 2 * E) << csl);
+        for (int x = threadIdx.x; x < ASM_VB * cs; x += blockDim.x) {
+            const int vl = x >> csl, si = x & (cs - 1);
+            double a = 0.0;
+            for (int j = 0; j < Wd; ++j) a = fma(gks[j][vl], slab[((int64_t)codes[j][vl] << csl) + si], a);
+            acc[vl][si] = a;
+        }
+        __syncthreads();
+        for (int x = threadIdx.x; x < ASM_VB * cs; x += blockDim.x) {
+            const int si = x / ASM_VB, vl = x % ASM_VB;
+            const int v = vb * ASM_VB + vl;
+            const int64_t s = (tile << csl) + si;
+            if (v < V) {
+                const double wv = Wn[(s < S ? s : S - 1) * g.N + g.NI + v];
+                rhs[((tl << csl) + si) * (int64_t)V + v] = wv + acc[vl][si];
+            }
+        }
+        __syncthreads();
+    }
 }
 
 }  // namespace
@@ -414,12 +464,16 @@ void launch_pcg_tables(const DevGraph& g, const DevPlan& p, cudaStream_t st) {
 }
 
 void launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* W,
-                const double* ends, double* uG, int32_t* iters, double* relres, cudaStream_t st) {
+                const double* ends, double* rhs, double* uG, int32_t* iters, double* relres, cudaStream_t st) {
+    const int32_t csl = sample_tile_log2(n_samples);
+    const int64_t work = ((n_samples + (1 << csl) - 1) >> csl) * p.L * ((g.V + ASM_VB - 1) / ASM_VB);
+    int blocks = (int)(work < 148 * 8 ? work : 148 * 8);
+    assemble_rhs_kernel<<<blocks, 256, 0, st>>>(g, p.L, p.ops, n_samples, csl, W, ends, rhs);
     switch (g.ell_w) {
-        case 4: launch_w<4>(g, p, n_samples, prm, W, ends, uG, iters, relres, st); break;
-        case 8: launch_w<8>(g, p, n_samples, prm, W, ends, uG, iters, relres, st); break;
-        case 16: launch_w<16>(g, p, n_samples, prm, W, ends, uG, iters, relres, st); break;
-        default: launch_w<32>(g, p, n_samples, prm, W, ends, uG, iters, relres, st); break;
+        case 4: launch_w<4>(g, p, n_samples, prm, rhs, uG, iters, relres, st); break;
+        case 8: launch_w<8>(g, p, n_samples, prm, rhs, uG, iters, relres, st); break;
+        case 16: launch_w<16>(g, p, n_samples, prm, rhs, uG, iters, relres, st); break;
+        default: launch_w<32>(g, p, n_samples, prm, rhs, uG, iters, relres, st); break;
     }
 }
 

@@ -1,0 +1,227 @@
+// K4 warp-per-system variant of the batched NN-PCG (pcg.cu has the operator definitions,
+// the table layout and the thread-group variant for larger vertex sets).
+#include "grf_internal.h"
+
+namespace grf {
+namespace {
+
+constexpr size_t SMEM_LIMIT = 227 * 1024;
+// per node l: [DS (V) | DM (V) | DJ (V) | OS (W*V) | OM (W*V) | GK (W*V)], slot-major [j][v] (pcg.cu)
+__host__ __device__ inline int64_t table_stride(int V, int W) { return 3 * (int64_t)V + 3 * (int64_t)W * V; }
+
+// ---------------------------------------------------------------------------------------
+// Warp-per-system variant (V <= 1024).  CTA = 8 warps = node l x one octet of consecutive
+// samples per pass (the CTA walks `octs` octets); each warp solves one (l, s) system alone:
+// r and p in shared memory (neighbour access of the two operators), x, q = S p and
+// z = M^{-1} r in registers (VPL vertices v = lane + 32 k per lane), dot products by
+// 5-level xor shuffles (fixed order), __syncwarp between the phases -- no block barriers
+// after the optional staging of node l's operator tables and ELL neighbour indices.
+constexpr int WARP_NW = 8;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int VPL, int W, bool STAGE>
+__global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int32_t L, const double* __restrict__ ops,
+                                                                PcgParams prm, int64_t S, int32_t octs, int32_t csl,
+                                                                const double* __restrict__ rhs, double* __restrict__ uG,
+                                                                int32_t* __restrict__ iters, double* __restrict__ relres) {
+    extern __shared__ double sm[];
+    const int V = g.V;
+    const int l = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t stride = table_stride(V, W);
+    const double* tab = ops + l * stride;
+    const double* DS = tab;
+    const double* DM = DS + V;
+    const double* DJ = DM + V;
+    const double* OS = DJ + V;
+    const double* OM = OS + (size_t)W * V;
+    const int* eo = g.ell_other;
+    double* r = sm + (size_t)warp * 2 * V;
+    double* p = r + V;
+    if (STAGE) {  // DS, DM, OS, OM and the neighbour indices of node l, once per CTA
+        double* st = sm + (size_t)WARP_NW * 2 * V;
+        int* so = reinterpret_cast<int*>(st + (size_t)(2 + 2 * W) * V);
+        for (int i = threadIdx.x; i < 2 * V; i += WARP_NW * 32) st[i] = tab[i];                      // DS, DM
+        for (int i = threadIdx.x; i < 2 * W * V; i += WARP_NW * 32) st[2 * V + i] = tab[3 * V + i];  // OS, OM
+        for (int i = threadIdx.x; i < W * V; i += WARP_NW * 32) so[i] = eo[i];
+        __syncthreads();
+        DS = st;
+        DM = st + V;
+        OS = st + 2 * V;
+        OM = OS + (size_t)W * V;
+        eo = so;
+    }
+    // y = D x + sum_j O_j x_{o_j} for this lane's vertices (x in shared memory)
+    auto apply = [&](const double* D, const double* O, const double* xs, double (&y)[VPL]) {
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            const int v = lane + 32 * k;
+            if (v < V) {
+                double a = D[v] * xs[v];
+#pragma unroll
+                for (int j = 0; j < W; ++j) a = fma(O[j * V + v], xs[eo[j * V + v]], a);
+                y[k] = a;
+            }
+        }
+    };
+    auto precond = [&](double (&z)[VPL]) {
+        if (prm.precond == 0) {
+            apply(DM, OM, r, z);
+        } else {
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+                const int v = lane + 32 * k;
+                if (v < V) z[k] = (prm.precond == 1 ? DJ[v] : 1.0) * r[v];
+            }
+        }
+    };
+
+    for (int oc = 0; oc < octs; ++oc) {
+        const int64_t s = ((int64_t)blockIdx.y * octs + oc) * WARP_NW + warp;
+        if (s >= S) break;  // warp-uniform; no block barriers below
+        double x[VPL], t[VPL];  // t holds q = S p, then z = M^{-1} r (disjoint lifetimes)
+        // condensed rhs g_v = W_v + sum_j (c_L/h_e) w_{code_j(v)} (P233-239); x_0 = 0, r = g
+        double gg = 0.0;
+        const double* gs = rhs + rhs_index(s, l, 0, L, V, csl);
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            const int v = lane + 32 * k;
+            x[k] = 0.0;
+            if (v < V) {
+                const double gv = gs[v];
+                r[v] = gv;
+                gg = fma(gv, gv, gg);
+            }
+        }
+        gg = warp_sum(gg);
+        __syncwarp();
+        precond(t);
+        double rz = 0.0;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            const int v = lane + 32 * k;
+            if (v < V) {
+                p[v] = t[k];
+                rz = fma(r[v], t[k], rz);
+            }
+        }
+        rz = warp_sum(rz);
+        __syncwarp();
+        const double tol2 = prm.rtol * prm.rtol * gg;
+        bool done = !(gg > 0.0);
+        double rr = gg;
+        int it = 0;
+        while (!done && it < prm.max_iter) {
+            ++it;
+            apply(DS, OS, p, t);  // Dirichlet step (P247-258): t = q
+            double pq = 0.0;
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+                const int v = lane + 32 * k;
+                if (v < V) pq = fma(p[v], t[k], pq);
+            }
+            pq = warp_sum(pq);
+            const double alpha = rz / pq;
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+                const int v = lane + 32 * k;
+                if (v < V) {
+                    x[k] = fma(alpha, p[v], x[k]);
+                    r[v] = fma(-alpha, t[k], r[v]);
+                }
+            }
+            __syncwarp();
+            precond(t);  // Neumann step (P260-298): t = z
+            double t_rr = 0.0, t_rz = 0.0;
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+                const int v = lane + 32 * k;
+                if (v < V) {
+                    t_rr = fma(r[v], r[v], t_rr);
+                    t_rz = fma(r[v], t[k], t_rz);
+                }
+            }
+            t_rr = warp_sum(t_rr);
+            t_rz = warp_sum(t_rz);
+            rr = t_rr;
+            if (t_rr <= tol2) break;
+            const double beta = t_rz / rz;
+            rz = t_rz;
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+                const int v = lane + 32 * k;
+                if (v < V) p[v] = fma(beta, p[v], t[k]);
+            }
+            __syncwarp();
+        }
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            const int v = lane + 32 * k;
+            if (v < V) uG[ug_index(s, v, l, L, V, csl)] = x[k];
+        }
+        if (lane == 0) {
+            iters[s * L + l] = it;
+            relres[s * L + l] = gg > 0.0 ? sqrt(rr / gg) : 0.0;
+        }
+        __syncwarp();  // r / p are rewritten by the next octet
+    }
+}
+
+size_t warp_smem_bytes(const DevGraph& g, int W, bool stage) {
+    size_t b = sizeof(double) * (size_t)WARP_NW * 2 * g.V;
+    if (stage) b += sizeof(double) * (size_t)(2 + 2 * W) * g.V + sizeof(int) * (size_t)W * g.V;
+    return b;
+}
+
+template <int VPL, int W>
+bool launch_warp_t(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* rhs,
+                   double* uG, int32_t* iters, double* relres, cudaStream_t st) {
+    const bool stage = warp_smem_bytes(g, W, true) <= SMEM_LIMIT;
+    const size_t smem = warp_smem_bytes(g, W, stage);
+    if (smem > SMEM_LIMIT) return false;
+    const int64_t n_oct = (n_samples + WARP_NW - 1) / WARP_NW;
+    // octets per CTA: about four CTAs per SM over the whole (node x octet) grid
+    int64_t octs = (p.L * n_oct + 4 * 148 - 1) / (4 * 148);
+    if (octs < 1) octs = 1;
+    if (octs > n_oct) octs = n_oct;
+    const dim3 grid(p.L, (unsigned)((n_oct + octs - 1) / octs));
+    const int32_t csl = sample_tile_log2(n_samples);
+    if (stage) {
+        cudaFuncSetAttribute(pcg_warp_kernel<VPL, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        pcg_warp_kernel<VPL, W, true><<<grid, WARP_NW * 32, smem, st>>>(g, p.L, p.ops, prm, n_samples, (int32_t)octs, csl,
+                                                                      rhs, uG, iters, relres);
+    } else {
+        cudaFuncSetAttribute(pcg_warp_kernel<VPL, W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        pcg_warp_kernel<VPL, W, false><<<grid, WARP_NW * 32, smem, st>>>(g, p.L, p.ops, prm, n_samples, (int32_t)octs,
+                                                                       csl, rhs, uG, iters, relres);
+    }
+    return true;
+}
+
+template <int W>
+bool launch_warp(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* rhs,
+                 double* uG, int32_t* iters, double* relres, cudaStream_t st) {
+    const int vpl = (g.V + 31) / 32;
+#define GRF_PW(N) \
+    if (vpl <= N) return launch_warp_t<N, W>(g, p, n_samples, prm, rhs, uG, iters, relres, st);
+    GRF_PW(1) GRF_PW(2) GRF_PW(4) GRF_PW(8) GRF_PW(16) GRF_PW(32)
+#undef GRF_PW
+    return false;
+}
+
+}  // namespace
+
+bool launch_pcg_warp(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* rhs,
+                     double* uG, int32_t* iters, double* relres, cudaStream_t st) {
+    if (g.V > 32 * 32) return false;
+    if (g.ell_w == 4) return launch_warp<4>(g, p, n_samples, prm, rhs, uG, iters, relres, st);
+    if (g.ell_w == 8) return launch_warp<8>(g, p, n_samples, prm, rhs, uG, iters, relres, st);
+    return false;
+}
+
+}  // namespace grf

@@ -35,6 +35,14 @@ sweep::Args make_args(const DevGraph& g, const DevPlan& p, int64_t S, const doub
 }
 }  // namespace
 
+int32_t sample_tile_log2(int64_t S) {
+    switch (sweep::variant_for(S)) {
+        case sweep::V2: return 5;
+        case sweep::V1: return 4;
+        default: return 0;
+    }
+}
+
 void plan_tiling(int32_t L, int32_t* Lp, int32_t* tl, int32_t* rounds) {
     const int q0 = (L + sweep::NLT - 1) / sweep::NLT;
     const int r = (q0 + TL_MAX - 1) / TL_MAX;
@@ -70,26 +78,31 @@ namespace grf {
 namespace {
 // vertex values of the sample (P313-324): u_v = sum_l u_G^{(l)}(v); one warp per (s, v),
 // lanes stride over l, fixed-order shuffle sum
-__global__ void vertex_sum_kernel(int64_t S, int32_t V, int64_t N, int64_t NI, int32_t L, const double* __restrict__ uG,
-                                  double* __restrict__ u) {
-    const int lane = threadIdx.x & 31;
-    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    if (w >= S * V) return;
-    const int64_t s = w / V, v = w - s * V;
-    const double* src = uG + w * L;
+__global__ void vertex_sum_kernel(int64_t S, int32_t V, int64_t N, int64_t NI, int32_t L, int32_t csl,
+                                  const double* __restrict__ uG, double* __restrict__ u) {
+    // thread per (tile, v, sample-in-tile): consecutive threads read consecutive samples
+    const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int cs = 1 << csl;
+    const int64_t tiles = (S + cs - 1) >> csl;
+    if (x >= tiles * V * cs) return;
+    const int si = (int)(x & (cs - 1));
+    const int64_t tv = x >> csl;
+    const int64_t tile = tv / V, v = tv - tile * V;
+    const int64_t s = (tile << csl) + si;
+    if (s >= S) return;
+    const double* src = uG + ((tile * V + v) * (int64_t)L << csl) + si;
     double acc = 0.0;
-    for (int l = lane; l < L; l += 32) acc += src[l];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) u[s * N + NI + v] = acc;
+    for (int l = 0; l < L; ++l) acc += src[(int64_t)l << csl];
+    u[s * N + NI + v] = acc;
 }
 }  // namespace
 
 cudaError_t launch_vertex_sum(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* uG, double* u,
                               cudaStream_t st) {
-    const int64_t warps = n_samples * g.V;
-    const int64_t blocks = (warps * 32 + 255) / 256;
-    vertex_sum_kernel<<<(unsigned)blocks, 256, 0, st>>>(n_samples, g.V, g.N, g.NI, p.L, uG, u);
+    const int32_t csl = sample_tile_log2(n_samples);
+    const int64_t tiles = (n_samples + (1 << csl) - 1) >> csl;
+    const int64_t threads = (tiles * g.V) << csl;
+    vertex_sum_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(n_samples, g.V, g.N, g.NI, p.L, csl, uG, u);
     return cudaGetLastError();
 }
 

@@ -65,7 +65,6 @@ struct Args {
     int32_t* counter;       // work-queue counter (zeroed by the launcher)
     int32_t chunks;         // sample tiles per edge
     int32_t n_items;        // E * chunks
-    int32_t nws;            // s-warps per CTA (blockDim.x = 32 * NWL * nws)
     int32_t tile_ms;        // recover: max (m | 1) the shared-memory output tile holds (0: none)
 };
 
@@ -111,7 +110,8 @@ struct Cfg {
     static constexpr int NWL = 32 / LW;             // l-warps
     static constexpr int SLW = 32 / LW;             // s-lanes per warp
     static constexpr int NT = 32 * NWL * NWS;       // threads per CTA
-    static constexpr int CS = NWS * SLW * TS;       // samples per item
+    static constexpr int CS = NWS * SLW * TS;       // samples per item (= the sample tile of ends / uG)
+    static constexpr int CSL = CS == 32 ? 5 : (CS == 16 ? 4 : (CS == 8 ? 3 : (CS == 4 ? 2 : (CS == 2 ? 1 : 0))));
     static constexpr int NTAB = REC ? 2 : 1;        // staged tables: mu (, g)
     static constexpr int RN = NLT * TL;             // nodes per round
     static constexpr int IBK = REC ? 8 : 16;        // steps per staging block
@@ -131,7 +131,7 @@ struct Cfg {
 template <int TL, int TS, int LW, int NWS, bool REC>
 __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Args A) {
     using C = Cfg<TL, TS, LW, NWS, REC>;
-    constexpr int NWL = C::NWL, SLW = C::SLW, NT = C::NT, CS = C::CS, NTAB = C::NTAB, RN = C::RN;
+    constexpr int NWL = C::NWL, SLW = C::SLW, NT = C::NT, CS = C::CS, CSL = C::CSL, NTAB = C::NTAB, RN = C::RN;
     constexpr int IBK = C::IBK, NC = C::NC;
     constexpr bool PERM = C::PERM;
     constexpr int NP = TL / 2;               // node pairs per thread
@@ -187,10 +187,11 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
         }
 
         if (m == 0) {
-            if (!REC) {  // no interior: zero end values
-                for (int x = tid; x < CS * 2 * L; x += NT) {
-                    const int s = x / (2 * L), r = x - s * 2 * L;
-                    if (c0 + s < A.S) A.out[((c0 + s) * g.E + e) * 2 * (int64_t)L + r] = 0.0;
+            if (!REC) {  // no interior: zero end values (ends layout [tile][l][code][CS], grf_internal.h)
+                const int64_t tile = it % A.chunks;
+                for (int x = tid; x < L * 2 * CS; x += NT) {
+                    const int l = x / (2 * CS), r = x % (2 * CS);
+                    A.out[((tile * L + l) * 2 * (int64_t)g.E + 2 * e) * CS + r] = 0.0;
                 }
             }
             continue;
@@ -211,8 +212,8 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                     const double beta = ok ? A.cL[l] / h : 0.0;
 #pragma unroll
                     for (int j = 0; j < TS; ++j) {
-                        const double ul = ok ? A.uG[(sidx[j] * g.V + vu) * (int64_t)L + l] : 0.0;
-                        const double ur = ok ? A.uG[(sidx[j] * g.V + vv) * (int64_t)L + l] : 0.0;
+                        const double ul = ok ? A.uG[ug_index(sidx[j], vu, l, L, g.V, CSL)] : 0.0;
+                        const double ur = ok ? A.uG[ug_index(sidx[j], vv, l, L, g.V, CSL)] : 0.0;
                         Y[n][j] = beta * (m == 1 ? ul + ur : ul);
                         Z[n][j] = beta * (m == 1 ? ul + ur : ur);
                     }
@@ -446,8 +447,8 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                             const double nk = gg * mu;
 #pragma unroll
                             for (int j = 0; j < TS; ++j) {
-                                const double ul = ok ? A.uG[(sidx[j] * g.V + vu) * (int64_t)L + l] : 0.0;
-                                const double ur = ok ? A.uG[(sidx[j] * g.V + vv) * (int64_t)L + l] : 0.0;
+                                const double ul = ok ? A.uG[ug_index(sidx[j], vu, l, L, g.V, CSL)] : 0.0;
+                                const double ur = ok ? A.uG[ug_index(sidx[j], vv, l, L, g.V, CSL)] : 0.0;
                                 aL[j] = fma(-nk, Y[n][j], aL[j]);
                                 Y[n][j] = fma(beta, ur, fma(-mu, Y[n][j], wl[j]));
                                 Z[n][j] = fma(beta, ul, fma(-mu, Z[n][j], wr[j]));
@@ -529,19 +530,19 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                 __syncthreads();
                 fold(nblk - 1);
             } else {
-                // w_1 = g_0 Z (right sweep end, position 0), w_m = g_0 Y (left sweep end); g_0 = g_{m-1}
+                // w_1 = g_0 Z (right sweep end, position 0), w_m = g_0 Y (left sweep end); g_0 = g_{m-1}.
+                // ends layout [tile][l][code][CS]: the item's 2 codes x CS samples are contiguous per l;
+                // slots past S land in the tile's padding (never read)
+                const int64_t tile = it % A.chunks;
 #pragma unroll
-                for (int j = 0; j < TS; ++j) {
-                    const int64_t s = c0 + st0 + j;
-                    if (s < A.S) {
-                        double* o = A.out + (s * g.E + e) * 2 * (int64_t)L + rb;
+                for (int n = 0; n < TL; ++n) {
+                    const int l = rb + slot(n);
+                    if (l < L) {
+                        double* o = A.out + ((tile * L + l) * 2 * (int64_t)g.E + 2 * e) * CS + st0;
 #pragma unroll
-                        for (int n = 0; n < TL; ++n) {
-                            const int sn = slot(n);
-                            if (rb + sn < L) {
-                                o[sn] = g0[n] * Z[n][j];
-                                o[L + sn] = g0[n] * Y[n][j];
-                            }
+                        for (int j = 0; j < TS; ++j) {
+                            o[j] = g0[n] * Z[n][j];
+                            o[CS + j] = g0[n] * Y[n][j];
                         }
                     }
                 }
