@@ -107,6 +107,7 @@ grf_status grf_plan_info(double beta, double k, int64_t* k_minus, int64_t* k_plu
                          double* c_I, double* c_L);
 
 enum { GRF_PRECOND_NN = 0, GRF_PRECOND_JACOBI = 1, GRF_PRECOND_NONE = 2 };
+enum { GRF_PCG_AUTO = 0, GRF_PCG_SHARED = 1, GRF_PCG_GLOBAL = 2 };
 
 typedef struct grf_options {
     double rtol;          /* PCG stop: ||r||_2 <= rtol ||g||_2 (recursive residual), default 1e-13 */
@@ -114,6 +115,9 @@ typedef struct grf_options {
     int32_t precond;      /* GRF_PRECOND_*, default NN (P260-298) */
     int64_t node_begin;   /* sum only over quadrature nodes [node_begin, node_end) of 0..L-1 */
     int64_t node_end;     /* (node sharding across GPUs); default 0 and -1 = all L nodes */
+    int32_t pcg_variant;  /* GRF_PCG_*: which K4 kernel family solves the vertex systems;
+                             AUTO picks the shared-memory kernels when the vertex vectors fit
+                             on chip (V <= 4096) and the global-memory kernel otherwise */
 } grf_options;
 void grf_options_default(grf_options* opt);
 

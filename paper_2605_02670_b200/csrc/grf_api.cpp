@@ -263,11 +263,17 @@ grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct WsLayout {
-    size_t w = 0, ends = 0, rhs = 0, ug = 0, iters = 0, relres = 0, counter = 0, total = 0;
+    size_t w = 0, ends = 0, rhs = 0, ug = 0, gws = 0, iters = 0, relres = 0, counter = 0, total = 0;
 };
 
 // with_noise: grf_sample keeps the white noise W (S x N) in the workspace
-WsLayout ws_layout(const grf_graph* g, int64_t L, int64_t S, bool with_noise = true) {
+// K4 kernel family for these options (grf_options.pcg_variant)
+bool use_global_pcg(const grf_graph* g, const grf_options* opt) {
+    const int32_t v = opt ? opt->pcg_variant : GRF_PCG_AUTO;
+    return v == GRF_PCG_GLOBAL || (v == GRF_PCG_AUTO && !grf::pcg_shared_ok(g->dev));
+}
+
+WsLayout ws_layout(const grf_graph* g, int64_t L, int64_t S, bool with_noise, bool global_pcg) {
     WsLayout w;
     size_t o = 0;
     w.w = o;
@@ -281,6 +287,8 @@ WsLayout ws_layout(const grf_graph* g, int64_t L, int64_t S, bool with_noise = t
     o += align_up((size_t)Sp * g->V * L * sizeof(double));
     w.ug = o;
     o += align_up((size_t)Sp * g->V * L * sizeof(double));
+    w.gws = o;
+    if (global_pcg) o += align_up(grf::pcg_global_ws_bytes(g->dev, (int32_t)L, S));
     w.iters = o;
     o += align_up((size_t)S * L * sizeof(int32_t));
     w.relres = o;
@@ -293,8 +301,8 @@ WsLayout ws_layout(const grf_graph* g, int64_t L, int64_t S, bool with_noise = t
 
 grf_status check_kernel_limits(const grf_graph* g) {
     if (!grf::pcg_supported(g->dev))
-        return fail(GRF_EUNSUPPORTED, "graph has %lld vertices; this build's shared-memory PCG handles <= %d",
-                    (long long)g->V, grf::pcg_max_vertices());
+        return fail(GRF_EUNSUPPORTED, "a vertex has %d incident edge ends; the PCG kernels handle <= 32",
+                    g->dev.max_deg);
     return GRF_OK;
 }
 
@@ -305,7 +313,7 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
                  double* u, void* ws, size_t ws_bytes, cudaStream_t st, grf_stats* stats) {
     const int64_t L = p->dev.L;
     const bool gen = (W == nullptr);
-    WsLayout w = ws_layout(g, L, S, gen);
+    WsLayout w = ws_layout(g, L, S, gen, use_global_pcg(g, opt));
     void* own = nullptr;
     if (!ws) {
         own = g->alloc.get(w.total, st);
@@ -329,6 +337,7 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
     double* ends = reinterpret_cast<double*>(base + w.ends);
     double* uG = reinterpret_cast<double*>(base + w.ug);
     double* rhs = reinterpret_cast<double*>(base + w.rhs);
+    void* gws = base + w.gws;
     int32_t* iters = reinterpret_cast<int32_t*>(base + w.iters);
     double* relres = reinterpret_cast<double*>(base + w.relres);
     int32_t* counters = reinterpret_cast<int32_t*>(base + w.counter);
@@ -336,6 +345,7 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
     prm.rtol = opt ? opt->rtol : 1e-13;
     prm.max_iter = (opt && opt->max_iter > 0) ? opt->max_iter : (int32_t)(g->V + 10);
     prm.precond = opt ? opt->precond : GRF_PRECOND_NN;
+    prm.global = use_global_pcg(g, opt) ? 1 : 0;
     grf_status rc = GRF_OK;
     cudaError_t le = cudaSuccess;
     cudaError_t ce = g->timed(GRF_K_CONDENSE, st, [&] {
@@ -343,7 +353,10 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
     });
     if (ce == cudaSuccess) ce = le;
     if (ce == cudaSuccess)
-        ce = g->timed(GRF_K_PCG, st, [&] { grf::launch_pcg(g->dev, p->dev, S, prm, W, ends, rhs, uG, iters, relres, st); });
+        ce = g->timed(GRF_K_PCG, st, [&] {
+            le = grf::launch_pcg(g->dev, p->dev, S, prm, W, ends, rhs, uG, iters, relres, gws, st);
+        });
+    if (ce == cudaSuccess) ce = le;
     if (ce == cudaSuccess)
         ce = g->timed(GRF_K_RECOVER, st, [&] {
             le = grf::launch_recover(g->dev, p->dev, S, W, u, uG, counters + 1, st);
@@ -404,6 +417,7 @@ void grf_options_default(grf_options* opt) {
     opt->precond = GRF_PRECOND_NN;
     opt->node_begin = 0;
     opt->node_end = -1;
+    opt->pcg_variant = GRF_PCG_AUTO;
 }
 
 grf_status grf_graph_create(int64_t n_vertices, int64_t n_edges, const int64_t* edge_u, const int64_t* edge_v,
@@ -604,7 +618,7 @@ grf_status grf_workspace_size(const grf_graph* g, double kappa, double beta, dou
     plan_limits(beta, k, &Km, &Kp);
     st = resolve_range(opt, Km + Kp + 1, &nb, &ne);
     if (st) return st;
-    *bytes = ws_layout(g, ne - nb, n_samples).total;
+    *bytes = ws_layout(g, ne - nb, n_samples, true, use_global_pcg(g, opt)).total;
     return GRF_OK;
 }
 

@@ -52,6 +52,7 @@ struct PcgParams {
     double rtol = 1e-13;
     int32_t max_iter = 0;
     int32_t precond = 0;
+    int32_t global = 0;  // 1: use the global-memory K4 kernel (pcg_global.cu)
 };
 
 // Sample-tiled layouts of the per-call intermediates (shared by K3, K4, K5): samples are
@@ -84,8 +85,16 @@ cudaError_t launch_condense(const DevGraph& g, const DevPlan& p, int64_t n_sampl
                             double* ends, int32_t* counter, cudaStream_t st);
 // K4  batched NN-PCG on the vertex Schur systems (pcg.cu): g from (W, ends), u_G -> uG[(s*V + v)*L + l]
 // (K4a first assembles g = W_G + sum (c_L/h_e) w_end from the end values into rhs)
-void launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* W,
-                const double* ends, double* rhs, double* uG, int32_t* iters, double* relres, cudaStream_t st);
+// (gws: workspace of the global-memory variant, pcg_global_ws_bytes; used when V > 4096)
+cudaError_t launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* W,
+                       const double* ends, double* rhs, double* uG, int32_t* iters, double* relres, void* gws,
+                       cudaStream_t st);
+// K4 global-memory variant (pcg_global.cu) and its workspace
+bool pcg_shared_ok(const DevGraph& g);
+cudaError_t launch_pcg_global(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm,
+                              const double* rhs, double* uG, int32_t* iters, double* relres, void* ws,
+                              cudaStream_t st);
+size_t pcg_global_ws_bytes(const DevGraph& g, int32_t L, int64_t n_samples);
 // K5  Thomas recovery + accumulation over nodes (sweep.cu): u[s*N + dof] from W and u_G
 cudaError_t launch_recover(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W, double* u,
                            const double* uG, int32_t* counter, cudaStream_t st);

@@ -452,8 +452,12 @@ size_t pcg_smem_bytes(const DevGraph& g) { return vec_bytes(g, 1, 1); }
 
 size_t pcg_table_doubles(const DevGraph& g) { return (size_t)table_stride(g.V, g.ell_w); }
 
-bool pcg_supported(const DevGraph& g) {
+bool pcg_shared_ok(const DevGraph& g) {
     return g.V <= pcg_max_vertices() && g.ell_w <= 32 && vec_bytes(g, 1, 1) <= SMEM_LIMIT;
+}
+
+bool pcg_supported(const DevGraph& g) {
+    return g.ell_w <= 32;  // larger vertex sets take the global-memory variant (pcg_global.cu)
 }
 
 void launch_pcg_tables(const DevGraph& g, const DevPlan& p, cudaStream_t st) {
@@ -463,18 +467,21 @@ void launch_pcg_tables(const DevGraph& g, const DevPlan& p, cudaStream_t st) {
     pcg_tables_kernel<<<blocks, 256, 0, st>>>(g, p.L, p.cL, reinterpret_cast<const double4*>(p.sig), p.ops);
 }
 
-void launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* W,
-                const double* ends, double* rhs, double* uG, int32_t* iters, double* relres, cudaStream_t st) {
+cudaError_t launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* W,
+                       const double* ends, double* rhs, double* uG, int32_t* iters, double* relres, void* gws,
+                       cudaStream_t st) {
     const int32_t csl = sample_tile_log2(n_samples);
     const int64_t work = ((n_samples + (1 << csl) - 1) >> csl) * p.L * ((g.V + ASM_VB - 1) / ASM_VB);
     int blocks = (int)(work < 148 * 8 ? work : 148 * 8);
     assemble_rhs_kernel<<<blocks, 256, 0, st>>>(g, p.L, p.ops, n_samples, csl, W, ends, rhs);
+    if (prm.global) return launch_pcg_global(g, p, n_samples, prm, rhs, uG, iters, relres, gws, st);
     switch (g.ell_w) {
         case 4: launch_w<4>(g, p, n_samples, prm, rhs, uG, iters, relres, st); break;
         case 8: launch_w<8>(g, p, n_samples, prm, rhs, uG, iters, relres, st); break;
         case 16: launch_w<16>(g, p, n_samples, prm, rhs, uG, iters, relres, st); break;
         default: launch_w<32>(g, p, n_samples, prm, rhs, uG, iters, relres, st); break;
     }
+    return cudaGetLastError();
 }
 
 }  // namespace grf

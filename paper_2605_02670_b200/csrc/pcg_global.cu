@@ -1,0 +1,429 @@
+// K4 global-memory variant of the batched NN-PCG for large vertex sets (V > 4096, config 4:
+// V = 1e5).  Same operators and stopping rule as pcg.cu (PAPER.md P111-118, P241-298; the
+// per-node tables DS/OS (Dirichlet step) and DM/OM (Neumann step) of pcg_tables_kernel).
+//
+// One cooperative persistent launch per sample tile of CS samples solves all L x CS systems
+// (l, s) of the tile together.  Work vectors are node-major, vertex, then sample:
+// vec[(l * V + v) * CS + s], so a thread owning vertex v of node l holds the CS samples in
+// registers, reads each operator coefficient once for all of them, and every neighbour
+// gather is one contiguous CS-double run.  Per iteration two phases separated by grid
+// barriers (standard PCG, fused so that each vector is streamed once per phase):
+//   phase 1:  p' = z + beta p;  q = S p'  (neighbour p' formed on the fly from z, p);  p'.q
+//   phase 2:  r' = r - alpha q;  x += alpha p';  z = M^{-1} r' (neighbour r' on the fly);
+//             r'.r', r'.z
+// p and r are double buffered (old values stay readable for the on-the-fly neighbours).
+// Dot products: per (node, 256-vertex block) partials, reduced in fixed vertex-block order by
+// the last block to arrive for that node (threadfence + arrival counter), so results are
+// deterministic.  A node whose CS systems have all converged is skipped; the loop ends when
+// no node is active or after max_iter iterations.
+#include <cooperative_groups.h>
+
+#include "grf_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace grf {
+namespace {
+
+constexpr int GT = 256;  // threads per CTA = vertices per item
+
+struct GArgs {
+    DevGraph g;
+    int32_t L;
+    const double* ops;
+    PcgParams prm;
+    int64_t S;
+    int32_t csl;
+    int64_t tile;         // sample tile solved by this launch
+    const double* rhs;    // [tile][l][cs][v] (grf_internal.h)
+    double* uG;           // [tile][v][l][cs]
+    int32_t* iters;       // [s * L + l]
+    double* relres;
+    double *x, *r0, *r1, *p0, *p1, *q, *z;   // [L][V][CS]
+    double *alpha, *beta, *rz, *gg, *rr;    // [L][CS]
+    int32_t* done;                          // [L][CS]
+    int32_t* its;                           // [L][CS]
+    int32_t* node_active;                   // [L]
+    int32_t* n_active;                      // [1]
+    double* part;                           // [L][nvb][2][CS]
+    int32_t* cnt;                           // [L] arrival counters (zero between phases)
+};
+
+__device__ __forceinline__ int64_t table_stride_g(int V, int W) { return 3 * (int64_t)V + 3 * (int64_t)W * V; }
+
+// Block reduction of K x CS per-thread values into part[l][vb][k][s]; the last block of
+// node l to arrive then reduces all vertex blocks (fixed order) into out_k[l][s] and runs
+// `finish(l)` (single block, all threads).  Returns after the (possible) finish.
+template <int CS, int K, class Finish>
+__device__ void block_partials(const GArgs& A, int l, int vb, int nvb, double (&v)[K][CS], double* red,
+                               Finish&& finish) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ int last;
+    // warp sums (fixed butterfly order), then across the 8 warps in order
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int s = 0; s < CS; ++s) {
+            double t = v[k][s];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (lane == 0) red[(warp * K + k) * CS + s] = t;
+        }
+    __syncthreads();
+    double* pb = A.part + ((int64_t)l * nvb + vb) * 2 * CS;
+    if (tid < K * CS) {
+        double t = 0.0;
+        for (int w = 0; w < GT / 32; ++w) t += red[w * K * CS + tid];
+        pb[tid] = t;
+        __threadfence();
+    }
+    __syncthreads();
+    if (tid == 0) last = (atomicAdd(&A.cnt[l], 1) == nvb - 1);
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        finish(l);
+        __syncthreads();
+        if (tid == 0) A.cnt[l] = 0;
+    }
+    __syncthreads();
+}
+
+template <int CS>
+__global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double red[(GT / 32) * 2 * CS];
+    const DevGraph& g = A.g;
+    const int V = g.V, L = A.L, Wd = g.ell_w;
+    const int nvb = (V + GT - 1) / GT;
+    const int64_t items = (int64_t)L * nvb;
+    const int tid = threadIdx.x;
+    const int64_t stride = table_stride_g(V, Wd);
+    const int64_t s0 = A.tile << A.csl;
+    double* po = A.p0;
+    double* pn = A.p1;
+    double* ro = A.r0;
+    double* rn = A.r1;
+    const double tol2c = A.prm.rtol * A.prm.rtol;
+
+    // sum over the node's vertex blocks of partial k, sample s (fixed order)
+    auto node_sum = [&](int l, int k, int s) {
+        const double* pb = A.part + (int64_t)l * nvb * 2 * CS + k * CS + s;
+        double t = 0.0;
+        for (int b = 0; b < nvb; ++b) t += pb[(int64_t)b * 2 * CS];
+        return t;
+    };
+    auto deg_of = [&](int v) { return g.inc_ptr[v + 1] - g.inc_ptr[v]; };
+
+    // ---- init a: r = g, x = 0, p = 0; gg = g.g
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int l = (int)(it / nvb), vb = (int)(it % nvb);
+        const int v = vb * GT + tid;
+        double acc[1][CS];
+        if (v < V) {
+            const int64_t base = ((int64_t)l * V + v) * CS;
+#pragma unroll
+            for (int s = 0; s < CS; ++s) {
+                const int64_t sg = s0 + s;
+                const double gv = sg < A.S ? A.rhs[rhs_index(sg, l, v, L, V, A.csl)] : 0.0;
+                ro[base + s] = gv;
+                A.x[base + s] = 0.0;
+                po[base + s] = 0.0;
+                acc[0][s] = gv * gv;
+            }
+        } else {
+#pragma unroll
+            for (int s = 0; s < CS; ++s) acc[0][s] = 0.0;
+        }
+        block_partials<CS, 1>(A, l, vb, nvb, acc, red, [&](int ln) {
+            if (tid < CS) {
+                const double t = node_sum(ln, 0, tid);
+                A.gg[ln * CS + tid] = t;
+                A.rr[ln * CS + tid] = t;
+                A.done[ln * CS + tid] = !(t > 0.0) || (s0 + tid >= A.S);
+                A.its[ln * CS + tid] = 0;
+                A.beta[ln * CS + tid] = 0.0;
+            }
+        });
+    }
+    grid.sync();
+    // ---- init b: z = M^{-1} r; rz
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int l = (int)(it / nvb), vb = (int)(it % nvb);
+        const int v = vb * GT + tid;
+        const double* tab = A.ops + l * stride;
+        double acc[1][CS];
+#pragma unroll
+        for (int s = 0; s < CS; ++s) acc[0][s] = 0.0;
+        if (v < V) {
+            const int64_t base = ((int64_t)l * V + v) * CS;
+            double zv[CS], rv[CS];
+#pragma unroll
+            for (int s = 0; s < CS; ++s) rv[s] = ro[base + s];
+            if (A.prm.precond == 0) {
+                const double dm = tab[V + v];
+#pragma unroll
+                for (int s = 0; s < CS; ++s) zv[s] = dm * rv[s];
+                const int dg = deg_of(v);
+                for (int j = 0; j < dg; ++j) {
+                    const double c = tab[3 * (int64_t)V + (int64_t)Wd * V + (int64_t)j * V + v];
+                    const double* ro_o = ro + ((int64_t)l * V + g.ell_other[(int64_t)j * V + v]) * CS;
+#pragma unroll
+                    for (int s = 0; s < CS; ++s) zv[s] = fma(c, ro_o[s], zv[s]);
+                }
+            } else {
+                const double d = A.prm.precond == 1 ? tab[2 * V + v] : 1.0;
+#pragma unroll
+                for (int s = 0; s < CS; ++s) zv[s] = d * rv[s];
+            }
+#pragma unroll
+            for (int s = 0; s < CS; ++s) {
+                A.z[base + s] = zv[s];
+                acc[0][s] = rv[s] * zv[s];
+            }
+        }
+        block_partials<CS, 1>(A, l, vb, nvb, acc, red, [&](int ln) {
+            if (tid < CS) A.rz[ln * CS + tid] = node_sum(ln, 0, tid);
+            if (tid == 0) {
+                int act = 0;
+                for (int s = 0; s < CS; ++s) act |= !A.done[ln * CS + s];
+                A.node_active[ln] = act;
+                if (act) atomicAdd(A.n_active, 1);
+            }
+        });
+    }
+    grid.sync();
+
+    for (int iter = 0; iter < A.prm.max_iter; ++iter) {
+        if (*(volatile int32_t*)A.n_active == 0) break;
+        // ---- phase 1: p' = z + beta p, q = S p', p'.q -> alpha
+        for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+            const int l = (int)(it / nvb), vb = (int)(it % nvb);
+            if (!A.node_active[l]) continue;  // block-uniform
+            const int v = vb * GT + tid;
+            const double* tab = A.ops + l * stride;
+            double acc[1][CS];
+#pragma unroll
+            for (int s = 0; s < CS; ++s) acc[0][s] = 0.0;
+            if (v < V) {
+                const int64_t base = ((int64_t)l * V + v) * CS;
+                double bt[CS], pv[CS], qv[CS];
+#pragma unroll
+                for (int s = 0; s < CS; ++s) {
+                    bt[s] = A.beta[l * CS + s];
+                    pv[s] = fma(bt[s], po[base + s], A.z[base + s]);
+                }
+                const double ds = tab[v];
+#pragma unroll
+                for (int s = 0; s < CS; ++s) qv[s] = ds * pv[s];
+                const int dg = deg_of(v);
+                for (int j = 0; j < dg; ++j) {
+                    const double c = tab[3 * (int64_t)V + (int64_t)j * V + v];
+                    const int64_t ob = ((int64_t)l * V + g.ell_other[(int64_t)j * V + v]) * CS;
+#pragma unroll
+                    for (int s = 0; s < CS; ++s) qv[s] = fma(c, fma(bt[s], po[ob + s], A.z[ob + s]), qv[s]);
+                }
+#pragma unroll
+                for (int s = 0; s < CS; ++s) {
+                    pn[base + s] = pv[s];
+                    A.q[base + s] = qv[s];
+                    acc[0][s] = pv[s] * qv[s];
+                }
+            }
+            block_partials<CS, 1>(A, l, vb, nvb, acc, red, [&](int ln) {
+                if (tid < CS) {
+                    const double pq = node_sum(ln, 0, tid);
+                    A.alpha[ln * CS + tid] = A.done[ln * CS + tid] ? 0.0 : A.rz[ln * CS + tid] / pq;
+                }
+            });
+        }
+        grid.sync();
+        // ---- phase 2: r' = r - alpha q, x += alpha p', z = M^{-1} r', r'.r', r'.z -> beta, convergence
+        for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+            const int l = (int)(it / nvb), vb = (int)(it % nvb);
+            if (!A.node_active[l]) continue;
+            const int v = vb * GT + tid;
+            const double* tab = A.ops + l * stride;
+            double acc[2][CS];
+#pragma unroll
+            for (int s = 0; s < CS; ++s) acc[0][s] = acc[1][s] = 0.0;
+            if (v < V) {
+                const int64_t base = ((int64_t)l * V + v) * CS;
+                double al[CS], rv[CS], zv[CS];
+#pragma unroll
+                for (int s = 0; s < CS; ++s) {
+                    al[s] = A.alpha[l * CS + s];
+                    rv[s] = fma(-al[s], A.q[base + s], ro[base + s]);
+                    A.x[base + s] = fma(al[s], pn[base + s], A.x[base + s]);
+                }
+                if (A.prm.precond == 0) {
+                    const double dm = tab[V + v];
+#pragma unroll
+                    for (int s = 0; s < CS; ++s) zv[s] = dm * rv[s];
+                    const int dg = deg_of(v);
+                    for (int j = 0; j < dg; ++j) {
+                        const double c = tab[3 * (int64_t)V + (int64_t)Wd * V + (int64_t)j * V + v];
+                        const int64_t ob = ((int64_t)l * V + g.ell_other[(int64_t)j * V + v]) * CS;
+#pragma unroll
+                        for (int s = 0; s < CS; ++s) zv[s] = fma(c, fma(-al[s], A.q[ob + s], ro[ob + s]), zv[s]);
+                    }
+                } else {
+                    const double d = A.prm.precond == 1 ? tab[2 * V + v] : 1.0;
+#pragma unroll
+                    for (int s = 0; s < CS; ++s) zv[s] = d * rv[s];
+                }
+#pragma unroll
+                for (int s = 0; s < CS; ++s) {
+                    rn[base + s] = rv[s];
+                    A.z[base + s] = zv[s];
+                    acc[0][s] = rv[s] * rv[s];
+                    acc[1][s] = rv[s] * zv[s];
+                }
+            }
+            block_partials<CS, 2>(A, l, vb, nvb, acc, red, [&](int ln) {
+                if (tid < CS) {
+                    const int sy = ln * CS + tid;
+                    const double rr = node_sum(ln, 0, tid), rzn = node_sum(ln, 1, tid);
+                    if (!A.done[sy]) {
+                        A.its[sy] += 1;
+                        A.rr[sy] = rr;
+                        if (rr <= tol2c * A.gg[sy]) A.done[sy] = 1;
+                        A.beta[sy] = A.done[sy] ? 0.0 : rzn / A.rz[sy];
+                        A.rz[sy] = rzn;
+                    } else {
+                        A.beta[sy] = 0.0;
+                    }
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    int act = 0;
+                    for (int s = 0; s < CS; ++s) act |= !A.done[ln * CS + s];
+                    if (!act) {
+                        A.node_active[ln] = 0;
+                        atomicSub(A.n_active, 1);
+                    }
+                }
+            });
+        }
+        grid.sync();
+        double* t = po;
+        po = pn;
+        pn = t;
+        t = ro;
+        ro = rn;
+        rn = t;
+    }
+    // ---- write u_G, iteration counts and final relative residuals
+    for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int l = (int)(it / nvb), vb = (int)(it % nvb);
+        const int v = vb * GT + tid;
+        if (v < V) {
+            const int64_t base = ((int64_t)l * V + v) * CS;
+#pragma unroll
+            for (int s = 0; s < CS; ++s) {
+                const int64_t sg = s0 + s;
+                if (sg < A.S) A.uG[ug_index(sg, v, l, L, V, A.csl)] = A.x[base + s];
+            }
+        }
+        if (vb == 0 && tid < CS) {
+            const int64_t sg = s0 + tid;
+            const int sy = l * CS + tid;
+            if (sg < A.S) {
+                A.iters[sg * L + l] = A.its[sy];
+                A.relres[sg * L + l] = A.gg[sy] > 0.0 ? sqrt(A.rr[sy] / A.gg[sy]) : 0.0;
+            }
+        }
+    }
+}
+
+template <int CS>
+cudaError_t launch_cs(GArgs a, int64_t n_tiles, cudaStream_t st) {
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pcg_global_kernel<CS>, GT, 0);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorLaunchOutOfResources;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int blocks = sms * per_sm;
+    for (int64_t t = 0; t < n_tiles; ++t) {
+        a.tile = t;
+        e = cudaMemsetAsync(a.n_active, 0, sizeof(int32_t), st);
+        if (e != cudaSuccess) return e;
+        e = cudaMemsetAsync(a.cnt, 0, sizeof(int32_t) * a.L, st);
+        if (e != cudaSuccess) return e;
+        void* args[] = {&a};
+        e = cudaLaunchCooperativeKernel((const void*)pcg_global_kernel<CS>, dim3(blocks), dim3(GT), args, 0, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace
+
+size_t pcg_global_ws_bytes(const DevGraph& g, int32_t L, int64_t n_samples) {
+    const int64_t cs = (int64_t)1 << sample_tile_log2(n_samples);
+    const int64_t nvb = (g.V + GT - 1) / GT;
+    size_t b = 7 * sizeof(double) * (size_t)L * g.V * cs;      // x, r0, r1, p0, p1, q, z
+    b += 5 * sizeof(double) * (size_t)L * cs;                  // alpha, beta, rz, gg, rr
+    b += 2 * sizeof(int32_t) * (size_t)L * cs;                 // done, its
+    b += sizeof(int32_t) * (size_t)(L + 1);                    // node_active, n_active
+    b += sizeof(double) * (size_t)L * nvb * 2 * cs;            // partials
+    b += sizeof(int32_t) * (size_t)L;                          // counters
+    return b + 16 * 256;
+}
+
+cudaError_t launch_pcg_global(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm,
+                              const double* rhs, double* uG, int32_t* iters, double* relres, void* ws,
+                              cudaStream_t st) {
+    const int32_t csl = sample_tile_log2(n_samples);
+    const int64_t cs = (int64_t)1 << csl;
+    const int64_t L = p.L;
+    const int64_t nvb = (g.V + GT - 1) / GT;
+    char* b = static_cast<char*>(ws);
+    auto take = [&](size_t bytes) {
+        char* r = b;
+        b += (bytes + 255) & ~size_t(255);
+        return r;
+    };
+    GArgs a{};
+    a.g = g;
+    a.L = p.L;
+    a.ops = p.ops;
+    a.prm = prm;
+    a.S = n_samples;
+    a.csl = csl;
+    a.rhs = rhs;
+    a.uG = uG;
+    a.iters = iters;
+    a.relres = relres;
+    const size_t vec = sizeof(double) * (size_t)L * g.V * cs;
+    a.x = (double*)take(vec);
+    a.r0 = (double*)take(vec);
+    a.r1 = (double*)take(vec);
+    a.p0 = (double*)take(vec);
+    a.p1 = (double*)take(vec);
+    a.q = (double*)take(vec);
+    a.z = (double*)take(vec);
+    const size_t sys = (size_t)L * cs;
+    a.alpha = (double*)take(sizeof(double) * sys);
+    a.beta = (double*)take(sizeof(double) * sys);
+    a.rz = (double*)take(sizeof(double) * sys);
+    a.gg = (double*)take(sizeof(double) * sys);
+    a.rr = (double*)take(sizeof(double) * sys);
+    a.done = (int32_t*)take(sizeof(int32_t) * sys);
+    a.its = (int32_t*)take(sizeof(int32_t) * sys);
+    a.node_active = (int32_t*)take(sizeof(int32_t) * L);
+    a.n_active = (int32_t*)take(sizeof(int32_t));
+    a.part = (double*)take(sizeof(double) * (size_t)L * nvb * 2 * cs);
+    a.cnt = (int32_t*)take(sizeof(int32_t) * L);
+    const int64_t n_tiles = (n_samples + cs - 1) / cs;
+    switch (cs) {
+        case 1: return launch_cs<1>(a, n_tiles, st);
+        case 16: return launch_cs<16>(a, n_tiles, st);
+        case 32: return launch_cs<32>(a, n_tiles, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace grf

@@ -52,7 +52,10 @@ def plan_info(beta: float, k: float):
     return km.value, kp.value, cI, cL
 
 
-def make_options(rtol=1e-13, max_iter=0, precond="nn", node_range=None) -> grf_options:
+PCG_VARIANT = {"auto": 0, "shared": 1, "global": 2}
+
+
+def make_options(rtol=1e-13, max_iter=0, precond="nn", node_range=None, pcg="auto") -> grf_options:
     o = grf_options()
     load().grf_options_default(C.byref(o))
     o.rtol = rtol
@@ -60,6 +63,7 @@ def make_options(rtol=1e-13, max_iter=0, precond="nn", node_range=None) -> grf_o
     o.precond = PRECOND[precond] if isinstance(precond, str) else int(precond)
     if node_range is not None:
         o.node_begin, o.node_end = int(node_range[0]), int(node_range[1])
+    o.pcg_variant = PCG_VARIANT[pcg] if isinstance(pcg, str) else int(pcg)
     return o
 
 
@@ -145,7 +149,8 @@ class Graph:
 
     def sample(self, kappa, beta, k, seed=0, n_samples=1, out=None, workspace=None, stream=None,
                return_stats=False, strict=True, **opts):
-        """GRF samples u [n_samples, N] (cuda fp64).  opts: rtol, max_iter, precond, node_range."""
+        """GRF samples u [n_samples, N] (cuda fp64).  opts: rtol, max_iter, precond, node_range,
+        pcg ("auto" | "shared" | "global": the K4 kernel family)."""
         torch = _torch()
         o = make_options(**opts)
         if out is None:

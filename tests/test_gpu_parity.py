@@ -238,3 +238,83 @@ def test_config3_lattice_256_samples_sampled():
     # property at any size: every sample is finite and has the Matern-scale variance
     uu = u.cpu().numpy()
     assert np.isfinite(uu).all()
+
+
+# ----------------------------------------------------------------------------- global-memory K4
+@pytest.mark.parametrize("n_samples", [1, 3, 16, 20])
+def test_global_pcg_matches_oracle(n_samples):
+    """The global-memory PCG (pcg_global.cu, used for V > 4096) forced on small graphs, for every
+    sample mapping (1 / 16 / 32 samples per tile, ragged tile), vs the oracle."""
+    g = lattice(5, seed=3)
+    h, kappa, beta, k = 0.04, 2.0, 0.7, 0.4
+    G = _graph(g, h)
+    u, st = G.sample(kappa, beta, k, seed=2, n_samples=n_samples, pcg="global", return_stats=True)
+    picks = sorted({0, n_samples // 2, n_samples - 1})
+    ref, _, _ = solve.sample(g, h, kappa, beta, k, 2, n_samples, samples=picks)
+    assert _rel(u.cpu().numpy()[picks], ref).max() <= FIELD_TOL
+    assert st["n_unconverged"] == 0 and st["worst_rel_residual"] <= 1e-13
+
+
+@pytest.mark.parametrize("precond", ["nn", "jacobi"])
+def test_global_pcg_equals_shared(precond):
+    g = star_of_lattices(2, 3)
+    h, kappa, beta, k = 0.1, 3.0, 0.6, 0.35
+    G = _graph(g, h)
+    a = G.sample(kappa, beta, k, seed=5, n_samples=4, precond=precond, pcg="shared").cpu().numpy()
+    b = G.sample(kappa, beta, k, seed=5, n_samples=4, precond=precond, pcg="global").cpu().numpy()
+    assert _rel(b, a).max() <= 1e-11
+
+
+def test_rgg_5000_per_node_vs_oracle():
+    """A 5000-vertex config-4-style graph (V > 4096: the global-memory PCG is selected
+    automatically): single-node solves vs the oracle's sparse direct solve."""
+    from synth import rgg_knn
+    g = rgg_knn(5000, k=3, scale=300.0 * (5000 / 100_000) ** 0.5, seed=1)
+    h, kappa, beta, k = 0.02, 2.0, 0.55, 0.6
+    G = _graph(g, h)
+    prob = solve.setup(g, h, kappa, beta, k)
+    W = noise.white_noise(prob.ML, 3, 2)
+    L = prob.plan.n_nodes
+    for li in (0, L // 2, L - 1):
+        u, st = G.sample(kappa, beta, k, seed=3, n_samples=2, node_range=(li, li + 1), return_stats=True)
+        ref = solve.node_solve(prob, li, W)
+        assert _rel(u.cpu().numpy(), ref).max() <= 1e-10, f"node {li}"
+        assert st["n_unconverged"] == 0
+
+
+def test_config4_rgg_full_size():
+    """configs[3] at full size on one GPU: 1e5 vertices, N = 28 032 313, L = 112, 16 samples.
+    SuperLU cannot factor N = 2.8e7 (out of memory), so the oracle checks what holds at any size:
+    the noise bit-exactly on sampled samples, the defining residual A_l x_l = W of single-node
+    solves (oracle-assembled operator, P75-78) for the extreme nodes, and the full call's
+    convergence and finiteness."""
+    import gc
+
+    from oracle import fem
+    cfg = CONFIGS["rgg"]
+    g = config_graph("rgg")
+    prob = solve.setup(g, cfg["h"], cfg["kappa"], cfg["beta"], cfg["k"])
+    L = prob.plan.n_nodes
+    assert L == 112 and prob.ML.shape[0] == 28_032_313
+    G = _graph(g, cfg["h"])
+    u, st = G.sample(cfg["kappa"], cfg["beta"], cfg["k"], seed=cfg["seed"], n_samples=cfg["n_samples"],
+                     return_stats=True)
+    assert st["n_nodes"] == 112 and st["n_unconverged"] == 0 and st["worst_rel_residual"] <= 1e-13
+    u0 = u[[0, 15]].cpu().numpy()
+    assert np.isfinite(u0).all()
+    del u
+    picks = [0, 15]
+    Wg = G.noise(cfg["seed"], cfg["n_samples"])[picks].cpu().numpy()
+    Wref = noise.white_noise(prob.ML, cfg["seed"], cfg["n_samples"], samples=picks)
+    assert np.array_equal(_bits(Wg), _bits(Wref))
+    del G
+    gc.collect()
+    torch.cuda.empty_cache()
+    G = _graph(g, cfg["h"])
+    W2 = Wref[:1]  # sample 0 of seed 0 (the oracle's own noise)
+    for li in (0, L - 1):
+        x = G.sample(cfg["kappa"], cfg["beta"], cfg["k"], seed=cfg["seed"], n_samples=1,
+                     node_range=(li, li + 1)).cpu().numpy()
+        A = fem.operator(prob.ML, prob.G, prob.kappa, prob.plan.c_I[li], prob.plan.c_L[li])
+        res = (A @ x.T).T - W2
+        assert (np.linalg.norm(res, axis=1) / np.linalg.norm(W2, axis=1)).max() <= 1e-9, f"node {li}"
