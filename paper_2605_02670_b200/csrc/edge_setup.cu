@@ -9,7 +9,8 @@
 //
 // Thomas factorisation of A_II (P187-194 [eq:thomas_coefficients], thomas.cuh):
 //     d'_1 = a,  d'_lo,i = b / d'_{i-1},  d'_i = a - d'_lo,i b
-// K3/K5 (sweep_impl.cuh) use them through two node-minor tables [(off_e + t) * Lp + l]
+// K3/K5 (sweep_impl.cuh) use them through two node-minor tables [(toff_e + t) * Lp + l]
+// (one set of rows per class of edges with identical (m_e, h_e), written by its representative)
 // (row padded to the sweep tiling Lp >= L with zeros, which makes padded nodes inert):
 //     mu_t = d'_lo,t = b / d'_{t-1} (mu_1 = 0),  g_t = 1 / (d'_t + d'_{m+1-t} - a)
 // (g_t is the diagonal of A_II^{-1}; see sweep_impl.cuh for the twisted-factorisation use).
@@ -40,10 +41,14 @@ __global__ void edge_setup_kernel(DevGraph g, int32_t L, int32_t Lp, const doubl
     const int e = blockIdx.x;
     const double h = g.h[e];
     const int m = g.m[e];
-    double* tmu = mu_t + g.off[e] * Lp;
-    double* tgam = gam_t + g.off[e] * Lp;
-    for (int l = L + threadIdx.x; l < Lp; l += blockDim.x) {  // padded nodes: inert zeros
-        for (int t = 0; t < m; ++t) tmu[(int64_t)t * Lp + l] = tgam[(int64_t)t * Lp + l] = 0.0;
+    // the class representative writes the shared table rows; every edge computes its Schur block
+    const bool rep = g.tab_rep[e] != 0;
+    double* tmu = mu_t + g.toff[e] * Lp;
+    double* tgam = gam_t + g.toff[e] * Lp;
+    if (rep) {
+        for (int l = L + threadIdx.x; l < Lp; l += blockDim.x) {  // padded nodes: inert zeros
+            for (int t = 0; t < m; ++t) tmu[(int64_t)t * Lp + l] = tgam[(int64_t)t * Lp + l] = 0.0;
+        }
     }
     for (int l = threadIdx.x; l < L; l += blockDim.x) {
         const double cI = cIt[l], cL = cLt[l];
@@ -59,13 +64,15 @@ __global__ void edge_setup_kernel(DevGraph g, int32_t L, int32_t Lp, const doubl
             double prod = 1.0;  // prod_{t=1}^{m-1} (-mu_t) = prod_{i<m} (-b / d'_i)
             for (int t = 0; t < m; ++t) {
                 const double mu = thomas_step(c, inv);
-                tmu[(int64_t)t * Lp + l] = mu;
-                tgam[(int64_t)t * Lp + l] = c.a - mu * c.b;  // d'_t, the same expression thomas_step inverted
+                if (rep) {
+                    tmu[(int64_t)t * Lp + l] = mu;
+                    tgam[(int64_t)t * Lp + l] = c.a - mu * c.b;  // d'_t, the same expression thomas_step inverted
+                }
                 if (t > 0) prod *= -mu;
             }
             // twisted-factorisation diagonal g_t = (A_II^{-1})_tt = 1 / (d'_t + d'_{m+1-t} - a), computed in
             // mirrored pairs (t, m-1-t) so the in-place overwrite of the pivots is safe
-            for (int t = 0; t <= (m - 1) / 2; ++t) {
+            for (int t = 0; rep && t <= (m - 1) / 2; ++t) {
                 const int tm = m - 1 - t;
                 const double gv = 1.0 / (tgam[(int64_t)t * Lp + l] + tgam[(int64_t)tm * Lp + l] - c.a);
                 tgam[(int64_t)t * Lp + l] = gv;

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <list>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -221,7 +222,7 @@ grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf
     };
     double* dcI = (double*)grab(L * sizeof(double));
     double* dcL = (double*)grab(Lp * sizeof(double));
-    const size_t tab = (size_t)std::max<int64_t>(g->NI, 1) * Lp * sizeof(double);
+    const size_t tab = (size_t)std::max<int64_t>(g->dev.NT, 1) * Lp * sizeof(double);
     double* mu = (double*)grab(tab);
     double* gam = (double*)grab(tab);
     double* sig = (double*)grab((size_t)L * g->E * 4 * sizeof(double));
@@ -474,6 +475,26 @@ grf_status grf_graph_create(int64_t n_vertices, int64_t n_edges, const int64_t* 
     }
     g->NI = NI;
     g->N = NI + V;
+    // Thomas-table classes: edges with the same (m_e, bits of h_e) share table rows
+    std::vector<int64_t> toff(E);
+    std::vector<int32_t> tab_rep(E, 0);
+    int64_t NT = 0;
+    {
+        std::map<std::pair<int32_t, uint64_t>, int64_t> cls;
+        for (int64_t e = 0; e < E; ++e) {
+            uint64_t hb;
+            std::memcpy(&hb, &g->he[e], sizeof(hb));
+            auto it = cls.find({mm[e], hb});
+            if (it == cls.end()) {
+                cls[{mm[e], hb}] = NT;
+                toff[e] = NT;
+                tab_rep[e] = 1;
+                NT += mm[e];
+            } else {
+                toff[e] = it->second;
+            }
+        }
+    }
     // lumped mass (P137-145): interior h_e/2 + h_e/2; vertices sum h_e/2 in ascending edge, u end then v end
     g->ml.assign(g->N, 0.0);
     for (int64_t e = 0; e < E; ++e) {
@@ -533,7 +554,10 @@ grf_status grf_graph_create(int64_t n_vertices, int64_t n_edges, const int64_t* 
     d.N = g->N;
     d.NI = NI;
     d.max_m = max_m;
+    d.NT = NT;
     d.eu = g->upload(eu32, &st);
+    if (!st) d.toff = g->upload(toff, &st);
+    if (!st) d.tab_rep = g->upload(tab_rep, &st);
     if (!st) d.ev = g->upload(ev32, &st);
     if (!st) d.m = g->upload(mm, &st);
     if (!st) d.off = g->upload(g->off, &st);

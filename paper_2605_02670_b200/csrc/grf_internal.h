@@ -26,6 +26,11 @@ struct DevGraph {
     const int32_t* owner = nullptr;   // [V] incidence code that writes the vertex value in recovery
     const double* sqrt_ml = nullptr;  // [N] sqrt of the lumped mass diagonal
     const int32_t* edge_order = nullptr; // [E] edges by descending interior length (work-queue order)
+    // Thomas tables depend on an edge only through (m_e, h_e): edges with identical meshes share
+    // one set of table rows (config 5: all 3848 edges share one).
+    int64_t NT = 0;                   // table rows (sum of m_e over distinct (m_e, h_e))
+    const int64_t* toff = nullptr;    // [E] first table row of the edge's (m_e, h_e) class
+    const int32_t* tab_rep = nullptr; // [E] 1 for the edge that writes its class's rows
     int32_t max_deg = 0;              // max vertex degree (incident edge ends)
     int32_t ell_w = 0;                // ELL width = max_deg rounded up to 4/8/16/32
     const int32_t* ell_other = nullptr; // [ell_w][V] other endpoint of incidence slot j of v (v if padding)
@@ -42,8 +47,8 @@ struct DevPlan {
     int32_t Lp = 0;                   // padded node row of the Thomas tables (sweep_impl.cuh tiling)
     int32_t TL = 0;                   // nodes per thread of the sweep kernels
     int32_t rounds = 0;               // node rounds: Lp = rounds * 32 * TL
-    double* mu = nullptr;             // [NI * Lp] Thomas multipliers  b/d'_{t-1}, layout [(off_e + t) * Lp + l]
-    double* gam = nullptr;            // [NI * Lp] diag of A_II^{-1}: 1/(d'_t + d'_{m+1-t} - a); 0 for l >= L
+    double* mu = nullptr;             // [NT * Lp] Thomas multipliers  b/d'_{t-1}, layout [(toff_e + t) * Lp + l]
+    double* gam = nullptr;            // [NT * Lp] diag of A_II^{-1}: 1/(d'_t + d'_{m+1-t} - a); 0 for l >= L
     double* sig = nullptr;            // [L * E * 4]: (s_d, s_o, p_d, p_o) local Schur + its inverse
     double* ops = nullptr;            // [L * (3V + 4E)]: per-node CSR tables of S and M^{-1} (pcg.cu)
 };

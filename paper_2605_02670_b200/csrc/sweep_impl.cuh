@@ -26,7 +26,7 @@
 // (2 lt + 64 q, +1), q < TL/2, and for odd TL the node 64 (TL/2) + lt, so a warp's
 // coefficient loads are conflict-free LDS.128 broadcasts over its s-lanes.
 //
-// Staging.  Per block of IB steps the node-minor tables mu, g [(off_e + t) * Lp + l] are
+// Staging.  Per block of IB steps the node-minor tables mu, g [(toff_e + t) * Lp + l] are
 // brought into shared memory by the bulk-copy engine (cp.async.bulk + mbarrier transaction
 // count; one thread issues), and the noise of the CTA's samples by per-lane cp.async;
 // both double buffered, one __syncthreads per block.
@@ -175,6 +175,7 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
         const int64_t c0 = (int64_t)(it % A.chunks) * CS;
         const int m = g.m[e];
         const int64_t off = g.off[e];
+        const int64_t toff = g.toff[e];  // Thomas-table rows of the edge's (m, h) class
         const double h = g.h[e];
         const int vu = g.eu[e], vv = g.ev[e];
         const int ms = m | 1;
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
 #pragma unroll
                 for (int n = 0; n < TL; ++n) {
                     const int l = rb + slot(n);
-                    g0[n] = l < L ? A.gam[off * (int64_t)Lp + l] : 0.0;  // g_0 = g_{m-1} for the end values
+                    g0[n] = l < L ? A.gam[toff * (int64_t)Lp + l] : 0.0;  // g_0 = g_{m-1} for the end values
 #pragma unroll
                     for (int j = 0; j < TS; ++j) Y[n][j] = Z[n][j] = 0.0;
                 }
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                     mbar_expect_tx(&bar[buf], (uint32_t)(NTAB * nb) * row);
 #pragma unroll
                     for (int tb = 0; tb < NTAB; ++tb) {
-                        const double* tab = (tb == 0 ? A.mu : A.gam) + (off + t0) * (int64_t)Lp + rb;
+                        const double* tab = (tb == 0 ? A.mu : A.gam) + (toff + t0) * (int64_t)Lp + rb;
                         double* dst = coef + (buf * NTAB + tb) * IBK * RN;
                         if (A.rounds == 1) {
                             bulk_g2s(dst, tab, (uint32_t)nb * row, &bar[buf]);

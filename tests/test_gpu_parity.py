@@ -318,3 +318,59 @@ def test_config4_rgg_full_size():
         A = fem.operator(prob.ML, prob.G, prob.kappa, prob.plan.c_I[li], prob.plan.c_L[li])
         res = (A @ x.T).T - W2
         assert (np.linalg.norm(res, axis=1) / np.linalg.norm(W2, axis=1)).max() <= 1e-9, f"node {li}"
+
+
+# ----------------------------------------------------------------------------- config 5 (star of lattices)
+@pytest.mark.parametrize("beta", [0.3, 0.5, 0.75, 0.9])
+def test_config5_star_coarsest_all_betas(beta):
+    """configs[4] at h = 2^-4 (N = 59 769), every beta of the sweep (L = 296 / 249 / 331 / 687),
+    kappa = 8, k = 0.2, 64 samples in one call; the oracle recomputes samples 0 and 63."""
+    g = star_of_lattices(8, 16)
+    h, kappa, k = 2.0 ** -4, 8.0, 0.2
+    G = _graph(g, h)
+    u, st = G.sample(kappa, beta, k, seed=0, n_samples=64, return_stats=True)
+    assert st["n_nodes"] == {0.3: 296, 0.5: 249, 0.75: 331, 0.9: 687}[beta]
+    assert st["n_unconverged"] == 0
+    ref, _, _ = solve.sample(g, h, kappa, beta, k, 0, 64, samples=[0, 63])
+    assert _rel(u.cpu().numpy()[[0, 63]], ref).max() <= FIELD_TOL
+
+
+def test_config5_star_default_level_per_node():
+    """configs[4] at the CONFIGS level h = 2^-8 (N = 983 289, L = 331, 64 samples): full call
+    converges; single-node solves vs the oracle's sparse direct solve."""
+    cfg = CONFIGS["star"]
+    g = config_graph("star")
+    G = _graph(g, cfg["h"])
+    u, st = G.sample(cfg["kappa"], cfg["beta"], cfg["k"], seed=cfg["seed"], n_samples=cfg["n_samples"],
+                     return_stats=True)
+    assert G.n_dofs == 983_289 and st["n_nodes"] == 331 and st["n_unconverged"] == 0
+    assert np.isfinite(u.cpu().numpy()).all()
+    prob = solve.setup(g, cfg["h"], cfg["kappa"], cfg["beta"], cfg["k"])
+    W = noise.white_noise(prob.ML, cfg["seed"], 2)
+    for li in (0, prob.plan.n_nodes // 2, prob.plan.n_nodes - 1):
+        x = G.sample(cfg["kappa"], cfg["beta"], cfg["k"], seed=cfg["seed"], n_samples=2,
+                     node_range=(li, li + 1)).cpu().numpy()
+        assert _rel(x, solve.node_solve(prob, li, W)).max() <= 1e-10, f"node {li}"
+
+
+def test_config5_star_finest_level():
+    """configs[4] at the finest level h = 2^-12 (N = 15 759 609, edges of 4095 interior nodes)
+    with beta = 0.9 (L = 687, the largest rule), 64 samples: one call fits on one GPU because
+    the 3848 identical edges share one Thomas table; the defining residual A_l x_l = W of
+    single-node solves is checked with the oracle's assembled operator."""
+    from oracle import fem
+    g = star_of_lattices(8, 16)
+    h, kappa, beta, k = 2.0 ** -12, 8.0, 0.9, 0.2
+    G = _graph(g, h)
+    u, st = G.sample(kappa, beta, k, seed=0, n_samples=64, return_stats=True)
+    assert G.n_dofs == 15_759_609 and st["n_nodes"] == 687 and st["n_unconverged"] == 0
+    assert bool(torch.isfinite(u).all())
+    del u
+    torch.cuda.empty_cache()
+    prob = solve.setup(g, h, kappa, beta, k)
+    W = noise.white_noise(prob.ML, 0, 1)
+    for li in (0, 686):
+        x = G.sample(kappa, beta, k, seed=0, n_samples=1, node_range=(li, li + 1)).cpu().numpy()
+        A = fem.operator(prob.ML, prob.G, prob.kappa, prob.plan.c_I[li], prob.plan.c_L[li])
+        res = (A @ x.T).T - W
+        assert (np.linalg.norm(res, axis=1) / np.linalg.norm(W, axis=1)).max() <= 1e-9, f"node {li}"
