@@ -63,6 +63,8 @@ def peaks():
     # fp64 vector peak derived from unit counts and clock:
     # 148 SMs x 64 FP64 FMA/clk/SM x 2 flop x sm_max_mhz
     p["fp64_tflops"] = 148 * 64 * 2 * p["sm_max_mhz"] * 1e6 / 1e12
+    # measured fp64 FMA throughput of tools/fp64_peak.cu on this pool's B200 (profiles/fp64_peak.txt)
+    p["fp64_measured_tflops"] = 33.56
     return p
 
 
@@ -246,7 +248,8 @@ def main():
         t = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_ms = float(t.item())
-    launches = sum(n for _, n in prof.values())
+    # kernels launched inside the timed region: the library's own per-call count (stats) x steps
+    launches = int(st["gpu_launches"]) * args.steps
 
     # end to end: the same call with a pinned HOST output (D2H + sync inside the timed region)
     e2e = None
@@ -315,7 +318,9 @@ def main():
         "pcg": {"iter_min": st["iter_min"], "iter_max": st["iter_max"], "iter_mean": st["iter_mean"],
                 "worst_rel_residual": st["worst_rel_residual"]},
         "gpu_launches": launches, "clocks": clk,
-        "peaks": {"hbm_gbs": pk["hbm_gbs"], "fp64_tflops": pk["fp64_tflops"], "source": pk["source"]},
+        "peaks": {"hbm_gbs": pk["hbm_gbs"], "fp64_tflops": pk["fp64_tflops"], "source": pk["source"],
+                  "fp64_measured_tflops": pk["fp64_measured_tflops"],
+                  "frac_of_measured_fp64": ach / pk["fp64_measured_tflops"]},
     }
     if e2e is not None:
         line["e2e"] = e2e

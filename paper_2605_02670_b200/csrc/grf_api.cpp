@@ -324,7 +324,10 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
         return fail(GRF_ENOMEM, "workspace too small: %zu < %zu bytes", ws_bytes, w.total);
     }
     char* base = static_cast<char*>(ws);
-    int64_t launches = 4;
+    // kernels this call launches: [noise] condense, assemble, K4 (one per sample tile for the
+    // global-memory variant), recover, vertex sum
+    const int64_t cs = (int64_t)1 << grf::sample_tile_log2(S);
+    int64_t launches = 5 + (use_global_pcg(g, opt) ? (S + cs - 1) / cs - 1 : 0);
     if (gen) {
         double* Wd = reinterpret_cast<double*>(base + w.w);
         cudaError_t ne = g->timed(GRF_K_NOISE, st, [&] { grf::launch_noise(g->dev, seed, S, Wd, st); });
@@ -333,7 +336,7 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
             return fail(GRF_ECUDA, "noise launch: %s", cudaGetErrorString(ne));
         }
         W = Wd;
-        launches = 5;
+        launches += 1;
     }
     double* ends = reinterpret_cast<double*>(base + w.ends);
     double* uG = reinterpret_cast<double*>(base + w.ug);

@@ -124,7 +124,7 @@ struct Cfg {
     static constexpr size_t PART = REC ? (size_t)2 * IBK * NWL * 2 * CS * sizeof(double) : 0;
     static constexpr size_t FIXED = 64 + COEF + WB + PART;
     static constexpr int WEL = IBK * 2 * NC * CS;   // staged noise elements per block
-    static_assert(REC ? ((TS == 4 && LW == 8) || (TS == 1 && LW == 32)) : true, "recover reduce shapes");
+    static_assert(REC ? ((TS == 4 && (LW == 8 || LW == 4)) || (TS == 1 && LW == 32)) : true, "recover reduce shapes");
     static_assert((CS & (CS - 1)) == 0, "CS must be a power of two");
 };
 
@@ -349,6 +349,7 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                 };
 
                 if (!REC) {
+#pragma unroll 2
                     for (int tt = 0; tt < nb; ++tt) {
                         double wl[TS], wr[TS];
                         load_w(tt, wl, wr);
@@ -469,8 +470,10 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                             aR[1 % TS] += __shfl_xor_sync(0xffffffffu, aR[3 % TS], 1);
                             aL[0] += __shfl_xor_sync(0xffffffffu, aL[1 % TS], 2);
                             aR[0] += __shfl_xor_sync(0xffffffffu, aR[1 % TS], 2);
-                            aL[0] += __shfl_xor_sync(0xffffffffu, aL[0], 4);
-                            aR[0] += __shfl_xor_sync(0xffffffffu, aR[0], 4);
+                            if (LW == 8) {
+                                aL[0] += __shfl_xor_sync(0xffffffffu, aL[0], 4);
+                                aR[0] += __shfl_xor_sync(0xffffffffu, aR[0], 4);
+                            }
                             if ((ll & 4) == 0) {
                                 pb[tt * NWL * 2 * CS] = aL[0];
                                 pb[tt * NWL * 2 * CS + CS] = aR[0];
@@ -503,6 +506,7 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                         tt = 1;
                         pend = true;
                     }
+#pragma unroll 2
                     for (; tt < tend; ++tt) {
                         double aL[TS], aR[TS];
                         body_mid(tt, aL, aR);
@@ -591,6 +595,8 @@ cudaError_t launch(Args a, cudaStream_t st) {
 
 // Sample mapping (the node tile TL is fixed by the plan's Lp):
 //   V2: TS = 4, LW = 8, NWS = 2  (CTA = 4 l-warps x 2 s-warps, 32 samples per item)   S >= 17
+//       (recover: LW = 4, NWS = 1 -- CTA = 8 l-warps of 4 l-lanes x 8 s-lanes, same 32 samples:
+//        two shuffle levels per step instead of three, the fold sums 8 warp partials)
 //   V1: TS = 4, LW = 8, NWS = 1  (CTA = 4 l-warps, 16 samples per item)               9 <= S <= 16
 //   V0: TS = 1, LW = 32, NWS = 1 (CTA = 1 warp, 1 sample per item)                    S <= 8
 enum Variant { V0 = 0, V1 = 1, V2 = 2 };
@@ -598,7 +604,9 @@ inline Variant variant_for(int64_t S) { return S >= 17 ? V2 : (S >= 9 ? V1 : V0)
 
 template <bool REC, int V>
 cudaError_t launch_v(int tl, Args a, cudaStream_t st) {
-    constexpr int TS = V == V0 ? 1 : 4, LW = V == V0 ? 32 : 8, NWS = V == V2 ? 2 : 1;
+    constexpr int TS = V == V0 ? 1 : 4;
+    constexpr int LW = V == V0 ? 32 : ((REC && V == V2) ? 4 : 8);
+    constexpr int NWS = (V == V2 && !REC) ? 2 : 1;
     switch (tl) {
         case 1: return launch<1, TS, LW, NWS, REC>(a, st);
         case 2: return launch<2, TS, LW, NWS, REC>(a, st);
