@@ -77,6 +77,7 @@ typedef struct grf_allocator {
 } grf_allocator;
 
 typedef struct grf_graph grf_graph;
+typedef struct grf_comm grf_comm;
 
 /* Create a metric graph + its P1 mesh (P122-123: n_e = ceil(l_e/h) in fp64,
  * h_e = l_e/n_e).  Host arrays of length n_edges, copied.  Self-loops and
@@ -88,6 +89,34 @@ typedef struct grf_graph grf_graph;
 grf_status grf_graph_create(int64_t n_vertices, int64_t n_edges, const int64_t* edge_u,
                             const int64_t* edge_v, const double* length, double h,
                             const grf_allocator* alloc, grf_graph** out);
+/* ---- edge-partitioned graphs (the largest graph, config 4) ------------
+ * The edges of a whole graph are split into parts; a part is the subgraph of its edges with
+ * every vertex they touch (local ids 0..n_vertices-1, edge orientation as in the whole
+ * graph).  Vertices touched by several parts are interface vertices.  A part needs, per
+ * local vertex / edge, what only the whole graph knows (all arrays host, copied):
+ *   vertex_gid[v]     global vertex id               (noise counter)
+ *   edge_goff[e]      global DOF index of the edge's first interior node (DOF order S97)
+ *   global_n_interior N_I of the whole graph          (vertex DOF = N_I + global id)
+ *   vertex_mass[v]    lumped mass of the vertex in the whole graph (P137-145)
+ *   vertex_degree[v]  incident edge ends in the whole graph (d_v of the NN step, P261)
+ *   vertex_owned[v]   1 on exactly one part per vertex (adds W_v, counts it in dot products)
+ *   vertex_iface[v]   interface id in [0, n_interface), -1 for a vertex of this part only
+ * EINVAL for NULL arrays, masses <= 0, degrees below the local count, ids out of range. */
+typedef struct grf_part_info {
+    int64_t global_n_interior;
+    const int64_t* vertex_gid;
+    const int64_t* edge_goff;
+    const double* vertex_mass;
+    const int32_t* vertex_degree;
+    const uint8_t* vertex_owned;
+    int64_t n_interface;
+    const int64_t* vertex_iface;
+} grf_part_info;
+grf_status grf_graph_create_part(int64_t n_vertices, int64_t n_edges, const int64_t* edge_u,
+                                 const int64_t* edge_v, const double* length, double h,
+                                 const grf_part_info* part, const grf_allocator* alloc,
+                                 grf_graph** out);
+
 /* Frees the handle and everything it allocated (synchronises the device first). */
 void grf_graph_destroy(grf_graph* g);
 
@@ -163,6 +192,22 @@ grf_status grf_apply(grf_graph* g, double kappa, double beta, double k, int64_t 
                      const double* rhs, const grf_options* opt, double* u_out,
                      void* workspace, size_t ws_bytes, void* stream, grf_stats* stats);
 
+/* Edge-partitioned grf_sample.  Same field as grf_sample on the whole graph:
+ * every part draws its DOFs' noise with the global counters, condenses its own edges,
+ * and the vertex Schur systems S^{(l)} = sum_e R_e^T S_e R_e (P242-244) are solved by an
+ * NN-PCG whose vectors stay assembled: each operator application (Dirichlet step, NN step
+ * with global degrees, P247-298) is followed by a halo sum of the interface vertices over
+ * all parts, and each dot product sums the owned vertices over all parts.
+ *   comm == NULL: all n_parts parts live in this process (sums on the device, fixed order);
+ *   comm != NULL: this rank passes its single part; halo and dot sums are NCCL allreduces.
+ * u_out[q]: device n_samples x N_q field on part q's local DOFs (interior of its edges,
+ * then its vertices).  Synchronises the stream (convergence is checked every iteration).
+ * GRF_ENOCONV is reported only when stats != NULL. */
+grf_status grf_sample_edgepart(grf_graph* const* parts, int32_t n_parts, struct grf_comm* comm,
+                               double kappa, double beta, double k, uint64_t seed, int64_t n_samples,
+                               const grf_options* opt, double* const* u_out, void* stream,
+                               grf_stats* stats);
+
 /* Stage entry point (tests, diagnostics): the local Schur blocks
  * S^{(l,e)} = [[s_d, s_o], [s_o, s_d]] (P204-213 [eq:local_reduced_schur]) for the
  * nodes of opt's range, into host array sigma[(l*E + e)*2 + {0,1}].  Synchronises. */
@@ -182,7 +227,6 @@ grf_status grf_profile_read(grf_graph* g, double* ms, int64_t* launches);
 /* ---- multi-GPU (one process per GPU, NCCL over NVLink/NVSwitch) ---------------
  * grf_comm_get_unique_id on rank 0, broadcast the 128 bytes with any process
  * group, then grf_comm_init on every rank (binds the current device). */
-typedef struct grf_comm grf_comm;
 grf_status grf_comm_get_unique_id(void* id128);
 grf_status grf_comm_init(const void* id128, int rank, int nranks, grf_comm** out);
 void grf_comm_destroy(grf_comm* c);

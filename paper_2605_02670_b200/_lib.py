@@ -23,6 +23,13 @@ class grf_allocator(C.Structure):
     _fields_ = [("alloc", ALLOC_FN), ("free", FREE_FN), ("ctx", C.c_void_p)]
 
 
+class grf_part_info(C.Structure):
+    _fields_ = [("global_n_interior", C.c_int64), ("vertex_gid", C.POINTER(C.c_int64)),
+                ("edge_goff", C.POINTER(C.c_int64)), ("vertex_mass", C.POINTER(C.c_double)),
+                ("vertex_degree", C.POINTER(C.c_int32)), ("vertex_owned", C.POINTER(C.c_uint8)),
+                ("n_interface", C.c_int64), ("vertex_iface", C.POINTER(C.c_int64))]
+
+
 class grf_options(C.Structure):
     _fields_ = [("rtol", C.c_double), ("max_iter", C.c_int32), ("precond", C.c_int32),
                 ("node_begin", C.c_int64), ("node_end", C.c_int64), ("pcg_variant", C.c_int32)]
@@ -43,7 +50,7 @@ EXPORTS = [
     "grf_graph_num_dofs", "grf_graph_edge_layout", "grf_graph_lumped_mass", "grf_plan_info",
     "grf_workspace_size", "grf_noise", "grf_sample", "grf_sample_host", "grf_apply", "grf_edge_schur",
     "grf_comm_get_unique_id", "grf_comm_init", "grf_comm_destroy", "grf_reduce_sum",
-    "grf_profile_enable", "grf_profile_read",
+    "grf_profile_enable", "grf_profile_read", "grf_graph_create_part", "grf_sample_edgepart",
 ]
 KERNEL_NAMES = ["noise", "edge_setup", "condense", "pcg", "recover"]
 
@@ -88,6 +95,10 @@ def load() -> C.CDLL:
         "grf_comm_destroy": (None, [P]),
         "grf_reduce_sum": (C.c_int, [P, P, P, I64, C.c_int, P]),
         "grf_profile_enable": (C.c_int, [P, C.c_int]),
+        "grf_graph_create_part": (C.c_int, [I64, I64, pi64, pi64, pd, D, C.POINTER(grf_part_info),
+                                            C.POINTER(grf_allocator), C.POINTER(P)]),
+        "grf_sample_edgepart": (C.c_int, [C.POINTER(P), C.c_int32, P, D, D, D, U64, I64, C.POINTER(grf_options),
+                                          C.POINTER(P), P, C.POINTER(grf_stats)]),
         "grf_profile_read": (C.c_int, [P, pd, pi64]),
     }
     for name, (res, args) in sig.items():

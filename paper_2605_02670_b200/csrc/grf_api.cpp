@@ -90,6 +90,8 @@ struct grf_graph {
     grf::DevGraph dev;
     std::vector<Block> blocks;  // graph-lifetime device allocations
     std::list<std::unique_ptr<Plan>> plans;  // most recent first
+    bool partitioned = false;                // created by grf_graph_create_part
+    int64_t n_iface = 0;                     // interface vertices of the whole partition
     // kernel timing (grf_profile_enable / grf_profile_read)
     bool prof = false;
     struct Rec {
@@ -424,8 +426,12 @@ void grf_options_default(grf_options* opt) {
     opt->pcg_variant = GRF_PCG_AUTO;
 }
 
-grf_status grf_graph_create(int64_t n_vertices, int64_t n_edges, const int64_t* edge_u, const int64_t* edge_v,
-                            const double* length, double h, const grf_allocator* alloc, grf_graph** out) {
+}  // extern "C"
+
+namespace {
+grf_status create_impl(int64_t n_vertices, int64_t n_edges, const int64_t* edge_u, const int64_t* edge_v,
+                       const double* length, double h, const grf_part_info* part, const grf_allocator* alloc,
+                       grf_graph** out) {
     if (!out) return fail(GRF_EINVAL, "out is NULL");
     *out = nullptr;
     if (n_vertices < 1) return fail(GRF_EINVAL, "n_vertices must be >= 1");
@@ -511,6 +517,32 @@ grf_status grf_graph_create(int64_t n_vertices, int64_t n_edges, const int64_t* 
     }
     std::vector<double> sq(g->N);
     for (int64_t i = 0; i < g->N; ++i) sq[i] = std::sqrt(g->ml[i]);
+    // edge-partitioned part: the noise of a vertex uses its WHOLE-graph lumped mass and its
+    // global DOF index as the Philox counter, so every part draws the same W_v
+    std::vector<int64_t> dof_gid;
+    std::vector<uint8_t> vowned;
+    std::vector<int64_t> viface;
+    if (part) {
+        if (!part->vertex_gid || !part->edge_goff || !part->vertex_mass || !part->vertex_degree ||
+            !part->vertex_owned || !part->vertex_iface || part->global_n_interior < 0 || part->n_interface < 0)
+            return fail(GRF_EINVAL, "grf_part_info: NULL array or negative size");
+        dof_gid.resize(g->N);
+        for (int64_t e = 0; e < E; ++e)
+            for (int64_t i = 0; i < g->n_el[e] - 1; ++i) dof_gid[g->off[e] + i] = part->edge_goff[e] + i;
+        vowned.resize(V);
+        viface.resize(V);
+        for (int64_t v = 0; v < V; ++v) {
+            if (!(part->vertex_mass[v] > 0.0) || part->vertex_degree[v] < deg[v])
+                return fail(GRF_EINVAL, "grf_part_info: vertex %lld has an inconsistent mass or degree", (long long)v);
+            if (part->vertex_iface[v] >= part->n_interface)
+                return fail(GRF_EINVAL, "grf_part_info: interface id out of range");
+            dof_gid[NI + v] = part->global_n_interior + part->vertex_gid[v];
+            sq[NI + v] = std::sqrt(part->vertex_mass[v]);
+            vowned[v] = part->vertex_owned[v] ? 1 : 0;
+            viface[v] = part->vertex_iface[v];
+        }
+        g->n_iface = part->n_interface;
+    }
     // incidence CSR in (edge, end) order, owner = first incidence, 1/d_v
     std::vector<int32_t> ptr(V + 1, 0), inc(2 * E), other(2 * E), owner(V, -1);
     for (int64_t v = 0; v < V; ++v) ptr[v + 1] = ptr[v] + (int32_t)deg[v];
@@ -540,7 +572,7 @@ grf_status grf_graph_create(int64_t n_vertices, int64_t n_edges, const int64_t* 
     std::vector<double> inv_deg(V);
     for (int64_t v = 0; v < V; ++v) {
         owner[v] = inc[ptr[v]];
-        inv_deg[v] = 1.0 / (double)deg[v];
+        inv_deg[v] = 1.0 / (double)(part ? part->vertex_degree[v] : deg[v]);  // GLOBAL d_v (P261)
     }
     std::vector<int32_t> order(E);
     for (int64_t e = 0; e < E; ++e) order[e] = (int32_t)e;
@@ -577,12 +609,34 @@ grf_status grf_graph_create(int64_t n_vertices, int64_t n_edges, const int64_t* 
     if (!st) d.ell_other = g->upload(ell_other, &st);
     if (!st) d.ell_code = g->upload(ell_code, &st);
     if (!st) d.ell_valid = g->upload(ell_valid, &st);
+    if (part) {
+        if (!st) d.dof_gid = g->upload(dof_gid, &st);
+        if (!st) d.vowned = g->upload(vowned, &st);
+        if (!st) d.viface = g->upload(viface, &st);
+        g->partitioned = true;
+    }
     if (st) {
         grf_graph_destroy(g.release());
         return st;
     }
     *out = g.release();
     return GRF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+grf_status grf_graph_create(int64_t n_vertices, int64_t n_edges, const int64_t* edge_u, const int64_t* edge_v,
+                            const double* length, double h, const grf_allocator* alloc, grf_graph** out) {
+    return create_impl(n_vertices, n_edges, edge_u, edge_v, length, h, nullptr, alloc, out);
+}
+
+grf_status grf_graph_create_part(int64_t n_vertices, int64_t n_edges, const int64_t* edge_u, const int64_t* edge_v,
+                                 const double* length, double h, const grf_part_info* part,
+                                 const grf_allocator* alloc, grf_graph** out) {
+    if (!part) return fail(GRF_EINVAL, "part is NULL");
+    return create_impl(n_vertices, n_edges, edge_u, edge_v, length, h, part, alloc, out);
 }
 
 void grf_graph_destroy(grf_graph* g) {
@@ -841,3 +895,259 @@ grf_status grf_reduce_sum(grf_comm* c, const double* send, double* recv, int64_t
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- edge-partitioned sampling
+namespace {
+typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+
+// sum of a device fp64 buffer over the ranks (in place); ncclDouble = 8, ncclSum = 0
+grf_status allreduce_sum(grf_comm* c, double* buf, int64_t n, cudaStream_t st) {
+    static nccl_allreduce_fn fn = nullptr;
+    if (!fn) fn = (nccl_allreduce_fn)dlsym(g_nccl.h, "ncclAllReduce");
+    if (!fn) return fail(GRF_ENCCL, "ncclAllReduce not found");
+    int r = fn(buf, buf, (size_t)n, 8, 0, c->comm, st);
+    if (r) return fail(GRF_ENCCL, "ncclAllReduce: %s", g_nccl.err ? g_nccl.err(r) : "error");
+    return GRF_OK;
+}
+
+// per-part device state of one grf_sample_edgepart call
+struct PartRun {
+    grf_graph* g = nullptr;
+    Plan* plan = nullptr;
+    std::vector<Block> mem;
+    double *W = nullptr, *ends = nullptr, *rhs = nullptr, *uG = nullptr, *relres = nullptr;
+    int32_t* iters = nullptr;
+    int32_t* counters = nullptr;
+    grf::dist::Vecs v{};
+    double *dpart = nullptr, *dots = nullptr, *halo = nullptr;
+    void* get(size_t bytes, cudaStream_t st) {
+        void* p = g->alloc.get(bytes, st);
+        if (p) mem.push_back({p, bytes});
+        return p;
+    }
+    void release(cudaStream_t st) {
+        cudaStreamSynchronize(st);
+        for (auto& b : mem) g->alloc.put(b.p, b.bytes, st);
+        mem.clear();
+    }
+};
+}  // namespace
+
+extern "C" grf_status grf_sample_edgepart(grf_graph* const* parts, int32_t n_parts, grf_comm* comm, double kappa,
+                                          double beta, double k, uint64_t seed, int64_t n_samples,
+                                          const grf_options* opt, double* const* u_out, void* stream,
+                                          grf_stats* stats) {
+    if (!parts || n_parts < 1 || !u_out) return fail(GRF_EINVAL, "grf_sample_edgepart: NULL argument or no parts");
+    if (comm && n_parts != 1) return fail(GRF_EINVAL, "with a communicator each rank passes exactly one part");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t I = parts[0]->n_iface;
+    for (int32_t q = 0; q < n_parts; ++q) {
+        grf_status s = check_params(parts[q], kappa, beta, k, n_samples);
+        if (s) return s;
+        if (!u_out[q]) return fail(GRF_EINVAL, "u_out[%d] is NULL", q);
+        if (!parts[q]->partitioned && (n_parts > 1 || comm))
+            return fail(GRF_EINVAL, "part %d was not created by grf_graph_create_part", q);
+        if (parts[q]->n_iface != I) return fail(GRF_EINVAL, "parts disagree on the interface count");
+        s = check_kernel_limits(parts[q]);
+        if (s) return s;
+    }
+    const int32_t csl = grf::sample_tile_log2(n_samples);
+    const int32_t cs = 1 << csl;
+    const int64_t tiles = (n_samples + cs - 1) / cs;
+    const int64_t Sp = tiles * cs;
+    std::vector<PartRun> R(n_parts);
+    grf_status rc = GRF_OK;
+    auto cleanup = [&]() {
+        for (auto& r : R) r.release(st);
+    };
+    int32_t L = 0;
+    int64_t V_sum = 0;
+    for (int32_t q = 0; q < n_parts && !rc; ++q) {
+        PartRun& r = R[q];
+        r.g = parts[q];
+        rc = get_plan(r.g, kappa, beta, k, opt, st, &r.plan);
+        if (rc) break;
+        L = r.plan->dev.L;
+        const int64_t N = r.g->N, V = r.g->V, E = r.g->E;
+        V_sum += V;
+        const size_t vec = sizeof(double) * (size_t)L * V * cs;
+        r.W = (double*)r.get(sizeof(double) * n_samples * N, st);
+        r.ends = (double*)r.get(sizeof(double) * Sp * E * 2 * L, st);
+        r.rhs = (double*)r.get(sizeof(double) * Sp * V * L, st);
+        r.uG = (double*)r.get(sizeof(double) * Sp * V * L, st);
+        r.iters = (int32_t*)r.get(sizeof(int32_t) * n_samples * L, st);
+        r.relres = (double*)r.get(sizeof(double) * n_samples * L, st);
+        r.counters = (int32_t*)r.get(2 * sizeof(int32_t), st);
+        double** vv[7] = {&r.v.x, &r.v.r0, &r.v.r1, &r.v.p0, &r.v.p1, &r.v.q, &r.v.z};
+        for (auto p : vv) *p = (double*)r.get(vec, st);
+        r.dpart = (double*)r.get(sizeof(double) * 2 * L * grf::dist::dot_blocks(r.g->dev) * cs, st);
+        r.dots = (double*)r.get(sizeof(double) * 2 * L * cs, st);
+        r.halo = (double*)r.get(sizeof(double) * std::max<int64_t>(I, 1) * L * cs, st);
+        for (auto& b : r.mem)
+            if (!b.p) rc = fail(GRF_ENOMEM, "edge-partitioned workspace could not be allocated");
+        if (!r.W || !r.ends || !r.rhs || !r.uG || !r.iters || !r.relres || !r.counters || !r.v.x || !r.v.r0 ||
+            !r.v.r1 || !r.v.p0 || !r.v.p1 || !r.v.q || !r.v.z || !r.dpart || !r.dots || !r.halo)
+            rc = fail(GRF_ENOMEM, "edge-partitioned workspace could not be allocated");
+    }
+    // shared (all-part) state: summed halo / dots and the system scalars, on part 0's allocator
+    PartRun& R0 = R[0];
+    const int32_t nsys = L * cs;
+    double *hsum = nullptr, *dsum = nullptr;
+    double** ptrs = nullptr;
+    grf::dist::Scal sc{};
+    if (!rc) {
+        hsum = (double*)R0.get(sizeof(double) * std::max<int64_t>(I, 1) * L * cs, st);
+        dsum = (double*)R0.get(sizeof(double) * 2 * nsys, st);
+        ptrs = (double**)R0.get(sizeof(double*) * 2 * n_parts, st);
+        double** sd[5] = {&sc.alpha, &sc.beta, &sc.rz, &sc.gg, &sc.rr};
+        for (auto p : sd) *p = (double*)R0.get(sizeof(double) * nsys, st);
+        sc.done = (int32_t*)R0.get(sizeof(int32_t) * nsys, st);
+        sc.its = (int32_t*)R0.get(sizeof(int32_t) * nsys, st);
+        sc.active = (int32_t*)R0.get(sizeof(int32_t), st);
+        if (!hsum || !dsum || !ptrs || !sc.alpha || !sc.beta || !sc.rz || !sc.gg || !sc.rr || !sc.done || !sc.its ||
+            !sc.active)
+            rc = fail(GRF_ENOMEM, "edge-partitioned workspace could not be allocated");
+    }
+    if (rc) {
+        cleanup();
+        return rc;
+    }
+    // device arrays of part pointers for the in-process sums: [halo_0..halo_P-1, dots_0..dots_P-1]
+    std::vector<double*> hp(2 * n_parts);
+    for (int32_t q = 0; q < n_parts; ++q) {
+        hp[q] = R[q].halo;
+        hp[n_parts + q] = R[q].dots;
+    }
+    CUDA_TRY(cudaMemcpyAsync(ptrs, hp.data(), sizeof(double*) * hp.size(), cudaMemcpyHostToDevice, st));
+    const int32_t pc = opt ? opt->precond : GRF_PRECOND_NN;
+    const double rtol = opt ? opt->rtol : 1e-13;
+    const int32_t max_iter = (opt && opt->max_iter > 0) ? opt->max_iter : (int32_t)(V_sum + 10);
+    const int64_t hn = I * L * cs;
+
+    // halo sum of vector X (per part pointer) over all parts: interface values become the totals
+    auto halo = [&](auto getX) -> grf_status {
+        if (I == 0) return GRF_OK;
+        for (int32_t q = 0; q < n_parts; ++q) {
+            CUDA_TRY(cudaMemsetAsync(R[q].halo, 0, sizeof(double) * hn, st));
+            grf::dist::pack(R[q].g->dev, L, cs, getX(R[q]), R[q].halo, st);
+        }
+        double* total = R0.halo;
+        if (comm) {
+            grf_status s = allreduce_sum(comm, R0.halo, hn, st);
+            if (s) return s;
+        } else {
+            grf::dist::sum_parts(n_parts, ptrs, hn, hsum, st);
+            total = hsum;
+        }
+        for (int32_t q = 0; q < n_parts; ++q) grf::dist::unpack(R[q].g->dev, L, cs, total, getX(R[q]), st);
+        return GRF_OK;
+    };
+    // dot products (owned vertices) summed over parts into dsum [K][nsys]
+    auto dotsum = [&](int K, auto a0, auto b0, auto a1, auto b1) -> grf_status {
+        for (int32_t q = 0; q < n_parts; ++q)
+            grf::dist::dots(R[q].g->dev, L, cs, K, a0(R[q]), b0(R[q]), a1(R[q]), b1(R[q]), R[q].dpart, R[q].dots, st);
+        if (comm) {
+            grf_status s = allreduce_sum(comm, R0.dots, (int64_t)K * nsys, st);
+            if (s) return s;
+            CUDA_TRY(cudaMemcpyAsync(dsum, R0.dots, sizeof(double) * K * nsys, cudaMemcpyDeviceToDevice, st));
+        } else {
+            grf::dist::sum_parts(n_parts, ptrs + n_parts, (int64_t)K * nsys, dsum, st);
+        }
+        return GRF_OK;
+    };
+
+    // stage 1 (per part, no communication): noise, condensation, partial condensed rhs
+    for (auto& r : R) {
+        grf::launch_noise(r.g->dev, seed, n_samples, r.W, st);
+        CUDA_TRY(grf::launch_condense(r.g->dev, r.plan->dev, n_samples, r.W, r.ends, r.counters, st));
+        grf::launch_assemble_rhs(r.g->dev, r.plan->dev, n_samples, r.W, r.ends, r.rhs, st);
+    }
+    // stage 2: distributed NN-PCG per sample tile
+    for (int64_t tile = 0; tile < tiles && !rc; ++tile) {
+        for (auto& r : R) grf::dist::init(r.g->dev, L, n_samples, csl, tile, r.rhs, r.v, st);
+        rc = halo([](PartRun& r) { return r.v.r0; });  // g = W_G + sum over ALL parts' edges
+        if (rc) break;
+        for (auto& r : R) grf::dist::precond(r.g->dev, r.plan->dev, pc, cs, r.v.r0, r.v.z, st);
+        rc = halo([](PartRun& r) { return r.v.z; });
+        if (rc) break;
+        rc = dotsum(2, [](PartRun& r) { return (const double*)r.v.r0; }, [](PartRun& r) { return (const double*)r.v.r0; },
+                    [](PartRun& r) { return (const double*)r.v.r0; }, [](PartRun& r) { return (const double*)r.v.z; });
+        if (rc) break;
+        CUDA_TRY(cudaMemsetAsync(sc.active, 0, sizeof(int32_t), st));
+        grf::dist::scal_init(nsys, cs, n_samples, tile, csl, dsum, sc, st);
+        bool flip = false;  // which of the double-buffered p / r is current
+        for (int32_t it = 0; it < max_iter; ++it) {
+            int32_t active = 0;
+            CUDA_TRY(cudaMemcpyAsync(&active, sc.active, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+            if (active == 0) break;
+            for (auto& r : R) {
+                double* po = flip ? r.v.p1 : r.v.p0;
+                double* pn = flip ? r.v.p0 : r.v.p1;
+                grf::dist::spmv(r.g->dev, r.plan->dev, cs, sc.beta, r.v.z, po, pn, r.v.q, st);
+            }
+            rc = halo([](PartRun& r) { return r.v.q; });
+            if (rc) break;
+            rc = dotsum(1, [&](PartRun& r) { return (const double*)(flip ? r.v.p0 : r.v.p1); },
+                        [](PartRun& r) { return (const double*)r.v.q; }, [](PartRun&) { return (const double*)nullptr; },
+                        [](PartRun&) { return (const double*)nullptr; });
+            if (rc) break;
+            grf::dist::scal_alpha(nsys, dsum, sc, st);
+            for (auto& r : R) {
+                double* pn = flip ? r.v.p0 : r.v.p1;
+                double* ro = flip ? r.v.r1 : r.v.r0;
+                double* rn = flip ? r.v.r0 : r.v.r1;
+                grf::dist::update(r.g->dev, r.plan->dev, pc, cs, sc.alpha, r.v.q, pn, ro, rn, r.v.x, r.v.z, st);
+            }
+            rc = halo([](PartRun& r) { return r.v.z; });
+            if (rc) break;
+            rc = dotsum(2, [&](PartRun& r) { return (const double*)(flip ? r.v.r0 : r.v.r1); },
+                        [&](PartRun& r) { return (const double*)(flip ? r.v.r0 : r.v.r1); },
+                        [&](PartRun& r) { return (const double*)(flip ? r.v.r0 : r.v.r1); },
+                        [](PartRun& r) { return (const double*)r.v.z; });
+            if (rc) break;
+            grf::dist::scal_beta(nsys, rtol * rtol, dsum, sc, st);
+            flip = !flip;
+        }
+        if (rc) break;
+        for (auto& r : R) grf::dist::finish(r.g->dev, L, n_samples, csl, tile, r.v.x, sc, r.uG, r.iters, r.relres, st);
+    }
+    // stage 3 (per part): recovery of the interiors and the vertex values
+    for (int32_t q = 0; q < n_parts && !rc; ++q) {
+        PartRun& r = R[q];
+        cudaError_t e = grf::launch_recover(r.g->dev, r.plan->dev, n_samples, r.W, u_out[q], r.uG, r.counters + 1, st);
+        if (e == cudaSuccess) e = grf::launch_vertex_sum(r.g->dev, r.plan->dev, n_samples, r.uG, u_out[q], st);
+        if (e != cudaSuccess) rc = fail(GRF_ECUDA, "edge-partitioned recovery: %s", cudaGetErrorString(e));
+    }
+    if (!rc) {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = fail(GRF_ECUDA, "edge-partitioned launch: %s", cudaGetErrorString(e));
+    }
+    if (!rc && stats) {
+        std::vector<int32_t> its((size_t)n_samples * L);
+        std::vector<double> rr((size_t)n_samples * L);
+        CUDA_TRY(cudaMemcpyAsync(its.data(), R0.iters, its.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaMemcpyAsync(rr.data(), R0.relres, rr.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        std::memset(stats, 0, sizeof(*stats));
+        stats->n_nodes = L;
+        stats->k_minus = R0.plan->Km;
+        stats->k_plus = R0.plan->Kp;
+        stats->n_systems = n_samples * L;
+        stats->iter_min = *std::min_element(its.begin(), its.end());
+        stats->iter_max = *std::max_element(its.begin(), its.end());
+        double sum = 0.0, worst = 0.0;
+        int64_t bad = 0;
+        for (size_t i = 0; i < its.size(); ++i) {
+            sum += its[i];
+            worst = std::max(worst, rr[i]);
+            if (!(rr[i] <= rtol)) ++bad;
+        }
+        stats->iter_mean = sum / its.size();
+        stats->worst_rel_residual = worst;
+        stats->n_unconverged = bad;
+        if (bad) rc = fail(GRF_ENOCONV, "%lld PCG systems missed rtol %g", (long long)bad, rtol);
+    }
+    cleanup();
+    return rc;
+}

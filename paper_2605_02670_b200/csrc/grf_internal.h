@@ -31,6 +31,10 @@ struct DevGraph {
     int64_t NT = 0;                   // table rows (sum of m_e over distinct (m_e, h_e))
     const int64_t* toff = nullptr;    // [E] first table row of the edge's (m_e, h_e) class
     const int32_t* tab_rep = nullptr; // [E] 1 for the edge that writes its class's rows
+    // edge-partitioned graphs (grf_graph_create_part; all null for a whole graph):
+    const int64_t* dof_gid = nullptr; // [N] global DOF index (noise counter) of each local DOF
+    const uint8_t* vowned = nullptr;  // [V] 1: this part owns the vertex (rhs W_v, dot products)
+    const int64_t* viface = nullptr;  // [V] interface id (vertex shared with other parts) or -1
     int32_t max_deg = 0;              // max vertex degree (incident edge ends)
     int32_t ell_w = 0;                // ELL width = max_deg rounded up to 4/8/16/32
     const int32_t* ell_other = nullptr; // [ell_w][V] other endpoint of incidence slot j of v (v if padding)
@@ -94,6 +98,9 @@ cudaError_t launch_condense(const DevGraph& g, const DevPlan& p, int64_t n_sampl
 cudaError_t launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* W,
                        const double* ends, double* rhs, double* uG, int32_t* iters, double* relres, void* gws,
                        cudaStream_t st);
+// K4a condensed rhs (pcg.cu): rhs [tile][l][cs][v] from W and the end values
+void launch_assemble_rhs(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W, const double* ends,
+                         double* rhs, cudaStream_t st);
 // K4 global-memory variant (pcg_global.cu) and its workspace
 bool pcg_shared_ok(const DevGraph& g);
 cudaError_t launch_pcg_global(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm,
@@ -112,6 +119,36 @@ void plan_tiling(int32_t L, int32_t* Lp, int32_t* tl, int32_t* rounds);
 // K4 warp-per-system variant (pcg_warp.cu); false if the graph is outside its range
 bool launch_pcg_warp(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* rhs,
                      double* uG, int32_t* iters, double* relres, cudaStream_t st);
+
+// Edge-partitioned NN-PCG stages (dist.cu); vectors [L][V][cs] per part
+namespace dist {
+struct Vecs {
+    double *x, *r0, *r1, *p0, *p1, *q, *z;
+};
+struct Scal {  // [L * cs] per system, shared by all parts of the problem
+    double *alpha, *beta, *rz, *gg, *rr;
+    int32_t *done, *its, *active;  // active: [1] count of unconverged systems
+};
+void init(const DevGraph& g, int32_t L, int64_t S, int32_t csl, int64_t tile, const double* rhs, const Vecs& v,
+          cudaStream_t st);
+void precond(const DevGraph& g, const DevPlan& p, int32_t pc, int32_t cs, const double* r, double* z, cudaStream_t st);
+void spmv(const DevGraph& g, const DevPlan& p, int32_t cs, const double* beta, const double* z, const double* po,
+          double* pn, double* q, cudaStream_t st);
+void update(const DevGraph& g, const DevPlan& p, int32_t pc, int32_t cs, const double* alpha, const double* q,
+            const double* pn, const double* ro, double* rn, double* x, double* z, cudaStream_t st);
+void dots(const DevGraph& g, int32_t L, int32_t cs, int K, const double* a0, const double* b0, const double* a1,
+          const double* b1, double* part, double* out, cudaStream_t st);
+void pack(const DevGraph& g, int32_t L, int32_t cs, const double* X, double* buf, cudaStream_t st);
+void unpack(const DevGraph& g, int32_t L, int32_t cs, const double* buf, double* X, cudaStream_t st);
+void sum_parts(int32_t P, double* const* in_dev, int64_t n, double* out, cudaStream_t st);
+void scal_init(int32_t n, int32_t cs, int64_t S, int64_t tile, int32_t csl, const double* dots, const Scal& sc,
+               cudaStream_t st);
+void scal_alpha(int32_t n, const double* pq, const Scal& sc, cudaStream_t st);
+void scal_beta(int32_t n, double tol2, const double* dots, const Scal& sc, cudaStream_t st);
+void finish(const DevGraph& g, int32_t L, int64_t S, int32_t csl, int64_t tile, const double* x, const Scal& sc,
+            double* uG, int32_t* iters, double* relres, cudaStream_t st);
+int32_t dot_blocks(const DevGraph& g);
+}  // namespace dist
 
 // K2b per-node CSR operator tables for K4 (pcg.cu)
 void launch_pcg_tables(const DevGraph& g, const DevPlan& p, cudaStream_t st);

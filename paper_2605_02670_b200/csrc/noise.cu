@@ -78,14 +78,16 @@ __device__ __forceinline__ double cos2pi_fixed(double u) {
     return qi == 0 ? c : (qi == 1 ? -sn : (qi == 2 ? -c : sn));
 }
 
-__global__ void __launch_bounds__(256) noise_kernel(const double* __restrict__ sqrt_ml, int64_t N,
+__global__ void __launch_bounds__(256) noise_kernel(const double* __restrict__ sqrt_ml,
+                                                    const int64_t* __restrict__ dof_gid, int64_t N,
                                                     int64_t total, uint64_t seed, double* __restrict__ W) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t s = t / N;
         const int64_t i = t - s * N;
         const uint64_t key = seed + (uint64_t)s;
-        const uint4 x = philox4x32_10(make_uint4((unsigned)i, (unsigned)((uint64_t)i >> 32), 0u, 0u),
+        const int64_t ig = dof_gid ? dof_gid[i] : i;  // counter = GLOBAL DOF index (edge-partitioned parts)
+        const uint4 x = philox4x32_10(make_uint4((unsigned)ig, (unsigned)((uint64_t)ig >> 32), 0u, 0u),
                                       make_uint2((unsigned)key, (unsigned)(key >> 32)));
         const uint64_t A = ((uint64_t)x.x << 21) | (uint64_t)(x.y >> 11);
         const uint64_t B = ((uint64_t)x.z << 21) | (uint64_t)(x.w >> 11);
@@ -105,7 +107,7 @@ void launch_noise(const DevGraph& g, uint64_t seed, int64_t n_samples, double* W
     int64_t blocks = (total + 255) / 256;
     const int64_t cap = 148 * 16;
     if (blocks > cap) blocks = cap;
-    noise_kernel<<<(unsigned)blocks, 256, 0, st>>>(g.sqrt_ml, g.N, total, seed, W);
+    noise_kernel<<<(unsigned)blocks, 256, 0, st>>>(g.sqrt_ml, g.dof_gid, g.N, total, seed, W);
 }
 
 }  // namespace grf

@@ -436,7 +436,9 @@ __global__ void __launch_bounds__(256) assemble_rhs_kernel(DevGraph g, int32_t L
             const int v = vb * ASM_VB + vl;
             const int64_t s = (tile << csl) + si;
             if (v < V) {
-                const double wv = Wn[(s < S ? s : S - 1) * g.N + g.NI + v];
+                // W_v enters once: only the owning part adds it (edge-partitioned graphs, dist.cu)
+                const bool own = g.vowned == nullptr || g.vowned[v];
+                const double wv = own ? Wn[(s < S ? s : S - 1) * g.N + g.NI + v] : 0.0;
                 rhs[((tl << csl) + si) * (int64_t)V + v] = wv + acc[vl][si];
             }
         }
@@ -467,13 +469,18 @@ void launch_pcg_tables(const DevGraph& g, const DevPlan& p, cudaStream_t st) {
     pcg_tables_kernel<<<blocks, 256, 0, st>>>(g, p.L, p.cL, reinterpret_cast<const double4*>(p.sig), p.ops);
 }
 
-cudaError_t launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* W,
-                       const double* ends, double* rhs, double* uG, int32_t* iters, double* relres, void* gws,
-                       cudaStream_t st) {
+void launch_assemble_rhs(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W, const double* ends,
+                         double* rhs, cudaStream_t st) {
     const int32_t csl = sample_tile_log2(n_samples);
     const int64_t work = ((n_samples + (1 << csl) - 1) >> csl) * p.L * ((g.V + ASM_VB - 1) / ASM_VB);
     int blocks = (int)(work < 148 * 8 ? work : 148 * 8);
     assemble_rhs_kernel<<<blocks, 256, 0, st>>>(g, p.L, p.ops, n_samples, csl, W, ends, rhs);
+}
+
+cudaError_t launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* W,
+                       const double* ends, double* rhs, double* uG, int32_t* iters, double* relres, void* gws,
+                       cudaStream_t st) {
+    launch_assemble_rhs(g, p, n_samples, W, ends, rhs, st);
     if (prm.global) return launch_pcg_global(g, p, n_samples, prm, rhs, uG, iters, relres, gws, st);
     switch (g.ell_w) {
         case 4: launch_w<4>(g, p, n_samples, prm, rhs, uG, iters, relres, st); break;

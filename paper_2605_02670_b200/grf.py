@@ -18,7 +18,7 @@ from typing import Optional, Tuple
 import numpy as np
 
 from ._lib import (ALLOC_FN, FREE_FN, GRF_ENOCONV, GRF_OK, GrfError, check, grf_allocator, grf_options,
-                   grf_stats, load)
+                   grf_part_info, grf_stats, load)
 
 PRECOND = {"nn": 0, "neumann-neumann": 0, "jacobi": 1, "none": 2}
 
@@ -70,7 +70,7 @@ def make_options(rtol=1e-13, max_iter=0, precond="nn", node_range=None, pcg="aut
 class Graph:
     """A metric graph + its P1 mesh, resident on the current CUDA device."""
 
-    def __init__(self, n_vertices, edge_u, edge_v, length, h, use_torch_allocator: bool = True):
+    def __init__(self, n_vertices, edge_u, edge_v, length, h, use_torch_allocator: bool = True, part=None):
         torch = _torch()
         lib = load()
         self._lib = lib
@@ -98,9 +98,27 @@ class Graph:
             self._alloc = grf_allocator(self._cb[0], self._cb[1], None)
         h_ = C.c_void_p()
         pi64 = C.POINTER(C.c_int64)
-        check(lib.grf_graph_create(self.n_vertices, self.n_edges, eu.ctypes.data_as(pi64), ev.ctypes.data_as(pi64),
-                                   ln.ctypes.data_as(C.POINTER(C.c_double)), self.h,
-                                   C.byref(self._alloc) if self._alloc is not None else None, C.byref(h_)))
+        alloc = C.byref(self._alloc) if self._alloc is not None else None
+        self.part = part
+        if part is None:
+            check(lib.grf_graph_create(self.n_vertices, self.n_edges, eu.ctypes.data_as(pi64),
+                                       ev.ctypes.data_as(pi64), ln.ctypes.data_as(C.POINTER(C.c_double)), self.h,
+                                       alloc, C.byref(h_)))
+        else:  # edge-partitioned part (edgepart.Part): grf_graph_create_part
+            keep = [np.ascontiguousarray(part.vertices, dtype=np.int64),
+                    np.ascontiguousarray(part.edge_goff, dtype=np.int64),
+                    np.ascontiguousarray(part.vertex_mass, dtype=np.float64),
+                    np.ascontiguousarray(part.vertex_degree, dtype=np.int32),
+                    np.ascontiguousarray(part.vertex_owned, dtype=np.uint8),
+                    np.ascontiguousarray(part.vertex_iface, dtype=np.int64)]
+            info = grf_part_info(part.global_n_interior, keep[0].ctypes.data_as(pi64), keep[1].ctypes.data_as(pi64),
+                                 keep[2].ctypes.data_as(C.POINTER(C.c_double)),
+                                 keep[3].ctypes.data_as(C.POINTER(C.c_int32)),
+                                 keep[4].ctypes.data_as(C.POINTER(C.c_uint8)), part.n_interface,
+                                 keep[5].ctypes.data_as(pi64))
+            check(lib.grf_graph_create_part(self.n_vertices, self.n_edges, eu.ctypes.data_as(pi64),
+                                            ev.ctypes.data_as(pi64), ln.ctypes.data_as(C.POINTER(C.c_double)),
+                                            self.h, C.byref(info), alloc, C.byref(h_)))
         self._h = h_
         n, ni = C.c_int64(), C.c_int64()
         check(lib.grf_graph_num_dofs(self._h, C.byref(n), C.byref(ni)))
@@ -110,6 +128,11 @@ class Graph:
     @classmethod
     def from_metric_graph(cls, g, h, **kw):
         return cls(g.n_vertices, g.edge_u, g.edge_v, g.length, h, **kw)
+
+    @classmethod
+    def from_part(cls, part, h, **kw):
+        """A part of an edge-partitioned graph (edgepart.Part) -> grf_graph_create_part."""
+        return cls(part.n_vertices, part.edge_u, part.edge_v, part.length, h, part=part, **kw)
 
     # ------------------------------------------------------------------ queries
     def edge_layout(self):
@@ -252,3 +275,57 @@ class Graph:
 
 def version() -> str:
     return load().grf_version().decode()
+
+
+def sample_edgepart(graphs, kappa, beta, k, seed=0, n_samples=1, comm=None, stream=None, return_stats=False,
+                    **opts):
+    """grf_sample_edgepart: the field on every part's local DOFs (list of cuda fp64 [S, N_q]).
+
+    graphs: the parts (Graph.from_part) held by this process -- all of them (comm=None, the
+    halo / dot sums run on the device in fixed order) or this rank's one part with an NCCL
+    communicator (comm: an object with a ``handle`` attribute from grf_comm_init)."""
+    torch = _torch()
+    lib = load()
+    o = make_options(**opts)
+    outs = [torch.empty((n_samples, g.n_dofs), dtype=torch.float64, device=f"cuda:{g.device}") for g in graphs]
+    hs = (C.c_void_p * len(graphs))(*[g._h.value for g in graphs])
+    us = (C.c_void_p * len(graphs))(*[u.data_ptr() for u in outs])
+    st = grf_stats() if return_stats else None
+    check(lib.grf_sample_edgepart(hs, len(graphs), comm.handle if comm is not None else None, kappa, beta, k,
+                                  C.c_uint64(seed & (2 ** 64 - 1)), n_samples, C.byref(o), us,
+                                  C.c_void_p(_stream_ptr(stream)), C.byref(st) if st is not None else None))
+    return (outs, st.as_dict()) if return_stats else outs
+
+
+class Comm:
+    """grf_comm: an NCCL communicator of the library for one rank (one process per GPU).
+
+    The 128-byte NCCL unique id is made on rank 0 and broadcast with a torch.distributed
+    process group (any backend); the library then talks NCCL directly on its streams."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        _torch()
+        lib = load()
+        self._lib = lib
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        uid = (C.c_char * 128)()
+        if self.rank == 0:
+            check(lib.grf_comm_get_unique_id(uid))
+        box = [bytes(uid.raw) if self.rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=group)
+        uid = (C.c_char * 128).from_buffer_copy(box[0])
+        h = C.c_void_p()
+        check(lib.grf_comm_init(uid, self.rank, self.world, C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            self._lib.grf_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,120 @@
+"""Edge-partitioned sampling on the GPU (grf_sample_edgepart) vs the oracle and vs
+the whole-graph call.  All parts run in this process (comm = NULL: halo and dot sums on the
+device); the NCCL path is exercised with a one-rank communicator."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle import solve  # noqa: E402
+from paper_2605_02670_b200 import Graph, sample_edgepart  # noqa: E402
+from paper_2605_02670_b200.edgepart import gather, partition  # noqa: E402
+from synth import CONFIGS, config_graph, lattice, star_of_lattices  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b, axis=-1) / np.linalg.norm(b, axis=-1)
+
+
+def _run_parts(g, h, P, kappa, beta, k, seed, S, **opts):
+    parts = partition(g, h, P)
+    gs = [Graph.from_part(p, h) for p in parts]
+    us, st = sample_edgepart(gs, kappa, beta, k, seed=seed, n_samples=S, return_stats=True, **opts)
+    N = int(sum(np.maximum(1, np.ceil(g.length / h)) - 1)) + g.n_vertices
+    return gather(parts, [u.cpu().numpy() for u in us], h, N), st, parts, gs
+
+
+@pytest.mark.parametrize("P,S", [(1, 2), (2, 1), (2, 3), (3, 16), (4, 20)])
+def test_edgepart_matches_oracle(P, S):
+    g = lattice(5, seed=1)
+    h, kappa, beta, k = 0.05, 2.0, 0.7, 0.4
+    u, st, _, _ = _run_parts(g, h, P, kappa, beta, k, seed=3, S=S)
+    assert np.isfinite(u).all()
+    picks = sorted({0, S - 1})
+    ref, _, _ = solve.sample(g, h, kappa, beta, k, 3, S, samples=picks)
+    assert _rel(u[picks], ref).max() <= 1e-9
+    assert st["n_unconverged"] == 0 and st["worst_rel_residual"] <= 1e-13
+
+
+def test_edgepart_noise_and_interfaces_consistent():
+    """Interface vertices get the same value on every part that holds them; the parts' noise is the
+    whole graph's noise (global Philox counters, whole-graph vertex masses)."""
+    g = star_of_lattices(3, 4)
+    h = 0.125
+    parts = partition(g, h, 3)
+    gs = [Graph.from_part(p, h) for p in parts]
+    whole = Graph.from_metric_graph(g, h)
+    Wall = whole.noise(7, 2).cpu().numpy()
+    for p, G in zip(parts, gs):
+        assert np.array_equal(G.noise(7, 2).cpu().numpy().view(np.uint64), Wall[:, p.dof_gid(h)].view(np.uint64))
+    us = sample_edgepart(gs, 3.0, 0.6, 0.35, seed=7, n_samples=2)
+    vals = {}
+    for p, u in zip(parts, us):
+        uu = u.cpu().numpy()
+        for i, v in enumerate(p.vertices):
+            x = uu[:, u.shape[1] - p.n_vertices + i]
+            if v in vals:
+                assert np.allclose(vals[v], x, rtol=1e-12, atol=1e-14)
+            vals[v] = x
+
+
+def test_edgepart_equals_whole_graph_rgg():
+    from synth import rgg_knn
+    g = rgg_knn(5000, k=3, scale=300.0 * (5000 / 100_000) ** 0.5, seed=1)
+    h, kappa, beta, k = 0.02, 2.0, 0.55, 0.6
+    whole = Graph.from_metric_graph(g, h).sample(kappa, beta, k, seed=4, n_samples=16).cpu().numpy()
+    for P in (2, 5):
+        u, st, _, _ = _run_parts(g, h, P, kappa, beta, k, seed=4, S=16)
+        assert _rel(u, whole).max() <= 1e-10, f"P={P}"
+
+
+def test_edgepart_nccl_one_rank():
+    """The NCCL code path (grf_comm) with a one-rank communicator."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2605_02670_b200 import Comm
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = Comm()
+        g = lattice(4, seed=3)
+        h = 0.05
+        part = partition(g, h, 1)[0]
+        G = Graph.from_part(part, h)
+        u = sample_edgepart([G], 3.0, 0.7, 0.4, seed=1, n_samples=4, comm=comm)[0].cpu().numpy()
+        ref = Graph.from_metric_graph(g, h).sample(3.0, 0.7, 0.4, seed=1, n_samples=4).cpu().numpy()
+        assert _rel(gather([part], [u], h, ref.shape[1]), ref).max() <= 1e-11
+        comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_config4_edge_partitioned_two_parts():
+    """configs[3] (1e5 vertices, N = 2.8e7, L = 112, 16 samples) split into 2 edge parts, both on
+    this GPU, vs the whole-graph call."""
+    import gc
+    cfg = CONFIGS["rgg"]
+    g = config_graph("rgg")
+    G = Graph.from_metric_graph(g, cfg["h"])
+    whole = G.sample(cfg["kappa"], cfg["beta"], cfg["k"], seed=0, n_samples=16)[[0, 15]].cpu().numpy()
+    del G
+    gc.collect()
+    torch.cuda.empty_cache()
+    u, st, _, _ = _run_parts(g, cfg["h"], 2, cfg["kappa"], cfg["beta"], cfg["k"], seed=0, S=16)
+    assert st["n_unconverged"] == 0
+    assert _rel(u[[0, 15]], whole).max() <= 1e-10
