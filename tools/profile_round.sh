@@ -11,5 +11,5 @@ python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${R}_bench_re
 CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/${R}_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${R}_launches.csv $CMD > gpurun_out/${R}_ncu_launch.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"sweep|pcg_kernel" -s 4 -c 3 -o gpurun_out/${R}_full $CMD > gpurun_out/${R}_ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"sweep|pcg_warp|assemble" -s 4 -c 4 -o gpurun_out/${R}_full $CMD > gpurun_out/${R}_ncu_full.log 2>&1
 echo done

@@ -15,15 +15,22 @@ CONFIG = sys.argv[2] if len(sys.argv) > 2 else "lattice256"
 G = "gpurun_out"
 P = "profiles"
 os.makedirs(P, exist_ok=True)
-NAMES = {"noise_kernel": "noise", "edge_setup_kernel": "edge_setup", "pcg_tables_kernel": "pcg_tables",
-         "sweep_kernel<16, 32, 0>": "condense", "sweep_kernel<16, 32, 1>": "recover", "pcg_kernel": "pcg"}
+import re
 
-
+# kernel -> bench.py bracket name (bench times brackets: pcg = assemble + K4, recover = K5 + vertex sum)
 def short(name):
-    for k, v in NAMES.items():
+    m = re.search(r"sweep_kernel<[^>]*?(\d)>", name)
+    if m:
+        return "condense" if m.group(1) == "0" else "recover"
+    for k, v in (("noise_kernel", "noise"), ("edge_setup_kernel", "edge_setup"), ("pcg_tables_kernel", "pcg_tables"),
+                 ("assemble_rhs_kernel", "assemble"), ("vertex_sum_kernel", "vertex_sum"),
+                 ("pcg_warp_kernel", "pcg"), ("pcg_global_kernel", "pcg"), ("pcg_kernel", "pcg")):
         if k in name:
             return v
     return name[:40]
+
+
+BRACKET = {"assemble": "pcg", "vertex_sum": "recover"}
 
 
 for f in (f"{R}_bench.json", f"{R}_bench_ref.json", f"{R}_gpu.txt", f"{R}_host.txt"):
@@ -42,7 +49,7 @@ cnt = collections.Counter()
 for k, us in rows:
     tot[k] += us
     cnt[k] += 1
-step = [k for k in tot if k in ("noise", "condense", "pcg", "recover")]
+step = [k for k in tot if k in ("noise", "condense", "assemble", "pcg", "recover", "vertex_sum")]
 stot = sum(tot[k] for k in step)
 bench = json.load(open(os.path.join(G, f"{R}_bench.json")))
 with open(os.path.join(P, f"{R}_launches.md"), "w") as fh:
@@ -53,8 +60,10 @@ with open(os.path.join(P, f"{R}_launches.md"), "w") as fh:
     fh.write("| kernel | launches | mean us (ncu) | share of step (ncu) | share of step (bench.py events) |\n|---|---|---|---|---|\n")
     for k in sorted(tot, key=lambda x: -tot[x]):
         sh = f"{tot[k] / stot:.3f}" if k in step else "setup (once per plan)"
-        bsh = bench["kernels"].get(k, {}).get("share")
-        fh.write(f"| {k} | {cnt[k]} | {tot[k] / cnt[k]:.1f} | {sh} | {'' if bsh is None else f'{bsh:.3f}'} |\n")
+        br = BRACKET.get(k, k)
+        bsh = bench["kernels"].get(br, {}).get("share")
+        note = "" if bsh is None else (f"{bsh:.3f}" if br == k else f"({br} bracket {bsh:.3f})")
+        fh.write(f"| {k} | {cnt[k]} | {tot[k] / cnt[k]:.1f} | {sh} | {note} |\n")
 
 # ---- full capture summary
 raw = subprocess.run(["ncu", "-i", os.path.join(G, f"{R}_full.ncu-rep"), "--page", "raw", "--csv"],
