@@ -43,35 +43,74 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
     const int* eo = g.ell_other;
     double* r = sm + (size_t)warp * 2 * V;
     double* p = r + V;
+    // packed staging (W = 4): per vertex the 4 neighbour indices as one int4 and the 4 slot
+    // coefficients of each operator as two double2, so a vertex's operator row is 3 LDS.128
+    constexpr bool PACK = STAGE && W == 4;
+    const int4* nb4 = nullptr;
+    const double2 *os01 = nullptr, *os23 = nullptr, *om01 = nullptr, *om23 = nullptr;
     if (STAGE) {  // DS, DM, OS, OM and the neighbour indices of node l, once per CTA
         double* st = sm + (size_t)WARP_NW * 2 * V;
-        int* so = reinterpret_cast<int*>(st + (size_t)(2 + 2 * W) * V);
-        for (int i = threadIdx.x; i < 2 * V; i += WARP_NW * 32) st[i] = tab[i];                      // DS, DM
-        for (int i = threadIdx.x; i < 2 * W * V; i += WARP_NW * 32) st[2 * V + i] = tab[3 * V + i];  // OS, OM
-        for (int i = threadIdx.x; i < W * V; i += WARP_NW * 32) so[i] = eo[i];
-        __syncthreads();
-        DS = st;
-        DM = st + V;
-        OS = st + 2 * V;
-        OM = OS + (size_t)W * V;
-        eo = so;
+        if (PACK) {
+            double* sD = st;                                          // DS [V], DM [V]
+            double2* sO = reinterpret_cast<double2*>(st + 2 * V);     // OS01, OS23, OM01, OM23: [V] each
+            int4* sN = reinterpret_cast<int4*>(sO + 4 * V);           // neighbours [V]
+            for (int i = threadIdx.x; i < 2 * V; i += WARP_NW * 32) sD[i] = tab[i];
+            for (int v = threadIdx.x; v < V; v += WARP_NW * 32) {
+                const double* oS = OS + v;
+                const double* oM = OM + v;
+                sO[v] = make_double2(oS[0], oS[V]);
+                sO[V + v] = make_double2(oS[2 * V], oS[3 * V]);
+                sO[2 * V + v] = make_double2(oM[0], oM[V]);
+                sO[3 * V + v] = make_double2(oM[2 * V], oM[3 * V]);
+                sN[v] = make_int4(eo[v], eo[V + v], eo[2 * V + v], eo[3 * V + v]);
+            }
+            __syncthreads();
+            DS = sD;
+            DM = sD + V;
+            os01 = sO;
+            os23 = sO + V;
+            om01 = sO + 2 * V;
+            om23 = sO + 3 * V;
+            nb4 = sN;
+        } else {
+            int* so = reinterpret_cast<int*>(st + (size_t)(2 + 2 * W) * V);
+            for (int i = threadIdx.x; i < 2 * V; i += WARP_NW * 32) st[i] = tab[i];                      // DS, DM
+            for (int i = threadIdx.x; i < 2 * W * V; i += WARP_NW * 32) st[2 * V + i] = tab[3 * V + i];  // OS, OM
+            for (int i = threadIdx.x; i < W * V; i += WARP_NW * 32) so[i] = eo[i];
+            __syncthreads();
+            DS = st;
+            DM = st + V;
+            OS = st + 2 * V;
+            OM = OS + (size_t)W * V;
+            eo = so;
+        }
     }
     // y = D x + sum_j O_j x_{o_j} for this lane's vertices (x in shared memory)
-    auto apply = [&](const double* D, const double* O, const double* xs, double (&y)[VPL]) {
+    auto apply = [&](const double* D, const double* O, const double2* O01, const double2* O23, const double* xs,
+                     double (&y)[VPL]) {
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
             const int v = lane + 32 * k;
             if (v < V) {
                 double a = D[v] * xs[v];
+                if (PACK) {
+                    const int4 nb = nb4[v];
+                    const double2 c01 = O01[v], c23 = O23[v];
+                    a = fma(c01.x, xs[nb.x], a);
+                    a = fma(c01.y, xs[nb.y], a);
+                    a = fma(c23.x, xs[nb.z], a);
+                    a = fma(c23.y, xs[nb.w], a);
+                } else {
 #pragma unroll
-                for (int j = 0; j < W; ++j) a = fma(O[j * V + v], xs[eo[j * V + v]], a);
+                    for (int j = 0; j < W; ++j) a = fma(O[j * V + v], xs[eo[j * V + v]], a);
+                }
                 y[k] = a;
             }
         }
     };
     auto precond = [&](double (&z)[VPL]) {
         if (prm.precond == 0) {
-            apply(DM, OM, r, z);
+            apply(DM, OM, om01, om23, r, z);
         } else {
 #pragma unroll
             for (int k = 0; k < VPL; ++k) {
@@ -118,7 +157,7 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
         int it = 0;
         while (!done && it < prm.max_iter) {
             ++it;
-            apply(DS, OS, p, t);  // Dirichlet step (P247-258): t = q
+            apply(DS, OS, os01, os23, p, t);  // Dirichlet step (P247-258): t = q
             double pq = 0.0;
 #pragma unroll
             for (int k = 0; k < VPL; ++k) {

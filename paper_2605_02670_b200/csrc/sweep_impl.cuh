@@ -506,8 +506,15 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                         tt = 1;
                         pend = true;
                     }
-#pragma unroll 2
-                    for (; tt < tend; ++tt) {
+                    // steps in pairs with alternating partial registers (no register copies)
+                    for (; tt + 1 < tend; tt += 2) {
+                        double aL[TS], aR[TS];
+                        body_mid(tt, aL, aR);
+                        reduce_store(pL, pR, tt - 1);
+                        body_mid(tt + 1, pL, pR);
+                        reduce_store(aL, aR, tt);
+                    }
+                    if (tt < tend) {
                         double aL[TS], aR[TS];
                         body_mid(tt, aL, aR);
                         reduce_store(pL, pR, tt - 1);
@@ -516,6 +523,7 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                             pL[j] = aL[j];
                             pR[j] = aR[j];
                         }
+                        ++tt;
                     }
                     if (last_here) {
                         double aL[TS], aR[TS];
