@@ -208,6 +208,23 @@ grf_status grf_sample_edgepart(grf_graph* const* parts, int32_t n_parts, struct 
                                const grf_options* opt, double* const* u_out, void* stream,
                                grf_stats* stats);
 
+/* ---- nested meshes (strong-error study, §4.1 P335; SPEC S119-127, S256-264) ----
+ * `coarse` and `fine` are meshes of the same graph (equal vertex/edge lists and lengths) with
+ * every fine n_e an integer multiple of the coarse n_e; EINVAL otherwise.  Device arrays are
+ * n x N_coarse / n x N_fine (DOF order of each graph), asynchronous on `stream`.
+ *   grf_prolong:       u_fine = P u_coarse, P = hat-function interpolation of coarse nodal
+ *                      values at the fine nodes (the "upsample" of P335)
+ *   grf_project_noise: W_coarse = P^T W_fine ("project the noise generated on the overkill
+ *                      mesh down", P335)
+ *   grf_mnorm_sq_diff: out[s] = (a_s - b_s)^T M_L (a_s - b_s) on g's mesh (device out[n]; the
+ *                      squared L2(Gamma) error of P335 with the lumped mass); synchronises. */
+grf_status grf_prolong(const grf_graph* coarse, const grf_graph* fine, int64_t n, const double* u_coarse,
+                       double* u_fine, void* stream);
+grf_status grf_project_noise(const grf_graph* fine, const grf_graph* coarse, int64_t n, const double* W_fine,
+                             double* W_coarse, void* stream);
+grf_status grf_mnorm_sq_diff(grf_graph* g, int64_t n, const double* a, const double* b, double* out,
+                             void* stream);
+
 /* Stage entry point (tests, diagnostics): the local Schur blocks
  * S^{(l,e)} = [[s_d, s_o], [s_o, s_d]] (P204-213 [eq:local_reduced_schur]) for the
  * nodes of opt's range, into host array sigma[(l*E + e)*2 + {0,1}].  Synchronises. */

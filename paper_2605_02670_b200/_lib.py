@@ -51,6 +51,7 @@ EXPORTS = [
     "grf_workspace_size", "grf_noise", "grf_sample", "grf_sample_host", "grf_apply", "grf_edge_schur",
     "grf_comm_get_unique_id", "grf_comm_init", "grf_comm_destroy", "grf_reduce_sum",
     "grf_profile_enable", "grf_profile_read", "grf_graph_create_part", "grf_sample_edgepart",
+    "grf_prolong", "grf_project_noise", "grf_mnorm_sq_diff",
 ]
 KERNEL_NAMES = ["noise", "edge_setup", "condense", "pcg", "recover"]
 
@@ -97,6 +98,9 @@ def load() -> C.CDLL:
         "grf_profile_enable": (C.c_int, [P, C.c_int]),
         "grf_graph_create_part": (C.c_int, [I64, I64, pi64, pi64, pd, D, C.POINTER(grf_part_info),
                                             C.POINTER(grf_allocator), C.POINTER(P)]),
+        "grf_prolong": (C.c_int, [P, P, I64, P, P, P]),
+        "grf_project_noise": (C.c_int, [P, P, I64, P, P, P]),
+        "grf_mnorm_sq_diff": (C.c_int, [P, I64, P, P, P, P]),
         "grf_sample_edgepart": (C.c_int, [C.POINTER(P), C.c_int32, P, D, D, D, U64, I64, C.POINTER(grf_options),
                                           C.POINTER(P), P, C.POINTER(grf_stats)]),
         "grf_profile_read": (C.c_int, [P, pd, pi64]),

@@ -603,6 +603,13 @@ grf_status create_impl(int64_t n_vertices, int64_t n_edges, const int64_t* edge_
     if (!st) d.inv_deg = g->upload(inv_deg, &st);
     if (!st) d.owner = g->upload(owner, &st);
     if (!st) d.sqrt_ml = g->upload(sq, &st);
+    if (!st) d.ml = g->upload(g->ml, &st);
+    {
+        std::vector<int32_t> dof_edge(std::max<int64_t>(NI, 1), 0);
+        for (int64_t e = 0; e < E; ++e)
+            for (int64_t t = 0; t < g->n_el[e] - 1; ++t) dof_edge[g->off[e] + t] = (int32_t)e;
+        if (!st) d.dof_edge = g->upload(dof_edge, &st);
+    }
     if (!st) d.edge_order = g->upload(order, &st);
     d.max_deg = max_deg;
     d.ell_w = ell_w;
@@ -1150,4 +1157,55 @@ extern "C" grf_status grf_sample_edgepart(grf_graph* const* parts, int32_t n_par
     }
     cleanup();
     return rc;
+}
+
+// ---------------------------------------------------------------- nested-mesh transfer (strong-error study)
+namespace {
+grf_status check_nested(const grf_graph* c, const grf_graph* f) {
+    if (!c || !f) return fail(GRF_EINVAL, "graph is NULL");
+    if (c->V != f->V || c->E != f->E || c->partitioned || f->partitioned)
+        return fail(GRF_EINVAL, "meshes of different (or partitioned) graphs");
+    for (int64_t e = 0; e < c->E; ++e) {
+        if (c->eu[e] != f->eu[e] || c->ev[e] != f->ev[e] || std::memcmp(&c->len[e], &f->len[e], sizeof(double)))
+            return fail(GRF_EINVAL, "edge %lld differs between the two graphs", (long long)e);
+        if (f->n_el[e] % c->n_el[e])
+            return fail(GRF_EINVAL, "edge %lld: fine n_e = %lld is not a multiple of coarse n_e = %lld (not nested)",
+                        (long long)e, (long long)f->n_el[e], (long long)c->n_el[e]);
+    }
+    return GRF_OK;
+}
+}  // namespace
+
+extern "C" grf_status grf_prolong(const grf_graph* coarse, const grf_graph* fine, int64_t n, const double* u_coarse,
+                                  double* u_fine, void* stream) {
+    grf_status s = check_nested(coarse, fine);
+    if (s) return s;
+    if (n < 1 || !u_coarse || !u_fine) return fail(GRF_EINVAL, "bad prolongation arguments");
+    grf::launch_prolong(coarse->dev, fine->dev, fine->dev.dof_edge, n, u_coarse, u_fine, (cudaStream_t)stream);
+    CUDA_TRY(cudaGetLastError());
+    return GRF_OK;
+}
+
+extern "C" grf_status grf_project_noise(const grf_graph* fine, const grf_graph* coarse, int64_t n, const double* W_fine,
+                                        double* W_coarse, void* stream) {
+    grf_status s = check_nested(coarse, fine);
+    if (s) return s;
+    if (n < 1 || !W_fine || !W_coarse) return fail(GRF_EINVAL, "bad projection arguments");
+    grf::launch_project(coarse->dev, fine->dev, coarse->dev.dof_edge, n, W_fine, W_coarse, (cudaStream_t)stream);
+    CUDA_TRY(cudaGetLastError());
+    return GRF_OK;
+}
+
+extern "C" grf_status grf_mnorm_sq_diff(grf_graph* g, int64_t n, const double* a, const double* b, double* out,
+                                        void* stream) {
+    if (!g || n < 1 || !a || !b || !out) return fail(GRF_EINVAL, "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t bytes = sizeof(double) * (size_t)n * 148;
+    void* part = g->alloc.get(bytes, st);
+    if (!part) return fail(GRF_ENOMEM, "partial buffer");
+    grf::launch_mnorm_sq_diff(g->dev, n, a, b, (double*)part, out, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    g->alloc.put(part, bytes, st);
+    if (e != cudaSuccess) return fail(GRF_ECUDA, "mnorm: %s", cudaGetErrorString(e));
+    return GRF_OK;
 }

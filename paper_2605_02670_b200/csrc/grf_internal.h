@@ -24,7 +24,9 @@ struct DevGraph {
     const int32_t* inc_other = nullptr; // [2E] the other endpoint of that edge
     const double* inv_deg = nullptr;  // [V] 1 / d_v, d_v = incident edge ends (P261)
     const int32_t* owner = nullptr;   // [V] incidence code that writes the vertex value in recovery
-    const double* sqrt_ml = nullptr;  // [N] sqrt of the lumped mass diagonal
+    const double* sqrt_ml = nullptr;  // [N] sqrt of the lumped mass diagonal (noise scaling)
+    const double* ml = nullptr;       // [N] lumped mass diagonal of this mesh
+    const int32_t* dof_edge = nullptr; // [NI] edge of each interior DOF
     const int32_t* edge_order = nullptr; // [E] edges by descending interior length (work-queue order)
     // Thomas tables depend on an edge only through (m_e, h_e): edges with identical meshes share
     // one set of table rows (config 5: all 3848 edges share one).
@@ -149,6 +151,14 @@ void finish(const DevGraph& g, int32_t L, int64_t S, int32_t csl, int64_t tile, 
             double* uG, int32_t* iters, double* relres, cudaStream_t st);
 int32_t dot_blocks(const DevGraph& g);
 }  // namespace dist
+
+// nested-mesh transfer for the strong-error study (refine.cu)
+void launch_prolong(const DevGraph& gc, const DevGraph& gf, const int32_t* fedge, int64_t S, const double* uc,
+                    double* uf, cudaStream_t st);
+void launch_project(const DevGraph& gc, const DevGraph& gf, const int32_t* cedge, int64_t S, const double* wf,
+                    double* wc, cudaStream_t st);
+void launch_mnorm_sq_diff(const DevGraph& g, int64_t S, const double* a, const double* b, double* part, double* out,
+                          cudaStream_t st);
 
 // K2b per-node CSR operator tables for K4 (pcg.cu)
 void launch_pcg_tables(const DevGraph& g, const DevPlan& p, cudaStream_t st);

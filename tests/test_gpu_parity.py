@@ -374,3 +374,40 @@ def test_config5_star_finest_level():
         A = fem.operator(prob.ML, prob.G, prob.kappa, prob.plan.c_I[li], prob.plan.c_L[li])
         res = (A @ x.T).T - W
         assert (np.linalg.norm(res, axis=1) / np.linalg.norm(W, axis=1)).max() <= 1e-9, f"node {li}"
+
+
+# ----------------------------------------------------------------------------- NEXT-1 strong-error study
+def test_nested_transfer_kernels_vs_oracle():
+    """grf_project_noise / grf_prolong vs the oracle's hat-function matrices (P335, SPEC S119-127)."""
+    from oracle.mesh import build_mesh
+    from oracle.refine import prolongation
+    from paper_2605_02670_b200.study import project_noise, prolong
+    g = MetricGraph(4, np.array([0, 0, 1, 2, 3]), np.array([1, 2, 2, 3, 3]),
+                    np.array([1.0, 0.5, 0.75, 1.25, 0.5]))  # includes a loop edge (3, 3)
+    hc, hf = 0.25, 0.25 / 4
+    Gc, Gf = _graph(g, hc), _graph(g, hf)
+    P = prolongation(build_mesh(g, hc), build_mesh(g, hf))
+    rng = np.random.default_rng(0)
+    uc = rng.standard_normal((3, Gc.n_dofs))
+    wf = rng.standard_normal((3, Gf.n_dofs))
+    up = prolong(Gc, Gf, torch.from_numpy(uc).cuda()).cpu().numpy()
+    wc = project_noise(Gf, Gc, torch.from_numpy(wf).cuda()).cpu().numpy()
+    assert np.abs(up - (P @ uc.T).T).max() <= 1e-15
+    assert np.abs(wc - (P.T @ wf.T).T).max() <= 1e-14
+    with pytest.raises(Exception):
+        prolong(_graph(g, 0.22), Gf, torch.zeros((1, _graph(g, 0.22).n_dofs), dtype=torch.float64, device="cuda"))
+
+
+def test_strong_error_study_vs_oracle():
+    """The whole study pipeline on a small star of lattices: per-realization squared errors vs
+    the oracle's definition (oracle/refine.strong_error)."""
+    from oracle.refine import strong_error
+    from paper_2605_02670_b200.study import strong_error as gpu_study
+    g = star_of_lattices(2, 3)
+    kappa, beta, k, ok = 4.0, 0.75, 0.5, 5
+    res = gpu_study(g, [2, 3], ok, kappa, beta, k, seed=11, n_samples=4, batch=4)
+    Gf = _graph(g, 2.0 ** -ok)
+    W = Gf.noise(11, 4).cpu().numpy()
+    for j in (2, 3):
+        ref = strong_error(g, 2.0 ** -j, 2.0 ** -ok, kappa, beta, k, W)
+        assert np.max(np.abs(res["per_sample_sq"][j] - ref) / ref) <= 1e-9
