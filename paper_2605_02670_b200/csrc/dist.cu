@@ -23,7 +23,6 @@ namespace {
 
 constexpr int BT = 256;
 
-__device__ __forceinline__ int64_t tstride(int V, int W) { return 3 * (int64_t)V + 3 * (int64_t)W * V; }
 
 // r = rhs (partial sums at interface vertices), x = 0, p = 0
 template <int CS>
@@ -47,11 +46,12 @@ __global__ void init_kernel(DevGraph g, int32_t L, int64_t S, int32_t csl, int64
 template <int CS>
 __global__ void precond_kernel(DevGraph g, int32_t L, const double* __restrict__ ops, int32_t precond,
                                const double* __restrict__ r, double* __restrict__ z) {
-    const int V = g.V, Wd = g.ell_w;
+    const int V = g.V;
+    const int64_t ns = ops_nslots(g);
     const int64_t n = (int64_t)L * V;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
         const int l = (int)(t / V), v = (int)(t % V);
-        const double* tab = ops + l * tstride(V, Wd);
+        const double* tab = ops + l * ops_stride(g);
         double zv[CS];
         if (precond == 0) {
             const double dm = tab[V + v];
@@ -59,8 +59,9 @@ __global__ void precond_kernel(DevGraph g, int32_t L, const double* __restrict__
             for (int s = 0; s < CS; ++s) zv[s] = dm * r[t * CS + s];
             const int dg = g.inc_ptr[v + 1] - g.inc_ptr[v];
             for (int j = 0; j < dg; ++j) {
-                const double c = tab[3 * (int64_t)V + (int64_t)Wd * V + (int64_t)j * V + v];
-                const double* ro = r + ((int64_t)l * V + g.ell_other[(int64_t)j * V + v]) * CS;
+                const int64_t k = ops_slot(g, v, j);
+                const double c = tab[3 * (int64_t)V + ns + k];
+                const double* ro = r + ((int64_t)l * V + ops_other(g, k)) * CS;
 #pragma unroll
                 for (int s = 0; s < CS; ++s) zv[s] = fma(c, ro[s], zv[s]);
             }
@@ -79,11 +80,12 @@ template <int CS>
 __global__ void spmv_kernel(DevGraph g, int32_t L, const double* __restrict__ ops, const double* __restrict__ beta,
                             const double* __restrict__ z, const double* __restrict__ po, double* __restrict__ pn,
                             double* __restrict__ q) {
-    const int V = g.V, Wd = g.ell_w;
+    const int V = g.V;
+    const int64_t ns = ops_nslots(g);
     const int64_t n = (int64_t)L * V;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
         const int l = (int)(t / V), v = (int)(t % V);
-        const double* tab = ops + l * tstride(V, Wd);
+        const double* tab = ops + l * ops_stride(g);
         double bt[CS], pv[CS], qv[CS];
         const double ds = tab[v];
 #pragma unroll
@@ -94,8 +96,9 @@ __global__ void spmv_kernel(DevGraph g, int32_t L, const double* __restrict__ op
         }
         const int dg = g.inc_ptr[v + 1] - g.inc_ptr[v];
         for (int j = 0; j < dg; ++j) {
-            const double c = tab[3 * (int64_t)V + (int64_t)j * V + v];
-            const int64_t ob = ((int64_t)l * V + g.ell_other[(int64_t)j * V + v]) * CS;
+            const int64_t k = ops_slot(g, v, j);
+            const double c = tab[3 * (int64_t)V + k];
+            const int64_t ob = ((int64_t)l * V + ops_other(g, k)) * CS;
 #pragma unroll
             for (int s = 0; s < CS; ++s) qv[s] = fma(c, fma(bt[s], po[ob + s], z[ob + s]), qv[s]);
         }
@@ -113,11 +116,12 @@ __global__ void update_kernel(DevGraph g, int32_t L, const double* __restrict__ 
                               const double* __restrict__ alpha, const double* __restrict__ q,
                               const double* __restrict__ pn, const double* __restrict__ ro, double* __restrict__ rn,
                               double* __restrict__ x, double* __restrict__ z) {
-    const int V = g.V, Wd = g.ell_w;
+    const int V = g.V;
+    const int64_t ns = ops_nslots(g);
     const int64_t n = (int64_t)L * V;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
         const int l = (int)(t / V), v = (int)(t % V);
-        const double* tab = ops + l * tstride(V, Wd);
+        const double* tab = ops + l * ops_stride(g);
         double al[CS], rv[CS], zv[CS];
 #pragma unroll
         for (int s = 0; s < CS; ++s) {
@@ -131,8 +135,9 @@ __global__ void update_kernel(DevGraph g, int32_t L, const double* __restrict__ 
             for (int s = 0; s < CS; ++s) zv[s] = dm * rv[s];
             const int dg = g.inc_ptr[v + 1] - g.inc_ptr[v];
             for (int j = 0; j < dg; ++j) {
-                const double c = tab[3 * (int64_t)V + (int64_t)Wd * V + (int64_t)j * V + v];
-                const int64_t ob = ((int64_t)l * V + g.ell_other[(int64_t)j * V + v]) * CS;
+                const int64_t k = ops_slot(g, v, j);
+                const double c = tab[3 * (int64_t)V + ns + k];
+                const int64_t ob = ((int64_t)l * V + ops_other(g, k)) * CS;
 #pragma unroll
                 for (int s = 0; s < CS; ++s) zv[s] = fma(c, fma(-al[s], q[ob + s], ro[ob + s]), zv[s]);
             }

@@ -273,6 +273,7 @@ struct WsLayout {
 // K4 kernel family for these options (grf_options.pcg_variant)
 bool use_global_pcg(const grf_graph* g, const grf_options* opt) {
     const int32_t v = opt ? opt->pcg_variant : GRF_PCG_AUTO;
+    if (g->dev.csr) return true;  // hub vertices: only the global-memory kernel reads CSR tables
     return v == GRF_PCG_GLOBAL || (v == GRF_PCG_AUTO && !grf::pcg_shared_ok(g->dev));
 }
 
@@ -304,8 +305,7 @@ WsLayout ws_layout(const grf_graph* g, int64_t L, int64_t S, bool with_noise, bo
 
 grf_status check_kernel_limits(const grf_graph* g) {
     if (!grf::pcg_supported(g->dev))
-        return fail(GRF_EUNSUPPORTED, "a vertex has %d incident edge ends; the PCG kernels handle <= 32",
-                    g->dev.max_deg);
+        return fail(GRF_EUNSUPPORTED, "PCG operator tables unavailable for this graph");
     return GRF_OK;
 }
 
@@ -557,10 +557,12 @@ grf_status create_impl(int64_t n_vertices, int64_t n_edges, const int64_t* edge_
     // ELL (padded) copy of the incidence lists for the PCG kernels
     int32_t max_deg = 0;
     for (int64_t v = 0; v < V; ++v) max_deg = std::max<int32_t>(max_deg, (int32_t)deg[v]);
+    const bool csr = max_deg > 32;  // hubs (e.g. Barabasi-Albert graphs): CSR operator tables, no ELL copy
     int32_t ell_w = 4;
     while (ell_w < max_deg) ell_w *= 2;
+    if (csr) ell_w = 0;
     std::vector<int32_t> ell_other((size_t)ell_w * V), ell_code((size_t)ell_w * V, 0), ell_valid((size_t)ell_w * V, 0);
-    for (int64_t v = 0; v < V; ++v) {
+    for (int64_t v = 0; v < V && !csr; ++v) {
         for (int32_t j = 0; j < ell_w; ++j) ell_other[(size_t)j * V + v] = (int32_t)v;
         for (int32_t k = ptr[v]; k < ptr[v + 1]; ++k) {
             const int32_t j = k - ptr[v];
@@ -613,9 +615,12 @@ grf_status create_impl(int64_t n_vertices, int64_t n_edges, const int64_t* edge_
     if (!st) d.edge_order = g->upload(order, &st);
     d.max_deg = max_deg;
     d.ell_w = ell_w;
-    if (!st) d.ell_other = g->upload(ell_other, &st);
-    if (!st) d.ell_code = g->upload(ell_code, &st);
-    if (!st) d.ell_valid = g->upload(ell_valid, &st);
+    d.csr = csr ? 1 : 0;
+    if (!csr) {
+        if (!st) d.ell_other = g->upload(ell_other, &st);
+        if (!st) d.ell_code = g->upload(ell_code, &st);
+        if (!st) d.ell_valid = g->upload(ell_valid, &st);
+    }
     if (part) {
         if (!st) d.dof_gid = g->upload(dof_gid, &st);
         if (!st) d.vowned = g->upload(vowned, &st);

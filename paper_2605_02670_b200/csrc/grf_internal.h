@@ -38,11 +38,26 @@ struct DevGraph {
     const uint8_t* vowned = nullptr;  // [V] 1: this part owns the vertex (rhs W_v, dot products)
     const int64_t* viface = nullptr;  // [V] interface id (vertex shared with other parts) or -1
     int32_t max_deg = 0;              // max vertex degree (incident edge ends)
-    int32_t ell_w = 0;                // ELL width = max_deg rounded up to 4/8/16/32
+    int32_t csr = 0;                  // 1: operator tables in CSR incidence order (a vertex has > 32 edge ends)
+    int32_t ell_w = 0;                // ELL width = max_deg rounded up to 4/8/16/32 (0 in CSR mode)
     const int32_t* ell_other = nullptr; // [ell_w][V] other endpoint of incidence slot j of v (v if padding)
     const int32_t* ell_code = nullptr;  // [ell_w][V] incidence code 2e+end of slot j (0 if padding)
     const int32_t* ell_valid = nullptr; // [ell_w][V] 1 for a real incidence, 0 for padding
 };
+
+// Per-node PCG operator tables (pcg_tables_kernel): [DS (V) | DM (V) | DJ (V) | OS | OM | GK],
+// the three slot arrays indexed by an incidence slot k of vertex v: ELL mode k = j * V + v
+// (j < ell_w, padding slots point at v with zero coefficients), CSR mode k = inc_ptr[v] + j.
+// Slots j < deg(v) = inc_ptr[v+1] - inc_ptr[v] are the real incidences in both modes.
+__host__ __device__ inline int64_t ops_nslots(const DevGraph& g) {
+    return g.csr ? 2 * (int64_t)g.E : (int64_t)g.ell_w * g.V;
+}
+__host__ __device__ inline int64_t ops_stride(const DevGraph& g) { return 3 * (int64_t)g.V + 3 * ops_nslots(g); }
+__device__ __forceinline__ int64_t ops_slot(const DevGraph& g, int v, int j) {
+    return g.csr ? (int64_t)g.inc_ptr[v] + j : (int64_t)j * g.V + v;
+}
+__device__ __forceinline__ int ops_other(const DevGraph& g, int64_t k) { return g.csr ? g.inc_other[k] : g.ell_other[k]; }
+__device__ __forceinline__ int ops_code(const DevGraph& g, int64_t k) { return g.csr ? g.inc[k] : g.ell_code[k]; }
 
 // Device per-plan tables (one (kappa, beta, k, node range)).
 struct DevPlan {

@@ -42,8 +42,9 @@ __host__ __device__ inline int64_t table_stride(int V, int W) { return 3 * (int6
 
 __global__ void pcg_tables_kernel(DevGraph g, int32_t L, const double* __restrict__ cLt,
                                   const double4* __restrict__ sig, double* __restrict__ ops) {
-    const int V = g.V, E = g.E, Wd = g.ell_w;
-    const int64_t stride = table_stride(V, Wd);
+    const int V = g.V, E = g.E;
+    const int64_t stride = ops_stride(g), ns = ops_nslots(g);
+    const int slots = g.csr ? 0 : g.ell_w;  // ELL: also write the padding slots
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < (int64_t)L * V;
          x += (int64_t)gridDim.x * blockDim.x) {
         const int l = (int)(x / V), v = (int)(x - (int64_t)l * V);
@@ -53,17 +54,18 @@ __global__ void pcg_tables_kernel(DevGraph g, int32_t L, const double* __restric
         double* DM = DS + V;
         double* DJ = DM + V;
         double* OS = DJ + V;
-        double* OM = OS + (int64_t)Wd * V;
-        double* GK = OM + (int64_t)Wd * V;
+        double* OM = OS + ns;
+        double* GK = OM + ns;
         const double idv = g.inv_deg[v];
         const double cL = cLt[l];
+        const int dg = g.inc_ptr[v + 1] - g.inc_ptr[v];
         double ds = 0.0, dm = 0.0, diag = 0.0;
-        for (int j = 0; j < Wd; ++j) {
-            const int64_t sj = (int64_t)j * V + v;
-            if (g.ell_valid[sj]) {
-                const int e = g.ell_code[sj] >> 1;
+        for (int j = 0; j < (slots > dg ? slots : dg); ++j) {
+            const int64_t sj = ops_slot(g, v, j);
+            if (j < dg) {
+                const int e = ops_code(g, sj) >> 1;
                 const double4 c = sg[e];
-                const int o = g.ell_other[sj];
+                const int o = ops_other(g, sj);
                 ds += c.x;
                 dm += c.z;
                 OS[sj] = c.y;
@@ -404,23 +406,27 @@ __global__ void __launch_bounds__(256) assemble_rhs_kernel(DevGraph g, int32_t L
     __shared__ double acc[ASM_VB][33];
     __shared__ double gks[32][ASM_VB];  // c_L/h_e of incidence slot j of the block's vertices (0: padding)
     __shared__ int codes[32][ASM_VB];   // incidence code 2e+end of slot j (0 for padding: a valid row)
-    const int V = g.V, E = g.E, Wd = g.ell_w;
+    const int V = g.V, E = g.E;
     const int cs = 1 << csl;
     const int vblocks = (V + ASM_VB - 1) / ASM_VB;
     const int64_t tiles = (S + cs - 1) >> csl;
-    const int64_t stride = table_stride(V, Wd);
+    const int64_t stride = ops_stride(g);
+    // incidence slots per vertex handled through the staged arrays; hubs (CSR mode, > 32 slots)
+    // read their remaining slots from global memory
+    const int Wd = g.csr ? 32 : g.ell_w;
     for (int64_t b = blockIdx.x; b < tiles * L * vblocks; b += gridDim.x) {
         const int vb = (int)(b % vblocks);
         const int64_t tl = b / vblocks;  // tile * L + l
         const int l = (int)(tl % L);
         const int64_t tile = tl / L;
-        const double* GK = ops + l * stride + 3 * (int64_t)V + 2 * (int64_t)Wd * V;
+        const double* GK = ops + l * stride + 3 * (int64_t)V + 2 * ops_nslots(g);
         for (int x = threadIdx.x; x < Wd * ASM_VB; x += blockDim.x) {
             const int j = x / ASM_VB, vl = x % ASM_VB;
             const int v = vb * ASM_VB + vl;
-            const bool ok = v < V && g.ell_valid[j * V + v];
-            codes[j][vl] = ok ? g.ell_code[j * V + v] : 0;
-            gks[j][vl] = ok ? GK[j * V + v] : 0.0;
+            const bool ok = v < V && j < g.inc_ptr[v + 1] - g.inc_ptr[v];
+            const int64_t k = ok ? ops_slot(g, v, j) : 0;
+            codes[j][vl] = ok ? ops_code(g, k) : 0;
+            gks[j][vl] = ok ? GK[k] : 0.0;
         }
         __syncthreads();
         const double* slab = ends + ((tl * 2 * E) << csl);
@@ -428,6 +434,14 @@ __global__ void __launch_bounds__(256) assemble_rhs_kernel(DevGraph g, int32_t L
             const int vl = x >> csl, si = x & (cs - 1);
             double a = 0.0;
             for (int j = 0; j < Wd; ++j) a = fma(gks[j][vl], slab[((int64_t)codes[j][vl] << csl) + si], a);
+            const int v = vb * ASM_VB + vl;
+            if (g.csr && v < V) {
+                const int dg = g.inc_ptr[v + 1] - g.inc_ptr[v];
+                for (int j = Wd; j < dg; ++j) {
+                    const int64_t k = ops_slot(g, v, j);
+                    a = fma(GK[k], slab[((int64_t)ops_code(g, k) << csl) + si], a);
+                }
+            }
             acc[vl][si] = a;
         }
         __syncthreads();
@@ -452,14 +466,14 @@ int32_t pcg_max_vertices() { return 8 * PCG_THREADS; }
 
 size_t pcg_smem_bytes(const DevGraph& g) { return vec_bytes(g, 1, 1); }
 
-size_t pcg_table_doubles(const DevGraph& g) { return (size_t)table_stride(g.V, g.ell_w); }
+size_t pcg_table_doubles(const DevGraph& g) { return (size_t)ops_stride(g); }
 
 bool pcg_shared_ok(const DevGraph& g) {
-    return g.V <= pcg_max_vertices() && g.ell_w <= 32 && vec_bytes(g, 1, 1) <= SMEM_LIMIT;
+    return !g.csr && g.V <= pcg_max_vertices() && g.ell_w <= 32 && vec_bytes(g, 1, 1) <= SMEM_LIMIT;
 }
 
 bool pcg_supported(const DevGraph& g) {
-    return g.ell_w <= 32;  // larger vertex sets take the global-memory variant (pcg_global.cu)
+    return true;  // larger vertex sets and hubs take the global-memory variant (pcg_global.cu)
 }
 
 void launch_pcg_tables(const DevGraph& g, const DevPlan& p, cudaStream_t st) {

@@ -49,7 +49,6 @@ struct GArgs {
     int32_t* cnt;                           // [L] arrival counters (zero between phases)
 };
 
-__device__ __forceinline__ int64_t table_stride_g(int V, int W) { return 3 * (int64_t)V + 3 * (int64_t)W * V; }
 
 // Block reduction of K x CS per-thread values into part[l][vb][k][s]; the last block of
 // node l to arrive then reduces all vertex blocks (fixed order) into out_k[l][s] and runs
@@ -94,11 +93,12 @@ __global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
     cg::grid_group grid = cg::this_grid();
     __shared__ double red[(GT / 32) * 2 * CS];
     const DevGraph& g = A.g;
-    const int V = g.V, L = A.L, Wd = g.ell_w;
+    const int V = g.V, L = A.L;
+    const int64_t ns = ops_nslots(g);
     const int nvb = (V + GT - 1) / GT;
     const int64_t items = (int64_t)L * nvb;
     const int tid = threadIdx.x;
-    const int64_t stride = table_stride_g(V, Wd);
+    const int64_t stride = ops_stride(g);
     const int64_t s0 = A.tile << A.csl;
     double* po = A.p0;
     double* pn = A.p1;
@@ -166,8 +166,9 @@ __global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
                 for (int s = 0; s < CS; ++s) zv[s] = dm * rv[s];
                 const int dg = deg_of(v);
                 for (int j = 0; j < dg; ++j) {
-                    const double c = tab[3 * (int64_t)V + (int64_t)Wd * V + (int64_t)j * V + v];
-                    const double* ro_o = ro + ((int64_t)l * V + g.ell_other[(int64_t)j * V + v]) * CS;
+                    const int64_t k = ops_slot(g, v, j);
+                    const double c = tab[3 * (int64_t)V + ns + k];
+                    const double* ro_o = ro + ((int64_t)l * V + ops_other(g, k)) * CS;
 #pragma unroll
                     for (int s = 0; s < CS; ++s) zv[s] = fma(c, ro_o[s], zv[s]);
                 }
@@ -218,8 +219,9 @@ __global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
                 for (int s = 0; s < CS; ++s) qv[s] = ds * pv[s];
                 const int dg = deg_of(v);
                 for (int j = 0; j < dg; ++j) {
-                    const double c = tab[3 * (int64_t)V + (int64_t)j * V + v];
-                    const int64_t ob = ((int64_t)l * V + g.ell_other[(int64_t)j * V + v]) * CS;
+                    const int64_t k = ops_slot(g, v, j);
+                    const double c = tab[3 * (int64_t)V + k];
+                    const int64_t ob = ((int64_t)l * V + ops_other(g, k)) * CS;
 #pragma unroll
                     for (int s = 0; s < CS; ++s) qv[s] = fma(c, fma(bt[s], po[ob + s], A.z[ob + s]), qv[s]);
                 }
@@ -262,8 +264,9 @@ __global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
                     for (int s = 0; s < CS; ++s) zv[s] = dm * rv[s];
                     const int dg = deg_of(v);
                     for (int j = 0; j < dg; ++j) {
-                        const double c = tab[3 * (int64_t)V + (int64_t)Wd * V + (int64_t)j * V + v];
-                        const int64_t ob = ((int64_t)l * V + g.ell_other[(int64_t)j * V + v]) * CS;
+                        const int64_t k = ops_slot(g, v, j);
+                        const double c = tab[3 * (int64_t)V + ns + k];
+                        const int64_t ob = ((int64_t)l * V + ops_other(g, k)) * CS;
 #pragma unroll
                         for (int s = 0; s < CS; ++s) zv[s] = fma(c, fma(-al[s], A.q[ob + s], ro[ob + s]), zv[s]);
                     }

@@ -411,3 +411,36 @@ def test_strong_error_study_vs_oracle():
     for j in (2, 3):
         ref = strong_error(g, 2.0 ** -j, 2.0 ** -ok, kappa, beta, k, W)
         assert np.max(np.abs(res["per_sample_sq"][j] - ref) / ref) <= 1e-9
+
+
+# ----------------------------------------------------------------------------- hubs (CSR operator tables)
+def test_hub_graph_csr_tables_vs_oracle():
+    """A vertex with 41 incident edge ends (> 32: CSR operator tables, global-memory PCG) plus a
+    loop and a multi-edge at the hub, vs the oracle."""
+    n_leaf = 40
+    eu = np.concatenate([np.zeros(n_leaf, np.int64), [0, 1, 0]])
+    ev = np.concatenate([np.arange(1, n_leaf + 1), [0, 2, 1]])
+    ln = np.concatenate([np.linspace(0.3, 1.1, n_leaf), [0.7, 0.45, 0.9]])
+    g = MetricGraph(n_leaf + 1, eu, ev, ln)
+    h, kappa, beta, k = 0.1, 2.0, 0.7, 0.45
+    G = _graph(g, h)
+    u, st = G.sample(kappa, beta, k, seed=3, n_samples=3, return_stats=True)
+    ref, _, _ = solve.sample(g, h, kappa, beta, k, 3, 3)
+    assert _rel(u.cpu().numpy(), ref).max() <= FIELD_TOL
+    assert st["n_unconverged"] == 0
+
+
+def test_barabasi_albert_per_node_vs_oracle():
+    """The paper's §4.3 workload family (P340-341): Barabasi-Albert m = 2, unit edges, h = 2^-6;
+    n = 2000 (hubs of degree > 32 -> CSR tables); single-node solves vs the oracle."""
+    from synth import barabasi_albert
+    g = barabasi_albert(2000, 2, seed=0)
+    h, kappa, beta = 2.0 ** -6, 1.0, 0.75
+    k = -1.0 / (beta * np.log(h))  # the paper's step rule (P335)
+    G = _graph(g, h)
+    prob = solve.setup(g, h, kappa, beta, k)
+    assert prob.plan.n_nodes == 131
+    W = noise.white_noise(prob.ML, 0, 2)
+    for li in (0, 65, 130):
+        x = G.sample(kappa, beta, k, seed=0, n_samples=2, node_range=(li, li + 1)).cpu().numpy()
+        assert _rel(x, solve.node_solve(prob, li, W)).max() <= 1e-10, f"node {li}"
