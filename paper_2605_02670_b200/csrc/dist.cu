@@ -252,9 +252,14 @@ __global__ void scal_init_kernel(int32_t n, int32_t cs, int64_t S, int64_t tile,
 }
 
 __global__ void scal_alpha_kernel(int32_t n, const double* __restrict__ pq, const double* __restrict__ rz,
-                                  const int32_t* __restrict__ done, double* __restrict__ alpha) {
+                                  int32_t* __restrict__ done, double* __restrict__ alpha, int32_t* active) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < n) alpha[t] = done[t] ? 0.0 : rz[t] / pq[t];
+    if (t >= n) return;
+    if (!done[t] && !(pq[t] > 0.0)) {  // p = 0 (underflowed rhs): nothing left to reduce
+        done[t] = 1;
+        atomicSub(active, 1);
+    }
+    alpha[t] = done[t] ? 0.0 : rz[t] / pq[t];
 }
 
 __global__ void scal_beta_kernel(int32_t n, double tol2, const double* __restrict__ dots /* [2][n] */,
@@ -384,7 +389,7 @@ void scal_init(int32_t n, int32_t cs, int64_t S, int64_t tile, int32_t csl, cons
 }
 
 void scal_alpha(int32_t n, const double* pq, const Scal& sc, cudaStream_t st) {
-    scal_alpha_kernel<<<(n + BT - 1) / BT, BT, 0, st>>>(n, pq, sc.rz, sc.done, sc.alpha);
+    scal_alpha_kernel<<<(n + BT - 1) / BT, BT, 0, st>>>(n, pq, sc.rz, sc.done, sc.alpha, sc.active);
 }
 
 void scal_beta(int32_t n, double tol2, const double* dots, const Scal& sc, cudaStream_t st) {

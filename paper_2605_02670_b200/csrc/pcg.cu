@@ -113,6 +113,30 @@ __device__ __forceinline__ void group_sum(double (&v)[NV], double* red /* [2][GT
     flip ^= 1;
 }
 
+// group-wide max of NV non-negative doubles per thread (same buffering as group_sum)
+template <int GT, int NV>
+__device__ __forceinline__ void group_max(double (&v)[NV], double* red, int& flip, int bar_id) {
+    constexpr int NW = GT / 32;
+    const int lane = threadIdx.x & 31, w = (threadIdx.x % GT) >> 5;
+    double* rb = red + flip * NW * NV;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        double t = v[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, o));
+        if (lane == 0) rb[w * NV + j] = t;
+    }
+    group_bar(bar_id, GT);
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) t = fmax(t, rb[q * NV + j]);
+        v[j] = t;
+    }
+    flip ^= 1;
+}
+
 template <int GT, int SB, int VPT, int W, bool STAGED>
 __global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L, const double* __restrict__ ops,
                                                           PcgParams prm, int64_t S, int32_t spc, int32_t csl,
@@ -200,7 +224,30 @@ __global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L,
         double gg[SB];
 #pragma unroll
         for (int j = 0; j < SB; ++j) gg[j] = 0.0;
-        // ---- condensed rhs g (gathered end values), x = 0, r = g
+        // ---- condensed rhs g, x = 0, r = g scaled by a power of two (see pcg_warp.cu: exact, and it
+        // keeps the iteration away from underflow for rhs that decayed to ~1e-300)
+        double gmax[SB];
+#pragma unroll
+        for (int j = 0; j < SB; ++j) gmax[j] = 0.0;
+#pragma unroll
+        for (int a = 0; a < VPT; ++a) {
+            const int v = gt + a * GT;
+            if (v < V) {
+#pragma unroll
+                for (int j = 0; j < SB; ++j) {
+                    const int64_t s = s0 + (j < ns ? j : 0);
+                    gmax[j] = fmax(gmax[j], j < ns ? fabs(rhs[rhs_index(s, l, v, L, V, csl)]) : 0.0);
+                }
+            }
+        }
+        group_max<GT, SB>(gmax, red, flip, bar_id);
+        int sexp[SB];
+#pragma unroll
+        for (int j = 0; j < SB; ++j) {
+            int e = 0;
+            if (gmax[j] > 0.0) frexp(gmax[j], &e);
+            sexp[j] = e;
+        }
 #pragma unroll
         for (int a = 0; a < VPT; ++a) {
             const int v = gt + a * GT;
@@ -210,7 +257,7 @@ __global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L,
 #pragma unroll
                 for (int j = 0; j < SB; ++j) {
                     const int64_t s = s0 + (j < ns ? j : 0);
-                    double gv = rhs[rhs_index(s, l, v, L, V, csl)];
+                    double gv = ldexp(rhs[rhs_index(s, l, v, L, V, csl)], -sexp[j]);
                     if (j >= ns) gv = 0.0;
                     r[v * SB + j] = gv;
                     gg[j] += gv * gv;
@@ -267,7 +314,10 @@ __global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L,
             group_sum<GT, SB>(pq, red, flip, bar_id);
             double alpha[SB];
 #pragma unroll
-            for (int j = 0; j < SB; ++j) alpha[j] = done[j] ? 0.0 : rz[j] / pq[j];
+            for (int j = 0; j < SB; ++j) {
+                if (!(pq[j] > 0.0)) done[j] = true;  // p = 0 (underflowed rhs): nothing left to reduce
+                alpha[j] = done[j] ? 0.0 : rz[j] / pq[j];
+            }
 #pragma unroll
             for (int a = 0; a < VPT; ++a) {
                 const int v = gt + a * GT;
@@ -330,7 +380,7 @@ __global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L,
             if (v < V) {
 #pragma unroll
                 for (int j = 0; j < SB; ++j)
-                    if (j < ns) uG[ug_index(s0 + j, v, l, L, V, csl)] = x[a][j];
+                    if (j < ns) uG[ug_index(s0 + j, v, l, L, V, csl)] = ldexp(x[a][j], sexp[j]);
             }
         }
         if (gt == 0) {

@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
             block_partials<CS, 1>(A, l, vb, nvb, acc, red, [&](int ln) {
                 if (tid < CS) {
                     const double pq = node_sum(ln, 0, tid);
+                    if (!(pq > 0.0)) A.done[ln * CS + tid] = 1;  // p = 0 (underflowed rhs)
                     A.alpha[ln * CS + tid] = A.done[ln * CS + tid] ? 0.0 : A.rz[ln * CS + tid] / pq;
                 }
             });

@@ -91,8 +91,13 @@ class Graph:
                 except Exception:
                     return None
 
+            cad = torch.cuda.caching_allocator_delete  # bound now: module globals may be gone at exit
+
             def _f(ptr, nbytes, ctx, stream):
-                torch.cuda.caching_allocator_delete(int(ptr))
+                try:
+                    cad(int(ptr))
+                except Exception:  # interpreter shutdown: the process is releasing the device anyway
+                    pass
 
             self._cb = (ALLOC_FN(_a), FREE_FN(_f))
             self._alloc = grf_allocator(self._cb[0], self._cb[1], None)

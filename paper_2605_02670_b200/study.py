@@ -73,3 +73,42 @@ def strong_error(graph, levels, ok_level, kappa, beta, k, seed=0, n_samples=64, 
     return {"levels": list(levels), "ok_level": ok_level, "h": h, "mean_sq_err": ms,
             "rms_err": [float(np.sqrt(m)) for m in ms], "rate_mean_sq": rate_ms, "rate_rms": rate_ms / 2,
             "theory_rate_rms": 2 * beta - 0.5, "n_samples": n_samples, "per_sample_sq": {j: np.concatenate(sq[j]) for j in levels}}
+
+
+def covariance(g: Graph, kappa, beta, k, batch=4096, **opts):
+    """Covariance matrix C = B M_L B of the discrete field u = B W, Cov(W) = M_L (P99-109),
+    B = sum_l (A^{(l)})^{-1} (symmetric): B is applied to the identity columns with batched
+    grf_apply (the sampler's own kernels); the dense products are cuBLAS GEMMs (torch)."""
+    torch = _torch()
+    N = g.n_dofs
+    dev = f"cuda:{g.device}"
+    B = torch.empty((N, N), dtype=torch.float64, device=dev)
+    for c0 in range(0, N, batch):
+        nb = min(batch, N - c0)
+        E = torch.zeros((nb, N), dtype=torch.float64, device=dev)
+        E[torch.arange(nb), torch.arange(c0, c0 + nb)] = 1.0
+        g.apply(kappa, beta, k, E, out=B[c0:c0 + nb], **opts)
+    M = torch.from_numpy(g.lumped_mass()).to(dev)
+    return B @ (M[:, None] * B)
+
+
+def covariance_error(graph, levels, ok_level, kappa, beta, k, **opts):
+    """L2(Gamma x Gamma) covariance errors ||C_ok - P C_h P^T||, the norm with the overkill lumped
+    mass on both factors (P337-338; overkill h = 2^-8), and the
+    fitted rate (theory min(4 beta - 1/2, 2))."""
+    torch = _torch()
+    Gf = Graph.from_metric_graph(graph, 2.0 ** -ok_level)
+    Cok = covariance(Gf, kappa, beta, k, **opts)
+    Mf = torch.from_numpy(Gf.lumped_mass()).to(Cok.device)
+    errs = []
+    for j in levels:
+        Gc = Graph.from_metric_graph(graph, 2.0 ** -j)
+        Cc = covariance(Gc, kappa, beta, k, **opts)
+        Nc = Gc.n_dofs
+        Pt = prolong(Gc, Gf, torch.eye(Nc, dtype=torch.float64, device=Cok.device))  # row i = P e_i -> P^T
+        D = Cok - Pt.T @ Cc @ Pt
+        errs.append(float(torch.sqrt(((Mf[:, None] * D * D) * Mf[None, :]).sum()).item()))
+    h = [2.0 ** -j for j in levels]
+    r, _ = fit_rate(h, errs)
+    return {"levels": list(levels), "ok_level": ok_level, "h": h, "cov_err": errs, "rate": r,
+            "theory_rate": min(4 * beta - 0.5, 2.0)}

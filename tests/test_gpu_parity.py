@@ -444,3 +444,18 @@ def test_barabasi_albert_per_node_vs_oracle():
     for li in (0, 65, 130):
         x = G.sample(kappa, beta, k, seed=0, n_samples=2, node_range=(li, li + 1)).cpu().numpy()
         assert _rel(x, solve.node_solve(prob, li, W)).max() <= 1e-10, f"node {li}"
+
+
+def test_covariance_vs_oracle():
+    """NEXT-4: C = B M_L B from batched grf_apply on unit columns vs the oracle's definition
+    (B from oracle.solve.apply on the identity)."""
+    from paper_2605_02670_b200.study import covariance
+    g = tadpole()
+    h, kappa, beta, k = 0.125, 5.0, 0.75, 0.4
+    G = _graph(g, h)
+    C = covariance(G, kappa, beta, k, batch=7).cpu().numpy()
+    prob = solve.setup(g, h, kappa, beta, k)
+    B = solve.apply(prob, np.eye(prob.mesh.n_dofs))
+    Cref = B @ np.diag(prob.ML) @ B.T
+    assert np.abs(C - Cref).max() <= 1e-10 * np.abs(Cref).max()
+    assert np.allclose(C, C.T, rtol=0, atol=1e-14 * np.abs(C).max())
