@@ -137,6 +137,7 @@ grf_status grf_plan_info(double beta, double k, int64_t* k_minus, int64_t* k_plu
 
 enum { GRF_PRECOND_NN = 0, GRF_PRECOND_JACOBI = 1, GRF_PRECOND_NONE = 2 };
 enum { GRF_PCG_AUTO = 0, GRF_PCG_SHARED = 1, GRF_PCG_GLOBAL = 2 };
+enum { GRF_MASS_LUMPED = 0, GRF_MASS_CONSISTENT = 1 };
 
 typedef struct grf_options {
     double rtol;          /* PCG stop: ||r||_2 <= rtol ||g||_2 (recursive residual), default 1e-13 */
@@ -147,6 +148,10 @@ typedef struct grf_options {
     int32_t pcg_variant;  /* GRF_PCG_*: which K4 kernel family solves the vertex systems;
                              AUTO picks the shared-memory kernels when the vertex vectors fit
                              on chip (V <= 4096) and the global-memory kernel otherwise */
+    int32_t mass;         /* GRF_MASS_*: LUMPED (default, the paper's method, P106-109) or
+                             CONSISTENT (the paper's comparison baseline, P129-136: consistent M in
+                             the operator, noise W = R xi with R the natural-order Cholesky factor
+                             of M, P148-150; V <= 8192, not for edge-partitioned parts) */
 } grf_options;
 void grf_options_default(grf_options* opt);
 
@@ -167,6 +172,10 @@ grf_status grf_workspace_size(const grf_graph* g, double kappa, double beta, dou
 
 /* White noise only: W_out[j*N + i] = W_i of sample j (device, n_samples x N). */
 grf_status grf_noise(grf_graph* g, uint64_t seed, int64_t n_samples, double* W_out, void* stream);
+/* The same for either mass mode (GRF_MASS_*): CONSISTENT gives W = R xi, M = R R^T (natural-order
+ * Cholesky, the same standard normals xi as the lumped stream); synchronises. */
+grf_status grf_noise_mass(grf_graph* g, uint64_t seed, int64_t n_samples, int32_t mass, double* W_out,
+                          void* stream);
 
 /* GRF samples (see top of file).  u_out: device array n_samples x N, written.
  * workspace: device, >= grf_workspace_size bytes (NULL/0 -> allocated and freed

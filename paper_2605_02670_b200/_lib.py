@@ -32,7 +32,8 @@ class grf_part_info(C.Structure):
 
 class grf_options(C.Structure):
     _fields_ = [("rtol", C.c_double), ("max_iter", C.c_int32), ("precond", C.c_int32),
-                ("node_begin", C.c_int64), ("node_end", C.c_int64), ("pcg_variant", C.c_int32)]
+                ("node_begin", C.c_int64), ("node_end", C.c_int64), ("pcg_variant", C.c_int32),
+                ("mass", C.c_int32)]
 
 
 class grf_stats(C.Structure):
@@ -51,7 +52,7 @@ EXPORTS = [
     "grf_workspace_size", "grf_noise", "grf_sample", "grf_sample_host", "grf_apply", "grf_edge_schur",
     "grf_comm_get_unique_id", "grf_comm_init", "grf_comm_destroy", "grf_reduce_sum",
     "grf_profile_enable", "grf_profile_read", "grf_graph_create_part", "grf_sample_edgepart",
-    "grf_prolong", "grf_project_noise", "grf_mnorm_sq_diff",
+    "grf_prolong", "grf_project_noise", "grf_mnorm_sq_diff", "grf_noise_mass",
 ]
 KERNEL_NAMES = ["noise", "edge_setup", "condense", "pcg", "recover"]
 
@@ -99,6 +100,7 @@ def load() -> C.CDLL:
         "grf_graph_create_part": (C.c_int, [I64, I64, pi64, pi64, pd, D, C.POINTER(grf_part_info),
                                             C.POINTER(grf_allocator), C.POINTER(P)]),
         "grf_prolong": (C.c_int, [P, P, I64, P, P, P]),
+        "grf_noise_mass": (C.c_int, [P, U64, I64, C.c_int32, P, P]),
         "grf_project_noise": (C.c_int, [P, P, I64, P, P, P]),
         "grf_mnorm_sq_diff": (C.c_int, [P, I64, P, P, P, P]),
         "grf_sample_edgepart": (C.c_int, [C.POINTER(P), C.c_int32, P, D, D, D, U64, I64, C.POINTER(grf_options),

@@ -36,7 +36,7 @@ namespace grf {
 namespace {
 
 __global__ void edge_setup_kernel(DevGraph g, int32_t L, int32_t Lp, const double* __restrict__ cIt,
-                                  const double* __restrict__ cLt, double kappa2, double* __restrict__ mu_t,
+                                  const double* __restrict__ cLt, double kappa2, int32_t mass, double* __restrict__ mu_t,
                                   double* __restrict__ gam_t, double4* __restrict__ sig) {
     const int e = blockIdx.x;
     const double h = g.h[e];
@@ -52,8 +52,8 @@ __global__ void edge_setup_kernel(DevGraph g, int32_t L, int32_t Lp, const doubl
     }
     for (int l = threadIdx.x; l < L; l += blockDim.x) {
         const double cI = cIt[l], cL = cLt[l];
-        const EdgeCoef c = edge_coef(cI, cL, kappa2, h);
-        const double share = (cI + kappa2 * cL) * h * 0.5 + c.beta;
+        const EdgeCoef c = edge_coef(cI, cL, kappa2, h, mass);
+        const double share = c.share;
         double sd, so;
         if (m == 0) {
             sd = share;
@@ -92,7 +92,7 @@ __global__ void edge_setup_kernel(DevGraph g, int32_t L, int32_t Lp, const doubl
 void launch_edge_setup(const DevGraph& g, DevPlan& p, cudaStream_t st) {
     int threads = ((p.L + 31) / 32) * 32;
     if (threads > 256) threads = 256;
-    edge_setup_kernel<<<g.E, threads, 0, st>>>(g, p.L, p.Lp, p.cI, p.cL, p.kappa * p.kappa, p.mu, p.gam,
+    edge_setup_kernel<<<g.E, threads, 0, st>>>(g, p.L, p.Lp, p.cI, p.cL, p.kappa * p.kappa, p.mass, p.mu, p.gam,
                                                reinterpret_cast<double4*>(p.sig));
 }
 

@@ -66,6 +66,7 @@ struct Block {
 struct PlanKey {
     double kappa, beta, k;
     int64_t nb, ne;
+    int64_t mass;  // GRF_MASS_*
     bool operator==(const PlanKey& o) const {
         return std::memcmp(this, &o, sizeof(PlanKey)) == 0;
     }
@@ -91,6 +92,9 @@ struct grf_graph {
     std::vector<Block> blocks;  // graph-lifetime device allocations
     std::list<std::unique_ptr<Plan>> plans;  // most recent first
     bool partitioned = false;                // created by grf_graph_create_part
+    // consistent-mass noise factor (NEXT-3), built on first use: chain Cholesky factors per
+    // Thomas-table class (Ld, Lo) and the dense Cholesky factor of the vertex Schur complement
+    const double *cLd = nullptr, *cLo = nullptr, *cLs = nullptr;
     int64_t n_iface = 0;                     // interface vertices of the whole partition
     // kernel timing (grf_profile_enable / grf_profile_read)
     bool prof = false;
@@ -200,7 +204,7 @@ grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf
     int64_t nb, ne;
     s = resolve_range(opt, Lfull, &nb, &ne);
     if (s) return s;
-    PlanKey key{kappa, beta, k, nb, ne};
+    PlanKey key{kappa, beta, k, nb, ne, (int64_t)(opt ? opt->mass : GRF_MASS_LUMPED)};
     for (auto it = g->plans.begin(); it != g->plans.end(); ++it) {
         if ((*it)->key == key) {
             g->plans.splice(g->plans.begin(), g->plans, it);
@@ -241,6 +245,7 @@ grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf
     p->dev.TL = TL;
     p->dev.rounds = rounds;
     p->dev.kappa = kappa;
+    p->dev.mass = (int32_t)key.mass;
     p->dev.cI = dcI;
     p->dev.cL = dcL;
     p->dev.mu = mu;
@@ -266,7 +271,7 @@ grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct WsLayout {
-    size_t w = 0, ends = 0, rhs = 0, ug = 0, gws = 0, iters = 0, relres = 0, counter = 0, total = 0;
+    size_t w = 0, cnoise = 0, ends = 0, rhs = 0, ug = 0, gws = 0, iters = 0, relres = 0, counter = 0, total = 0;
 };
 
 // with_noise: grf_sample keeps the white noise W (S x N) in the workspace
@@ -277,11 +282,13 @@ bool use_global_pcg(const grf_graph* g, const grf_options* opt) {
     return v == GRF_PCG_GLOBAL || (v == GRF_PCG_AUTO && !grf::pcg_shared_ok(g->dev));
 }
 
-WsLayout ws_layout(const grf_graph* g, int64_t L, int64_t S, bool with_noise, bool global_pcg) {
+WsLayout ws_layout(const grf_graph* g, int64_t L, int64_t S, bool with_noise, bool global_pcg, bool consistent) {
     WsLayout w;
     size_t o = 0;
     w.w = o;
     if (with_noise) o += align_up((size_t)S * g->N * sizeof(double));
+    w.cnoise = o;  // consistent noise scratch: [S][2E] edge terms + [S][V] vertex values
+    if (with_noise && consistent) o += align_up((size_t)S * (2 * g->E + g->V) * sizeof(double));
     // ends / uG are sample-tiled (grf_internal.h): sized for whole tiles
     const int64_t cs = (int64_t)1 << grf::sample_tile_log2(S);
     const int64_t Sp = (S + cs - 1) / cs * cs;
@@ -309,6 +316,72 @@ grf_status check_kernel_limits(const grf_graph* g) {
     return GRF_OK;
 }
 
+// NEXT-3: the natural-order Cholesky factor of the consistent mass matrix (P148-150, SPEC S241),
+// in the block form R = [[L_II, 0], [M_GI L_II^{-T}, L_S]] (noise.cu):
+//   L_II: per interior chain tridiag(h/6, 2h/3, h/6): Ld_0 = sqrt(2h/3), Lo_t = (h/6)/Ld_{t-1},
+//         Ld_t = sqrt(2h/3 - Lo_t^2) -- one set per Thomas-table class;
+//   L_S:  dense Cholesky of S_M = M_GG - M_GI M_II^{-1} M_IG, assembled from each edge's 2x2 block
+//         (the local Schur formula of edge_setup.cu with a = 2h/3, b = h/6, share = h/3).
+// Dense on the host (O(V^3 / 3)), so limited to V <= 8192.
+grf_status ensure_consistent_factor(grf_graph* g) {
+    if (g->cLs) return GRF_OK;
+    if (g->V > 8192) return fail(GRF_EUNSUPPORTED, "consistent-mass noise: %lld vertices (dense vertex Cholesky "
+                                 "handles <= 8192)", (long long)g->V);
+    if (g->partitioned) return fail(GRF_EUNSUPPORTED, "consistent-mass noise on an edge-partitioned part");
+    const int64_t V = g->V, E = g->E, NT = std::max<int64_t>(g->dev.NT, 1);
+    std::vector<double> Ld(NT, 0.0), Lo(NT, 0.0), S((size_t)V * V, 0.0);
+    std::vector<int64_t> toff(E);
+    CUDA_TRY(cudaMemcpy(toff.data(), g->dev.toff, E * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    std::vector<int32_t> rep(E);
+    CUDA_TRY(cudaMemcpy(rep.data(), g->dev.tab_rep, E * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    for (int64_t e = 0; e < E; ++e) {
+        const double h = g->he[e];
+        const int64_t m = g->n_el[e] - 1;
+        const double a = 2.0 * h / 3.0, b = h / 6.0, share = h / 3.0;
+        if (rep[e]) {
+            for (int64_t t = 0; t < m; ++t) {
+                const double lo = t ? b / Ld[toff[e] + t - 1] : 0.0;
+                Lo[toff[e] + t] = lo;
+                Ld[toff[e] + t] = std::sqrt(a - lo * lo);
+            }
+        }
+        double sd = share, so = b;
+        if (m > 0) {
+            double inv = 0.0, prod = 1.0;
+            for (int64_t t = 0; t < m; ++t) {
+                const double mu = b * inv;
+                inv = 1.0 / (a - mu * b);
+                if (t > 0) prod *= -mu;
+            }
+            sd = share - b * b * inv;
+            so = -b * b * (prod * inv);
+        }
+        const int64_t u = g->eu[e], v = g->ev[e];
+        S[u * V + u] += sd;
+        S[v * V + v] += sd;
+        S[u * V + v] += so;
+        S[v * V + u] += so;
+    }
+    for (int64_t j = 0; j < V; ++j) {  // dense Cholesky, lower triangle, row-major
+        double d = S[j * V + j];
+        for (int64_t q = 0; q < j; ++q) d -= S[j * V + q] * S[j * V + q];
+        if (!(d > 0.0)) return fail(GRF_EINVAL, "consistent mass Schur complement not positive definite");
+        const double ljj = std::sqrt(d);
+        S[j * V + j] = ljj;
+        for (int64_t i = j + 1; i < V; ++i) {
+            double x = S[i * V + j];
+            for (int64_t q = 0; q < j; ++q) x -= S[i * V + q] * S[j * V + q];
+            S[i * V + j] = x / ljj;
+        }
+        for (int64_t q = j + 1; q < V; ++q) S[j * V + q] = 0.0;
+    }
+    grf_status st = GRF_OK;
+    g->cLd = g->upload(Ld, &st);
+    if (!st) g->cLo = g->upload(Lo, &st);
+    if (!st) g->cLs = g->upload(S, &st);
+    return st;
+}
+
 // Shared tail of grf_sample / grf_apply: u (holding W on entry) -> u.
 // W (S x N, device) -> u (S x N, device).  When W is null the noise for `seed` is first
 // generated into the workspace (grf_sample); otherwise W is the caller's rhs (grf_apply).
@@ -316,7 +389,12 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
                  double* u, void* ws, size_t ws_bytes, cudaStream_t st, grf_stats* stats) {
     const int64_t L = p->dev.L;
     const bool gen = (W == nullptr);
-    WsLayout w = ws_layout(g, L, S, gen, use_global_pcg(g, opt));
+    const bool consistent = p->dev.mass == GRF_MASS_CONSISTENT;
+    if (gen && consistent) {
+        grf_status cs = ensure_consistent_factor(g);
+        if (cs) return cs;
+    }
+    WsLayout w = ws_layout(g, L, S, gen, use_global_pcg(g, opt), consistent);
     void* own = nullptr;
     if (!ws) {
         own = g->alloc.get(w.total, st);
@@ -332,7 +410,14 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
     int64_t launches = 5 + (use_global_pcg(g, opt) ? (S + cs - 1) / cs - 1 : 0);
     if (gen) {
         double* Wd = reinterpret_cast<double*>(base + w.w);
-        cudaError_t ne = g->timed(GRF_K_NOISE, st, [&] { grf::launch_noise(g->dev, seed, S, Wd, st); });
+        cudaError_t ne = g->timed(GRF_K_NOISE, st, [&] {
+            if (consistent) {
+                double* ev = reinterpret_cast<double*>(base + w.cnoise);
+                grf::launch_noise_consistent(g->dev, g->cLd, g->cLo, g->cLs, seed, S, Wd, ev, ev + S * 2 * g->E, st);
+            } else {
+                grf::launch_noise(g->dev, seed, S, Wd, st);
+            }
+        });
         if (ne != cudaSuccess) {
             if (own) g->alloc.put(own, w.total, st);
             return fail(GRF_ECUDA, "noise launch: %s", cudaGetErrorString(ne));
@@ -424,6 +509,7 @@ void grf_options_default(grf_options* opt) {
     opt->node_begin = 0;
     opt->node_end = -1;
     opt->pcg_variant = GRF_PCG_AUTO;
+    opt->mass = GRF_MASS_LUMPED;
 }
 
 }  // extern "C"
@@ -711,7 +797,8 @@ grf_status grf_workspace_size(const grf_graph* g, double kappa, double beta, dou
     plan_limits(beta, k, &Km, &Kp);
     st = resolve_range(opt, Km + Kp + 1, &nb, &ne);
     if (st) return st;
-    *bytes = ws_layout(g, ne - nb, n_samples, true, use_global_pcg(g, opt)).total;
+    *bytes = ws_layout(g, ne - nb, n_samples, true, use_global_pcg(g, opt),
+                       opt && opt->mass == GRF_MASS_CONSISTENT).total;
     return GRF_OK;
 }
 
@@ -720,6 +807,24 @@ grf_status grf_noise(grf_graph* g, uint64_t seed, int64_t n_samples, double* W_o
     if (n_samples < 1) return fail(GRF_EINVAL, "n_samples must be >= 1");
     CUDA_TRY(g->timed(GRF_K_NOISE, (cudaStream_t)stream,
                       [&] { grf::launch_noise(g->dev, seed, n_samples, W_out, (cudaStream_t)stream); }));
+    return GRF_OK;
+}
+
+grf_status grf_noise_mass(grf_graph* g, uint64_t seed, int64_t n_samples, int32_t mass, double* W_out,
+                          void* stream) {
+    if (mass == GRF_MASS_LUMPED) return grf_noise(g, seed, n_samples, W_out, stream);
+    if (!g || !W_out || n_samples < 1 || mass != GRF_MASS_CONSISTENT) return fail(GRF_EINVAL, "bad arguments");
+    grf_status s = ensure_consistent_factor(g);
+    if (s) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t bytes = sizeof(double) * (size_t)n_samples * (2 * g->E + g->V);
+    double* ev = (double*)g->alloc.get(bytes, st);
+    if (!ev) return fail(GRF_ENOMEM, "consistent noise scratch");
+    grf::launch_noise_consistent(g->dev, g->cLd, g->cLo, g->cLs, seed, n_samples, W_out, ev,
+                                 ev + n_samples * 2 * g->E, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    g->alloc.put(ev, bytes, st);
+    if (e != cudaSuccess) return fail(GRF_ECUDA, "consistent noise: %s", cudaGetErrorString(e));
     return GRF_OK;
 }
 
@@ -951,6 +1056,8 @@ extern "C" grf_status grf_sample_edgepart(grf_graph* const* parts, int32_t n_par
                                           grf_stats* stats) {
     if (!parts || n_parts < 1 || !u_out) return fail(GRF_EINVAL, "grf_sample_edgepart: NULL argument or no parts");
     if (comm && n_parts != 1) return fail(GRF_EINVAL, "with a communicator each rank passes exactly one part");
+    if (opt && opt->mass != GRF_MASS_LUMPED)
+        return fail(GRF_EUNSUPPORTED, "edge-partitioned sampling uses the lumped mass (the paper's method)");
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t I = parts[0]->n_iface;
     for (int32_t q = 0; q < n_parts; ++q) {

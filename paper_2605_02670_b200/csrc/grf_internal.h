@@ -63,6 +63,7 @@ __device__ __forceinline__ int ops_code(const DevGraph& g, int64_t k) { return g
 struct DevPlan {
     int32_t L = 0;                    // nodes in this plan's range
     double kappa = 0.0;
+    int32_t mass = 0;                 // 0 lumped (P137-145), 1 consistent (P129-136) mass in the operator
     const double* cI = nullptr;       // [L]
     const double* cL = nullptr;       // [Lp] (zero for l >= L)
     int32_t Lp = 0;                   // padded node row of the Thomas tables (sweep_impl.cuh tiling)
@@ -103,6 +104,9 @@ int32_t sample_tile_log2(int64_t S);
 
 // K1  noise (noise.cu): W[s*N + i] = sqrt(M_L,ii) z(seed + s, i)
 void launch_noise(const DevGraph& g, uint64_t seed, int64_t n_samples, double* W, cudaStream_t st);
+// K1' consistent-mass noise W = R xi (noise.cu); evec [S][2E], vtmp [S][V] scratch
+void launch_noise_consistent(const DevGraph& g, const double* Ld, const double* Lo, const double* Ls, uint64_t seed,
+                             int64_t S, double* W, double* evec, double* vtmp, cudaStream_t st);
 // K2  per-(node, edge) Thomas pivots + local Schur blocks (edge_setup.cu)
 void launch_edge_setup(const DevGraph& g, DevPlan& p, cudaStream_t st);
 // K3  Thomas end values per (sample, edge, end, node) (sweep.cu): ends[((s*E + e)*2 + end)*L + l]

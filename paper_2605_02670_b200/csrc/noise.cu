@@ -95,8 +95,56 @@ __global__ void __launch_bounds__(256) noise_kernel(const double* __restrict__ s
         const double u2 = __dmul_rn((double)B, 0x1.0p-53);
         const double r = __dsqrt_rn(__dmul_rn(-2.0, ln_fixed(u1)));
         const double z = __dmul_rn(r, cos2pi_fixed(u2));
-        W[t] = __dmul_rn(sqrt_ml[i], z);
+        W[t] = sqrt_ml ? __dmul_rn(sqrt_ml[i], z) : z;  // sqrt_ml == nullptr: the raw normals xi
     }
+}
+
+// Consistent mass (P129-136, P148-150): W = R xi with R the natural-order Cholesky factor of M,
+// R = [[L_II, 0], [M_GI L_II^{-T}, L_S]]: L_II is block-diagonal over the edges (the Cholesky
+// factor of each interior chain tridiag(h/6, 2h/3, h/6): diagonal Ld, sub-diagonal Lo, per
+// table class), L_S the Cholesky factor of the vertex Schur complement M_GG - M_GI M_II^{-1} M_IG.
+// Thread per (sample, edge): y = L_II^{-T} xi_I by back substitution (its end values feed the
+// edge's two vertices through M_GI = h/6), then W_I = L_II xi_I in place.
+__global__ void cnoise_edge_kernel(DevGraph g, const double* __restrict__ Ld, const double* __restrict__ Lo,
+                                   int64_t S, double* __restrict__ W, double* __restrict__ evec) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= S * g.E) return;
+    const int64_t s = t / g.E;
+    const int e = (int)(t - s * g.E);
+    const int m = g.m[e];
+    const int64_t tb = g.toff[e];
+    double* w = W + s * g.N + g.off[e];
+    double y1 = 0.0, ym = 0.0;
+    if (m > 0) {
+        double y = w[m - 1] / Ld[tb + m - 1];  // y_m
+        ym = y;
+        for (int i = m - 2; i >= 0; --i) y = (w[i] - Lo[tb + i + 1] * y) / Ld[tb + i];
+        y1 = y;
+        double prev = 0.0;
+        for (int i = 0; i < m; ++i) {
+            const double xi = w[i];
+            w[i] = Ld[tb + i] * xi + (i ? Lo[tb + i] * prev : 0.0);
+            prev = xi;
+        }
+    }
+    const double c = g.h[e] / 6.0;
+    evec[s * 2 * g.E + 2 * e] = c * y1;      // to vertex edge_u (end 0)
+    evec[s * 2 * g.E + 2 * e + 1] = c * ym;  // to vertex edge_v (end 1)
+}
+
+// W_G = L_S xi_G + sum over the vertex's incidences (CSR order) of the edge terms; thread per (s, v)
+__global__ void cnoise_vertex_kernel(DevGraph g, const double* __restrict__ Ls, int64_t S, const double* __restrict__ W,
+                                     const double* __restrict__ evec, double* __restrict__ out) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= S * g.V) return;
+    const int64_t s = t / g.V;
+    const int v = (int)(t - s * g.V);
+    const double* xi = W + s * g.N + g.NI;
+    const double* row = Ls + (int64_t)v * g.V;
+    double acc = 0.0;
+    for (int k = 0; k <= v; ++k) acc = fma(row[k], xi[k], acc);
+    for (int q = g.inc_ptr[v]; q < g.inc_ptr[v + 1]; ++q) acc += evec[s * 2 * g.E + g.inc[q]];
+    out[t] = acc;
 }
 
 }  // namespace
@@ -108,6 +156,18 @@ void launch_noise(const DevGraph& g, uint64_t seed, int64_t n_samples, double* W
     const int64_t cap = 148 * 16;
     if (blocks > cap) blocks = cap;
     noise_kernel<<<(unsigned)blocks, 256, 0, st>>>(g.sqrt_ml, g.dof_gid, g.N, total, seed, W);
+}
+
+void launch_noise_consistent(const DevGraph& g, const double* Ld, const double* Lo, const double* Ls, uint64_t seed,
+                             int64_t S, double* W, double* evec, double* vtmp, cudaStream_t st) {
+    const int64_t total = S * g.N;
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > 148 * 64) blocks = 148 * 64;
+    noise_kernel<<<(unsigned)blocks, 256, 0, st>>>(nullptr, g.dof_gid, g.N, total, seed, W);
+    cnoise_edge_kernel<<<(unsigned)((S * g.E + 127) / 128), 128, 0, st>>>(g, Ld, Lo, S, W, evec);
+    cnoise_vertex_kernel<<<(unsigned)((S * g.V + 127) / 128), 128, 0, st>>>(g, Ls, S, W, evec, vtmp);
+    cudaMemcpy2DAsync(W + g.NI, g.N * sizeof(double), vtmp, g.V * sizeof(double), g.V * sizeof(double), S,
+                      cudaMemcpyDeviceToDevice, st);
 }
 
 }  // namespace grf

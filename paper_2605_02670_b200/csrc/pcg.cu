@@ -30,6 +30,7 @@
 #include <cstdlib>
 
 #include "grf_internal.h"
+#include "thomas.cuh"
 
 namespace grf {
 namespace {
@@ -40,7 +41,8 @@ constexpr size_t SMEM_LIMIT = 220 * 1024;
 // per node l: [DS (V) | DM (V) | DJ (V) | OS (W*V) | OM (W*V) | GK (W*V)], slot-major [j][v]
 __host__ __device__ inline int64_t table_stride(int V, int W) { return 3 * (int64_t)V + 3 * (int64_t)W * V; }
 
-__global__ void pcg_tables_kernel(DevGraph g, int32_t L, const double* __restrict__ cLt,
+__global__ void pcg_tables_kernel(DevGraph g, int32_t L, const double* __restrict__ cIt,
+                                  const double* __restrict__ cLt, double kappa2, int32_t mass,
                                   const double4* __restrict__ sig, double* __restrict__ ops) {
     const int V = g.V, E = g.E;
     const int64_t stride = ops_stride(g), ns = ops_nslots(g);
@@ -70,7 +72,7 @@ __global__ void pcg_tables_kernel(DevGraph g, int32_t L, const double* __restric
                 dm += c.z;
                 OS[sj] = c.y;
                 OM[sj] = c.w * idv * g.inv_deg[o];
-                GK[sj] = cL / g.h[e];
+                GK[sj] = mass ? edge_coef(cIt[l], cL, kappa2, g.h[e], 1).beta : cL / g.h[e];  // -b (A_GI)
                 diag += c.x + (o == v ? c.y : 0.0);
             } else {
                 OS[sj] = OM[sj] = GK[sj] = 0.0;
@@ -530,7 +532,7 @@ void launch_pcg_tables(const DevGraph& g, const DevPlan& p, cudaStream_t st) {
     const int64_t n = (int64_t)p.L * g.V;
     int blocks = (int)((n + 255) / 256);
     if (blocks > 148 * 8) blocks = 148 * 8;
-    pcg_tables_kernel<<<blocks, 256, 0, st>>>(g, p.L, p.cL, reinterpret_cast<const double4*>(p.sig), p.ops);
+    pcg_tables_kernel<<<blocks, 256, 0, st>>>(g, p.L, p.cI, p.cL, p.kappa * p.kappa, p.mass, reinterpret_cast<const double4*>(p.sig), p.ops);
 }
 
 void launch_assemble_rhs(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W, const double* ends,

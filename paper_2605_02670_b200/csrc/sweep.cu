@@ -24,6 +24,9 @@ sweep::Args make_args(const DevGraph& g, const DevPlan& p, int64_t S, const doub
     a.Lp = p.Lp;
     a.rounds = p.rounds;
     a.cL = p.cL;
+    a.cI = p.cI;
+    a.kappa2 = p.kappa * p.kappa;
+    a.mass = p.mass;
     a.mu = p.mu;
     a.gam = p.gam;
     a.S = S;

@@ -43,6 +43,7 @@
 #include <cuda_pipeline.h>
 
 #include "grf_internal.h"
+#include "thomas.cuh"
 
 namespace grf {
 namespace sweep {
@@ -56,6 +57,9 @@ struct Args {
     int32_t L, Lp;          // nodes; padded table row (multiple of 32 * TL * rounds)
     int32_t rounds;         // node rounds (Lp = rounds * 32 * TL)
     const double* cL;       // [Lp] c_L per node (zero padded)
+    const double* cI;       // [L] c_I per node
+    double kappa2;
+    int32_t mass;           // 0 lumped, 1 consistent: the end coupling -b of A_IG (thomas.cuh edge_coef)
     const double* mu;       // [(off + t) * Lp + l]
     const double* gam;      // [(off + t) * Lp + l]
     int64_t S;
@@ -210,7 +214,7 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                 for (int n = 0; n < TL; ++n) {
                     const int l = rb + slot(n);
                     const bool ok = l < L;
-                    const double beta = ok ? A.cL[l] / h : 0.0;
+                    const double beta = ok ? (A.mass ? edge_coef(A.cI[l], A.cL[l], A.kappa2, h, 1).beta : A.cL[l] / h) : 0.0;
 #pragma unroll
                     for (int j = 0; j < TS; ++j) {
                         const double ul = ok ? A.uG[ug_index(sidx[j], vu, l, L, g.V, CSL)] : 0.0;
@@ -444,7 +448,7 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                             const int sn = slot(n);
                             const int l = rb + sn;
                             const bool ok = l < L;
-                            const double beta = ok ? A.cL[l] / h : 0.0;
+                            const double beta = ok ? (A.mass ? edge_coef(A.cI[l], A.cL[l], A.kappa2, h, 1).beta : A.cL[l] / h) : 0.0;
                             const double mu = rmu[sn], gg = rga[sn];
                             const double nk = gg * mu;
 #pragma unroll

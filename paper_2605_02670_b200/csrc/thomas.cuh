@@ -15,13 +15,18 @@
 namespace grf {
 
 struct EdgeCoef {
-    double a, b, beta;  // beta = -b = c_L / h_e
+    double a, b, beta, share;  // beta = -b (end coupling), share = one end's part of A_GG
 };
 
-__device__ __forceinline__ EdgeCoef edge_coef(double cI, double cL, double kappa2, double h) {
-    const double mass = cI + kappa2 * cL;
+// Local operator of edge e at node l: c_I M_e + c_L (kappa^2 M_e + G_e), M_e lumped (mass = 0:
+// h per interior node, h/2 per end, P137-145) or consistent (mass = 1: 2h/3 diagonal, h/6
+// off-diagonal, h/3 per end, P129-136).
+__host__ __device__ __forceinline__ EdgeCoef edge_coef(double cI, double cL, double kappa2, double h, int mass = 0) {
+    const double mc = cI + kappa2 * cL;
     const double stiff = cL / h;
-    return EdgeCoef{mass * h + 2.0 * stiff, -stiff, stiff};
+    if (mass == 0) return EdgeCoef{mc * h + 2.0 * stiff, -stiff, stiff, mc * h * 0.5 + stiff};
+    const double b = mc * (h / 6.0) - stiff;
+    return EdgeCoef{mc * (2.0 * h / 3.0) + 2.0 * stiff, b, -b, mc * (h / 3.0) + stiff};
 }
 
 // advance: given inv_prev = 1/d'_{i-1} (0 at i = 1) return mu_i = b / d'_{i-1} and 1/d'_i

@@ -55,7 +55,10 @@ def plan_info(beta: float, k: float):
 PCG_VARIANT = {"auto": 0, "shared": 1, "global": 2}
 
 
-def make_options(rtol=1e-13, max_iter=0, precond="nn", node_range=None, pcg="auto") -> grf_options:
+MASS = {"lumped": 0, "consistent": 1}
+
+
+def make_options(rtol=1e-13, max_iter=0, precond="nn", node_range=None, pcg="auto", mass="lumped") -> grf_options:
     o = grf_options()
     load().grf_options_default(C.byref(o))
     o.rtol = rtol
@@ -64,6 +67,7 @@ def make_options(rtol=1e-13, max_iter=0, precond="nn", node_range=None, pcg="aut
     if node_range is not None:
         o.node_begin, o.node_end = int(node_range[0]), int(node_range[1])
     o.pcg_variant = PCG_VARIANT[pcg] if isinstance(pcg, str) else int(pcg)
+    o.mass = MASS[mass] if isinstance(mass, str) else int(mass)
     return o
 
 
@@ -161,13 +165,18 @@ class Graph:
         return b.value
 
     # ------------------------------------------------------------------ compute
-    def noise(self, seed: int, n_samples: int, out=None, stream=None):
+    def noise(self, seed: int, n_samples: int, out=None, stream=None, mass="lumped"):
+        """grf_noise (lumped, sqrt(M_L) xi) or grf_noise_mass (mass="consistent": R xi, M = R R^T)."""
         torch = _torch()
         if out is None:
             out = torch.empty((n_samples, self.n_dofs), dtype=torch.float64, device=f"cuda:{self.device}")
         self._check_out(out, n_samples)
-        check(self._lib.grf_noise(self._h, C.c_uint64(seed & (2 ** 64 - 1)), n_samples, C.c_void_p(out.data_ptr()),
-                                  C.c_void_p(_stream_ptr(stream))))
+        if mass == "lumped":
+            check(self._lib.grf_noise(self._h, C.c_uint64(seed & (2 ** 64 - 1)), n_samples,
+                                      C.c_void_p(out.data_ptr()), C.c_void_p(_stream_ptr(stream))))
+        else:
+            check(self._lib.grf_noise_mass(self._h, C.c_uint64(seed & (2 ** 64 - 1)), n_samples, MASS[mass],
+                                           C.c_void_p(out.data_ptr()), C.c_void_p(_stream_ptr(stream))))
         return out
 
     def _check_out(self, out, n):

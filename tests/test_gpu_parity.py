@@ -459,3 +459,28 @@ def test_covariance_vs_oracle():
     Cref = B @ np.diag(prob.ML) @ B.T
     assert np.abs(C - Cref).max() <= 1e-10 * np.abs(Cref).max()
     assert np.allclose(C, C.T, rtol=0, atol=1e-14 * np.abs(C).max())
+
+
+# ----------------------------------------------------------------------------- NEXT-3 consistent mass
+@pytest.mark.parametrize("gname", ["tadpole", "ragged", "lattice"])
+def test_consistent_mass_vs_oracle(gname):
+    """Consistent mass in operator and noise (P129-150): noise R xi vs the oracle's dense
+    natural-order Cholesky (same xi; different arithmetic order, so to rounding), field to 1e-9."""
+    from oracle import consistent
+    from oracle.mesh import build_mesh
+    g, h = {"tadpole": (tadpole(), 0.05),
+            "ragged": (MetricGraph(4, np.array([0, 0, 1, 1, 2, 3, 2, 0]), np.array([1, 1, 2, 1, 3, 3, 0, 3]),
+                                   np.array([0.01, 0.019, 0.031, 0.005, 0.9, 0.008, 0.43, 1.37])), 0.01),
+            "lattice": (lattice(4, seed=2), 0.05)}[gname]
+    kappa, beta, k = 4.0, 0.7, 0.35
+    G = _graph(g, h)
+    W = G.noise(5, 3, mass="consistent").cpu().numpy()
+    Wref = consistent.white_noise(build_mesh(g, h), 5, 3)
+    assert np.abs(W - Wref).max() <= 1e-13 * np.abs(Wref).max()
+    u, st = G.sample(kappa, beta, k, seed=5, n_samples=3, mass="consistent", return_stats=True)
+    ref, _ = consistent.sample(g, h, kappa, beta, k, 5, 3)
+    assert _rel(u.cpu().numpy(), ref).max() <= FIELD_TOL
+    assert st["n_unconverged"] == 0
+    # the consistent field is a different discretization from the lumped one (but close)
+    ul = G.sample(kappa, beta, k, seed=5, n_samples=3).cpu().numpy()
+    assert _rel(ul, ref).max() > 1e-6
