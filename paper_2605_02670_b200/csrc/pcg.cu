@@ -243,12 +243,14 @@ __global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L,
             }
         }
         group_max<GT, SB>(gmax, red, flip, bar_id);
-        int sexp[SB];
+        double sdown[SB], sup[SB];  // exact powers of two
 #pragma unroll
         for (int j = 0; j < SB; ++j) {
             int e = 0;
             if (gmax[j] > 0.0) frexp(gmax[j], &e);
-            sexp[j] = e;
+            e = e < -1000 ? -1000 : (e > 1000 ? 1000 : e);
+            sdown[j] = ldexp(1.0, -e);
+            sup[j] = ldexp(1.0, e);
         }
 #pragma unroll
         for (int a = 0; a < VPT; ++a) {
@@ -259,7 +261,7 @@ __global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L,
 #pragma unroll
                 for (int j = 0; j < SB; ++j) {
                     const int64_t s = s0 + (j < ns ? j : 0);
-                    double gv = ldexp(rhs[rhs_index(s, l, v, L, V, csl)], -sexp[j]);
+                    double gv = rhs[rhs_index(s, l, v, L, V, csl)] * sdown[j];
                     if (j >= ns) gv = 0.0;
                     r[v * SB + j] = gv;
                     gg[j] += gv * gv;
@@ -382,7 +384,7 @@ __global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L,
             if (v < V) {
 #pragma unroll
                 for (int j = 0; j < SB; ++j)
-                    if (j < ns) uG[ug_index(s0 + j, v, l, L, V, csl)] = ldexp(x[a][j], sexp[j]);
+                    if (j < ns) uG[ug_index(s0 + j, v, l, L, V, csl)] = x[a][j] * sup[j];
             }
         }
         if (gt == 0) {

@@ -125,33 +125,50 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
         if (s >= S) break;  // warp-uniform; no block barriers below
         double x[VPL], t[VPL];  // t holds q = S p, then z = M^{-1} r (disjoint lifetimes)
         // condensed rhs g_v = W_v + sum_j (c_L/h_e) w_{code_j(v)} (P233-239); x_0 = 0, r = g
-        // the system is solved for g / 2^e with 2^e ~ max|g|: power-of-two scaling is exact (every
-        // PCG quantity scales exactly, alpha and beta are unchanged), so results are bitwise those
-        // of the unscaled iteration, but a rhs that decayed to ~1e-300 (unit rhs deep inside a long
-        // edge at a mass-dominated node) no longer underflows in the dot products
+        // a rhs whose squared norm is near the fp64 range limits (e.g. a unit rhs deep inside a long
+        // edge at a mass-dominated node decays to ~1e-300) is solved for g / 2^e with 2^e ~ max|g|:
+        // power-of-two scaling is exact (every PCG quantity scales exactly, alpha and beta are
+        // unchanged) and keeps the dot products away from underflow
         double gg = 0.0;
         const double* gs = rhs + rhs_index(s, l, 0, L, V, csl);
-        double gmax = 0.0;
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) {
-            const int v = lane + 32 * k;
-            if (v < V) gmax = fmax(gmax, fabs(gs[v]));
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
-        int sexp = 0;
-        if (gmax > 0.0) frexp(gmax, &sexp);
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
             const int v = lane + 32 * k;
             x[k] = 0.0;
             if (v < V) {
-                const double gv = ldexp(gs[v], -sexp);
+                const double gv = gs[v];
                 r[v] = gv;
                 gg = fma(gv, gv, gg);
             }
         }
         gg = warp_sum(gg);
+        double sup = 1.0;
+        if (gg > 0.0 && (gg < 0x1p-900 || gg > 0x1p900)) {  // rare: rescale by a power of two (exact)
+            double gmax = 0.0;
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+                const int v = lane + 32 * k;
+                if (v < V) gmax = fmax(gmax, fabs(r[v]));
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+            int e = 0;
+            frexp(gmax, &e);
+            e = e < -1000 ? -1000 : (e > 1000 ? 1000 : e);
+            const double sdown = ldexp(1.0, -e);
+            sup = ldexp(1.0, e);
+            gg = 0.0;
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+                const int v = lane + 32 * k;
+                if (v < V) {
+                    const double gv = r[v] * sdown;
+                    r[v] = gv;
+                    gg = fma(gv, gv, gg);
+                }
+            }
+            gg = warp_sum(gg);
+        }
         __syncwarp();
         precond(t);
         double rz = 0.0;
@@ -216,7 +233,7 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
             const int v = lane + 32 * k;
-            if (v < V) uG[ug_index(s, v, l, L, V, csl)] = ldexp(x[k], sexp);
+            if (v < V) uG[ug_index(s, v, l, L, V, csl)] = x[k] * sup;
         }
         if (lane == 0) {
             iters[s * L + l] = it;

@@ -556,10 +556,19 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                     const int l = rb + slot(n);
                     if (l < L) {
                         double* o = A.out + ((tile * L + l) * 2 * (int64_t)g.E + 2 * e) * CS + st0;
+                        if (TS % 2 == 0) {  // 16-byte stores: st0 and CS are multiples of TS
 #pragma unroll
-                        for (int j = 0; j < TS; ++j) {
-                            o[j] = g0[n] * Z[n][j];
-                            o[CS + j] = g0[n] * Y[n][j];
+                            for (int j = 0; j < TS; j += 2) {
+                                *reinterpret_cast<double2*>(o + j) = make_double2(g0[n] * Z[n][j], g0[n] * Z[n][j + 1 < TS ? j + 1 : j]);
+                                *reinterpret_cast<double2*>(o + CS + j) =
+                                    make_double2(g0[n] * Y[n][j], g0[n] * Y[n][j + 1 < TS ? j + 1 : j]);
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < TS; ++j) {
+                                o[j] = g0[n] * Z[n][j];
+                                o[CS + j] = g0[n] * Y[n][j];
+                            }
                         }
                     }
                 }
