@@ -50,29 +50,34 @@ struct GArgs {
 };
 
 
-// Block reduction of K x CS per-thread values into part[l][vb][k][s]; the last block of
-// node l to arrive then reduces all vertex blocks (fixed order) into out_k[l][s] and runs
-// `finish(l)` (single block, all threads).  Returns after the (possible) finish.
+// Threads: one per (vertex, sample) -- thread t of a CTA owns sample s = t % CS of vertex
+// sub-row t / CS; an item = (node l, block of VPI vertices) walked in sub-chunks of GT / CS
+// vertices, so a thread keeps only scalars (small register footprint, many resident warps
+// for the latency of the neighbour gathers), and the CS threads of a vertex read one
+// contiguous CS-double run of each vector and share the vertex's operator coefficients.
+constexpr int VPI = 256;  // vertices per item: per-node partials have ceil(V / VPI) rows
+
+// Reduce K per-thread values over the CTA's vertices into part[l][vb][k][s]; the last CTA of
+// node l to arrive reduces the node's rows (columns in parallel, each in fixed order) and runs
+// finish(l, totals) with totals[k * CS + s] in shared memory (all threads of that CTA).
 template <int CS, int K, class Finish>
-__device__ void block_partials(const GArgs& A, int l, int vb, int nvb, double (&v)[K][CS], double* red,
+__device__ void block_partials(const GArgs& A, int l, int vb, int nvb, const double (&v)[K], double* red,
                                Finish&& finish) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     __shared__ int last;
-    // warp sums (fixed butterfly order), then across the 8 warps in order
 #pragma unroll
-    for (int k = 0; k < K; ++k)
+    for (int k = 0; k < K; ++k) {
+        double t = v[k];
 #pragma unroll
-        for (int s = 0; s < CS; ++s) {
-            double t = v[k][s];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-            if (lane == 0) red[(warp * K + k) * CS + s] = t;
-        }
+        for (int o = 16; o >= CS && o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);  // over vertex lanes
+        if (lane < (CS < 32 ? CS : 32)) red[(warp * K + k) * CS + lane % CS] = t;
+    }
     __syncthreads();
     double* pb = A.part + ((int64_t)l * nvb + vb) * 2 * CS;
     if (tid < K * CS) {
+        const int k = tid / CS, s = tid % CS;
         double t = 0.0;
-        for (int w = 0; w < GT / 32; ++w) t += red[w * K * CS + tid];
+        for (int w = 0; w < GT / 32; ++w) t += red[(w * K + k) * CS + s];
         pb[tid] = t;
         __threadfence();
     }
@@ -81,7 +86,24 @@ __device__ void block_partials(const GArgs& A, int l, int vb, int nvb, double (&
     __syncthreads();
     if (last) {
         __threadfence();
-        finish(l);
+        constexpr int NCOL = K * CS;
+        constexpr int TPC = GT / NCOL;
+        const int col = tid / TPC, sub = tid % TPC;
+        double t = 0.0;
+        if (col < NCOL) {
+            const double* pc = A.part + (int64_t)l * nvb * 2 * CS + col;
+            for (int b = sub; b < nvb; b += TPC) t += pc[(int64_t)b * 2 * CS];
+        }
+        __syncthreads();  // red is reused
+        red[tid] = t;
+        __syncthreads();
+        if (tid < NCOL) {
+            double u = 0.0;
+            for (int q = 0; q < TPC; ++q) u += red[tid * TPC + q];
+            red[GT + tid] = u;
+        }
+        __syncthreads();
+        finish(l, red + GT);
         __syncthreads();
         if (tid == 0) A.cnt[l] = 0;
     }
@@ -91,13 +113,15 @@ __device__ void block_partials(const GArgs& A, int l, int vb, int nvb, double (&
 template <int CS>
 __global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ double red[(GT / 32) * 2 * CS];
+    constexpr int VBK = GT / CS;  // vertices per sub-chunk
+    constexpr int RED = (GT + 2 * CS) > ((GT / 32) * 2 * CS) ? (GT + 2 * CS) : ((GT / 32) * 2 * CS);
+    __shared__ double red[RED];
     const DevGraph& g = A.g;
     const int V = g.V, L = A.L;
     const int64_t ns = ops_nslots(g);
-    const int nvb = (V + GT - 1) / GT;
+    const int nvb = (V + VPI - 1) / VPI;
     const int64_t items = (int64_t)L * nvb;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, s = tid % CS, vl = tid / CS;
     const int64_t stride = ops_stride(g);
     const int64_t s0 = A.tile << A.csl;
     double* po = A.p0;
@@ -105,39 +129,28 @@ __global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
     double* ro = A.r0;
     double* rn = A.r1;
     const double tol2c = A.prm.rtol * A.prm.rtol;
-
-    // sum over the node's vertex blocks of partial k, sample s (fixed order)
-    auto node_sum = [&](int l, int k, int s) {
-        const double* pb = A.part + (int64_t)l * nvb * 2 * CS + k * CS + s;
-        double t = 0.0;
-        for (int b = 0; b < nvb; ++b) t += pb[(int64_t)b * 2 * CS];
-        return t;
-    };
     auto deg_of = [&](int v) { return g.inc_ptr[v + 1] - g.inc_ptr[v]; };
+    // the vertex of sub-chunk c of item vb for this thread (or V: none)
+    auto vert = [&](int vb, int c) { const int v = vb * VPI + c * VBK + vl; return v < V ? v : -1; };
 
     // ---- init a: r = g, x = 0, p = 0; gg = g.g
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
         const int l = (int)(it / nvb), vb = (int)(it % nvb);
-        const int v = vb * GT + tid;
-        double acc[1][CS];
-        if (v < V) {
-            const int64_t base = ((int64_t)l * V + v) * CS;
-#pragma unroll
-            for (int s = 0; s < CS; ++s) {
-                const int64_t sg = s0 + s;
-                const double gv = sg < A.S ? A.rhs[rhs_index(sg, l, v, L, V, A.csl)] : 0.0;
-                ro[base + s] = gv;
-                A.x[base + s] = 0.0;
-                po[base + s] = 0.0;
-                acc[0][s] = gv * gv;
-            }
-        } else {
-#pragma unroll
-            for (int s = 0; s < CS; ++s) acc[0][s] = 0.0;
+        double acc[1] = {0.0};
+        for (int c = 0; c < VPI / VBK; ++c) {
+            const int v = vert(vb, c);
+            if (v < 0) continue;
+            const int64_t e = ((int64_t)l * V + v) * CS + s;
+            const int64_t sg = s0 + s;
+            const double gv = sg < A.S ? A.rhs[rhs_index(sg, l, v, L, V, A.csl)] : 0.0;
+            ro[e] = gv;
+            A.x[e] = 0.0;
+            po[e] = 0.0;
+            acc[0] = fma(gv, gv, acc[0]);
         }
-        block_partials<CS, 1>(A, l, vb, nvb, acc, red, [&](int ln) {
+        block_partials<CS, 1>(A, l, vb, nvb, acc, red, [&](int ln, const double* tot) {
             if (tid < CS) {
-                const double t = node_sum(ln, 0, tid);
+                const double t = tot[tid];
                 A.gg[ln * CS + tid] = t;
                 A.rr[ln * CS + tid] = t;
                 A.done[ln * CS + tid] = !(t > 0.0) || (s0 + tid >= A.S);
@@ -150,44 +163,32 @@ __global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
     // ---- init b: z = M^{-1} r; rz
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
         const int l = (int)(it / nvb), vb = (int)(it % nvb);
-        const int v = vb * GT + tid;
         const double* tab = A.ops + l * stride;
-        double acc[1][CS];
-#pragma unroll
-        for (int s = 0; s < CS; ++s) acc[0][s] = 0.0;
-        if (v < V) {
-            const int64_t base = ((int64_t)l * V + v) * CS;
-            double zv[CS], rv[CS];
-#pragma unroll
-            for (int s = 0; s < CS; ++s) rv[s] = ro[base + s];
+        double acc[1] = {0.0};
+        for (int c = 0; c < VPI / VBK; ++c) {
+            const int v = vert(vb, c);
+            if (v < 0) continue;
+            const int64_t e = ((int64_t)l * V + v) * CS + s;
+            const double rv = ro[e];
+            double zv;
             if (A.prm.precond == 0) {
-                const double dm = tab[V + v];
-#pragma unroll
-                for (int s = 0; s < CS; ++s) zv[s] = dm * rv[s];
+                zv = tab[V + v] * rv;
                 const int dg = deg_of(v);
                 for (int j = 0; j < dg; ++j) {
                     const int64_t k = ops_slot(g, v, j);
-                    const double c = tab[3 * (int64_t)V + ns + k];
-                    const double* ro_o = ro + ((int64_t)l * V + ops_other(g, k)) * CS;
-#pragma unroll
-                    for (int s = 0; s < CS; ++s) zv[s] = fma(c, ro_o[s], zv[s]);
+                    zv = fma(tab[3 * (int64_t)V + ns + k], ro[((int64_t)l * V + ops_other(g, k)) * CS + s], zv);
                 }
             } else {
-                const double d = A.prm.precond == 1 ? tab[2 * V + v] : 1.0;
-#pragma unroll
-                for (int s = 0; s < CS; ++s) zv[s] = d * rv[s];
+                zv = (A.prm.precond == 1 ? tab[2 * V + v] : 1.0) * rv;
             }
-#pragma unroll
-            for (int s = 0; s < CS; ++s) {
-                A.z[base + s] = zv[s];
-                acc[0][s] = rv[s] * zv[s];
-            }
+            A.z[e] = zv;
+            acc[0] = fma(rv, zv, acc[0]);
         }
-        block_partials<CS, 1>(A, l, vb, nvb, acc, red, [&](int ln) {
-            if (tid < CS) A.rz[ln * CS + tid] = node_sum(ln, 0, tid);
+        block_partials<CS, 1>(A, l, vb, nvb, acc, red, [&](int ln, const double* tot) {
+            if (tid < CS) A.rz[ln * CS + tid] = tot[tid];
             if (tid == 0) {
                 int act = 0;
-                for (int s = 0; s < CS; ++s) act |= !A.done[ln * CS + s];
+                for (int q = 0; q < CS; ++q) act |= !A.done[ln * CS + q];
                 A.node_active[ln] = act;
                 if (act) atomicAdd(A.n_active, 1);
             }
@@ -201,40 +202,28 @@ __global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
         for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
             const int l = (int)(it / nvb), vb = (int)(it % nvb);
             if (!A.node_active[l]) continue;  // block-uniform
-            const int v = vb * GT + tid;
             const double* tab = A.ops + l * stride;
-            double acc[1][CS];
-#pragma unroll
-            for (int s = 0; s < CS; ++s) acc[0][s] = 0.0;
-            if (v < V) {
-                const int64_t base = ((int64_t)l * V + v) * CS;
-                double bt[CS], pv[CS], qv[CS];
-#pragma unroll
-                for (int s = 0; s < CS; ++s) {
-                    bt[s] = A.beta[l * CS + s];
-                    pv[s] = fma(bt[s], po[base + s], A.z[base + s]);
-                }
-                const double ds = tab[v];
-#pragma unroll
-                for (int s = 0; s < CS; ++s) qv[s] = ds * pv[s];
+            const double bt = A.beta[l * CS + s];
+            double acc[1] = {0.0};
+            for (int c = 0; c < VPI / VBK; ++c) {
+                const int v = vert(vb, c);
+                if (v < 0) continue;
+                const int64_t e = ((int64_t)l * V + v) * CS + s;
+                const double pv = fma(bt, po[e], A.z[e]);
+                double qv = tab[v] * pv;
                 const int dg = deg_of(v);
                 for (int j = 0; j < dg; ++j) {
                     const int64_t k = ops_slot(g, v, j);
-                    const double c = tab[3 * (int64_t)V + k];
-                    const int64_t ob = ((int64_t)l * V + ops_other(g, k)) * CS;
-#pragma unroll
-                    for (int s = 0; s < CS; ++s) qv[s] = fma(c, fma(bt[s], po[ob + s], A.z[ob + s]), qv[s]);
+                    const int64_t ob = ((int64_t)l * V + ops_other(g, k)) * CS + s;
+                    qv = fma(tab[3 * (int64_t)V + k], fma(bt, po[ob], A.z[ob]), qv);
                 }
-#pragma unroll
-                for (int s = 0; s < CS; ++s) {
-                    pn[base + s] = pv[s];
-                    A.q[base + s] = qv[s];
-                    acc[0][s] = pv[s] * qv[s];
-                }
+                pn[e] = pv;
+                A.q[e] = qv;
+                acc[0] = fma(pv, qv, acc[0]);
             }
-            block_partials<CS, 1>(A, l, vb, nvb, acc, red, [&](int ln) {
+            block_partials<CS, 1>(A, l, vb, nvb, acc, red, [&](int ln, const double* tot) {
                 if (tid < CS) {
-                    const double pq = node_sum(ln, 0, tid);
+                    const double pq = tot[tid];
                     if (!(pq > 0.0)) A.done[ln * CS + tid] = 1;  // p = 0 (underflowed rhs)
                     A.alpha[ln * CS + tid] = A.done[ln * CS + tid] ? 0.0 : A.rz[ln * CS + tid] / pq;
                 }
@@ -245,49 +234,36 @@ __global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
         for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
             const int l = (int)(it / nvb), vb = (int)(it % nvb);
             if (!A.node_active[l]) continue;
-            const int v = vb * GT + tid;
             const double* tab = A.ops + l * stride;
-            double acc[2][CS];
-#pragma unroll
-            for (int s = 0; s < CS; ++s) acc[0][s] = acc[1][s] = 0.0;
-            if (v < V) {
-                const int64_t base = ((int64_t)l * V + v) * CS;
-                double al[CS], rv[CS], zv[CS];
-#pragma unroll
-                for (int s = 0; s < CS; ++s) {
-                    al[s] = A.alpha[l * CS + s];
-                    rv[s] = fma(-al[s], A.q[base + s], ro[base + s]);
-                    A.x[base + s] = fma(al[s], pn[base + s], A.x[base + s]);
-                }
+            const double al = A.alpha[l * CS + s];
+            double acc[2] = {0.0, 0.0};
+            for (int c = 0; c < VPI / VBK; ++c) {
+                const int v = vert(vb, c);
+                if (v < 0) continue;
+                const int64_t e = ((int64_t)l * V + v) * CS + s;
+                const double rv = fma(-al, A.q[e], ro[e]);
+                A.x[e] = fma(al, pn[e], A.x[e]);
+                double zv;
                 if (A.prm.precond == 0) {
-                    const double dm = tab[V + v];
-#pragma unroll
-                    for (int s = 0; s < CS; ++s) zv[s] = dm * rv[s];
+                    zv = tab[V + v] * rv;
                     const int dg = deg_of(v);
                     for (int j = 0; j < dg; ++j) {
                         const int64_t k = ops_slot(g, v, j);
-                        const double c = tab[3 * (int64_t)V + ns + k];
-                        const int64_t ob = ((int64_t)l * V + ops_other(g, k)) * CS;
-#pragma unroll
-                        for (int s = 0; s < CS; ++s) zv[s] = fma(c, fma(-al[s], A.q[ob + s], ro[ob + s]), zv[s]);
+                        const int64_t ob = ((int64_t)l * V + ops_other(g, k)) * CS + s;
+                        zv = fma(tab[3 * (int64_t)V + ns + k], fma(-al, A.q[ob], ro[ob]), zv);
                     }
                 } else {
-                    const double d = A.prm.precond == 1 ? tab[2 * V + v] : 1.0;
-#pragma unroll
-                    for (int s = 0; s < CS; ++s) zv[s] = d * rv[s];
+                    zv = (A.prm.precond == 1 ? tab[2 * V + v] : 1.0) * rv;
                 }
-#pragma unroll
-                for (int s = 0; s < CS; ++s) {
-                    rn[base + s] = rv[s];
-                    A.z[base + s] = zv[s];
-                    acc[0][s] = rv[s] * rv[s];
-                    acc[1][s] = rv[s] * zv[s];
-                }
+                rn[e] = rv;
+                A.z[e] = zv;
+                acc[0] = fma(rv, rv, acc[0]);
+                acc[1] = fma(rv, zv, acc[1]);
             }
-            block_partials<CS, 2>(A, l, vb, nvb, acc, red, [&](int ln) {
+            block_partials<CS, 2>(A, l, vb, nvb, acc, red, [&](int ln, const double* tot) {
                 if (tid < CS) {
                     const int sy = ln * CS + tid;
-                    const double rr = node_sum(ln, 0, tid), rzn = node_sum(ln, 1, tid);
+                    const double rr = tot[tid], rzn = tot[CS + tid];
                     if (!A.done[sy]) {
                         A.its[sy] += 1;
                         A.rr[sy] = rr;
@@ -301,7 +277,7 @@ __global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
                 __syncthreads();
                 if (tid == 0) {
                     int act = 0;
-                    for (int s = 0; s < CS; ++s) act |= !A.done[ln * CS + s];
+                    for (int q = 0; q < CS; ++q) act |= !A.done[ln * CS + q];
                     if (!act) {
                         A.node_active[ln] = 0;
                         atomicSub(A.n_active, 1);
@@ -320,22 +296,16 @@ __global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
     // ---- write u_G, iteration counts and final relative residuals
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
         const int l = (int)(it / nvb), vb = (int)(it % nvb);
-        const int v = vb * GT + tid;
-        if (v < V) {
-            const int64_t base = ((int64_t)l * V + v) * CS;
-#pragma unroll
-            for (int s = 0; s < CS; ++s) {
-                const int64_t sg = s0 + s;
-                if (sg < A.S) A.uG[ug_index(sg, v, l, L, V, A.csl)] = A.x[base + s];
-            }
+        const int64_t sg = s0 + s;
+        for (int c = 0; c < VPI / VBK; ++c) {
+            const int v = vert(vb, c);
+            if (v < 0 || sg >= A.S) continue;
+            A.uG[ug_index(sg, v, l, L, V, A.csl)] = A.x[((int64_t)l * V + v) * CS + s];
         }
-        if (vb == 0 && tid < CS) {
-            const int64_t sg = s0 + tid;
+        if (vb == 0 && tid < CS && s0 + tid < A.S) {
             const int sy = l * CS + tid;
-            if (sg < A.S) {
-                A.iters[sg * L + l] = A.its[sy];
-                A.relres[sg * L + l] = A.gg[sy] > 0.0 ? sqrt(A.rr[sy] / A.gg[sy]) : 0.0;
-            }
+            A.iters[(s0 + tid) * L + l] = A.its[sy];
+            A.relres[(s0 + tid) * L + l] = A.gg[sy] > 0.0 ? sqrt(A.rr[sy] / A.gg[sy]) : 0.0;
         }
     }
 }
@@ -367,7 +337,7 @@ cudaError_t launch_cs(GArgs a, int64_t n_tiles, cudaStream_t st) {
 
 size_t pcg_global_ws_bytes(const DevGraph& g, int32_t L, int64_t n_samples) {
     const int64_t cs = (int64_t)1 << sample_tile_log2(n_samples);
-    const int64_t nvb = (g.V + GT - 1) / GT;
+    const int64_t nvb = (g.V + VPI - 1) / VPI;
     size_t b = 7 * sizeof(double) * (size_t)L * g.V * cs;      // x, r0, r1, p0, p1, q, z
     b += 5 * sizeof(double) * (size_t)L * cs;                  // alpha, beta, rz, gg, rr
     b += 2 * sizeof(int32_t) * (size_t)L * cs;                 // done, its
@@ -383,7 +353,7 @@ cudaError_t launch_pcg_global(const DevGraph& g, const DevPlan& p, int64_t n_sam
     const int32_t csl = sample_tile_log2(n_samples);
     const int64_t cs = (int64_t)1 << csl;
     const int64_t L = p.L;
-    const int64_t nvb = (g.V + GT - 1) / GT;
+    const int64_t nvb = (g.V + VPI - 1) / VPI;
     char* b = static_cast<char*>(ws);
     auto take = [&](size_t bytes) {
         char* r = b;
