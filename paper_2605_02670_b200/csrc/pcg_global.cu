@@ -16,6 +16,8 @@
 // the last block to arrive for that node (threadfence + arrival counter), so results are
 // deterministic.  A node whose CS systems have all converged is skipped; the loop ends when
 // no node is active or after max_iter iterations.
+#include <algorithm>
+#include <cmath>
 #include <cooperative_groups.h>
 
 #include "grf_internal.h"
@@ -47,6 +49,8 @@ struct GArgs {
     int32_t* n_active;                      // [1]
     double* part;                           // [L][nvb][2][CS]
     int32_t* cnt;                           // [L] arrival counters (zero between phases)
+    int32_t group;                          // nodes solved together (their work vectors stay L2-resident)
+    int32_t vpi;                            // vertices per item (multiple of GT / CS)
 };
 
 
@@ -55,7 +59,7 @@ struct GArgs {
 // vertices, so a thread keeps only scalars (small register footprint, many resident warps
 // for the latency of the neighbour gathers), and the CS threads of a vertex read one
 // contiguous CS-double run of each vector and share the vertex's operator coefficients.
-constexpr int VPI = 256;  // vertices per item: per-node partials have ceil(V / VPI) rows
+constexpr int VPI_MAX = 256;  // vertices per item (at most): per-node partials have ceil(V / vpi) rows
 
 // Reduce K per-thread values over the CTA's vertices into part[l][vb][k][s]; the last CTA of
 // node l to arrive reduces the node's rows (columns in parallel, each in fixed order) and runs
@@ -111,7 +115,7 @@ __device__ void block_partials(const GArgs& A, int l, int vb, int nvb, const dou
 }
 
 template <int CS>
-__global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
+__global__ void __launch_bounds__(GT, 4) pcg_global_kernel(GArgs A) {
     cg::grid_group grid = cg::this_grid();
     constexpr int VBK = GT / CS;  // vertices per sub-chunk
     constexpr int RED = (GT + 2 * CS) > ((GT / 32) * 2 * CS) ? (GT + 2 * CS) : ((GT / 32) * 2 * CS);
@@ -119,33 +123,49 @@ __global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
     const DevGraph& g = A.g;
     const int V = g.V, L = A.L;
     const int64_t ns = ops_nslots(g);
+    const int VPI = A.vpi;
     const int nvb = (V + VPI - 1) / VPI;
-    const int64_t items = (int64_t)L * nvb;
     const int tid = threadIdx.x, s = tid % CS, vl = tid / CS;
     const int64_t stride = ops_stride(g);
     const int64_t s0 = A.tile << A.csl;
-    double* po = A.p0;
-    double* pn = A.p1;
-    double* ro = A.r0;
-    double* rn = A.r1;
+    double *po, *pn, *ro, *rn;
     const double tol2c = A.prm.rtol * A.prm.rtol;
     auto deg_of = [&](int v) { return g.inc_ptr[v + 1] - g.inc_ptr[v]; };
     // the vertex of sub-chunk c of item vb for this thread (or V: none)
     auto vert = [&](int vb, int c) { const int v = vb * VPI + c * VBK + vl; return v < V ? v : -1; };
 
+    // Node groups are solved one after the other (the launcher currently uses one group of all
+    // nodes: per-group barriers outweighed the L2 residency they buy on config 4).
+    for (int l0 = 0; l0 < L; l0 += A.group) {
+    po = A.p0;
+    pn = A.p1;
+    ro = A.r0;
+    rn = A.r1;
+    const int lg = (L - l0) < A.group ? (L - l0) : A.group;
+    const int64_t items = (int64_t)lg * nvb;
+    if (blockIdx.x == 0 && tid == 0) *A.n_active = 0;  // all blocks have left the previous group's loop
     // ---- init a: r = g, x = 0, p = 0; gg = g.g
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const int l = (int)(it / nvb), vb = (int)(it % nvb);
+        const int l = l0 + (int)(it / nvb), vb = (int)(it % nvb);
+        const int64_t lb = (int64_t)l * V * CS;  // node l's [V][CS] slab
+        double* const ro_l = ro + lb;
+        double* const po_l = po + lb;
+        double* const pn_l = pn + lb;
+        double* const rn_l = rn + lb;
+        double* const x_l = A.x + lb;
+        double* const z_l = A.z + lb;
+        double* const q_l = A.q + lb;
+        (void)ro_l; (void)po_l; (void)pn_l; (void)rn_l; (void)x_l; (void)z_l; (void)q_l;
         double acc[1] = {0.0};
         for (int c = 0; c < VPI / VBK; ++c) {
             const int v = vert(vb, c);
             if (v < 0) continue;
-            const int64_t e = ((int64_t)l * V + v) * CS + s;
+            const int e = v * CS + s;  // offset within node l's [V][CS] slab (32-bit)
             const int64_t sg = s0 + s;
             const double gv = sg < A.S ? A.rhs[rhs_index(sg, l, v, L, V, A.csl)] : 0.0;
-            ro[e] = gv;
-            A.x[e] = 0.0;
-            po[e] = 0.0;
+            ro_l[e] = gv;
+            x_l[e] = 0.0;
+            po_l[e] = 0.0;
             acc[0] = fma(gv, gv, acc[0]);
         }
         block_partials<CS, 1>(A, l, vb, nvb, acc, red, [&](int ln, const double* tot) {
@@ -162,26 +182,35 @@ __global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
     grid.sync();
     // ---- init b: z = M^{-1} r; rz
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const int l = (int)(it / nvb), vb = (int)(it % nvb);
+        const int l = l0 + (int)(it / nvb), vb = (int)(it % nvb);
+        const int64_t lb = (int64_t)l * V * CS;  // node l's [V][CS] slab
+        double* const ro_l = ro + lb;
+        double* const po_l = po + lb;
+        double* const pn_l = pn + lb;
+        double* const rn_l = rn + lb;
+        double* const x_l = A.x + lb;
+        double* const z_l = A.z + lb;
+        double* const q_l = A.q + lb;
+        (void)ro_l; (void)po_l; (void)pn_l; (void)rn_l; (void)x_l; (void)z_l; (void)q_l;
         const double* tab = A.ops + l * stride;
         double acc[1] = {0.0};
         for (int c = 0; c < VPI / VBK; ++c) {
             const int v = vert(vb, c);
             if (v < 0) continue;
-            const int64_t e = ((int64_t)l * V + v) * CS + s;
-            const double rv = ro[e];
+            const int e = v * CS + s;  // offset within node l's [V][CS] slab (32-bit)
+            const double rv = ro_l[e];
             double zv;
             if (A.prm.precond == 0) {
                 zv = tab[V + v] * rv;
                 const int dg = deg_of(v);
                 for (int j = 0; j < dg; ++j) {
                     const int64_t k = ops_slot(g, v, j);
-                    zv = fma(tab[3 * (int64_t)V + ns + k], ro[((int64_t)l * V + ops_other(g, k)) * CS + s], zv);
+                    zv = fma(tab[3 * (int64_t)V + ns + k], ro_l[ops_other(g, k) * CS + s], zv);
                 }
             } else {
                 zv = (A.prm.precond == 1 ? tab[2 * V + v] : 1.0) * rv;
             }
-            A.z[e] = zv;
+            z_l[e] = zv;
             acc[0] = fma(rv, zv, acc[0]);
         }
         block_partials<CS, 1>(A, l, vb, nvb, acc, red, [&](int ln, const double* tot) {
@@ -200,7 +229,16 @@ __global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
         if (*(volatile int32_t*)A.n_active == 0) break;
         // ---- phase 1: p' = z + beta p, q = S p', p'.q -> alpha
         for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-            const int l = (int)(it / nvb), vb = (int)(it % nvb);
+            const int l = l0 + (int)(it / nvb), vb = (int)(it % nvb);
+            const int64_t lb = (int64_t)l * V * CS;  // node l's [V][CS] slab
+            double* const ro_l = ro + lb;
+            double* const po_l = po + lb;
+            double* const pn_l = pn + lb;
+            double* const rn_l = rn + lb;
+            double* const x_l = A.x + lb;
+            double* const z_l = A.z + lb;
+            double* const q_l = A.q + lb;
+            (void)ro_l; (void)po_l; (void)pn_l; (void)rn_l; (void)x_l; (void)z_l; (void)q_l;
             if (!A.node_active[l]) continue;  // block-uniform
             const double* tab = A.ops + l * stride;
             const double bt = A.beta[l * CS + s];
@@ -208,17 +246,17 @@ __global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
             for (int c = 0; c < VPI / VBK; ++c) {
                 const int v = vert(vb, c);
                 if (v < 0) continue;
-                const int64_t e = ((int64_t)l * V + v) * CS + s;
-                const double pv = fma(bt, po[e], A.z[e]);
+                const int e = v * CS + s;  // offset within node l's [V][CS] slab (32-bit)
+                const double pv = fma(bt, po_l[e], z_l[e]);
                 double qv = tab[v] * pv;
                 const int dg = deg_of(v);
                 for (int j = 0; j < dg; ++j) {
                     const int64_t k = ops_slot(g, v, j);
-                    const int64_t ob = ((int64_t)l * V + ops_other(g, k)) * CS + s;
-                    qv = fma(tab[3 * (int64_t)V + k], fma(bt, po[ob], A.z[ob]), qv);
+                    const int ob = ops_other(g, k) * CS + s;
+                    qv = fma(tab[3 * (int64_t)V + k], fma(bt, po_l[ob], z_l[ob]), qv);
                 }
-                pn[e] = pv;
-                A.q[e] = qv;
+                pn_l[e] = pv;
+                q_l[e] = qv;
                 acc[0] = fma(pv, qv, acc[0]);
             }
             block_partials<CS, 1>(A, l, vb, nvb, acc, red, [&](int ln, const double* tot) {
@@ -232,7 +270,16 @@ __global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
         grid.sync();
         // ---- phase 2: r' = r - alpha q, x += alpha p', z = M^{-1} r', r'.r', r'.z -> beta, convergence
         for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-            const int l = (int)(it / nvb), vb = (int)(it % nvb);
+            const int l = l0 + (int)(it / nvb), vb = (int)(it % nvb);
+            const int64_t lb = (int64_t)l * V * CS;  // node l's [V][CS] slab
+            double* const ro_l = ro + lb;
+            double* const po_l = po + lb;
+            double* const pn_l = pn + lb;
+            double* const rn_l = rn + lb;
+            double* const x_l = A.x + lb;
+            double* const z_l = A.z + lb;
+            double* const q_l = A.q + lb;
+            (void)ro_l; (void)po_l; (void)pn_l; (void)rn_l; (void)x_l; (void)z_l; (void)q_l;
             if (!A.node_active[l]) continue;
             const double* tab = A.ops + l * stride;
             const double al = A.alpha[l * CS + s];
@@ -240,23 +287,23 @@ __global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
             for (int c = 0; c < VPI / VBK; ++c) {
                 const int v = vert(vb, c);
                 if (v < 0) continue;
-                const int64_t e = ((int64_t)l * V + v) * CS + s;
-                const double rv = fma(-al, A.q[e], ro[e]);
-                A.x[e] = fma(al, pn[e], A.x[e]);
+                const int e = v * CS + s;  // offset within node l's [V][CS] slab (32-bit)
+                const double rv = fma(-al, q_l[e], ro_l[e]);
+                x_l[e] = fma(al, pn_l[e], x_l[e]);
                 double zv;
                 if (A.prm.precond == 0) {
                     zv = tab[V + v] * rv;
                     const int dg = deg_of(v);
                     for (int j = 0; j < dg; ++j) {
                         const int64_t k = ops_slot(g, v, j);
-                        const int64_t ob = ((int64_t)l * V + ops_other(g, k)) * CS + s;
-                        zv = fma(tab[3 * (int64_t)V + ns + k], fma(-al, A.q[ob], ro[ob]), zv);
+                        const int ob = ops_other(g, k) * CS + s;
+                        zv = fma(tab[3 * (int64_t)V + ns + k], fma(-al, q_l[ob], ro_l[ob]), zv);
                     }
                 } else {
                     zv = (A.prm.precond == 1 ? tab[2 * V + v] : 1.0) * rv;
                 }
-                rn[e] = rv;
-                A.z[e] = zv;
+                rn_l[e] = rv;
+                z_l[e] = zv;
                 acc[0] = fma(rv, rv, acc[0]);
                 acc[1] = fma(rv, zv, acc[1]);
             }
@@ -295,18 +342,20 @@ __global__ void __launch_bounds__(GT) pcg_global_kernel(GArgs A) {
     }
     // ---- write u_G, iteration counts and final relative residuals
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
-        const int l = (int)(it / nvb), vb = (int)(it % nvb);
+        const int l = l0 + (int)(it / nvb), vb = (int)(it % nvb);
         const int64_t sg = s0 + s;
         for (int c = 0; c < VPI / VBK; ++c) {
             const int v = vert(vb, c);
             if (v < 0 || sg >= A.S) continue;
-            A.uG[ug_index(sg, v, l, L, V, A.csl)] = A.x[((int64_t)l * V + v) * CS + s];
+            A.uG[ug_index(sg, v, l, L, V, A.csl)] = A.x[((int64_t)l * V) * CS + v * CS + s];
         }
         if (vb == 0 && tid < CS && s0 + tid < A.S) {
             const int sy = l * CS + tid;
             A.iters[(s0 + tid) * L + l] = A.its[sy];
             A.relres[(s0 + tid) * L + l] = A.gg[sy] > 0.0 ? sqrt(A.rr[sy] / A.gg[sy]) : 0.0;
         }
+    }
+    grid.sync();  // before the next group resets n_active
     }
 }
 
@@ -320,6 +369,14 @@ cudaError_t launch_cs(GArgs a, int64_t n_tiles, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int blocks = sms * per_sm;
+    // node groups: all nodes together.  (Solving L2-sized groups one after the other was measured
+    // on config 4: the per-group grid barriers cost more than the HBM traffic they save.)
+    a.group = a.L;
+    // vertices per item: enough items per phase for about two per CTA
+    const int vbk = GT / CS;
+    a.vpi = VPI_MAX;
+    while (a.vpi > vbk && (int64_t)a.group * ((a.g.V + a.vpi - 1) / a.vpi) < 2 * (int64_t)blocks) a.vpi /= 2;
+    if (a.vpi < vbk) a.vpi = vbk;
     for (int64_t t = 0; t < n_tiles; ++t) {
         a.tile = t;
         e = cudaMemsetAsync(a.n_active, 0, sizeof(int32_t), st);
@@ -337,7 +394,7 @@ cudaError_t launch_cs(GArgs a, int64_t n_tiles, cudaStream_t st) {
 
 size_t pcg_global_ws_bytes(const DevGraph& g, int32_t L, int64_t n_samples) {
     const int64_t cs = (int64_t)1 << sample_tile_log2(n_samples);
-    const int64_t nvb = (g.V + VPI - 1) / VPI;
+    const int64_t nvb = (g.V + (GT / cs) - 1) / (GT / cs);  // rows for the smallest item size
     size_t b = 7 * sizeof(double) * (size_t)L * g.V * cs;      // x, r0, r1, p0, p1, q, z
     b += 5 * sizeof(double) * (size_t)L * cs;                  // alpha, beta, rz, gg, rr
     b += 2 * sizeof(int32_t) * (size_t)L * cs;                 // done, its
@@ -353,7 +410,7 @@ cudaError_t launch_pcg_global(const DevGraph& g, const DevPlan& p, int64_t n_sam
     const int32_t csl = sample_tile_log2(n_samples);
     const int64_t cs = (int64_t)1 << csl;
     const int64_t L = p.L;
-    const int64_t nvb = (g.V + VPI - 1) / VPI;
+    const int64_t nvb = (g.V + (GT / cs) - 1) / (GT / cs);
     char* b = static_cast<char*>(ws);
     auto take = [&](size_t bytes) {
         char* r = b;
