@@ -115,7 +115,7 @@ __device__ void block_partials(const GArgs& A, int l, int vb, int nvb, const dou
 }
 
 template <int CS>
-__global__ void __launch_bounds__(GT, 4) pcg_global_kernel(GArgs A) {
+__global__ void __launch_bounds__(GT, 6) pcg_global_kernel(GArgs A) {
     cg::grid_group grid = cg::this_grid();
     constexpr int VBK = GT / CS;  // vertices per sub-chunk
     constexpr int RED = (GT + 2 * CS) > ((GT / 32) * 2 * CS) ? (GT + 2 * CS) : ((GT / 32) * 2 * CS);
