@@ -257,6 +257,22 @@ grf_status grf_comm_get_unique_id(void* id128);
 grf_status grf_comm_init(const void* id128, int rank, int nranks, grf_comm** out);
 void grf_comm_destroy(grf_comm* c);
 
+/* Sample-then-node sharding (policy BY_SAMPLE_THEN_NODE) of one grf_sample call
+ * over the communicator's ranks: P_s = min(world, n_samples) contiguous sample ranges, and the
+ * P_l = world / P_s ranks sharing a range split the quadrature nodes into contiguous ranges
+ * (their partial sums, P313-324, are sent to the range's root over NCCL and added in rank
+ * order).  grf_dist_shard (host only) fills out[6] = {sample_begin, sample_end, node_begin,
+ * node_end, root_rank, flags}, flags = active | is_root << 1 | P_l << 2.  grf_sample_dist
+ * writes range_out[6] likewise and, on an active rank, u_out (device, n_local x N, n_local =
+ * sample_end - sample_begin): the full field of the range on its root, the rank's node-shard
+ * partial sum elsewhere.  Inactive ranks (world > P_s P_l) return GRF_OK and touch nothing.
+ * opt's node range must be left at its default.  Synchronises when P_l > 1.
+ * (The EDGE_PARTITION policy is grf_sample_edgepart.) */
+grf_status grf_dist_shard(int32_t world, int32_t rank, int64_t n_samples, int64_t n_nodes, int64_t* out);
+grf_status grf_sample_dist(grf_graph* g, grf_comm* comm, double kappa, double beta, double k, uint64_t seed,
+                           int64_t n_samples, const grf_options* opt, double* u_out, int64_t* range_out,
+                           void* stream, grf_stats* stats);
+
 /* Sum-reduce a device fp64 buffer of `count` elements to `root` over NCCL on
  * `stream` (the l-shard reduction of partial quadrature sums). */
 grf_status grf_reduce_sum(grf_comm* c, const double* send, double* recv, int64_t count,

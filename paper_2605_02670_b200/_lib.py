@@ -52,7 +52,8 @@ EXPORTS = [
     "grf_workspace_size", "grf_noise", "grf_sample", "grf_sample_host", "grf_apply", "grf_edge_schur",
     "grf_comm_get_unique_id", "grf_comm_init", "grf_comm_destroy", "grf_reduce_sum",
     "grf_profile_enable", "grf_profile_read", "grf_graph_create_part", "grf_sample_edgepart",
-    "grf_prolong", "grf_project_noise", "grf_mnorm_sq_diff", "grf_noise_mass",
+    "grf_prolong", "grf_project_noise", "grf_mnorm_sq_diff", "grf_noise_mass", "grf_dist_shard",
+    "grf_sample_dist",
 ]
 KERNEL_NAMES = ["noise", "edge_setup", "condense", "pcg", "recover"]
 
@@ -101,6 +102,9 @@ def load() -> C.CDLL:
                                             C.POINTER(grf_allocator), C.POINTER(P)]),
         "grf_prolong": (C.c_int, [P, P, I64, P, P, P]),
         "grf_noise_mass": (C.c_int, [P, U64, I64, C.c_int32, P, P]),
+        "grf_dist_shard": (C.c_int, [C.c_int32, C.c_int32, I64, I64, pi64]),
+        "grf_sample_dist": (C.c_int, [P, P, D, D, D, U64, I64, C.POINTER(grf_options), P, pi64, P,
+                                      C.POINTER(grf_stats)]),
         "grf_project_noise": (C.c_int, [P, P, I64, P, P, P]),
         "grf_mnorm_sq_diff": (C.c_int, [P, I64, P, P, P, P]),
         "grf_sample_edgepart": (C.c_int, [C.POINTER(P), C.c_int32, P, D, D, D, U64, I64, C.POINTER(grf_options),

@@ -1321,3 +1321,92 @@ extern "C" grf_status grf_mnorm_sq_diff(grf_graph* g, int64_t n, const double* a
     if (e != cudaSuccess) return fail(GRF_ECUDA, "mnorm: %s", cudaGetErrorString(e));
     return GRF_OK;
 }
+
+// ---------------------------------------------------------------- sample-then-node sharded sampling
+namespace {
+typedef int (*nccl_p2p_fn)(void*, size_t, int, int, void*, cudaStream_t);  // ncclSend / ncclRecv
+typedef int (*nccl_group_fn)();
+
+int64_t split_lo(int64_t n, int64_t parts, int64_t i) {
+    const int64_t base = n / parts, extra = n % parts;
+    return i * base + std::min(i, extra);
+}
+}  // namespace
+
+extern "C" grf_status grf_dist_shard(int32_t world, int32_t rank, int64_t n_samples, int64_t n_nodes, int64_t* out) {
+    if (!out || world < 1 || rank < 0 || rank >= world || n_samples < 1 || n_nodes < 1)
+        return fail(GRF_EINVAL, "bad shard arguments");
+    const int64_t ps = std::min<int64_t>(world, n_samples);
+    const int64_t pl = std::max<int64_t>(1, std::min<int64_t>(world / ps, n_nodes));
+    const bool active = rank < ps * pl;
+    const int64_t gi = active ? rank / pl : 0, li = active ? rank % pl : 0;
+    out[0] = active ? split_lo(n_samples, ps, gi) : 0;
+    out[1] = active ? split_lo(n_samples, ps, gi + 1) : 0;
+    out[2] = active ? split_lo(n_nodes, pl, li) : 0;
+    out[3] = active ? split_lo(n_nodes, pl, li + 1) : 0;
+    out[4] = gi * pl;                       // root rank of the sample range
+    out[5] = (active ? 1 : 0) | ((active && li == 0) ? 2 : 0) | (pl << 2);  // active, is_root, ranks per range
+    return GRF_OK;
+}
+
+extern "C" grf_status grf_sample_dist(grf_graph* g, grf_comm* comm, double kappa, double beta, double k,
+                                      uint64_t seed, int64_t n_samples, const grf_options* opt, double* u_out,
+                                      int64_t* range_out, void* stream, grf_stats* stats) {
+    if (!g || !comm || !range_out) return fail(GRF_EINVAL, "NULL argument");
+    grf_status st = check_params(g, kappa, beta, k, n_samples);
+    if (st) return st;
+    int64_t Km, Kp;
+    st = plan_limits(beta, k, &Km, &Kp);
+    if (st) return st;
+    int64_t L = Km + Kp + 1;
+    if (opt && (opt->node_begin != 0 || opt->node_end >= 0))
+        return fail(GRF_EINVAL, "grf_sample_dist shards the whole node range; leave node_begin/node_end default");
+    int64_t sh[6];
+    st = grf_dist_shard(comm->nranks, comm->rank, n_samples, L, sh);
+    if (st) return st;
+    for (int i = 0; i < 6; ++i) range_out[i] = sh[i];
+    const bool active = sh[5] & 1, is_root = sh[5] & 2;
+    const int64_t pl = sh[5] >> 2;
+    if (!active) return GRF_OK;
+    if (!u_out) return fail(GRF_EINVAL, "u_out is NULL");
+    const int64_t s0 = sh[0], ns = sh[1] - sh[0];
+    grf_options o;
+    grf_options_default(&o);
+    if (opt) o = *opt;
+    o.node_begin = sh[2];
+    o.node_end = sh[3];
+    cudaStream_t s = (cudaStream_t)stream;
+    st = grf_sample(g, kappa, beta, k, seed + (uint64_t)s0, ns, &o, u_out, nullptr, 0, s, stats);
+    if (st && st != GRF_ENOCONV) return st;
+    if (pl > 1) {  // the node shards of this sample range: partial sums to the root, added in rank order
+        static nccl_p2p_fn send = nullptr, recv = nullptr;
+        static nccl_group_fn gstart = nullptr, gend = nullptr;
+        if (!send) {
+            send = (nccl_p2p_fn)dlsym(g_nccl.h, "ncclSend");
+            recv = (nccl_p2p_fn)dlsym(g_nccl.h, "ncclRecv");
+            gstart = (nccl_group_fn)dlsym(g_nccl.h, "ncclGroupStart");
+            gend = (nccl_group_fn)dlsym(g_nccl.h, "ncclGroupEnd");
+        }
+        if (!send || !recv) return fail(GRF_ENCCL, "ncclSend/ncclRecv not found");
+        const size_t count = (size_t)ns * g->N;
+        const int root = (int)sh[4];
+        if (is_root) {
+            double* tmp = (double*)g->alloc.get(count * sizeof(double), s);
+            if (!tmp) return fail(GRF_ENOMEM, "reduce buffer");
+            for (int64_t r = root + 1; r < root + pl; ++r) {
+                int e = recv(tmp, count, 8, (int)r, comm->comm, s);
+                if (e) return fail(GRF_ENCCL, "ncclRecv: %s", g_nccl.err ? g_nccl.err(e) : "error");
+                grf::launch_add(u_out, tmp, (int64_t)count, s);
+            }
+            cudaStreamSynchronize(s);
+            g->alloc.put(tmp, count * sizeof(double), s);
+        } else {
+            int e = send(u_out, count, 8, root, comm->comm, s);
+            if (e) return fail(GRF_ENCCL, "ncclSend: %s", g_nccl.err ? g_nccl.err(e) : "error");
+        }
+        (void)gstart;
+        (void)gend;
+    }
+    CUDA_TRY(cudaGetLastError());
+    return st;
+}

@@ -171,6 +171,8 @@ void finish(const DevGraph& g, int32_t L, int64_t S, int32_t csl, int64_t tile, 
 int32_t dot_blocks(const DevGraph& g);
 }  // namespace dist
 
+// y += x (refine.cu)
+void launch_add(double* y, const double* x, int64_t n, cudaStream_t st);
 // nested-mesh transfer for the strong-error study (refine.cu)
 void launch_prolong(const DevGraph& gc, const DevGraph& gf, const int32_t* fedge, int64_t S, const double* uc,
                     double* uf, cudaStream_t st);

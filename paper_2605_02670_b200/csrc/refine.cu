@@ -112,7 +112,18 @@ __global__ void mnorm_final_kernel(int64_t S, int nblk, const double* __restrict
     out[s] = t;
 }
 
+// y += x (fixed order per element: used for the rank-ordered reduce of node-shard partial sums)
+__global__ void add_kernel(double* __restrict__ y, const double* __restrict__ x, int64_t n) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        y[t] += x[t];
+}
+
 }  // namespace
+
+void launch_add(double* y, const double* x, int64_t n, cudaStream_t st) {
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    add_kernel<<<blocks, 256, 0, st>>>(y, x, n);
+}
 
 void launch_prolong(const DevGraph& gc, const DevGraph& gf, const int32_t* fedge, int64_t S, const double* uc,
                     double* uf, cudaStream_t st) {

@@ -343,3 +343,27 @@ class Comm:
             self.close()
         except Exception:
             pass
+
+
+def dist_shard(world: int, rank: int, n_samples: int, n_nodes: int):
+    """grf_dist_shard: (sample_range, node_range, root, active, is_root, ranks_per_range)."""
+    out = (C.c_int64 * 6)()
+    check(load().grf_dist_shard(world, rank, n_samples, n_nodes, out))
+    f = out[5]
+    return (out[0], out[1]), (out[2], out[3]), out[4], bool(f & 1), bool(f & 2), f >> 2
+
+
+def sample_dist(graph: "Graph", comm: "Comm", kappa, beta, k, seed=0, n_samples=1, stream=None, **opts):
+    """grf_sample_dist (sample-then-node sharding in the library, NCCL reduce of node shards):
+    returns (u or None, sample_range, is_root); u is the rank's [n_local, N] result."""
+    torch = _torch()
+    o = make_options(**opts)
+    km, kp, _, _ = plan_info(beta, k)
+    (s0, s1), _, _, active, is_root, _ = dist_shard(comm.world, comm.rank, n_samples, km + kp + 1)
+    if not active:
+        return None, (0, 0), False
+    u = torch.empty((s1 - s0, graph.n_dofs), dtype=torch.float64, device=f"cuda:{graph.device}")
+    rng = (C.c_int64 * 6)()
+    check(load().grf_sample_dist(graph._h, comm.handle, kappa, beta, k, C.c_uint64(seed & (2 ** 64 - 1)), n_samples,
+                                 C.byref(o), C.c_void_p(u.data_ptr()), rng, C.c_void_p(_stream_ptr(stream)), None))
+    return u, (s0, s1), is_root

@@ -118,3 +118,29 @@ def test_config4_edge_partitioned_two_parts():
     u, st, _, _ = _run_parts(g, cfg["h"], 2, cfg["kappa"], cfg["beta"], cfg["k"], seed=0, S=16)
     assert st["n_unconverged"] == 0
     assert _rel(u[[0, 15]], whole).max() <= 1e-10
+
+
+def test_sample_dist_one_rank():
+    """grf_sample_dist (sample-then-node sharding in the library) with a one-rank communicator."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2605_02670_b200 import Comm
+    from paper_2605_02670_b200.grf import sample_dist
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = Comm()
+        G = Graph.from_metric_graph(lattice(4, seed=3), 0.05)
+        u, rng, root = sample_dist(G, comm, 3.0, 0.7, 0.4, seed=2, n_samples=5)
+        ref = G.sample(3.0, 0.7, 0.4, seed=2, n_samples=5)
+        assert rng == (0, 5) and root
+        assert torch.equal(u, ref)
+        comm.close()
+    finally:
+        dist.destroy_process_group()

@@ -67,3 +67,17 @@ def test_gloo_node_shard_reduce(S, L):
         for s in range(s0, s1):
             got[s] = arr[s - s0, 0]
     assert got == {s: float(v) for s, v in full.items()}
+
+
+@pytest.mark.parametrize("world,S,L", [(1, 1, 55), (2, 1, 259), (8, 1, 259), (8, 256, 212), (8, 3, 10),
+                                      (4, 16, 112), (3, 2, 7), (8, 64, 687), (5, 2, 3)])
+def test_library_shard_matches_host_logic(world, S, L):
+    """grf_dist_shard (the C ABI's copy of the sharding rule) agrees with parallel.shard."""
+    from paper_2605_02670_b200.grf import dist_shard
+    for r in range(world):
+        sh = shard(world, r, S, L)
+        srange, nrange, root, active, is_root, pl = dist_shard(world, r, S, L)
+        assert active == sh.active and is_root == sh.is_root and pl == sh.n_node_shards
+        if sh.active:
+            assert srange == sh.sample_range and nrange == sh.node_range
+            assert root == sh.group_index * sh.n_node_shards
