@@ -190,6 +190,17 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
             const int64_t s = c0 + st0 + (j ^ sig);
             sidx[j] = s < A.S ? s : A.S - 1;
         }
+        // u_G of the edge's two vertices for this thread's samples: node l at uGu[j][l << CSL]
+        // (layout [tile][v][l][cs], grf_internal.h) -- base pointers once per item
+        const double* uGu[REC ? TS : 1];
+        const double* uGv[REC ? TS : 1];
+        if (REC) {
+#pragma unroll
+            for (int j = 0; j < TS; ++j) {
+                uGu[j] = A.uG + ug_index(sidx[j], vu, 0, L, g.V, CSL);
+                uGv[j] = A.uG + ug_index(sidx[j], vv, 0, L, g.V, CSL);
+            }
+        }
 
         if (m == 0) {
             if (!REC) {  // no interior: zero end values (ends layout [tile][l][code][CS], grf_internal.h)
@@ -217,8 +228,8 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                     const double beta = ok ? (A.mass ? edge_coef(A.cI[l], A.cL[l], A.kappa2, h, 1).beta : A.cL[l] / h) : 0.0;
 #pragma unroll
                     for (int j = 0; j < TS; ++j) {
-                        const double ul = ok ? A.uG[ug_index(sidx[j], vu, l, L, g.V, CSL)] : 0.0;
-                        const double ur = ok ? A.uG[ug_index(sidx[j], vv, l, L, g.V, CSL)] : 0.0;
+                        const double ul = ok ? uGu[j][l << CSL] : 0.0;
+                        const double ur = ok ? uGv[j][l << CSL] : 0.0;
                         Y[n][j] = beta * (m == 1 ? ul + ur : ul);
                         Z[n][j] = beta * (m == 1 ? ul + ur : ur);
                     }
@@ -453,8 +464,8 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                             const double nk = gg * mu;
 #pragma unroll
                             for (int j = 0; j < TS; ++j) {
-                                const double ul = ok ? A.uG[ug_index(sidx[j], vu, l, L, g.V, CSL)] : 0.0;
-                                const double ur = ok ? A.uG[ug_index(sidx[j], vv, l, L, g.V, CSL)] : 0.0;
+                                const double ul = ok ? uGu[j][l << CSL] : 0.0;
+                                const double ur = ok ? uGv[j][l << CSL] : 0.0;
                                 aL[j] = fma(-nk, Y[n][j], aL[j]);
                                 Y[n][j] = fma(beta, ur, fma(-mu, Y[n][j], wl[j]));
                                 Z[n][j] = fma(beta, ul, fma(-mu, Z[n][j], wr[j]));
@@ -497,6 +508,19 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                     // software pipeline: the reduction of step tt-1 is independent of step tt's FMAs, so
                     // the scheduler overlaps the shuffle latency with them
                     const bool last_here = (t0 + nb == m) && (m > 1);
+                    if (last_here && nb > 1) {  // the last step re-reads both vertices' u_G: pull it into L1 now
+#pragma unroll
+                        for (int n = 0; n < TL; ++n) {
+                            const int l = rb + slot(n);
+                            if (l < L) {
+#pragma unroll
+                                for (int j = 0; j < TS; ++j) {
+                                    asm volatile("prefetch.global.L1 [%0];" ::"l"(uGu[j] + (l << CSL)));
+                                    asm volatile("prefetch.global.L1 [%0];" ::"l"(uGv[j] + (l << CSL)));
+                                }
+                            }
+                        }
+                    }
                     const int tend = last_here ? nb - 1 : nb;
                     double pL[TS], pR[TS];
                     bool pend = false;
@@ -576,8 +600,12 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
         }
         if (in_tile) {
             __syncthreads();
+            const float inv_m = 1.0f / (float)m;  // x / m without an integer division (exact after the fix-up)
             for (int x = tid; x < CS * m; x += NT) {
-                const int s = x / m, p = x - s * m;
+                int s = (int)((float)x * inv_m);
+                s -= (s * m > x);
+                s += ((s + 1) * m <= x);
+                const int p = x - s * m;
                 if (c0 + s < A.S) A.out[(c0 + s) * N + off + p] = otile[s * ms + p];
             }
         }
