@@ -241,7 +241,7 @@ def test_config3_lattice_256_samples_sampled():
 
 
 # ----------------------------------------------------------------------------- global-memory K4
-@pytest.mark.parametrize("n_samples", [1, 3, 16, 20])
+@pytest.mark.parametrize("n_samples", [1, 3, 16, 20, 40])
 def test_global_pcg_matches_oracle(n_samples):
     """The global-memory PCG (pcg_global.cu, used for V > 4096) forced on small graphs, for every
     sample mapping (1 / 16 / 32 samples per tile, ragged tile), vs the oracle."""
