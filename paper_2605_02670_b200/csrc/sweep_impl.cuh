@@ -169,19 +169,28 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
     // node slot (within a round) of this thread's node n (0..TL-1)
     auto slot = [&](int n) -> int { return (n < 2 * NP) ? (2 * lt + 64 * (n >> 1) + (n & 1)) : (64 * NP + lt); };
 
-    for (;;) {
-        if (tid == 0) *item_sh = atomicAdd(A.counter, 1);
-        __syncthreads();
-        const int it = *item_sh;
-        __syncthreads();
+    // work queue, one item ahead: the index of the next item is fetched when the current one starts
+    // and published at its end barrier, so the atomic's latency never stalls the CTA
+    if (tid == 0) item_sh[0] = atomicAdd(A.counter, 1);
+    __syncthreads();
+    for (int cur = 0;; cur ^= 1) {
+        const int it = item_sh[cur];
         if (it >= A.n_items) break;
+        int next = 0;
+        if (tid == 0) next = atomicAdd(A.counter, 1);
         const int e = g.edge_order[it / A.chunks];
         const int64_t c0 = (int64_t)(it % A.chunks) * CS;
         const int m = g.m[e];
         const int64_t off = g.off[e];
         const int64_t toff = g.toff[e];  // Thomas-table rows of the edge's (m, h) class
         const double h = g.h[e];
+        const double inv_h = 1.0 / h;
         const int vu = g.eu[e], vv = g.ev[e];
+        // coupling of node l's boundary rows to the vertex values: c_L/h (lumped), -b (consistent)
+        auto beta_of = [&](int l) -> double {
+            if (l >= L) return 0.0;
+            return A.mass ? edge_coef(A.cI[l], A.cL[l], A.kappa2, h, 1).beta : A.cL[l] * inv_h;
+        };
         const int ms = m | 1;
         const bool in_tile = REC && ms <= A.tile_ms;
         int64_t sidx[TS];  // sample of slot j (clamped for loads; writes check c0 + st0 + (j ^ sig) < S)
@@ -202,36 +211,32 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
             }
         }
 
-        if (m == 0) {
-            if (!REC) {  // no interior: zero end values (ends layout [tile][l][code][CS], grf_internal.h)
-                const int64_t tile = it % A.chunks;
-                for (int x = tid; x < L * 2 * CS; x += NT) {
-                    const int l = x / (2 * CS), r = x % (2 * CS);
-                    A.out[((tile * L + l) * 2 * (int64_t)g.E + 2 * e) * CS + r] = 0.0;
-                }
+        if (m == 0 && !REC) {  // no interior: zero end values (ends layout [tile][l][code][CS], grf_internal.h)
+            const int64_t tile = it % A.chunks;
+            for (int x = tid; x < L * 2 * CS; x += NT) {
+                const int l = x / (2 * CS), r = x % (2 * CS);
+                A.out[((tile * L + l) * 2 * (int64_t)g.E + 2 * e) * CS + r] = 0.0;
             }
-            continue;
         }
         const int nblk = (m + IBK - 1) / IBK;
 
-        for (int rd = 0; rd < A.rounds; ++rd) {
+        for (int rd = 0; rd < (m == 0 ? 0 : A.rounds); ++rd) {
             const int rb = rd * RN;  // first node of the round
             double Y[TL][TS], Z[TL][TS];
             double g0[REC ? 1 : TL];
             if (REC) {
                 // boundary rows (P310): f_0 += (c_L/h) u_left, f_{m-1} += (c_L/h) u_right; both
-                // enter the chains at step 0 (mu_0 = 0): preload beta*u into the chain registers
+                // enter the chains at step 0 (mu_0 = 0).  The raw u_G loads are issued here and
+                // scaled by beta after block 0's barrier (scale_boundary), so their latency
+                // overlaps the staging of block 0.
 #pragma unroll
                 for (int n = 0; n < TL; ++n) {
                     const int l = rb + slot(n);
                     const bool ok = l < L;
-                    const double beta = ok ? (A.mass ? edge_coef(A.cI[l], A.cL[l], A.kappa2, h, 1).beta : A.cL[l] / h) : 0.0;
 #pragma unroll
                     for (int j = 0; j < TS; ++j) {
-                        const double ul = ok ? uGu[j][l << CSL] : 0.0;
-                        const double ur = ok ? uGv[j][l << CSL] : 0.0;
-                        Y[n][j] = beta * (m == 1 ? ul + ur : ul);
-                        Z[n][j] = beta * (m == 1 ? ul + ur : ur);
+                        Y[n][j] = ok ? uGu[j][l << CSL] : 0.0;
+                        Z[n][j] = ok ? uGv[j][l << CSL] : 0.0;
                     }
                 }
             } else {
@@ -339,6 +344,18 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                 __syncthreads();  // block b staged and visible; block b-1 buffers and partials free/complete
                 if (b + 1 < nblk) stage(b + 1);
                 if (REC && b > 0) fold(b - 1);
+                if (REC && b == 0) {  // Y = beta u_left, Z = beta u_right (both ends for m = 1)
+#pragma unroll
+                    for (int n = 0; n < TL; ++n) {
+                        const double bt = beta_of(rb + slot(n));
+#pragma unroll
+                        for (int j = 0; j < TS; ++j) {
+                            const double ul = Y[n][j], ur = Z[n][j];
+                            Y[n][j] = bt * (m == 1 ? ul + ur : ul);
+                            Z[n][j] = bt * (m == 1 ? ul + ur : ur);
+                        }
+                    }
+                }
                 const double* cmu = coef + (buf * NTAB + 0) * IBK * RN;
                 const double* cga = coef + (buf * NTAB + 1) * IBK * RN;
                 const double* wb = wbuf + buf * IBK * 2 * NC * CS;
@@ -459,7 +476,7 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                             const int sn = slot(n);
                             const int l = rb + sn;
                             const bool ok = l < L;
-                            const double beta = ok ? (A.mass ? edge_coef(A.cI[l], A.cL[l], A.kappa2, h, 1).beta : A.cL[l] / h) : 0.0;
+                            const double beta = beta_of(l);
                             const double mu = rmu[sn], gg = rga[sn];
                             const double nk = gg * mu;
 #pragma unroll
@@ -609,6 +626,8 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                 if (c0 + s < A.S) A.out[(c0 + s) * N + off + p] = otile[s * ms + p];
             }
         }
+        if (tid == 0) item_sh[cur ^ 1] = next;
+        __syncthreads();  // next index visible; output tile and staging buffers free
     }
 }
 
