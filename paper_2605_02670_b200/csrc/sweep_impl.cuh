@@ -152,17 +152,20 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);           // [2]
-    int* item_sh = reinterpret_cast<int*>(smem_raw + 16);
+    int* item_sh = reinterpret_cast<int*>(smem_raw + 16);           // [2] work-queue indices
     double* coef = reinterpret_cast<double*>(smem_raw + 64);         // [2][NTAB][IBK][RN]
     double* wbuf = coef + 2 * NTAB * IBK * RN;                       // [2][IBK][2][NC][CS]
     double* part = wbuf + 2 * IBK * 2 * NC * CS;                     // [2][IBK][NWL][2][CS] (REC)
-    double* otile = part + (REC ? 2 * IBK * NWL * 2 * CS : 0);       // [CS][tile_ms] (REC)
+    double* cLs = part + (REC ? 2 * IBK * NWL * 2 * CS : 0);         // [Lp] c_L (REC)
+    double* otile = cLs + (REC ? A.Lp : 0);                          // [CS][tile_ms] (REC)
 
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (REC)
+        for (int i = tid; i < A.Lp; i += NT) cLs[i] = A.cL[i];  // zero padded past L
     __syncthreads();
     uint32_t phases = 0u;  // bit b: parity of the next completion of bar[b]
 
@@ -189,7 +192,7 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
         // coupling of node l's boundary rows to the vertex values: c_L/h (lumped), -b (consistent)
         auto beta_of = [&](int l) -> double {
             if (l >= L) return 0.0;
-            return A.mass ? edge_coef(A.cI[l], A.cL[l], A.kappa2, h, 1).beta : A.cL[l] * inv_h;
+            return A.mass ? edge_coef(A.cI[l], A.cL[l], A.kappa2, h, 1).beta : cLs[l] * inv_h;
         };
         const int ms = m | 1;
         const bool in_tile = REC && ms <= A.tile_ms;
@@ -298,11 +301,16 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                 const int t0 = b * IBK;
                 const int nb = (m - t0) < IBK ? (m - t0) : IBK;
                 const double* pb = part + (b & 1) * IBK * NWL * 2 * CS;
-                auto psum = [&](int tt, int side, int s) {
-                    double v = 0.0;
+                auto psum = [&](int tt, int side, int s) {  // pairwise tree over the l-warps (fixed order)
+                    double v[NWL];
 #pragma unroll
-                    for (int q = 0; q < NWL; ++q) v += pb[((tt * NWL + q) * 2 + side) * CS + s];
-                    return v;
+                    for (int q = 0; q < NWL; ++q) v[q] = pb[((tt * NWL + q) * 2 + side) * CS + s];
+#pragma unroll
+                    for (int w = 1; w < NWL; w <<= 1) {
+#pragma unroll
+                        for (int q = 0; q + w < NWL; q += 2 * w) v[q] += v[q + w];
+                    }
+                    return v[0];
                 };
                 auto put = [&](int s, int p, double v, bool first) {
                     if (in_tile) {
@@ -343,7 +351,6 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                 __pipeline_wait_prior(0);
                 __syncthreads();  // block b staged and visible; block b-1 buffers and partials free/complete
                 if (b + 1 < nblk) stage(b + 1);
-                if (REC && b > 0) fold(b - 1);
                 if (REC && b == 0) {  // Y = beta u_left, Z = beta u_right (both ends for m = 1)
 #pragma unroll
                     for (int n = 0; n < TL; ++n) {
@@ -582,6 +589,9 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                         pend = true;
                     }
                     if (pend) reduce_store(pL, pR, nb - 1);
+                    // block b-1's partials are complete since this block's barrier and are not
+                    // overwritten before the next one: fold them while other warps still compute
+                    if (b > 0) fold(b - 1);
                 }
             }
             if (REC) {
@@ -637,7 +647,7 @@ cudaError_t launch(Args a, cudaStream_t st) {
     using C = Cfg<TL, TS, LW, NWS, REC>;
     a.chunks = (int32_t)((a.S + C::CS - 1) / C::CS);
     a.n_items = a.g.E * a.chunks;
-    size_t smem = C::FIXED;
+    size_t smem = C::FIXED + (REC ? (size_t)a.Lp * sizeof(double) : 0);
     a.tile_ms = 0;
     if (REC) {
         // the output tile holds edges with (m | 1) <= tile_ms; sized for the longest edge if it fits
