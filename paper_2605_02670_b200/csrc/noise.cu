@@ -66,25 +66,28 @@ __device__ __forceinline__ double cos2pi_fixed(double u) {
     const double f = __dsub_rn(t, q);
     const double th = __dmul_rn(f, HALF_PI);
     const double th2 = __dmul_rn(th, th);
-    double pc = 1.0, ps = 1.0;
+    // only the polynomial the quadrant needs is evaluated (the same operations as that branch of
+    // the two-polynomial definition): odd quadrants take the sine series, even ones the cosine
+    const int qi = ((int)q) & 3;
+    const bool odd = qi & 1;
+    double p = 1.0;
 #pragma unroll
     for (int j = 10; j >= 1; --j) {
-        pc = __dsub_rn(1.0, __dmul_rn(__dmul_rn(th2, 1.0 / (double)((2 * j) * (2 * j - 1))), pc));
-        ps = __dsub_rn(1.0, __dmul_rn(__dmul_rn(th2, 1.0 / (double)((2 * j + 1) * (2 * j))), ps));
+        const double k = odd ? 1.0 / (double)((2 * j + 1) * (2 * j)) : 1.0 / (double)((2 * j) * (2 * j - 1));
+        p = __dsub_rn(1.0, __dmul_rn(__dmul_rn(th2, k), p));
     }
-    const double c = pc;
-    const double sn = __dmul_rn(th, ps);
-    const int qi = ((int)q) & 3;
-    return qi == 0 ? c : (qi == 1 ? -sn : (qi == 2 ? -c : sn));
+    const double v = odd ? __dmul_rn(th, p) : p;
+    return (qi == 1 || qi == 2) ? -v : v;
 }
 
 __global__ void __launch_bounds__(256) noise_kernel(const double* __restrict__ sqrt_ml,
                                                     const int64_t* __restrict__ dof_gid, int64_t N,
                                                     int64_t total, uint64_t seed, double* __restrict__ W) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t s = t / N;
-        const int64_t i = t - s * N;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t s = t / N, i = t - s * N;  // (sample, dof) of t, advanced without a 64-bit division
+    const int64_t ds = stride / N, di = stride - ds * N;
+    for (; t < total; t += stride) {
         const uint64_t key = seed + (uint64_t)s;
         const int64_t ig = dof_gid ? dof_gid[i] : i;  // counter = GLOBAL DOF index (edge-partitioned parts)
         const uint4 x = philox4x32_10(make_uint4((unsigned)ig, (unsigned)((uint64_t)ig >> 32), 0u, 0u),
@@ -96,6 +99,12 @@ __global__ void __launch_bounds__(256) noise_kernel(const double* __restrict__ s
         const double r = __dsqrt_rn(__dmul_rn(-2.0, ln_fixed(u1)));
         const double z = __dmul_rn(r, cos2pi_fixed(u2));
         W[t] = sqrt_ml ? __dmul_rn(sqrt_ml[i], z) : z;  // sqrt_ml == nullptr: the raw normals xi
+        s += ds;
+        i += di;
+        if (i >= N) {
+            i -= N;
+            ++s;
+        }
     }
 }
 

@@ -388,28 +388,45 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                 };
 
                 if (!REC) {
-#pragma unroll 2
-                    for (int tt = 0; tt < nb; ++tt) {
-                        double wl[TS], wr[TS];
-                        load_w(tt, wl, wr);
+                    // step tt+1's multipliers and noise are loaded into registers while step tt's
+                    // FMAs run (the last step re-loads its own row: no read past the block)
+                    double wln[TS], wrn[TS], mon = 0.0;
+                    double2 m2n[NP > 0 ? NP : 1];
+                    auto ld = [&](int tt) {
+                        load_w(tt, wln, wrn);
                         const double* rmu = cmu + tt * RN;
 #pragma unroll
+                        for (int q = 0; q < NP; ++q) m2n[q] = *reinterpret_cast<const double2*>(rmu + 2 * lt + 64 * q);
+                        if (ODD) mon = rmu[64 * NP + lt];
+                    };
+                    ld(0);
+#pragma unroll 2
+                    for (int tt = 0; tt < nb; ++tt) {
+                        double wl[TS], wr[TS], mo = mon;
+                        double2 m2[NP > 0 ? NP : 1];
+#pragma unroll
+                        for (int j = 0; j < TS; ++j) {
+                            wl[j] = wln[j];
+                            wr[j] = wrn[j];
+                        }
+#pragma unroll
+                        for (int q = 0; q < NP; ++q) m2[q] = m2n[q];
+                        ld(tt + 1 < nb ? tt + 1 : tt);
+#pragma unroll
                         for (int q = 0; q < NP; ++q) {
-                            const double2 m2 = *reinterpret_cast<const double2*>(rmu + 2 * lt + 64 * q);
 #pragma unroll
                             for (int j = 0; j < TS; ++j) {
-                                Y[2 * q][j] = fma(-m2.x, Y[2 * q][j], wl[j]);
-                                Z[2 * q][j] = fma(-m2.x, Z[2 * q][j], wr[j]);
-                                Y[2 * q + 1][j] = fma(-m2.y, Y[2 * q + 1][j], wl[j]);
-                                Z[2 * q + 1][j] = fma(-m2.y, Z[2 * q + 1][j], wr[j]);
+                                Y[2 * q][j] = fma(-m2[q].x, Y[2 * q][j], wl[j]);
+                                Z[2 * q][j] = fma(-m2[q].x, Z[2 * q][j], wr[j]);
+                                Y[2 * q + 1][j] = fma(-m2[q].y, Y[2 * q + 1][j], wl[j]);
+                                Z[2 * q + 1][j] = fma(-m2[q].y, Z[2 * q + 1][j], wr[j]);
                             }
                         }
                         if (ODD) {
-                            const double mu = rmu[64 * NP + lt];
 #pragma unroll
                             for (int j = 0; j < TS; ++j) {
-                                Y[TL - 1][j] = fma(-mu, Y[TL - 1][j], wl[j]);
-                                Z[TL - 1][j] = fma(-mu, Z[TL - 1][j], wr[j]);
+                                Y[TL - 1][j] = fma(-mo, Y[TL - 1][j], wl[j]);
+                                Z[TL - 1][j] = fma(-mo, Z[TL - 1][j], wr[j]);
                             }
                         }
                     }
