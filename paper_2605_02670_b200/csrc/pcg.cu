@@ -468,11 +468,11 @@ __global__ void __launch_bounds__(256) assemble_rhs_kernel(DevGraph g, int32_t L
     // incidence slots per vertex handled through the staged arrays; hubs (CSR mode, > 32 slots)
     // read their remaining slots from global memory
     const int Wd = g.csr ? 32 : g.ell_w;
-    for (int64_t b = blockIdx.x; b < tiles * L * vblocks; b += gridDim.x) {
+    // work unit = (node l, vertex block): the incidence codes and coefficients are staged once
+    // and reused for every sample tile
+    for (int64_t b = blockIdx.x; b < (int64_t)L * vblocks; b += gridDim.x) {
         const int vb = (int)(b % vblocks);
-        const int64_t tl = b / vblocks;  // tile * L + l
-        const int l = (int)(tl % L);
-        const int64_t tile = tl / L;
+        const int l = (int)(b / vblocks);
         const double* GK = ops + l * stride + 3 * (int64_t)V + 2 * ops_nslots(g);
         for (int x = threadIdx.x; x < Wd * ASM_VB; x += blockDim.x) {
             const int j = x / ASM_VB, vl = x % ASM_VB;
@@ -483,6 +483,8 @@ __global__ void __launch_bounds__(256) assemble_rhs_kernel(DevGraph g, int32_t L
             gks[j][vl] = ok ? GK[k] : 0.0;
         }
         __syncthreads();
+      for (int64_t tile = 0; tile < tiles; ++tile) {
+        const int64_t tl = tile * L + l;
         const double* slab = ends + ((tl * 2 * E) << csl);
         for (int x = threadIdx.x; x < ASM_VB * cs; x += blockDim.x) {
             const int vl = x >> csl, si = x & (cs - 1);
@@ -511,6 +513,7 @@ __global__ void __launch_bounds__(256) assemble_rhs_kernel(DevGraph g, int32_t L
             }
         }
         __syncthreads();
+      }
     }
 }
 
@@ -540,7 +543,7 @@ void launch_pcg_tables(const DevGraph& g, const DevPlan& p, cudaStream_t st) {
 void launch_assemble_rhs(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W, const double* ends,
                          double* rhs, cudaStream_t st) {
     const int32_t csl = sample_tile_log2(n_samples);
-    const int64_t work = ((n_samples + (1 << csl) - 1) >> csl) * p.L * ((g.V + ASM_VB - 1) / ASM_VB);
+    const int64_t work = (int64_t)p.L * ((g.V + ASM_VB - 1) / ASM_VB);
     int blocks = (int)(work < 148 * 8 ? work : 148 * 8);
     assemble_rhs_kernel<<<blocks, 256, 0, st>>>(g, p.L, p.ops, n_samples, csl, W, ends, rhs);
 }
