@@ -43,17 +43,18 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
     const int* eo = g.ell_other;
     double* r = sm + (size_t)warp * 2 * V;
     double* p = r + V;
-    // packed staging (W = 4): per vertex the 4 neighbour indices as one int4 and the 4 slot
-    // coefficients of each operator as two double2, so a vertex's operator row is 3 LDS.128
+    // packed staging (W = 4): per vertex the 4 neighbour indices as one ushort4 (V <= 1024) and
+    // the 4 slot coefficients of each operator as two double2: a vertex's operator row is one
+    // LDS.64 + two LDS.128
     constexpr bool PACK = STAGE && W == 4;
-    const int4* nb4 = nullptr;
+    const ushort4* nb4 = nullptr;
     const double2 *os01 = nullptr, *os23 = nullptr, *om01 = nullptr, *om23 = nullptr;
     if (STAGE) {  // DS, DM, OS, OM and the neighbour indices of node l, once per CTA
         double* st = sm + (size_t)WARP_NW * 2 * V;
         if (PACK) {
             double* sD = st;                                          // DS [V], DM [V]
             double2* sO = reinterpret_cast<double2*>(st + 2 * V);     // OS01, OS23, OM01, OM23: [V] each
-            int4* sN = reinterpret_cast<int4*>(sO + 4 * V);           // neighbours [V]
+            ushort4* sN = reinterpret_cast<ushort4*>(sO + 4 * V);     // neighbours [V]
             for (int i = threadIdx.x; i < 2 * V; i += WARP_NW * 32) sD[i] = tab[i];
             for (int v = threadIdx.x; v < V; v += WARP_NW * 32) {
                 const double* oS = OS + v;
@@ -62,7 +63,8 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
                 sO[V + v] = make_double2(oS[2 * V], oS[3 * V]);
                 sO[2 * V + v] = make_double2(oM[0], oM[V]);
                 sO[3 * V + v] = make_double2(oM[2 * V], oM[3 * V]);
-                sN[v] = make_int4(eo[v], eo[V + v], eo[2 * V + v], eo[3 * V + v]);
+                sN[v] = make_ushort4((unsigned short)eo[v], (unsigned short)eo[V + v], (unsigned short)eo[2 * V + v],
+                                     (unsigned short)eo[3 * V + v]);
             }
             __syncthreads();
             DS = sD;
@@ -85,16 +87,19 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
             eo = so;
         }
     }
-    // y = D x + sum_j O_j x_{o_j} for this lane's vertices (x in shared memory)
+    // y = D x + sum_j O_j x_{o_j} for this lane's vertices (x in shared memory), with the lane
+    // partials of the dot products that read the same x_v fused in (same per-lane order as a
+    // separate pass): MODE 1: d1 += x.y (p.q); MODE 2: d1 += x.x, d2 += x.y (r.r, r.z)
     auto apply = [&](const double* D, const double* O, const double2* O01, const double2* O23, const double* xs,
-                     double (&y)[VPL]) {
+                     double (&y)[VPL], int mode, double& d1, double& d2) {
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
             const int v = lane + 32 * k;
             if (v < V) {
-                double a = D[v] * xs[v];
+                const double xv = xs[v];
+                double a = D[v] * xv;
                 if (PACK) {
-                    const int4 nb = nb4[v];
+                    const ushort4 nb = nb4[v];
                     const double2 c01 = O01[v], c23 = O23[v];
                     a = fma(c01.x, xs[nb.x], a);
                     a = fma(c01.y, xs[nb.y], a);
@@ -105,17 +110,29 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
                     for (int j = 0; j < W; ++j) a = fma(O[j * V + v], xs[eo[j * V + v]], a);
                 }
                 y[k] = a;
+                if (mode == 1) d1 = fma(xv, a, d1);
+                if (mode == 2) {
+                    d1 = fma(xv, xv, d1);
+                    d2 = fma(xv, a, d2);
+                }
             }
         }
     };
-    auto precond = [&](double (&z)[VPL]) {
+    auto precond = [&](double (&z)[VPL], int mode, double& d1, double& d2) {
         if (prm.precond == 0) {
-            apply(DM, OM, om01, om23, r, z);
+            apply(DM, OM, om01, om23, r, z, mode, d1, d2);
         } else {
 #pragma unroll
             for (int k = 0; k < VPL; ++k) {
                 const int v = lane + 32 * k;
-                if (v < V) z[k] = (prm.precond == 1 ? DJ[v] : 1.0) * r[v];
+                if (v < V) {
+                    const double rv = r[v];
+                    z[k] = (prm.precond == 1 ? DJ[v] : 1.0) * rv;
+                    if (mode == 2) {
+                        d1 = fma(rv, rv, d1);
+                        d2 = fma(rv, z[k], d2);
+                    }
+                }
             }
         }
     };
@@ -170,7 +187,8 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
             gg = warp_sum(gg);
         }
         __syncwarp();
-        precond(t);
+        double d0a = 0.0, d0b = 0.0;
+        precond(t, 0, d0a, d0b);
         double rz = 0.0;
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
@@ -188,13 +206,8 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
         int it = 0;
         while (!done && it < prm.max_iter) {
             ++it;
-            apply(DS, OS, os01, os23, p, t);  // Dirichlet step (P247-258): t = q
-            double pq = 0.0;
-#pragma unroll
-            for (int k = 0; k < VPL; ++k) {
-                const int v = lane + 32 * k;
-                if (v < V) pq = fma(p[v], t[k], pq);
-            }
+            double pq = 0.0, unused = 0.0;
+            apply(DS, OS, os01, os23, p, t, 1, pq, unused);  // Dirichlet step (P247-258): t = q, pq = p.q
             pq = warp_sum(pq);
             if (!(pq > 0.0)) break;  // p = 0 (e.g. an underflowed rhs): nothing left to reduce
             const double alpha = rz / pq;
@@ -207,16 +220,8 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
                 }
             }
             __syncwarp();
-            precond(t);  // Neumann step (P260-298): t = z
             double t_rr = 0.0, t_rz = 0.0;
-#pragma unroll
-            for (int k = 0; k < VPL; ++k) {
-                const int v = lane + 32 * k;
-                if (v < V) {
-                    t_rr = fma(r[v], r[v], t_rr);
-                    t_rz = fma(r[v], t[k], t_rz);
-                }
-            }
+            precond(t, 2, t_rr, t_rz);  // Neumann step (P260-298): t = z, with r.r and r.z
             t_rr = warp_sum(t_rr);
             t_rz = warp_sum(t_rz);
             rr = t_rr;
