@@ -138,113 +138,124 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
     };
 
     for (int oc = 0; oc < octs; ++oc) {
-        const int64_t s = ((int64_t)blockIdx.y * octs + oc) * WARP_NW + warp;
-        if (s >= S) break;  // warp-uniform; no block barriers below
-        double x[VPL], t[VPL];  // t holds q = S p, then z = M^{-1} r (disjoint lifetimes)
-        // condensed rhs g_v = W_v + sum_j (c_L/h_e) w_{code_j(v)} (P233-239); x_0 = 0, r = g
-        // a rhs whose squared norm is near the fp64 range limits (e.g. a unit rhs deep inside a long
-        // edge at a mass-dominated node decays to ~1e-300) is solved for g / 2^e with 2^e ~ max|g|:
-        // power-of-two scaling is exact (every PCG quantity scales exactly, alpha and beta are
-        // unchanged) and keeps the dot products away from underflow
-        double gg = 0.0;
-        const double* gs = rhs + rhs_index(s, l, 0, L, V, csl);
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) {
-            const int v = lane + 32 * k;
-            x[k] = 0.0;
-            if (v < V) {
-                const double gv = gs[v];
-                r[v] = gv;
-                gg = fma(gv, gv, gg);
-            }
-        }
-        gg = warp_sum(gg);
-        double sup = 1.0;
-        if (gg > 0.0 && (gg < 0x1p-900 || gg > 0x1p900)) {  // rare: rescale by a power of two (exact)
-            double gmax = 0.0;
-#pragma unroll
+        const int64_t s0 = ((int64_t)blockIdx.y * octs + oc) * WARP_NW;
+        if (s0 >= S) break;  // block-uniform
+        const int64_t s = s0 + warp;
+        if (s < S) {  // warp-uniform; no block barriers inside
+            double x[VPL], t[VPL];  // t holds q = S p, then z = M^{-1} r (disjoint lifetimes)
+            // condensed rhs g_v = W_v + sum_j (c_L/h_e) w_{code_j(v)} (P233-239); x_0 = 0, r = g
+            // a rhs whose squared norm is near the fp64 range limits (e.g. a unit rhs deep inside a long
+            // edge at a mass-dominated node decays to ~1e-300) is solved for g / 2^e with 2^e ~ max|g|:
+            // power-of-two scaling is exact (every PCG quantity scales exactly, alpha and beta are
+            // unchanged) and keeps the dot products away from underflow
+            double gg = 0.0;
+            const double* gs = rhs + rhs_index(s, l, 0, L, V, csl);
+    #pragma unroll
             for (int k = 0; k < VPL; ++k) {
                 const int v = lane + 32 * k;
-                if (v < V) gmax = fmax(gmax, fabs(r[v]));
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
-            int e = 0;
-            frexp(gmax, &e);
-            e = e < -1000 ? -1000 : (e > 1000 ? 1000 : e);
-            const double sdown = ldexp(1.0, -e);
-            sup = ldexp(1.0, e);
-            gg = 0.0;
-#pragma unroll
-            for (int k = 0; k < VPL; ++k) {
-                const int v = lane + 32 * k;
+                x[k] = 0.0;
                 if (v < V) {
-                    const double gv = r[v] * sdown;
+                    const double gv = gs[v];
                     r[v] = gv;
                     gg = fma(gv, gv, gg);
                 }
             }
             gg = warp_sum(gg);
-        }
-        __syncwarp();
-        double d0a = 0.0, d0b = 0.0;
-        precond(t, 0, d0a, d0b);
-        double rz = 0.0;
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) {
-            const int v = lane + 32 * k;
-            if (v < V) {
-                p[v] = t[k];
-                rz = fma(r[v], t[k], rz);
+            double sup = 1.0;
+            if (gg > 0.0 && (gg < 0x1p-900 || gg > 0x1p900)) {  // rare: rescale by a power of two (exact)
+                double gmax = 0.0;
+    #pragma unroll
+                for (int k = 0; k < VPL; ++k) {
+                    const int v = lane + 32 * k;
+                    if (v < V) gmax = fmax(gmax, fabs(r[v]));
+                }
+    #pragma unroll
+                for (int o = 16; o > 0; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+                int e = 0;
+                frexp(gmax, &e);
+                e = e < -1000 ? -1000 : (e > 1000 ? 1000 : e);
+                const double sdown = ldexp(1.0, -e);
+                sup = ldexp(1.0, e);
+                gg = 0.0;
+    #pragma unroll
+                for (int k = 0; k < VPL; ++k) {
+                    const int v = lane + 32 * k;
+                    if (v < V) {
+                        const double gv = r[v] * sdown;
+                        r[v] = gv;
+                        gg = fma(gv, gv, gg);
+                    }
+                }
+                gg = warp_sum(gg);
             }
-        }
-        rz = warp_sum(rz);
-        __syncwarp();
-        const double tol2 = prm.rtol * prm.rtol * gg;
-        bool done = !(gg > 0.0);
-        double rr = gg;
-        int it = 0;
-        while (!done && it < prm.max_iter) {
-            ++it;
-            double pq = 0.0, unused = 0.0;
-            apply(DS, OS, os01, os23, p, t, 1, pq, unused);  // Dirichlet step (P247-258): t = q, pq = p.q
-            pq = warp_sum(pq);
-            if (!(pq > 0.0)) break;  // p = 0 (e.g. an underflowed rhs): nothing left to reduce
-            const double alpha = rz / pq;
-#pragma unroll
+            __syncwarp();
+            double d0a = 0.0, d0b = 0.0;
+            precond(t, 0, d0a, d0b);
+            double rz = 0.0;
+    #pragma unroll
             for (int k = 0; k < VPL; ++k) {
                 const int v = lane + 32 * k;
                 if (v < V) {
-                    x[k] = fma(alpha, p[v], x[k]);
-                    r[v] = fma(-alpha, t[k], r[v]);
+                    p[v] = t[k];
+                    rz = fma(r[v], t[k], rz);
                 }
             }
+            rz = warp_sum(rz);
             __syncwarp();
-            double t_rr = 0.0, t_rz = 0.0;
-            precond(t, 2, t_rr, t_rz);  // Neumann step (P260-298): t = z, with r.r and r.z
-            t_rr = warp_sum(t_rr);
-            t_rz = warp_sum(t_rz);
-            rr = t_rr;
-            if (t_rr <= tol2) break;
-            const double beta = t_rz / rz;
-            rz = t_rz;
-#pragma unroll
-            for (int k = 0; k < VPL; ++k) {
-                const int v = lane + 32 * k;
-                if (v < V) p[v] = fma(beta, p[v], t[k]);
+            const double tol2 = prm.rtol * prm.rtol * gg;
+            bool done = !(gg > 0.0);
+            double rr = gg;
+            int it = 0;
+            while (!done && it < prm.max_iter) {
+                ++it;
+                double pq = 0.0, unused = 0.0;
+                apply(DS, OS, os01, os23, p, t, 1, pq, unused);  // Dirichlet step (P247-258): t = q, pq = p.q
+                pq = warp_sum(pq);
+                if (!(pq > 0.0)) break;  // p = 0 (e.g. an underflowed rhs): nothing left to reduce
+                const double alpha = rz / pq;
+    #pragma unroll
+                for (int k = 0; k < VPL; ++k) {
+                    const int v = lane + 32 * k;
+                    if (v < V) {
+                        x[k] = fma(alpha, p[v], x[k]);
+                        r[v] = fma(-alpha, t[k], r[v]);
+                    }
+                }
+                __syncwarp();
+                double t_rr = 0.0, t_rz = 0.0;
+                precond(t, 2, t_rr, t_rz);  // Neumann step (P260-298): t = z, with r.r and r.z
+                t_rr = warp_sum(t_rr);
+                t_rz = warp_sum(t_rz);
+                rr = t_rr;
+                if (t_rr <= tol2) break;
+                const double beta = t_rz / rz;
+                rz = t_rz;
+    #pragma unroll
+                for (int k = 0; k < VPL; ++k) {
+                    const int v = lane + 32 * k;
+                    if (v < V) p[v] = fma(beta, p[v], t[k]);
+                }
+                __syncwarp();
             }
             __syncwarp();
+    #pragma unroll
+            for (int k = 0; k < VPL; ++k) {  // u_G of this system parked in r (free now)
+                const int v = lane + 32 * k;
+                if (v < V) r[v] = x[k] * sup;
+            }
+            if (lane == 0) {
+                iters[s * L + l] = it;
+                relres[s * L + l] = gg > 0.0 ? sqrt(rr / gg) : 0.0;
+            }
         }
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) {
-            const int v = lane + 32 * k;
-            if (v < V) uG[ug_index(s, v, l, L, V, csl)] = x[k] * sup;
+        __syncthreads();
+        // the octet's 8 samples are consecutive slots of one sample tile: write u_G [tile][v][l][cs]
+        // as 64-byte runs (vertex-major, sample fastest) instead of 8-byte scatters
+        for (int i = threadIdx.x; i < V * WARP_NW; i += WARP_NW * 32) {
+            const int v = i / WARP_NW, w = i % WARP_NW;
+            if (s0 + w < S) uG[ug_index(s0 + w, v, l, L, V, csl)] = sm[(size_t)w * 2 * V + v];
         }
-        if (lane == 0) {
-            iters[s * L + l] = it;
-            relres[s * L + l] = gg > 0.0 ? sqrt(rr / gg) : 0.0;
-        }
-        __syncwarp();  // r / p are rewritten by the next octet
+        __syncthreads();  // r / p are rewritten by the next octet
     }
 }
 
