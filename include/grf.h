@@ -190,7 +190,12 @@ grf_status grf_sample(grf_graph* g, double kappa, double beta, double k, uint64_
                       void* workspace, size_t ws_bytes, void* stream, grf_stats* stats);
 
 /* Same as grf_sample with HOST output u_host (n_samples x N): device staging,
- * device->host copy and a stream synchronisation happen inside the call. */
+ * device->host copy and a stream synchronisation happen inside the call.  For n_samples >= 64
+ * the samples are computed in chunks (multiples of 32, about eight per call, the last one taking
+ * the remainder) whose device->host copies overlap the next chunk's computation on an internal
+ * stream; the field is bitwise the one-call field (chunk c uses seed + its first sample index,
+ * the noise stream's per-sample key, and the same kernel variants).  Page-locked u_host lets the
+ * copies run asynchronously. */
 grf_status grf_sample_host(grf_graph* g, double kappa, double beta, double k, uint64_t seed,
                            int64_t n_samples, const grf_options* opt, double* u_host,
                            void* stream, grf_stats* stats);

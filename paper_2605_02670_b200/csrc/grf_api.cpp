@@ -867,17 +867,83 @@ grf_status grf_sample_host(grf_graph* g, double kappa, double beta, double k, ui
     if (st) return st;
     if (!u_host) return fail(GRF_EINVAL, "u_host is NULL");
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t ubytes = (size_t)n_samples * g->N * sizeof(double);
-    void* du = g->alloc.get(ubytes, s);
-    if (!du) return fail(GRF_ENOMEM, "staging buffer of %zu bytes could not be allocated", ubytes);
-    st = grf_sample(g, kappa, beta, k, seed, n_samples, opt, (double*)du, nullptr, 0, s, stats);
-    if (st == GRF_OK || st == GRF_ENOCONV) {
-        cudaError_t ce = cudaMemcpyAsync(u_host, du, ubytes, cudaMemcpyDeviceToHost, s);
-        if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+    // Sample chunks of a multiple of 32 (about eight per call; the last one also takes the
+    // remainder, so every chunk runs the same kernel variants as the whole call and the field is
+    // bitwise the one-call field): chunk c's device->host copy runs on a second stream while chunk
+    // c+1 is computed; two device staging buffers alternate.  Chunk c draws samples [c0, c0 + n_c)
+    // with seed + c0, so its noise is that of the same samples in one call (key = seed + sample
+    // index, noise.cu).
+    const int64_t chunk = n_samples >= 64 ? std::max<int64_t>(32, ((n_samples / 8 + 31) / 32) * 32) : n_samples;
+    const int64_t n_chunks = n_samples / chunk;
+    const int64_t max_chunk = n_samples - (n_chunks - 1) * chunk;
+    const size_t cbytes = (size_t)max_chunk * g->N * sizeof(double);
+    void* du[2] = {g->alloc.get(cbytes, s), n_chunks > 1 ? g->alloc.get(cbytes, s) : nullptr};
+    if (!du[0] || (n_chunks > 1 && !du[1])) {
+        if (du[0]) g->alloc.put(du[0], cbytes, s);
+        if (du[1]) g->alloc.put(du[1], cbytes, s);
+        return fail(GRF_ENOMEM, "staging buffers of 2 x %zu bytes could not be allocated", cbytes);
+    }
+    cudaStream_t cs = nullptr;
+    cudaEvent_t done[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
+    cudaError_t ce = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    for (int b = 0; b < 2 && ce == cudaSuccess; ++b) {
+        ce = cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming);
+        if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming);
+    }
+    grf_stats tot{};
+    double iter_sum = 0.0;
+    bool enoconv = false;
+    if (ce != cudaSuccess) st = fail(GRF_ECUDA, "copy stream / events: %s", cudaGetErrorString(ce));
+    for (int64_t c = 0; c < n_chunks && st == GRF_OK; ++c) {
+        const int b = (int)(c & 1);
+        const int64_t c0 = c * chunk, nc = c + 1 < n_chunks ? chunk : n_samples - c0;
+        if (c >= 2) cudaStreamWaitEvent(s, copied[b], 0);  // staging buffer b has been copied out
+        grf_stats cst{};
+        grf_status sc = grf_sample(g, kappa, beta, k, seed + (uint64_t)c0, nc, opt, (double*)du[b], nullptr, 0, s,
+                                   stats ? &cst : nullptr);
+        if (sc == GRF_ENOCONV) {
+            enoconv = true;
+        } else if (sc != GRF_OK) {
+            st = sc;
+            break;
+        }
+        ce = cudaEventRecord(done[b], s);
+        if (ce == cudaSuccess) ce = cudaStreamWaitEvent(cs, done[b], 0);
+        if (ce == cudaSuccess)
+            ce = cudaMemcpyAsync(u_host + c0 * g->N, du[b], (size_t)nc * g->N * sizeof(double), cudaMemcpyDeviceToHost,
+                                 cs);
+        if (ce == cudaSuccess) ce = cudaEventRecord(copied[b], cs);
         if (ce != cudaSuccess) st = fail(GRF_ECUDA, "device->host copy: %s", cudaGetErrorString(ce));
+        if (stats) {
+            if (c == 0) {
+                tot = cst;
+            } else {
+                tot.n_systems += cst.n_systems;
+                tot.n_unconverged += cst.n_unconverged;
+                tot.iter_min = std::min(tot.iter_min, cst.iter_min);
+                tot.iter_max = std::max(tot.iter_max, cst.iter_max);
+                tot.worst_rel_residual = std::max(tot.worst_rel_residual, cst.worst_rel_residual);
+                tot.gpu_launches += cst.gpu_launches;
+            }
+            iter_sum += cst.iter_mean * (double)cst.n_systems;
+        }
+    }
+    if (cs) {
+        ce = cudaStreamSynchronize(cs);
+        if (ce != cudaSuccess && st == GRF_OK) st = fail(GRF_ECUDA, "device->host copy: %s", cudaGetErrorString(ce));
     }
     cudaStreamSynchronize(s);
-    g->alloc.put(du, ubytes, s);
+    for (int b = 0; b < 2; ++b) {
+        if (done[b]) cudaEventDestroy(done[b]);
+        if (copied[b]) cudaEventDestroy(copied[b]);
+        if (du[b]) g->alloc.put(du[b], cbytes, s);
+    }
+    if (cs) cudaStreamDestroy(cs);
+    if (stats && st == GRF_OK) {
+        tot.iter_mean = tot.n_systems > 0 ? iter_sum / (double)tot.n_systems : 0.0;
+        *stats = tot;
+    }
+    if (st == GRF_OK && enoconv) return GRF_ENOCONV;
     return st;
 }
 

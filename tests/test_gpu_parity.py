@@ -190,12 +190,17 @@ def test_node_range_partial_sums_add_up():
     assert _rel(parts, full).max() <= 1e-13
 
 
-def test_host_output_matches_device():
+@pytest.mark.parametrize("n_samples", [2, 100, 256])
+def test_host_output_matches_device(n_samples):
+    # n_samples >= 64 runs grf_sample_host in overlapped chunks (32 / 32 / 36 and 8 x 32):
+    # every chunk reseeds with seed + its first sample, so the field is bitwise the one-call field
     g = lattice(3, seed=8)
     G = _graph(g, 0.05)
-    a = G.sample(2.0, 0.6, 0.3, seed=0, n_samples=2).cpu().numpy()
-    b = G.sample_host(2.0, 0.6, 0.3, seed=0, n_samples=2)
+    a = G.sample(2.0, 0.6, 0.3, seed=7, n_samples=n_samples).cpu().numpy()
+    b, st = G.sample_host(2.0, 0.6, 0.3, seed=7, n_samples=n_samples, return_stats=True)
     assert np.array_equal(_bits(a), _bits(b))
+    assert st["n_systems"] == n_samples * st["n_nodes"]
+    assert st["worst_rel_residual"] <= 1e-13
 
 
 def test_invalid_arguments():
