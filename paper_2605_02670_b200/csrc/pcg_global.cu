@@ -59,7 +59,7 @@ struct GArgs {
 // vertices, so a thread keeps only scalars (small register footprint, many resident warps
 // for the latency of the neighbour gathers), and the CS threads of a vertex read one
 // contiguous CS-double run of each vector and share the vertex's operator coefficients.
-constexpr int VPI_MAX = 256;  // vertices per item (at most): per-node partials have ceil(V / vpi) rows
+constexpr int VPI_MAX = 512;  // vertices per item (at most): per-node partials have ceil(V / vpi) rows
 
 // Reduce K per-thread values over the CTA's vertices into part[l][vb][k][s]; the last CTA of
 // node l to arrive reduces the node's rows (columns in parallel, each in fixed order) and runs
@@ -255,8 +255,8 @@ __global__ void __launch_bounds__(GT, 6) pcg_global_kernel(GArgs A) {
                     const int ob = ops_other(g, k) * CS + s;
                     qv = fma(tab[3 * (int64_t)V + k], fma(bt, po_l[ob], z_l[ob]), qv);
                 }
-                pn_l[e] = pv;
-                q_l[e] = qv;
+                __stcs(pn_l + e, pv);  // streaming stores: keep L2 for the neighbour gathers
+                __stcs(q_l + e, qv);
                 acc[0] = fma(pv, qv, acc[0]);
             }
             block_partials<CS, 1>(A, l, vb, nvb, acc, red, [&](int ln, const double* tot) {
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(GT, 6) pcg_global_kernel(GArgs A) {
                 if (v < 0) continue;
                 const int e = v * CS + s;  // offset within node l's [V][CS] slab (32-bit)
                 const double rv = fma(-al, q_l[e], ro_l[e]);
-                x_l[e] = fma(al, pn_l[e], x_l[e]);
+                __stcs(x_l + e, fma(al, pn_l[e], x_l[e]));
                 double zv;
                 if (A.prm.precond == 0) {
                     zv = tab[V + v] * rv;
@@ -302,8 +302,8 @@ __global__ void __launch_bounds__(GT, 6) pcg_global_kernel(GArgs A) {
                 } else {
                     zv = (A.prm.precond == 1 ? tab[2 * V + v] : 1.0) * rv;
                 }
-                rn_l[e] = rv;
-                z_l[e] = zv;
+                __stcs(rn_l + e, rv);
+                __stcs(z_l + e, zv);
                 acc[0] = fma(rv, rv, acc[0]);
                 acc[1] = fma(rv, zv, acc[1]);
             }
