@@ -233,7 +233,8 @@ grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf
     double* gam = (double*)grab(tab);
     double* sig = (double*)grab((size_t)L * g->E * 4 * sizeof(double));
     double* ops = (double*)grab((size_t)L * grf::pcg_table_doubles(g->dev) * sizeof(double));
-    if (!dcI || !dcL || !mu || !gam || !sig || !ops) {
+    double* ops_pos = (double*)grab((size_t)L * (3 * (size_t)g->dev.V + 4 * (size_t)g->dev.E) * sizeof(double));
+    if (!dcI || !dcL || !mu || !gam || !sig || !ops || !ops_pos) {
         for (auto& b : p->blocks) g->alloc.put(b.p, b.bytes, st);
         return fail(GRF_ENOMEM, "plan tables (%.1f MB) could not be allocated",
                     (double)(2 * tab + (size_t)L * g->E * 32) / 1e6);
@@ -252,9 +253,11 @@ grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf
     p->dev.gam = gam;
     p->dev.sig = sig;
     p->dev.ops = ops;
+    p->dev.ops_pos = ops_pos;
     CUDA_TRY(g->timed(GRF_K_EDGE_SETUP, st, [&] {
         grf::launch_edge_setup(g->dev, p->dev, st);
         grf::launch_pcg_tables(g->dev, p->dev, st);
+        grf::launch_pcg_tables_pos(g->dev, p->dev, st);
     }));
     CUDA_TRY(cudaStreamSynchronize(st));  // host vectors cI/cL die at return
     // keep at most 4 plans
@@ -662,6 +665,35 @@ grf_status create_impl(int64_t n_vertices, int64_t n_edges, const int64_t* edge_
         owner[v] = inc[ptr[v]];
         inv_deg[v] = 1.0 / (double)(part ? part->vertex_degree[v] : deg[v]);  // GLOBAL d_v (P261)
     }
+    // breadth-first vertex positions (each component from its lowest-numbered vertex) and the
+    // incidence lists in that order, for the global-memory PCG
+    std::vector<int32_t> vorder, vpos(V, -1), gp_ptr(V + 1, 0), gp_other(std::max<int64_t>(2 * E, 1)),
+        gp_code(std::max<int64_t>(2 * E, 1));
+    vorder.reserve(V);
+    for (int64_t r = 0; r < V; ++r) {
+        if (vpos[r] >= 0) continue;
+        size_t head = vorder.size();
+        vpos[r] = (int32_t)vorder.size();
+        vorder.push_back((int32_t)r);
+        while (head < vorder.size()) {
+            const int32_t v = vorder[head++];
+            for (int32_t k = ptr[v]; k < ptr[v + 1]; ++k) {
+                const int32_t o = other[k];
+                if (vpos[o] < 0) {
+                    vpos[o] = (int32_t)vorder.size();
+                    vorder.push_back(o);
+                }
+            }
+        }
+    }
+    for (int64_t q = 0; q < V; ++q) {
+        const int32_t v = vorder[q];
+        gp_ptr[q + 1] = gp_ptr[q] + (ptr[v + 1] - ptr[v]);
+        for (int32_t k = ptr[v]; k < ptr[v + 1]; ++k) {
+            gp_other[gp_ptr[q] + (k - ptr[v])] = vpos[other[k]];
+            gp_code[gp_ptr[q] + (k - ptr[v])] = inc[k];
+        }
+    }
     std::vector<int32_t> order(E);
     for (int64_t e = 0; e < E; ++e) order[e] = (int32_t)e;
     std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return mm[a] > mm[b]; });
@@ -689,6 +721,10 @@ grf_status create_impl(int64_t n_vertices, int64_t n_edges, const int64_t* edge_
     if (!st) d.inc = g->upload(inc, &st);
     if (!st) d.inc_other = g->upload(other, &st);
     if (!st) d.inv_deg = g->upload(inv_deg, &st);
+    if (!st) d.vorder = g->upload(vorder, &st);
+    if (!st) d.gp_ptr = g->upload(gp_ptr, &st);
+    if (!st) d.gp_other = g->upload(gp_other, &st);
+    if (!st) d.gp_code = g->upload(gp_code, &st);
     if (!st) d.owner = g->upload(owner, &st);
     if (!st) d.sqrt_ml = g->upload(sq, &st);
     if (!st) d.ml = g->upload(g->ml, &st);

@@ -28,6 +28,12 @@ struct DevGraph {
     const double* ml = nullptr;       // [N] lumped mass diagonal of this mesh
     const int32_t* dof_edge = nullptr; // [NI] edge of each interior DOF
     const int32_t* edge_order = nullptr; // [E] edges by descending interior length (work-queue order)
+    // breadth-first vertex positions for the global-memory PCG (pcg_global.cu): its vectors and
+    // tables are stored in this order so that a vertex's neighbours sit close by (L2 reuse)
+    const int32_t* vorder = nullptr;  // [V] position -> vertex
+    const int32_t* gp_ptr = nullptr;  // [V+1] incidence list of the vertex at each position
+    const int32_t* gp_other = nullptr; // [2E] position of the other endpoint
+    const int32_t* gp_code = nullptr; // [2E] incidence code 2e+end
     // Thomas tables depend on an edge only through (m_e, h_e): edges with identical meshes share
     // one set of table rows (config 5: all 3848 edges share one).
     int64_t NT = 0;                   // table rows (sum of m_e over distinct (m_e, h_e))
@@ -72,7 +78,8 @@ struct DevPlan {
     double* mu = nullptr;             // [NT * Lp] Thomas multipliers  b/d'_{t-1}, layout [(toff_e + t) * Lp + l]
     double* gam = nullptr;            // [NT * Lp] diag of A_II^{-1}: 1/(d'_t + d'_{m+1-t} - a); 0 for l >= L
     double* sig = nullptr;            // [L * E * 4]: (s_d, s_o, p_d, p_o) local Schur + its inverse
-    double* ops = nullptr;            // [L * (3V + 4E)]: per-node CSR tables of S and M^{-1} (pcg.cu)
+    double* ops = nullptr;            // per-node tables of S and M^{-1} (pcg.cu, ops_stride)
+    double* ops_pos = nullptr;        // [L * (3V + 4E)]: the same in breadth-first positions (pcg_global.cu)
 };
 
 struct PcgParams {
@@ -124,6 +131,7 @@ void launch_assemble_rhs(const DevGraph& g, const DevPlan& p, int64_t n_samples,
                          double* rhs, cudaStream_t st);
 // K4 global-memory variant (pcg_global.cu) and its workspace
 bool pcg_shared_ok(const DevGraph& g);
+void launch_pcg_tables_pos(const DevGraph& g, const DevPlan& p, cudaStream_t st);
 cudaError_t launch_pcg_global(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm,
                               const double* rhs, double* uG, int32_t* iters, double* relres, void* ws,
                               cudaStream_t st);

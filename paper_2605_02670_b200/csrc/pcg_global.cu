@@ -3,10 +3,13 @@
 // per-node tables DS/OS (Dirichlet step) and DM/OM (Neumann step) of pcg_tables_kernel).
 //
 // One cooperative persistent launch per sample tile of CS samples solves all L x CS systems
-// (l, s) of the tile together.  Work vectors are node-major, vertex, then sample:
-// vec[(l * V + v) * CS + s], so a thread owning vertex v of node l holds the CS samples in
-// registers, reads each operator coefficient once for all of them, and every neighbour
-// gather is one contiguous CS-double run.  Per iteration two phases separated by grid
+// (l, s) of the tile together.  Vertices are handled in breadth-first POSITIONS p (g.vorder,
+// built at graph creation): work vectors are node-major, position, then sample:
+// vec[(l * V + p) * CS + s], and the operator tables ops_pos are position-ordered CSR
+// [DS (V) | DM (V) | DJ (V) | OS (2E) | OM (2E)] per node, so the CS threads of a vertex share
+// its coefficients, every neighbour gather is one contiguous CS-double run, and a vertex's
+// neighbours lie at nearby positions (their rows are reused from L2 instead of HBM).  Only
+// the rhs read and the u_G write map positions back to vertices.  Per iteration two phases separated by grid
 // barriers (standard PCG, fused so that each vector is streamed once per phase):
 //   phase 1:  p' = z + beta p;  q = S p'  (neighbour p' formed on the fly from z, p);  p'.q
 //   phase 2:  r' = r - alpha q;  x += alpha p';  z = M^{-1} r' (neighbour r' on the fly);
@@ -32,7 +35,7 @@ constexpr int GT = 256;  // threads per CTA = vertices per item
 struct GArgs {
     DevGraph g;
     int32_t L;
-    const double* ops;
+    const double* ops;    // ops_pos (position-ordered CSR tables)
     PcgParams prm;
     int64_t S;
     int32_t csl;
@@ -122,15 +125,15 @@ __global__ void __launch_bounds__(GT, 6) pcg_global_kernel(GArgs A) {
     __shared__ double red[RED];
     const DevGraph& g = A.g;
     const int V = g.V, L = A.L;
-    const int64_t ns = ops_nslots(g);
+    const int64_t E2 = 2 * (int64_t)g.E;
     const int VPI = A.vpi;
     const int nvb = (V + VPI - 1) / VPI;
     const int tid = threadIdx.x, s = tid % CS, vl = tid / CS;
-    const int64_t stride = ops_stride(g);
+    const int64_t stride = 3 * (int64_t)V + 2 * E2;  // position table per node
     const int64_t s0 = A.tile << A.csl;
     double *po, *pn, *ro, *rn;
     const double tol2c = A.prm.rtol * A.prm.rtol;
-    auto deg_of = [&](int v) { return g.inc_ptr[v + 1] - g.inc_ptr[v]; };
+
     // the vertex of sub-chunk c of item vb for this thread (or V: none)
     auto vert = [&](int vb, int c) { const int v = vb * VPI + c * VBK + vl; return v < V ? v : -1; };
 
@@ -162,7 +165,7 @@ __global__ void __launch_bounds__(GT, 6) pcg_global_kernel(GArgs A) {
             if (v < 0) continue;
             const int e = v * CS + s;  // offset within node l's [V][CS] slab (32-bit)
             const int64_t sg = s0 + s;
-            const double gv = sg < A.S ? A.rhs[rhs_index(sg, l, v, L, V, A.csl)] : 0.0;
+            const double gv = sg < A.S ? A.rhs[rhs_index(sg, l, g.vorder[v], L, V, A.csl)] : 0.0;
             ro_l[e] = gv;
             x_l[e] = 0.0;
             po_l[e] = 0.0;
@@ -202,11 +205,8 @@ __global__ void __launch_bounds__(GT, 6) pcg_global_kernel(GArgs A) {
             double zv;
             if (A.prm.precond == 0) {
                 zv = tab[V + v] * rv;
-                const int dg = deg_of(v);
-                for (int j = 0; j < dg; ++j) {
-                    const int64_t k = ops_slot(g, v, j);
-                    zv = fma(tab[3 * (int64_t)V + ns + k], ro_l[ops_other(g, k) * CS + s], zv);
-                }
+                for (int k = g.gp_ptr[v]; k < g.gp_ptr[v + 1]; ++k)
+                    zv = fma(tab[3 * (int64_t)V + E2 + k], ro_l[g.gp_other[k] * CS + s], zv);
             } else {
                 zv = (A.prm.precond == 1 ? tab[2 * V + v] : 1.0) * rv;
             }
@@ -249,10 +249,8 @@ __global__ void __launch_bounds__(GT, 6) pcg_global_kernel(GArgs A) {
                 const int e = v * CS + s;  // offset within node l's [V][CS] slab (32-bit)
                 const double pv = fma(bt, po_l[e], z_l[e]);
                 double qv = tab[v] * pv;
-                const int dg = deg_of(v);
-                for (int j = 0; j < dg; ++j) {
-                    const int64_t k = ops_slot(g, v, j);
-                    const int ob = ops_other(g, k) * CS + s;
+                for (int k = g.gp_ptr[v]; k < g.gp_ptr[v + 1]; ++k) {
+                    const int ob = g.gp_other[k] * CS + s;
                     qv = fma(tab[3 * (int64_t)V + k], fma(bt, po_l[ob], z_l[ob]), qv);
                 }
                 __stcs(pn_l + e, pv);  // streaming stores: keep L2 for the neighbour gathers
@@ -293,11 +291,9 @@ __global__ void __launch_bounds__(GT, 6) pcg_global_kernel(GArgs A) {
                 double zv;
                 if (A.prm.precond == 0) {
                     zv = tab[V + v] * rv;
-                    const int dg = deg_of(v);
-                    for (int j = 0; j < dg; ++j) {
-                        const int64_t k = ops_slot(g, v, j);
-                        const int ob = ops_other(g, k) * CS + s;
-                        zv = fma(tab[3 * (int64_t)V + ns + k], fma(-al, q_l[ob], ro_l[ob]), zv);
+                    for (int k = g.gp_ptr[v]; k < g.gp_ptr[v + 1]; ++k) {
+                        const int ob = g.gp_other[k] * CS + s;
+                        zv = fma(tab[3 * (int64_t)V + E2 + k], fma(-al, q_l[ob], ro_l[ob]), zv);
                     }
                 } else {
                     zv = (A.prm.precond == 1 ? tab[2 * V + v] : 1.0) * rv;
@@ -347,7 +343,7 @@ __global__ void __launch_bounds__(GT, 6) pcg_global_kernel(GArgs A) {
         for (int c = 0; c < VPI / VBK; ++c) {
             const int v = vert(vb, c);
             if (v < 0 || sg >= A.S) continue;
-            A.uG[ug_index(sg, v, l, L, V, A.csl)] = A.x[((int64_t)l * V) * CS + v * CS + s];
+            A.uG[ug_index(sg, g.vorder[v], l, L, V, A.csl)] = A.x[((int64_t)l * V) * CS + v * CS + s];
         }
         if (vb == 0 && tid < CS && s0 + tid < A.S) {
             const int sy = l * CS + tid;
@@ -390,7 +386,44 @@ cudaError_t launch_cs(GArgs a, int64_t n_tiles, cudaStream_t st) {
     return cudaSuccess;
 }
 
+// Position-ordered CSR tables of the two PCG operators (same values as pcg_tables_kernel in
+// pcg.cu, P247-298): DS_p = sum of the incident local Schur diagonals, OS_k = their off-diagonal,
+// DM_p = sum of the inverse blocks' diagonals / d_v^2, OM_k = off-diagonal / (d_v d_o), DJ = 1/diag S.
+__global__ void pcg_tables_pos_kernel(DevGraph g, int32_t L, const double4* __restrict__ sig, double* __restrict__ ops) {
+    const int V = g.V, E = g.E;
+    const int64_t E2 = 2 * (int64_t)E, stride = 3 * (int64_t)V + 2 * E2;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < (int64_t)L * V;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int l = (int)(x / V), p = (int)(x - (int64_t)l * V);
+        const int v = g.vorder[p];
+        const double4* sg = sig + (int64_t)l * E;
+        double* t = ops + l * stride;
+        const double idv = g.inv_deg[v];
+        double ds = 0.0, dm = 0.0, diag = 0.0;
+        for (int k = g.gp_ptr[p]; k < g.gp_ptr[p + 1]; ++k) {
+            const double4 c = sg[g.gp_code[k] >> 1];
+            const int op = g.gp_other[k];
+            ds += c.x;
+            dm += c.z;
+            t[3 * (int64_t)V + k] = c.y;
+            t[3 * (int64_t)V + E2 + k] = c.w * idv * g.inv_deg[g.vorder[op]];
+            diag += c.x + (op == p ? c.y : 0.0);
+        }
+        t[p] = ds;
+        t[V + p] = dm * idv * idv;
+        t[2 * V + p] = 1.0 / diag;
+    }
+}
+
 }  // namespace
+
+void launch_pcg_tables_pos(const DevGraph& g, const DevPlan& p, cudaStream_t st) {
+    const int64_t n = (int64_t)p.L * g.V;
+    if (n == 0) return;
+    int blocks = (int)((n + 255) / 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    pcg_tables_pos_kernel<<<blocks, 256, 0, st>>>(g, p.L, reinterpret_cast<const double4*>(p.sig), p.ops_pos);
+}
 
 size_t pcg_global_ws_bytes(const DevGraph& g, int32_t L, int64_t n_samples) {
     const int64_t cs = (int64_t)1 << sample_tile_log2(n_samples);
@@ -420,7 +453,7 @@ cudaError_t launch_pcg_global(const DevGraph& g, const DevPlan& p, int64_t n_sam
     GArgs a{};
     a.g = g;
     a.L = p.L;
-    a.ops = p.ops;
+    a.ops = p.ops_pos;
     a.prm = prm;
     a.S = n_samples;
     a.csl = csl;
