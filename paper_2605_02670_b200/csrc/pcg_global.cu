@@ -62,7 +62,7 @@ struct GArgs {
 // vertices, so a thread keeps only scalars (small register footprint, many resident warps
 // for the latency of the neighbour gathers), and the CS threads of a vertex read one
 // contiguous CS-double run of each vector and share the vertex's operator coefficients.
-constexpr int VPI_MAX = 512;  // vertices per item (at most): per-node partials have ceil(V / vpi) rows
+constexpr int VPI_MAX = 256;  // vertices per item (at most): per-node partials have ceil(V / vpi) rows
 
 // Reduce K per-thread values over the CTA's vertices into part[l][vb][k][s]; the last CTA of
 // node l to arrive reduces the node's rows (columns in parallel, each in fixed order) and runs
@@ -114,6 +114,52 @@ __device__ void block_partials(const GArgs& A, int l, int vb, int nvb, const dou
         __syncthreads();
         if (tid == 0) A.cnt[l] = 0;
     }
+    __syncthreads();
+}
+
+// Iteration phases: each item only writes its partial row (no arrival counter); after a grid
+// barrier one CTA per active node reduces the node's rows in the same fixed order as the
+// last-arriving CTA of block_partials does and runs finish(l, totals).
+template <int CS, int K>
+__device__ void item_partials(const GArgs& A, int l, int vb, int nvb, const double (&v)[K], double* red) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double t = v[k];
+#pragma unroll
+        for (int o = 16; o >= CS && o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);  // over vertex lanes
+        if (lane < (CS < 32 ? CS : 32)) red[(warp * K + k) * CS + lane % CS] = t;
+    }
+    __syncthreads();
+    if (tid < K * CS) {
+        const int k = tid / CS, s = tid % CS;
+        double t = 0.0;
+        for (int w = 0; w < GT / 32; ++w) t += red[(w * K + k) * CS + s];
+        A.part[((int64_t)l * nvb + vb) * 2 * CS + tid] = t;
+    }
+    __syncthreads();  // red is reused by the next item
+}
+
+template <int CS, int K, class Finish>
+__device__ void node_reduce(const GArgs& A, int l, int nvb, double* red, Finish&& finish) {
+    const int tid = threadIdx.x;
+    constexpr int NCOL = K * CS;
+    constexpr int TPC = GT / NCOL;
+    const int col = tid / TPC, sub = tid % TPC;
+    double t = 0.0;
+    if (col < NCOL) {
+        const double* pc = A.part + (int64_t)l * nvb * 2 * CS + col;
+        for (int b = sub; b < nvb; b += TPC) t += pc[(int64_t)b * 2 * CS];
+    }
+    red[tid] = t;
+    __syncthreads();
+    if (tid < NCOL) {
+        double u = 0.0;
+        for (int q = 0; q < TPC; ++q) u += red[tid * TPC + q];
+        red[GT + tid] = u;
+    }
+    __syncthreads();
+    finish(l, red + GT);
     __syncthreads();
 }
 
@@ -257,7 +303,12 @@ __global__ void __launch_bounds__(GT, 6) pcg_global_kernel(GArgs A) {
                 __stcs(q_l + e, qv);
                 acc[0] = fma(pv, qv, acc[0]);
             }
-            block_partials<CS, 1>(A, l, vb, nvb, acc, red, [&](int ln, const double* tot) {
+            item_partials<CS, 1>(A, l, vb, nvb, acc, red);
+        }
+        grid.sync();
+        for (int l = l0 + blockIdx.x; l < l0 + lg; l += gridDim.x) {
+            if (!A.node_active[l]) continue;  // block-uniform
+            node_reduce<CS, 1>(A, l, nvb, red, [&](int ln, const double* tot) {
                 if (tid < CS) {
                     const double pq = tot[tid];
                     if (!(pq > 0.0)) A.done[ln * CS + tid] = 1;  // p = 0 (underflowed rhs)
@@ -303,7 +354,12 @@ __global__ void __launch_bounds__(GT, 6) pcg_global_kernel(GArgs A) {
                 acc[0] = fma(rv, rv, acc[0]);
                 acc[1] = fma(rv, zv, acc[1]);
             }
-            block_partials<CS, 2>(A, l, vb, nvb, acc, red, [&](int ln, const double* tot) {
+            item_partials<CS, 2>(A, l, vb, nvb, acc, red);
+        }
+        grid.sync();
+        for (int l = l0 + blockIdx.x; l < l0 + lg; l += gridDim.x) {
+            if (!A.node_active[l]) continue;  // block-uniform
+            node_reduce<CS, 2>(A, l, nvb, red, [&](int ln, const double* tot) {
                 if (tid < CS) {
                     const int sy = ln * CS + tid;
                     const double rr = tot[tid], rzn = tot[CS + tid];
