@@ -22,7 +22,8 @@ def short(name):
     m = re.search(r"sweep_kernel<[^>]*?(\d)>", name)
     if m:
         return "condense" if m.group(1) == "0" else "recover"
-    for k, v in (("noise_kernel", "noise"), ("edge_setup_kernel", "edge_setup"), ("pcg_tables_kernel", "pcg_tables"),
+    for k, v in (("noise_kernel", "noise"), ("edge_setup_kernel", "edge_setup"), ("pcg_tables_pos_kernel", "pcg_tables_pos"),
+                 ("pcg_tables_kernel", "pcg_tables"),
                  ("assemble_rhs_kernel", "assemble"), ("vertex_sum_kernel", "vertex_sum"),
                  ("pcg_warp_kernel", "pcg"), ("pcg_global_kernel", "pcg"), ("pcg_kernel", "pcg")):
         if k in name:
