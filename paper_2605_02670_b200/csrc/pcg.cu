@@ -226,32 +226,9 @@ __global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L,
         double gg[SB];
 #pragma unroll
         for (int j = 0; j < SB; ++j) gg[j] = 0.0;
-        // ---- condensed rhs g, x = 0, r = g scaled by a power of two (see pcg_warp.cu: exact, and it
-        // keeps the iteration away from underflow for rhs that decayed to ~1e-300)
-        double gmax[SB];
-#pragma unroll
-        for (int j = 0; j < SB; ++j) gmax[j] = 0.0;
-#pragma unroll
-        for (int a = 0; a < VPT; ++a) {
-            const int v = gt + a * GT;
-            if (v < V) {
-#pragma unroll
-                for (int j = 0; j < SB; ++j) {
-                    const int64_t s = s0 + (j < ns ? j : 0);
-                    gmax[j] = fmax(gmax[j], j < ns ? fabs(rhs[rhs_index(s, l, v, L, V, csl)]) : 0.0);
-                }
-            }
-        }
-        group_max<GT, SB>(gmax, red, flip, bar_id);
-        double sdown[SB], sup[SB];  // exact powers of two
-#pragma unroll
-        for (int j = 0; j < SB; ++j) {
-            int e = 0;
-            if (gmax[j] > 0.0) frexp(gmax[j], &e);
-            e = e < -1000 ? -1000 : (e > 1000 ? 1000 : e);
-            sdown[j] = ldexp(1.0, -e);
-            sup[j] = ldexp(1.0, e);
-        }
+        // ---- condensed rhs g, x = 0, r = g; a rhs whose squared norm is near the fp64 range limits is
+        // rescaled by a power of two (see pcg_warp.cu: exact, and it keeps the iteration away from
+        // underflow for rhs that decayed to ~1e-300) -- a second pass only on that rare path
 #pragma unroll
         for (int a = 0; a < VPT; ++a) {
             const int v = gt + a * GT;
@@ -261,7 +238,7 @@ __global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L,
 #pragma unroll
                 for (int j = 0; j < SB; ++j) {
                     const int64_t s = s0 + (j < ns ? j : 0);
-                    double gv = rhs[rhs_index(s, l, v, L, V, csl)] * sdown[j];
+                    double gv = rhs[rhs_index(s, l, v, L, V, csl)];
                     if (j >= ns) gv = 0.0;
                     r[v * SB + j] = gv;
                     gg[j] += gv * gv;
@@ -269,6 +246,50 @@ __global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L,
             }
         }
         group_sum<GT, SB>(gg, red, flip, bar_id);  // (barrier: r complete)
+        double sup[SB];  // exact powers of two
+        bool rescale = false;
+#pragma unroll
+        for (int j = 0; j < SB; ++j) {
+            sup[j] = 1.0;
+            rescale = rescale || (gg[j] > 0.0 && (gg[j] < 0x1p-900 || gg[j] > 0x1p900));
+        }
+        if (rescale) {  // group-uniform (gg is the group sum)
+            double gmax[SB];
+#pragma unroll
+            for (int j = 0; j < SB; ++j) gmax[j] = 0.0;
+#pragma unroll
+            for (int a = 0; a < VPT; ++a) {
+                const int v = gt + a * GT;
+                if (v < V) {
+#pragma unroll
+                    for (int j = 0; j < SB; ++j) gmax[j] = fmax(gmax[j], fabs(r[v * SB + j]));
+                }
+            }
+            group_max<GT, SB>(gmax, red, flip, bar_id);
+            double sdown[SB];
+#pragma unroll
+            for (int j = 0; j < SB; ++j) {
+                int e = 0;
+                if (gmax[j] > 0.0) frexp(gmax[j], &e);
+                e = e < -1000 ? -1000 : (e > 1000 ? 1000 : e);
+                sdown[j] = ldexp(1.0, -e);
+                sup[j] = ldexp(1.0, e);
+                gg[j] = 0.0;
+            }
+#pragma unroll
+            for (int a = 0; a < VPT; ++a) {
+                const int v = gt + a * GT;
+                if (v < V) {
+#pragma unroll
+                    for (int j = 0; j < SB; ++j) {
+                        const double gv = r[v * SB + j] * sdown[j];
+                        r[v * SB + j] = gv;
+                        gg[j] += gv * gv;
+                    }
+                }
+            }
+            group_sum<GT, SB>(gg, red, flip, bar_id);
+        }
         double rz[SB], tol2[SB], rrj[SB];
         bool done[SB];
         int its[SB];
