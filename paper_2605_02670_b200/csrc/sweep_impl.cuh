@@ -70,6 +70,7 @@ struct Args {
     int32_t chunks;         // sample tiles per edge
     int32_t n_items;        // E * chunks
     int32_t tile_ms;        // recover: max (m | 1) the shared-memory output tile holds (0: none)
+    int32_t nk;             // recover: 1 if slot L is the correction node (edge_setup.cu; one round, L < Lp)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -132,7 +133,7 @@ struct Cfg {
     static_assert((CS & (CS - 1)) == 0, "CS must be a power of two");
 };
 
-template <int TL, int TS, int LW, int NWS, bool REC>
+template <int TL, int TS, int LW, int NWS, bool REC, bool NK>
 __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Args A) {
     using C = Cfg<TL, TS, LW, NWS, REC>;
     constexpr int NWL = C::NWL, SLW = C::SLW, NT = C::NT, CS = C::CS, CSL = C::CSL, NTAB = C::NTAB, RN = C::RN;
@@ -431,7 +432,10 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                         }
                     }
                 } else {
-                    // generic step: left chain gives -g mu Y_{t-1} to position t, right chain g Z to m-1-t
+                    // generic step: left chain gives -g mu Y_{t-1} = g (Y_t - f_t) to position t, right
+                    // chain g Z to m-1-t.  With the correction node (A.nk) the left chain gives g Y_t
+                    // instead (no g*mu product): the node's g_t = -G_t/2 and Y = Z = noise remove the
+                    // sum over nodes of g_t f_t, half through each chain (edge_setup.cu)
                     auto body_mid = [&](int tt, double (&aL)[TS], double (&aR)[TS]) {
                         double wl[TS], wr[TS];
                         load_w(tt, wl, wr);
@@ -439,6 +443,35 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                         const double* rga = cga + tt * RN;
 #pragma unroll
                         for (int j = 0; j < TS; ++j) aL[j] = aR[j] = 0.0;
+                        if (NK) {
+#pragma unroll
+                            for (int q = 0; q < NP; ++q) {
+                                const double2 m2 = *reinterpret_cast<const double2*>(rmu + 2 * lt + 64 * q);
+                                const double2 g2 = *reinterpret_cast<const double2*>(rga + 2 * lt + 64 * q);
+#pragma unroll
+                                for (int j = 0; j < TS; ++j) {
+                                    Y[2 * q][j] = fma(-m2.x, Y[2 * q][j], wl[j]);
+                                    aL[j] = fma(g2.x, Y[2 * q][j], aL[j]);
+                                    Z[2 * q][j] = fma(-m2.x, Z[2 * q][j], wr[j]);
+                                    aR[j] = fma(g2.x, Z[2 * q][j], aR[j]);
+                                    Y[2 * q + 1][j] = fma(-m2.y, Y[2 * q + 1][j], wl[j]);
+                                    aL[j] = fma(g2.y, Y[2 * q + 1][j], aL[j]);
+                                    Z[2 * q + 1][j] = fma(-m2.y, Z[2 * q + 1][j], wr[j]);
+                                    aR[j] = fma(g2.y, Z[2 * q + 1][j], aR[j]);
+                                }
+                            }
+                            if (ODD) {
+                                const double mu = rmu[64 * NP + lt], gg = rga[64 * NP + lt];
+#pragma unroll
+                                for (int j = 0; j < TS; ++j) {
+                                    Y[TL - 1][j] = fma(-mu, Y[TL - 1][j], wl[j]);
+                                    aL[j] = fma(gg, Y[TL - 1][j], aL[j]);
+                                    Z[TL - 1][j] = fma(-mu, Z[TL - 1][j], wr[j]);
+                                    aR[j] = fma(gg, Z[TL - 1][j], aR[j]);
+                                }
+                            }
+                            return;
+                        }
 #pragma unroll
                         for (int q = 0; q < NP; ++q) {
                             const double2 m2 = *reinterpret_cast<const double2*>(rmu + 2 * lt + 64 * q);
@@ -659,7 +692,8 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
 }
 
 // One instance: threads = NT, items = E * ceil(S / CS), persistent CTAs over an atomic queue.
-template <int TL, int TS, int LW, int NWS, bool REC>
+// NK (recover only): the interior steps use the correction-node form (A.nk, edge_setup.cu).
+template <int TL, int TS, int LW, int NWS, bool REC, bool NK>
 cudaError_t launch(Args a, cudaStream_t st) {
     using C = Cfg<TL, TS, LW, NWS, REC>;
     a.chunks = (int32_t)((a.S + C::CS - 1) / C::CS);
@@ -674,17 +708,17 @@ cudaError_t launch(Args a, cudaStream_t st) {
         a.tile_ms = want <= fit ? want : (fit >= 1 ? ((fit - 1) | 1) : 0);
         smem += (size_t)C::CS * a.tile_ms * sizeof(double);
     }
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<TL, TS, LW, NWS, REC>,
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<TL, TS, LW, NWS, REC, NK>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(a.counter, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return e;
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<TL, TS, LW, NWS, REC>, C::NT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<TL, TS, LW, NWS, REC, NK>, C::NT, smem);
     if (per_sm < 1) per_sm = 1;
     int blocks = 148 * per_sm;
     if (blocks > a.n_items) blocks = a.n_items;
-    sweep_kernel<TL, TS, LW, NWS, REC><<<blocks, C::NT, smem, st>>>(a);
+    sweep_kernel<TL, TS, LW, NWS, REC, NK><<<blocks, C::NT, smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -697,22 +731,22 @@ cudaError_t launch(Args a, cudaStream_t st) {
 enum Variant { V0 = 0, V1 = 1, V2 = 2 };
 inline Variant variant_for(int64_t S) { return S >= 17 ? V2 : (S >= 9 ? V1 : V0); }
 
-template <bool REC, int V>
+template <bool REC, int V, bool NK = false>
 cudaError_t launch_v(int tl, Args a, cudaStream_t st) {
     constexpr int TS = V == V0 ? 1 : 4;
     constexpr int LW = V == V0 ? 32 : ((REC && V == V2) ? 4 : 8);
     constexpr int NWS = (V == V2 && !REC) ? 2 : 1;
     switch (tl) {
-        case 1: return launch<1, TS, LW, NWS, REC>(a, st);
-        case 2: return launch<2, TS, LW, NWS, REC>(a, st);
-        case 3: return launch<3, TS, LW, NWS, REC>(a, st);
-        case 4: return launch<4, TS, LW, NWS, REC>(a, st);
-        case 5: return launch<5, TS, LW, NWS, REC>(a, st);
-        case 6: return launch<6, TS, LW, NWS, REC>(a, st);
-        case 7: return launch<7, TS, LW, NWS, REC>(a, st);
-        case 8: return launch<8, TS, LW, NWS, REC>(a, st);
-        case 9: return launch<9, TS, LW, NWS, REC>(a, st);
-        case 10: return launch<10, TS, LW, NWS, REC>(a, st);
+        case 1: return launch<1, TS, LW, NWS, REC, NK>(a, st);
+        case 2: return launch<2, TS, LW, NWS, REC, NK>(a, st);
+        case 3: return launch<3, TS, LW, NWS, REC, NK>(a, st);
+        case 4: return launch<4, TS, LW, NWS, REC, NK>(a, st);
+        case 5: return launch<5, TS, LW, NWS, REC, NK>(a, st);
+        case 6: return launch<6, TS, LW, NWS, REC, NK>(a, st);
+        case 7: return launch<7, TS, LW, NWS, REC, NK>(a, st);
+        case 8: return launch<8, TS, LW, NWS, REC, NK>(a, st);
+        case 9: return launch<9, TS, LW, NWS, REC, NK>(a, st);
+        case 10: return launch<10, TS, LW, NWS, REC, NK>(a, st);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -1,0 +1,9 @@
+// Sweep kernel instances (sweep_impl.cuh): K5 recover with the correction-node interior steps,
+// sample mapping V2, node tiles TL = 1..10.
+#include "sweep_impl.cuh"
+
+namespace grf {
+namespace sweep {
+cudaError_t launch_r2k(int tl, Args a, cudaStream_t st) { return launch_v<true, 2, true>(tl, a, st); }
+}  // namespace sweep
+}  // namespace grf

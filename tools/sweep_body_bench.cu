@@ -7,7 +7,7 @@
 
 constexpr int TL = 7, TS = 4, NP = TL / 2, IB = 8, RN = 32 * TL, CS = 32;
 
-template <bool REC, bool PF>
+template <bool REC, bool PF, bool NK = false>
 __global__ void __launch_bounds__(256) body(double* out, int steps) {
     __shared__ double cmu[IB * RN], cga[IB * RN], wb[IB * 2 * CS];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -53,7 +53,19 @@ __global__ void __launch_bounds__(256) body(double* out, int steps) {
         double aL[TS] = {0, 0, 0, 0}, aR[TS] = {0, 0, 0, 0};
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
-            if (REC) {
+            if (REC && NK) {
+#pragma unroll
+                for (int j = 0; j < TS; ++j) {
+                    Y[2 * q][j] = fma(-m2[q].x, Y[2 * q][j], wl[j]);
+                    aL[j] = fma(g2[q].x, Y[2 * q][j], aL[j]);
+                    Z[2 * q][j] = fma(-m2[q].x, Z[2 * q][j], wr[j]);
+                    aR[j] = fma(g2[q].x, Z[2 * q][j], aR[j]);
+                    Y[2 * q + 1][j] = fma(-m2[q].y, Y[2 * q + 1][j], wl[j]);
+                    aL[j] = fma(g2[q].y, Y[2 * q + 1][j], aL[j]);
+                    Z[2 * q + 1][j] = fma(-m2[q].y, Z[2 * q + 1][j], wr[j]);
+                    aR[j] = fma(g2[q].y, Z[2 * q + 1][j], aR[j]);
+                }
+            } else if (REC) {
                 const double k0 = g2[q].x * m2[q].x, k1 = g2[q].y * m2[q].y;
 #pragma unroll
                 for (int j = 0; j < TS; ++j) {
@@ -78,8 +90,9 @@ __global__ void __launch_bounds__(256) body(double* out, int steps) {
         }
 #pragma unroll
         for (int j = 0; j < TS; ++j) {
-            if (REC) aL[j] = fma(-go * mo, Y[TL - 1][j], aL[j]);
+            if (REC && !NK) aL[j] = fma(-go * mo, Y[TL - 1][j], aL[j]);
             Y[TL - 1][j] = fma(-mo, Y[TL - 1][j], wl[j]);
+            if (REC && NK) aL[j] = fma(go, Y[TL - 1][j], aL[j]);
             Z[TL - 1][j] = fma(-mo, Z[TL - 1][j], wr[j]);
             if (REC) aR[j] = fma(go, Z[TL - 1][j], aR[j]);
         }
@@ -99,7 +112,7 @@ __global__ void __launch_bounds__(256) body(double* out, int steps) {
     if (s == 1234.5) out[tid] = s;
 }
 
-template <bool REC, bool PF>
+template <bool REC, bool PF, bool NK = false>
 void run(double* d, const char* name) {
     const int steps = 20000;
     cudaEvent_t a, b;
@@ -108,7 +121,7 @@ void run(double* d, const char* name) {
     float ms = 0;
     for (int it = 0; it < 2; ++it) {
         cudaEventRecord(a);
-        body<REC, PF><<<148, 256>>>(d, steps);
+        body<REC, PF, NK><<<148, 256>>>(d, steps);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         cudaEventElapsedTime(&ms, a, b);
@@ -126,5 +139,6 @@ int main() {
     run<false, true>(d, "condense-pf");
     run<true, false>(d, "recover");
     run<true, true>(d, "recover-pf");
+    run<true, false, true>(d, "recover-nk");
     return 0;
 }
