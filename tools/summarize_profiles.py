@@ -19,7 +19,7 @@ import re
 
 # kernel -> bench.py bracket name (bench times brackets: pcg = assemble + K4, recover = K5 + vertex sum)
 def short(name):
-    m = re.search(r"sweep_kernel<[^>]*?(\d)>", name)
+    m = re.search(r"sweep_kernel<\s*\d+,\s*\d+,\s*\d+,\s*\d+,\s*(\d)", name)  # the REC argument
     if m:
         return "condense" if m.group(1) == "0" else "recover"
     for k, v in (("noise_kernel", "noise"), ("edge_setup_kernel", "edge_setup"), ("pcg_tables_pos_kernel", "pcg_tables_pos"),
