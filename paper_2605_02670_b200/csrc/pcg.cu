@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L,
     constexpr int NW = GT / 32;
     extern __shared__ double sm[];
     __shared__ double red_all[NG][2 * NW * 2 * SB];
-    const int V = g.V, E = g.E;
+    const int V = g.V;
     const int64_t stride = table_stride(V, W);
     const int l = blockIdx.x;
     const int tid = threadIdx.x;
@@ -180,7 +180,6 @@ __global__ void __launch_bounds__(PCG_THREADS) pcg_kernel(DevGraph g, int32_t L,
     const double* DJ = DM + V;
     const double* OS = DJ + V;
     const double* OM = OS + (size_t)W * V;
-    const double* GK = OM + (size_t)W * V;
 
     // y = D x + sum_j O_j x_{o_j} over the owner's vertices, for SB samples (x = r or p in smem)
     auto apply = [&](const double* D, const double* O, const double* xs, double (&y)[VPT][SB]) {

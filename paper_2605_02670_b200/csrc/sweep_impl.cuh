@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                         const double* rga = cga + tt * RN;
 #pragma unroll
                         for (int j = 0; j < TS; ++j) aL[j] = aR[j] = 0.0;
-                        if (NK) {
+                        if constexpr (NK) {
 #pragma unroll
                             for (int q = 0; q < NP; ++q) {
                                 const double2 m2 = *reinterpret_cast<const double2*>(rmu + 2 * lt + 64 * q);
@@ -470,34 +470,34 @@ __global__ void __launch_bounds__(Cfg<TL, TS, LW, NWS, REC>::NT) sweep_kernel(Ar
                                     aR[j] = fma(gg, Z[TL - 1][j], aR[j]);
                                 }
                             }
-                            return;
-                        }
+                        } else {
 #pragma unroll
-                        for (int q = 0; q < NP; ++q) {
-                            const double2 m2 = *reinterpret_cast<const double2*>(rmu + 2 * lt + 64 * q);
-                            const double2 g2 = *reinterpret_cast<const double2*>(rga + 2 * lt + 64 * q);
-                            const double k0 = g2.x * m2.x, k1 = g2.y * m2.y;
+                            for (int q = 0; q < NP; ++q) {
+                                const double2 m2 = *reinterpret_cast<const double2*>(rmu + 2 * lt + 64 * q);
+                                const double2 g2 = *reinterpret_cast<const double2*>(rga + 2 * lt + 64 * q);
+                                const double k0 = g2.x * m2.x, k1 = g2.y * m2.y;
 #pragma unroll
-                            for (int j = 0; j < TS; ++j) {
-                                aL[j] = fma(-k0, Y[2 * q][j], aL[j]);
-                                Y[2 * q][j] = fma(-m2.x, Y[2 * q][j], wl[j]);
-                                Z[2 * q][j] = fma(-m2.x, Z[2 * q][j], wr[j]);
-                                aR[j] = fma(g2.x, Z[2 * q][j], aR[j]);
-                                aL[j] = fma(-k1, Y[2 * q + 1][j], aL[j]);
-                                Y[2 * q + 1][j] = fma(-m2.y, Y[2 * q + 1][j], wl[j]);
-                                Z[2 * q + 1][j] = fma(-m2.y, Z[2 * q + 1][j], wr[j]);
-                                aR[j] = fma(g2.y, Z[2 * q + 1][j], aR[j]);
+                                for (int j = 0; j < TS; ++j) {
+                                    aL[j] = fma(-k0, Y[2 * q][j], aL[j]);
+                                    Y[2 * q][j] = fma(-m2.x, Y[2 * q][j], wl[j]);
+                                    Z[2 * q][j] = fma(-m2.x, Z[2 * q][j], wr[j]);
+                                    aR[j] = fma(g2.x, Z[2 * q][j], aR[j]);
+                                    aL[j] = fma(-k1, Y[2 * q + 1][j], aL[j]);
+                                    Y[2 * q + 1][j] = fma(-m2.y, Y[2 * q + 1][j], wl[j]);
+                                    Z[2 * q + 1][j] = fma(-m2.y, Z[2 * q + 1][j], wr[j]);
+                                    aR[j] = fma(g2.y, Z[2 * q + 1][j], aR[j]);
+                                }
                             }
-                        }
-                        if (ODD) {
-                            const double mu = rmu[64 * NP + lt], gg = rga[64 * NP + lt];
-                            const double nk = gg * mu;
+                            if (ODD) {
+                                const double mu = rmu[64 * NP + lt], gg = rga[64 * NP + lt];
+                                const double nk = gg * mu;
 #pragma unroll
-                            for (int j = 0; j < TS; ++j) {
-                                aL[j] = fma(-nk, Y[TL - 1][j], aL[j]);
-                                Y[TL - 1][j] = fma(-mu, Y[TL - 1][j], wl[j]);
-                                Z[TL - 1][j] = fma(-mu, Z[TL - 1][j], wr[j]);
-                                aR[j] = fma(gg, Z[TL - 1][j], aR[j]);
+                                for (int j = 0; j < TS; ++j) {
+                                    aL[j] = fma(-nk, Y[TL - 1][j], aL[j]);
+                                    Y[TL - 1][j] = fma(-mu, Y[TL - 1][j], wl[j]);
+                                    Z[TL - 1][j] = fma(-mu, Z[TL - 1][j], wr[j]);
+                                    aR[j] = fma(gg, Z[TL - 1][j], aR[j]);
+                                }
                             }
                         }
                     };
