@@ -272,10 +272,23 @@ bool launch_warp_t(const DevGraph& g, const DevPlan& p, int64_t n_samples, const
     const size_t smem = warp_smem_bytes(g, W, stage);
     if (smem > SMEM_LIMIT) return false;
     const int64_t n_oct = (n_samples + WARP_NW - 1) / WARP_NW;
-    // octets per CTA: about four CTAs per SM over the whole (node x octet) grid
-    int64_t octs = (p.L * n_oct + 4 * 148 - 1) / (4 * 148);
-    if (octs < 1) octs = 1;
-    if (octs > n_oct) octs = n_oct;
+    // octets per CTA: the CTAs run in waves of (resident CTAs per SM) x 148 and a wave lasts about
+    // `octs` octet solves, so pick the power of two minimising waves x octs (the partial last wave
+    // included); ties go to the larger octs (fewer table stagings).  Config 3: 2 (23 waves).
+    auto* kern = stage ? pcg_warp_kernel<VPL, W, true> : pcg_warp_kernel<VPL, W, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARP_NW * 32, smem);
+    const int64_t slots = 148 * (int64_t)(per_sm > 0 ? per_sm : 1);
+    int64_t octs = 1, best = -1;
+    for (int64_t o = 1; o <= n_oct; o *= 2) {
+        const int64_t ctas = p.L * ((n_oct + o - 1) / o);
+        const int64_t cost = ((ctas + slots - 1) / slots) * o;
+        if (best < 0 || cost <= best) {
+            best = cost;
+            octs = o;
+        }
+    }
     const dim3 grid(p.L, (unsigned)((n_oct + octs - 1) / octs));
     const int32_t csl = sample_tile_log2(n_samples);
     if (stage) {
