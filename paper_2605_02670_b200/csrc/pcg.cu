@@ -434,12 +434,25 @@ bool launch_t(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgP
     if (vb > SMEM_LIMIT) return false;
     const bool staged = vb + staged_bytes(g) <= SMEM_LIMIT;
     const size_t smem = staged ? vb + staged_bytes(g) : vb;
-    // chunks of samples per CTA: fill the GPU, keep every group busy
-    int64_t groups = (148 * 2 + p.L - 1) / p.L;
+    // chunks of samples per CTA: the CTAs run in waves over (resident CTAs per SM) x 148 slots and
+    // a wave lasts about one CTA's batches, so pick the CTA count per node minimising
+    // waves x (batches per group); ties go to fewer CTAs
     const int64_t batches = (n_samples + SB - 1) / SB;
     const int64_t maxg = (batches + NG - 1) / NG;
-    if (groups > maxg) groups = maxg;
-    if (groups < 1) groups = 1;
+    auto* kern = staged ? pcg_kernel<GT, SB, VPT, W, true> : pcg_kernel<GT, SB, VPT, W, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PCG_THREADS, smem);
+    const int64_t slots = 148 * (int64_t)(per_sm > 0 ? per_sm : 1);
+    int64_t groups = 1, best = -1;
+    for (int64_t gc = 1; gc <= maxg; gc *= 2) {
+        const int64_t per_group = (batches + gc * NG - 1) / (gc * NG);
+        const int64_t cost = ((p.L * gc + slots - 1) / slots) * per_group;
+        if (best < 0 || cost < best) {
+            best = cost;
+            groups = gc;
+        }
+    }
     const int32_t spc = (int32_t)(((batches + groups - 1) / groups) * SB);
     groups = (n_samples + spc - 1) / spc;
     const dim3 grid(p.L, (unsigned)groups);
