@@ -35,7 +35,7 @@
 namespace grf {
 namespace {
 
-__global__ void edge_setup_kernel(DevGraph g, int32_t L, int32_t Lp, int32_t rounds, const double* __restrict__ cIt,
+__global__ void edge_setup_kernel(DevGraph g, int32_t L, int32_t Lp, const double* __restrict__ cIt,
                                   const double* __restrict__ cLt, double kappa2, int32_t mass, double* __restrict__ mu_t,
                                   double* __restrict__ gam_t, double4* __restrict__ sig) {
     const int e = blockIdx.x;
@@ -85,11 +85,12 @@ __global__ void edge_setup_kernel(DevGraph g, int32_t L, int32_t Lp, int32_t rou
         const double det = sd * sd - so * so;
         sig[(int64_t)l * g.E + e] = make_double4(sd, so, sd / det, -so / det);
     }
-    // correction node (K5's interior steps, sweep_impl.cuh "body_mid"): with one node round and a
-    // padded slot l = L, that slot gets mu = 0 and g_t = -G_t / 2 with G_t = sum_{l<L} g_t for the
-    // interior rows 1 <= t <= m-2 (0 on the end rows), so its chains carry the noise itself and its
-    // two contributions remove G_i W_i once from every interior position
-    if (rep && rounds == 1 && L < Lp && m > 2) {
+    // correction node (K5's interior steps, sweep_impl.cuh "body_mid"): the padded slot l = L gets
+    // mu = 0 and g_t = -G_t / 2 with G_t = sum_{l<L} g_t for the interior rows 1 <= t <= m-2 (0 on
+    // the end rows), so its chains carry the noise itself and its two contributions remove G_i W_i
+    // once from every interior position.  With several node rounds the slot lies in the last one
+    // and corrects the sum over all of them (the rounds only partition the sum over l).
+    if (rep && L < Lp && m > 2) {
         __syncthreads();  // all g rows of this class written
         for (int t = 1 + threadIdx.x; t <= m - 2; t += blockDim.x) {
             double G = 0.0;
@@ -104,7 +105,7 @@ __global__ void edge_setup_kernel(DevGraph g, int32_t L, int32_t Lp, int32_t rou
 void launch_edge_setup(const DevGraph& g, DevPlan& p, cudaStream_t st) {
     int threads = ((p.L + 31) / 32) * 32;
     if (threads > 256) threads = 256;
-    edge_setup_kernel<<<g.E, threads, 0, st>>>(g, p.L, p.Lp, p.rounds, p.cI, p.cL, p.kappa * p.kappa, p.mass, p.mu, p.gam,
+    edge_setup_kernel<<<g.E, threads, 0, st>>>(g, p.L, p.Lp, p.cI, p.cL, p.kappa * p.kappa, p.mass, p.mu, p.gam,
                                                reinterpret_cast<double4*>(p.sig));
 }
 

@@ -34,7 +34,7 @@ sweep::Args make_args(const DevGraph& g, const DevPlan& p, int64_t S, const doub
     a.out = out;
     a.uG = uG;
     a.counter = counter;
-    a.nk = (p.rounds == 1 && p.L < p.Lp) ? 1 : 0;  // edge_setup.cu wrote the correction node at slot L
+    a.nk = p.L < p.Lp ? 1 : 0;  // edge_setup.cu wrote the correction node at slot L
     return a;
 }
 }  // namespace

@@ -70,7 +70,7 @@ struct Args {
     int32_t chunks;         // sample tiles per edge
     int32_t n_items;        // E * chunks
     int32_t tile_ms;        // recover: max (m | 1) the shared-memory output tile holds (0: none)
-    int32_t nk;             // recover: 1 if slot L is the correction node (edge_setup.cu; one round, L < Lp)
+    int32_t nk;             // recover: 1 if slot L is the correction node (edge_setup.cu; L < Lp)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
