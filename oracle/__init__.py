@@ -14,7 +14,9 @@ The oracle shares no code with the CUDA path.  Its only common dependency is
 
 PAPER.md P60-67 [eq:coefficients], P75-77 [eq:spde_approx_fem], P106-109 (§2.5
 lumping), P137-160 (stencils), P335 (K^-/K^+).  Each node's system is solved by
-a sparse direct LU (scipy SuperLU, a library primitive) -- no domain
+a sparse direct factorization -- the plain C LDL^T of ``ldlt.c`` with a fixed
+interior-first / minimum-degree-vertex ordering, or scipy's
+SuperLU, a library primitive, as the second route that pins it -- no domain
 decomposition, no Thomas, no PCG.  The sum runs in ascending l (SPEC S323).
 
 Modules:
@@ -23,6 +25,7 @@ Modules:
     quadrature  K^-, K^+, c_I, c_L; scalar sinc rule      (P54-67, P335)
     noise       Philox4x32-10 + fixed-algorithm Box-Muller (P99-109, P150)
     solve       per-node direct solves + quadrature sum  (P67-78, P313-324)
+    ldlt        sparse LDL^T direct solver (ldlt.c)
     spectral    dense generalized-eigen oracle (tiny)
     dd          Schur / NN-preconditioner DEFINITIONS     (P111-118, P204-213, P298)
     rates       OLS log-log rate fit                      (P335)
