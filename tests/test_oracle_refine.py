@@ -69,3 +69,93 @@ def test_non_nested_meshes_rejected():
     g = single_edge(1.0)
     with pytest.raises(ValueError):
         prolongation(build_mesh(g, 1 / 3), build_mesh(g, 1 / 4))
+
+
+# ----------------------------------------------------------------------------- the refinement sweep (P332-335)
+@pytest.mark.parametrize("beta", [0.5, 0.625, 0.75, 0.875])
+def test_strong_error_sweep_reproduces_paper_rates(beta):
+    """The oracle run through the paper's own study (P332-335): kappa = 1, k = -1/(beta ln h) per
+    level, overkill h = 2^-10, coarse h = 2^-3..2^-7, 32 realizations of the overkill noise
+    projected down with P^T, RMS error in the overkill lumped-mass norm.  The fitted rate must be
+    the theory's 2 beta - 1/2 (P334; the paper's Table 1, P450, prints 0.51 / 0.76 / 1.00 / 1.25
+    for these beta) within 0.1.  A dropped quadrature term, a wrong mass, a transposed
+    prolongation or an injected (instead of projected) noise all move the rate far outside."""
+    from oracle.refine import strong_error_sweep
+    hs, ms, r = strong_error_sweep(tadpole(), range(3, 8), 10, 1.0, beta, seed=0, n_real=32)
+    assert abs(r - (2 * beta - 0.5)) <= 0.1, f"rate {r:.3f} vs theory {2 * beta - 0.5}"
+    assert all(a > b for a, b in zip(ms, ms[1:]))  # monotone decay under refinement
+
+
+def test_strong_error_sweep_sensitive_to_injected_noise():
+    """Negative control: injecting the fine noise at the coarse nodes (instead of P^T W) breaks the
+    convergence (rate ~0.06 instead of 1.0), so the sweep pin above can fail."""
+    from oracle import noise, quadrature, solve
+    g, beta = tadpole(), 0.75
+    ok = solve.setup(g, 2.0 ** -10, 1.0, beta, quadrature.k_from_h(beta, 2.0 ** -10))
+    W = noise.white_noise(ok.ML, 0, 16)
+    u_ok = solve.apply(ok, W)
+    hs, errs = [2.0 ** -j for j in range(3, 8)], []
+    for hc in hs:
+        pc = solve.setup(g, hc, 1.0, beta, quadrature.k_from_h(beta, hc))
+        P = prolongation(pc.mesh, ok.mesh)
+        inj = (P.T == 1.0).astype(float)
+        d = u_ok - (P @ solve.apply(pc, (inj @ W.T).T).T).T
+        errs.append(np.einsum("si,i,si->s", d, ok.ML, d).mean())
+    from oracle.rates import fit_rate
+    assert fit_rate(hs, np.sqrt(errs))[0] < 0.5
+
+
+def test_strong_error_zero_on_the_overkill_mesh_itself():
+    """h_coarse = h_ok: P = I, P^T W = W and the same quadrature, so every error is exactly 0."""
+    from oracle import noise, solve
+    from oracle.refine import strong_error
+    g = star_of_lattices(2, 3)
+    h = 0.125
+    prob = solve.setup(g, h, 2.0, 0.7, 0.4)
+    W = noise.white_noise(prob.ML, 2, 3)
+    assert np.array_equal(strong_error(g, h, h, 2.0, 0.7, 0.4, W), np.zeros(3))
+
+
+def test_strong_error_matches_spectral_definition_on_one_edge():
+    """strong_error on a single edge equals the same quantity from the closed-form cosine
+    eigen-expansion of each mesh's lumped Neumann pencil (no matrix assembled, no prolongation
+    matrix: P u_c by linear interpolation of the coarse nodal values)."""
+    import math
+    from oracle import noise, quadrature, solve
+    from oracle.refine import strong_error
+    ell, kappa, beta, k = 1.0, 2.0, 0.7, 0.4
+    g = single_edge(ell)
+    hc, hf = 0.25, 0.25 / 8
+    plan = quadrature.plan(beta, k)
+
+    def spectral_solve(h, W):  # u = sum_j Q_k(lam_j) phi_j (phi_j^T W)/||phi_j||_M^2 in DOF order
+        n = math.ceil(ell / h)
+        he = ell / n
+        i = np.arange(n + 1)
+        order = np.concatenate([np.arange(1, n), [0, n]])
+        mass = np.full(n + 1, he)
+        mass[0] = mass[n] = he / 2
+        u = np.zeros_like(W)
+        for j in range(n + 1):
+            phi = np.cos(j * math.pi * i / n)
+            lam = kappa ** 2 + (4.0 / he ** 2) * math.sin(j * math.pi / (2 * n)) ** 2
+            ph = phi[order]
+            u += quadrature.sinc_scalar(lam, plan) * np.outer(W @ ph, ph) / (mass * phi * phi).sum()
+        return u, order, n, mass
+
+    ok = solve.setup(g, hf, kappa, beta, k)
+    W = noise.white_noise(ok.ML, 4, 3)
+    u_f, order_f, nf, mass_f = spectral_solve(hf, W)
+    r = nf // 4
+    # P^T W by hand: coarse node c collects fine node j with weight max(0, 1 - |j - r c| / r)
+    Wpos = W[:, np.argsort(order_f)]  # noise by position along the edge (DOF d sits at position order_f[d])
+    Wc_pos = np.stack([sum(max(0.0, 1 - abs(j - r * c) / r) * Wpos[:, j] for j in range(nf + 1)) for c in range(5)], 1)
+    order_c = np.concatenate([np.arange(1, 4), [0, 4]])
+    Wc = Wc_pos[:, order_c]
+    u_c, _, _, _ = spectral_solve(hc, Wc)
+    uc_pos = u_c[:, np.argsort(order_c)]
+    up_pos = np.stack([np.interp(j / r, np.arange(5), uc_pos[s]) for s in range(3) for j in range(nf + 1)]).reshape(3, nf + 1)
+    d = u_f[:, np.argsort(order_f)] - up_pos
+    ref = (d * d * mass_f).sum(1)
+    got = strong_error(g, hc, hf, kappa, beta, k, W)
+    assert np.max(np.abs(got - ref) / ref) <= 1e-10
