@@ -152,6 +152,8 @@ typedef struct grf_options {
                              CONSISTENT (the paper's comparison baseline, P129-136: consistent M in
                              the operator, noise W = R xi with R the natural-order Cholesky factor
                              of M, P148-150; V <= 8192, not for edge-partitioned parts) */
+    int64_t node_stride;  /* nodes node_begin, node_begin + node_stride, ... < node_end (round-robin
+                             node shards); default 1 (0 is read as 1) */
 } grf_options;
 void grf_options_default(grf_options* opt);
 
@@ -264,15 +266,20 @@ void grf_comm_destroy(grf_comm* c);
 
 /* Sample-then-node sharding (policy BY_SAMPLE_THEN_NODE) of one grf_sample call
  * over the communicator's ranks: P_s = min(world, n_samples) contiguous sample ranges, and the
- * P_l = world / P_s ranks sharing a range split the quadrature nodes into contiguous ranges
- * (their partial sums, P313-324, are sent to the range's root over NCCL and added in rank
- * order).  grf_dist_shard (host only) fills out[6] = {sample_begin, sample_end, node_begin,
- * node_end, root_rank, flags}, flags = active | is_root << 1 | P_l << 2.  grf_sample_dist
- * writes range_out[6] likewise and, on an active rank, u_out (device, n_local x N, n_local =
- * sample_end - sample_begin): the full field of the range on its root, the rank's node-shard
- * partial sum elsewhere.  Inactive ranks (world > P_s P_l) return GRF_OK and touch nothing.
- * opt's node range must be left at its default.  Synchronises when P_l > 1.
- * (The EDGE_PARTITION policy is grf_sample_edgepart.) */
+ * P_l = world / P_s ranks sharing a range split the quadrature nodes ROUND-ROBIN (shard li takes
+ * nodes li, li + P_l, li + 2 P_l, ...: the PCG cost varies strongly with l, P162-165, so strided
+ * shards balance it).  Their partial sums (P313-324) meet on the range's root through a binomial
+ * tree of NCCL send/recv pairs (fixed pairing: the same addition order on every call).
+ * grf_dist_shard (host only) fills out[6] = {sample_begin, sample_end, node_begin, node_end,
+ * root_rank, flags}, flags = active | is_root << 1 | P_l << 2; the shard's nodes are node_begin,
+ * node_begin + P_l, ... < node_end.  grf_sample_dist writes range_out[6] likewise and, on an
+ * active rank, u_out (device, n_local x N, n_local = sample_end - sample_begin): the full field of
+ * the range on its root, scratch elsewhere.  Inactive ranks (world > P_s P_l) touch no output.
+ * EVERY rank of the communicator must call grf_sample_dist with the same arguments: after its
+ * local work each rank joins one status allreduce, so a local failure on any rank makes every
+ * rank return an error (GRF_ENCCL "a peer rank ... failed" on the others) instead of blocking
+ * in the exchange.  opt's node range must be left at its default.  Synchronises the stream when
+ * world > 1.  (The EDGE_PARTITION policy is grf_sample_edgepart.) */
 grf_status grf_dist_shard(int32_t world, int32_t rank, int64_t n_samples, int64_t n_nodes, int64_t* out);
 grf_status grf_sample_dist(grf_graph* g, grf_comm* comm, double kappa, double beta, double k, uint64_t seed,
                            int64_t n_samples, const grf_options* opt, double* u_out, int64_t* range_out,

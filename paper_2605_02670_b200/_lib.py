@@ -33,7 +33,7 @@ class grf_part_info(C.Structure):
 class grf_options(C.Structure):
     _fields_ = [("rtol", C.c_double), ("max_iter", C.c_int32), ("precond", C.c_int32),
                 ("node_begin", C.c_int64), ("node_end", C.c_int64), ("pcg_variant", C.c_int32),
-                ("mass", C.c_int32)]
+                ("mass", C.c_int32), ("node_stride", C.c_int64)]
 
 
 class grf_stats(C.Structure):

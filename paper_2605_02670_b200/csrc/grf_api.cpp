@@ -65,8 +65,8 @@ struct Block {
 
 struct PlanKey {
     double kappa, beta, k;
-    int64_t nb, ne;
-    int64_t mass;  // GRF_MASS_*
+    int64_t nb, ne, stride;  // nodes nb, nb + stride, ... < ne of 0..L-1
+    int64_t mass;            // GRF_MASS_*
     bool operator==(const PlanKey& o) const {
         return std::memcmp(this, &o, sizeof(PlanKey)) == 0;
     }
@@ -161,28 +161,36 @@ grf_status plan_limits(double beta, double k, int64_t* Km, int64_t* Kp) {
 }
 
 // c_const = pi / (2 k sin(pi beta)); c_I = c_const e^{-2 beta y_l}; c_L = c_I e^{2 y_l}; y_l = l k  (P61-65)
-void plan_coefficients(double beta, double k, int64_t Km, int64_t lo, int64_t hi, double* cI, double* cL) {
+// for the nodes t = lo, lo + stride, ... < hi of 0..L-1 (l = t - K^-)
+void plan_coefficients(double beta, double k, int64_t Km, int64_t lo, int64_t hi, int64_t stride, double* cI,
+                       double* cL) {
     const double c_const = M_PI / (2.0 * k * std::sin(M_PI * beta));
-    for (int64_t t = lo; t < hi; ++t) {
+    int64_t q = 0;
+    for (int64_t t = lo; t < hi; t += stride, ++q) {
         const double y = (double)(t - Km) * k;
         const double ci = c_const * std::exp(-2.0 * beta * y);
-        cI[t - lo] = ci;
-        cL[t - lo] = ci * std::exp(2.0 * y);
+        cI[q] = ci;
+        cL[q] = ci * std::exp(2.0 * y);
     }
 }
 
-grf_status resolve_range(const grf_options* opt, int64_t L, int64_t* nb, int64_t* ne) {
-    int64_t b = 0, e = L;
+// nodes of opt's range: [node_begin, node_end) with stride node_stride (0 or 1: contiguous)
+grf_status resolve_range(const grf_options* opt, int64_t L, int64_t* nb, int64_t* ne, int64_t* stride) {
+    int64_t b = 0, e = L, d = 1;
     if (opt) {
         b = opt->node_begin;
         e = opt->node_end < 0 ? L : opt->node_end;
+        d = opt->node_stride > 1 ? opt->node_stride : 1;
+        if (opt->node_stride < 0) return fail(GRF_EINVAL, "node_stride must be >= 0");
     }
     if (b < 0 || e > L || b >= e) return fail(GRF_EINVAL, "node range [%lld, %lld) invalid for L=%lld",
                                               (long long)b, (long long)e, (long long)L);
     *nb = b;
     *ne = e;
+    *stride = d;
     return GRF_OK;
 }
+int64_t range_count(int64_t nb, int64_t ne, int64_t stride) { return (ne - nb + stride - 1) / stride; }
 
 grf_status check_params(const grf_graph* g, double kappa, double beta, double k, int64_t n) {
     if (!g) return fail(GRF_EINVAL, "graph is NULL");
@@ -201,10 +209,10 @@ grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf
     grf_status s = plan_limits(beta, k, &Km, &Kp);
     if (s) return s;
     const int64_t Lfull = Km + Kp + 1;
-    int64_t nb, ne;
-    s = resolve_range(opt, Lfull, &nb, &ne);
+    int64_t nb, ne, nd;
+    s = resolve_range(opt, Lfull, &nb, &ne, &nd);
     if (s) return s;
-    PlanKey key{kappa, beta, k, nb, ne, (int64_t)(opt ? opt->mass : GRF_MASS_LUMPED)};
+    PlanKey key{kappa, beta, k, nb, ne, nd, (int64_t)(opt ? opt->mass : GRF_MASS_LUMPED)};
     for (auto it = g->plans.begin(); it != g->plans.end(); ++it) {
         if ((*it)->key == key) {
             g->plans.splice(g->plans.begin(), g->plans, it);
@@ -212,7 +220,7 @@ grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf
             return GRF_OK;
         }
     }
-    const int64_t L = ne - nb;
+    const int64_t L = range_count(nb, ne, nd);
     int32_t Lp = 0, TL = 0, rounds = 0;
     grf::plan_tiling((int32_t)L, &Lp, &TL, &rounds);
     auto p = std::make_unique<Plan>();
@@ -220,7 +228,7 @@ grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf
     p->Km = Km;
     p->Kp = Kp;
     std::vector<double> cI(L), cL(Lp, 0.0);  // c_L zero padded to the table row Lp
-    plan_coefficients(beta, k, Km, nb, ne, cI.data(), cL.data());
+    plan_coefficients(beta, k, Km, nb, ne, nd, cI.data(), cL.data());
     auto grab = [&](size_t bytes) -> void* {
         void* q = g->alloc.get(bytes, st);
         if (q) p->blocks.push_back({q, bytes});
@@ -511,6 +519,7 @@ void grf_options_default(grf_options* opt) {
     opt->precond = GRF_PRECOND_NN;
     opt->node_begin = 0;
     opt->node_end = -1;
+    opt->node_stride = 1;
     opt->pcg_variant = GRF_PCG_AUTO;
     opt->mass = GRF_MASS_LUMPED;
 }
@@ -817,7 +826,7 @@ grf_status grf_plan_info(double beta, double k, int64_t* k_minus, int64_t* k_plu
     if (c_I || c_L) {
         const int64_t L = Km + Kp + 1;
         std::vector<double> a(L), b(L);
-        plan_coefficients(beta, k, Km, 0, L, a.data(), b.data());
+        plan_coefficients(beta, k, Km, 0, L, 1, a.data(), b.data());
         if (c_I) std::copy(a.begin(), a.end(), c_I);
         if (c_L) std::copy(b.begin(), b.end(), c_L);
     }
@@ -829,11 +838,11 @@ grf_status grf_workspace_size(const grf_graph* g, double kappa, double beta, dou
     grf_status st = check_params(g, kappa, beta, k, n_samples);
     if (st) return st;
     if (!bytes) return fail(GRF_EINVAL, "bytes is NULL");
-    int64_t Km, Kp, nb, ne;
+    int64_t Km, Kp, nb, ne, nd;
     plan_limits(beta, k, &Km, &Kp);
-    st = resolve_range(opt, Km + Kp + 1, &nb, &ne);
+    st = resolve_range(opt, Km + Kp + 1, &nb, &ne, &nd);
     if (st) return st;
-    *bytes = ws_layout(g, ne - nb, n_samples, true, use_global_pcg(g, opt),
+    *bytes = ws_layout(g, range_count(nb, ne, nd), n_samples, true, use_global_pcg(g, opt),
                        opt && opt->mass == GRF_MASS_CONSISTENT).total;
     return GRF_OK;
 }
@@ -1444,71 +1453,119 @@ extern "C" grf_status grf_dist_shard(int32_t world, int32_t rank, int64_t n_samp
     const int64_t gi = active ? rank / pl : 0, li = active ? rank % pl : 0;
     out[0] = active ? split_lo(n_samples, ps, gi) : 0;
     out[1] = active ? split_lo(n_samples, ps, gi + 1) : 0;
-    out[2] = active ? split_lo(n_nodes, pl, li) : 0;
-    out[3] = active ? split_lo(n_nodes, pl, li + 1) : 0;
+    out[2] = active ? li : 0;             // round-robin node shard: nodes li, li + P_l, ... < n_nodes
+    out[3] = active ? n_nodes : 0;
     out[4] = gi * pl;                       // root rank of the sample range
-    out[5] = (active ? 1 : 0) | ((active && li == 0) ? 2 : 0) | (pl << 2);  // active, is_root, ranks per range
+    out[5] = (active ? 1 : 0) | ((active && li == 0) ? 2 : 0) | (pl << 2);  // active, is_root, P_l (= node stride)
     return GRF_OK;
 }
+
+namespace {
+// max of an int32 over all ranks of the communicator (every rank must call it)
+grf_status allreduce_max_i32(grf_comm* c, int32_t* dev_buf, int32_t* host_val, cudaStream_t st) {
+    static nccl_allreduce_fn fn = nullptr;
+    if (!fn) fn = (nccl_allreduce_fn)dlsym(g_nccl.h, "ncclAllReduce");
+    if (!fn) return fail(GRF_ENCCL, "ncclAllReduce not found");
+    CUDA_TRY(cudaMemcpyAsync(dev_buf, host_val, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    int r = fn(dev_buf, dev_buf, 1, 2 /* ncclInt32 */, 2 /* ncclMax */, c->comm, st);
+    if (r) return fail(GRF_ENCCL, "ncclAllReduce: %s", g_nccl.err ? g_nccl.err(r) : "error");
+    CUDA_TRY(cudaMemcpyAsync(host_val, dev_buf, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return GRF_OK;
+}
+}  // namespace
 
 extern "C" grf_status grf_sample_dist(grf_graph* g, grf_comm* comm, double kappa, double beta, double k,
                                       uint64_t seed, int64_t n_samples, const grf_options* opt, double* u_out,
                                       int64_t* range_out, void* stream, grf_stats* stats) {
+    // Every rank of the communicator -- active or not -- takes part in one status agreement (an
+    // int32 max allreduce) after its local work, so that a rank whose local call failed cannot
+    // leave its peers blocked in the partial-sum exchange: on any failure every rank returns
+    // (GRF_ENCCL "a peer failed" on the others) before a single partial is sent.
     if (!g || !comm || !range_out) return fail(GRF_EINVAL, "NULL argument");
     grf_status st = check_params(g, kappa, beta, k, n_samples);
-    if (st) return st;
+    if (st) return st;  // identical arguments on every rank: every rank fails here alike
     int64_t Km, Kp;
     st = plan_limits(beta, k, &Km, &Kp);
     if (st) return st;
     int64_t L = Km + Kp + 1;
-    if (opt && (opt->node_begin != 0 || opt->node_end >= 0))
-        return fail(GRF_EINVAL, "grf_sample_dist shards the whole node range; leave node_begin/node_end default");
+    if (opt && (opt->node_begin != 0 || opt->node_end >= 0 || opt->node_stride > 1))
+        return fail(GRF_EINVAL, "grf_sample_dist shards the whole node range; leave the node range default");
     int64_t sh[6];
     st = grf_dist_shard(comm->nranks, comm->rank, n_samples, L, sh);
     if (st) return st;
     for (int i = 0; i < 6; ++i) range_out[i] = sh[i];
-    const bool active = sh[5] & 1, is_root = sh[5] & 2;
+    const bool active = sh[5] & 1;
     const int64_t pl = sh[5] >> 2;
-    if (!active) return GRF_OK;
-    if (!u_out) return fail(GRF_EINVAL, "u_out is NULL");
-    const int64_t s0 = sh[0], ns = sh[1] - sh[0];
-    grf_options o;
-    grf_options_default(&o);
-    if (opt) o = *opt;
-    o.node_begin = sh[2];
-    o.node_end = sh[3];
     cudaStream_t s = (cudaStream_t)stream;
-    st = grf_sample(g, kappa, beta, k, seed + (uint64_t)s0, ns, &o, u_out, nullptr, 0, s, stats);
-    if (st && st != GRF_ENOCONV) return st;
-    if (pl > 1) {  // the node shards of this sample range: partial sums to the root, added in rank order
+    const int64_t s0 = sh[0], ns = sh[1] - sh[0];
+    grf_status local = GRF_OK;
+    if (active) {
+        if (!u_out) {
+            local = fail(GRF_EINVAL, "u_out is NULL");
+        } else {
+            grf_options o;
+            grf_options_default(&o);
+            if (opt) o = *opt;
+            o.node_begin = sh[2];
+            o.node_end = sh[3];
+            o.node_stride = pl;
+            local = grf_sample(g, kappa, beta, k, seed + (uint64_t)s0, ns, &o, u_out, nullptr, 0, s, stats);
+        }
+    }
+    const std::string local_msg = g_err;
+    if (comm->nranks > 1) {
+        int32_t* flag = (int32_t*)g->alloc.get(sizeof(int32_t), s);
+        if (!flag) return fail(GRF_ENOMEM, "status buffer");  // (a peer then blocks: allocation of 8 B failed)
+        int32_t worst = (local == GRF_OK || local == GRF_ENOCONV) ? 0 : 1;
+        grf_status ar = allreduce_max_i32(comm, flag, &worst, s);
+        g->alloc.put(flag, sizeof(int32_t), s);
+        if (ar) return ar;
+        if (local != GRF_OK && local != GRF_ENOCONV) return fail(local, "%s", local_msg.c_str());
+        if (worst) return fail(GRF_ENCCL, "grf_sample_dist: a peer rank's local sampling failed");
+    } else if (local != GRF_OK && local != GRF_ENOCONV) {
+        return local;
+    }
+    if (active && pl > 1) {
+        // the P_l node shards of this sample range: a binomial tree over the range's ranks (fixed
+        // pairing, so the partial sums are added in the same order on every call): in round d
+        // (d = 1, 2, 4, ...) shard li with li % 2d == d sends its running sum to li - d, which adds it
         static nccl_p2p_fn send = nullptr, recv = nullptr;
-        static nccl_group_fn gstart = nullptr, gend = nullptr;
         if (!send) {
             send = (nccl_p2p_fn)dlsym(g_nccl.h, "ncclSend");
             recv = (nccl_p2p_fn)dlsym(g_nccl.h, "ncclRecv");
-            gstart = (nccl_group_fn)dlsym(g_nccl.h, "ncclGroupStart");
-            gend = (nccl_group_fn)dlsym(g_nccl.h, "ncclGroupEnd");
         }
         if (!send || !recv) return fail(GRF_ENCCL, "ncclSend/ncclRecv not found");
         const size_t count = (size_t)ns * g->N;
-        const int root = (int)sh[4];
-        if (is_root) {
-            double* tmp = (double*)g->alloc.get(count * sizeof(double), s);
-            if (!tmp) return fail(GRF_ENOMEM, "reduce buffer");
-            for (int64_t r = root + 1; r < root + pl; ++r) {
-                int e = recv(tmp, count, 8, (int)r, comm->comm, s);
-                if (e) return fail(GRF_ENCCL, "ncclRecv: %s", g_nccl.err ? g_nccl.err(e) : "error");
+        const int64_t root = sh[4], li = comm->rank - root;
+        double* tmp = nullptr;
+        grf_status rc = GRF_OK;
+        for (int64_t d = 1; d < pl && rc == GRF_OK; d <<= 1) {
+            if (li % (2 * d) == d) {
+                int e = send(u_out, count, 8, (int)(root + li - d), comm->comm, s);
+                if (e) rc = fail(GRF_ENCCL, "ncclSend: %s", g_nccl.err ? g_nccl.err(e) : "error");
+                break;  // this shard's sum has been handed on
+            }
+            if (li % (2 * d) == 0 && li + d < pl) {
+                if (!tmp) tmp = (double*)g->alloc.get(count * sizeof(double), s);
+                if (!tmp) {
+                    rc = fail(GRF_ENOMEM, "reduce buffer of %zu bytes", count * sizeof(double));
+                    break;
+                }
+                int e = recv(tmp, count, 8, (int)(root + li + d), comm->comm, s);
+                if (e) {
+                    rc = fail(GRF_ENCCL, "ncclRecv: %s", g_nccl.err ? g_nccl.err(e) : "error");
+                    break;
+                }
                 grf::launch_add(u_out, tmp, (int64_t)count, s);
             }
+        }
+        if (tmp) {
             cudaStreamSynchronize(s);
             g->alloc.put(tmp, count * sizeof(double), s);
-        } else {
-            int e = send(u_out, count, 8, root, comm->comm, s);
-            if (e) return fail(GRF_ENCCL, "ncclSend: %s", g_nccl.err ? g_nccl.err(e) : "error");
         }
-        (void)gstart;
-        (void)gend;
+        if (rc) return rc;
     }
     CUDA_TRY(cudaGetLastError());
-    return st;
+    return local;
 }

@@ -58,7 +58,8 @@ PCG_VARIANT = {"auto": 0, "shared": 1, "global": 2}
 MASS = {"lumped": 0, "consistent": 1}
 
 
-def make_options(rtol=1e-13, max_iter=0, precond="nn", node_range=None, pcg="auto", mass="lumped") -> grf_options:
+def make_options(rtol=1e-13, max_iter=0, precond="nn", node_range=None, pcg="auto", mass="lumped",
+                 node_stride=1) -> grf_options:
     o = grf_options()
     load().grf_options_default(C.byref(o))
     o.rtol = rtol
@@ -66,6 +67,7 @@ def make_options(rtol=1e-13, max_iter=0, precond="nn", node_range=None, pcg="aut
     o.precond = PRECOND[precond] if isinstance(precond, str) else int(precond)
     if node_range is not None:
         o.node_begin, o.node_end = int(node_range[0]), int(node_range[1])
+    o.node_stride = int(node_stride)
     o.pcg_variant = PCG_VARIANT[pcg] if isinstance(pcg, str) else int(pcg)
     o.mass = MASS[mass] if isinstance(mass, str) else int(mass)
     return o
@@ -247,7 +249,8 @@ class Graph:
         L = km + kp + 1
         nb = o.node_begin
         ne = L if o.node_end < 0 else o.node_end
-        buf = np.empty((ne - nb, self.n_edges, 2))
+        nd = max(1, o.node_stride)
+        buf = np.empty(((ne - nb + nd - 1) // nd, self.n_edges, 2))
         check(self._lib.grf_edge_schur(self._h, kappa, beta, k, C.byref(o), buf.ctypes.data_as(C.POINTER(C.c_double))))
         return buf
 

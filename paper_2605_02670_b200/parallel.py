@@ -5,8 +5,9 @@ node solutions (PAPER.md P313-324).  One process per GPU:
 
 * samples first: P_s = min(world, S) contiguous sample ranges -- no data-path collective;
 * then nodes: the P_l = world // P_s ranks sharing a sample range split the quadrature nodes
-  into contiguous ranges (grf_options.node_begin/end), and their partial sums are reduced to
-  the range's root with one NCCL reduce over NVLink (torch.distributed process group).
+  round-robin (shard li takes nodes li, li + P_l, ...: grf_options.node_begin / node_stride --
+  the PCG cost varies with l, P162-165, and strided shards balance it), and their partial sums
+  are reduced to the range's root with one NCCL reduce over NVLink (torch.distributed group).
 
 The library call for the local part is ``Graph.sample(..., node_range=...)``; the reduce is
 ``torch.distributed.reduce`` on a per-sample-range sub-group (NCCL on GPUs, gloo in the CPU
@@ -25,7 +26,8 @@ class Shard:
     n_sample_shards: int
     n_node_shards: int
     sample_range: Tuple[int, int]   # [s0, s1) of the call's samples
-    node_range: Tuple[int, int]     # [l0, l1) of 0..L-1
+    node_range: Tuple[int, int]     # nodes l0, l0 + node_stride, ... < l1 of 0..L-1
+    node_stride: int
     group_index: int                # which sample range (ranks with equal index share it)
     is_root: bool                   # receives the reduced sum for its sample range
     active: bool                    # False for ranks left over when world > P_s * P_l
@@ -45,7 +47,7 @@ def shard(world: int, rank: int, n_samples: int, n_nodes: int) -> Shard:
     active = rank < ps * pl
     gi, li = (rank // pl, rank % pl) if active else (0, 0)
     return Shard(rank, world, ps, pl, _split(n_samples, ps, gi) if active else (0, 0),
-                 _split(n_nodes, pl, li) if active else (0, 0), gi, active and li == 0, active)
+                 (li, n_nodes) if active else (0, 0), pl, gi, active and li == 0, active)
 
 
 def node_groups(world: int, n_samples: int, n_nodes: int):
@@ -92,5 +94,6 @@ def sample_dist(graph, kappa, beta, k, seed, n_samples, groups=None, **opts):
     if not sh.active:
         return sh, None
     s0, s1 = sh.sample_range
-    u = graph.sample(kappa, beta, k, seed=seed + s0, n_samples=s1 - s0, node_range=sh.node_range, **opts)
+    u = graph.sample(kappa, beta, k, seed=seed + s0, n_samples=s1 - s0, node_range=sh.node_range,
+                     node_stride=sh.node_stride, **opts)
     return sh, reduce_partial(u, sh, groups)

@@ -302,41 +302,29 @@ def test_rgg_5000_per_node_vs_oracle():
 
 
 def test_config4_rgg_full_size():
-    """configs[3] at full size on one GPU: 1e5 vertices, N = 28 032 313, L = 112, 16 samples.
-    SuperLU cannot factor N = 2.8e7 (out of memory), so the oracle checks what holds at any size:
-    the noise bit-exactly on sampled samples, the defining residual A_l x_l = W of single-node
-    solves (oracle-assembled operator, P75-78) for the extreme nodes, and the full call's
-    convergence and finiteness."""
-    import gc
-
-    from oracle import fem
+    """configs[3] at full size on one GPU in the production launch: 1e5 vertices,
+    N = 28 032 313, L = 112, 16 samples in one call (the global-memory PCG; sweep kernels of the
+    16-sample mapping).  The oracle (C sparse LDL^T with the interior-first + minimum-degree
+    ordering) recomputes samples 0 and 15 over all 112 nodes: fields <= 1e-9
+    relative L2, noise bit-exact."""
     cfg = CONFIGS["rgg"]
     g = config_graph("rgg")
-    prob = solve.setup(g, cfg["h"], cfg["kappa"], cfg["beta"], cfg["k"])
-    L = prob.plan.n_nodes
-    assert L == 112 and prob.ML.shape[0] == 28_032_313
     G = _graph(g, cfg["h"])
     u, st = G.sample(cfg["kappa"], cfg["beta"], cfg["k"], seed=cfg["seed"], n_samples=cfg["n_samples"],
                      return_stats=True)
+    assert G.n_dofs == 28_032_313
     assert st["n_nodes"] == 112 and st["n_unconverged"] == 0 and st["worst_rel_residual"] <= 1e-13
-    u0 = u[[0, 15]].cpu().numpy()
-    assert np.isfinite(u0).all()
-    del u
     picks = [0, 15]
+    got = u[picks].cpu().numpy()
+    del u
     Wg = G.noise(cfg["seed"], cfg["n_samples"])[picks].cpu().numpy()
-    Wref = noise.white_noise(prob.ML, cfg["seed"], cfg["n_samples"], samples=picks)
-    assert np.array_equal(_bits(Wg), _bits(Wref))
     del G
-    gc.collect()
     torch.cuda.empty_cache()
-    G = _graph(g, cfg["h"])
-    W2 = Wref[:1]  # sample 0 of seed 0 (the oracle's own noise)
-    for li in (0, L - 1):
-        x = G.sample(cfg["kappa"], cfg["beta"], cfg["k"], seed=cfg["seed"], n_samples=1,
-                     node_range=(li, li + 1)).cpu().numpy()
-        A = fem.operator(prob.ML, prob.G, prob.kappa, prob.plan.c_I[li], prob.plan.c_L[li])
-        res = (A @ x.T).T - W2
-        assert (np.linalg.norm(res, axis=1) / np.linalg.norm(W2, axis=1)).max() <= 1e-9, f"node {li}"
+    ref, Wref, _ = solve.sample(g, cfg["h"], cfg["kappa"], cfg["beta"], cfg["k"], cfg["seed"], cfg["n_samples"],
+                                samples=picks)
+    assert np.array_equal(_bits(Wg), _bits(Wref))
+    assert np.isfinite(got).all()
+    assert _rel(got, ref).max() <= FIELD_TOL
 
 
 # ----------------------------------------------------------------------------- config 5 (star of lattices)
@@ -354,45 +342,56 @@ def test_config5_star_coarsest_all_betas(beta):
     assert _rel(u.cpu().numpy()[[0, 63]], ref).max() <= FIELD_TOL
 
 
-def test_config5_star_default_level_per_node():
-    """configs[4] at the CONFIGS level h = 2^-8 (N = 983 289, L = 331, 64 samples): full call
-    converges; single-node solves vs the oracle's sparse direct solve."""
+def test_config5_star_default_level():
+    """configs[4] at the CONFIGS level h = 2^-8 (N = 983 289, L = 331, 64 samples in one call);
+    the oracle recomputes samples 0, 31 and 63 over all 331 nodes."""
     cfg = CONFIGS["star"]
     g = config_graph("star")
     G = _graph(g, cfg["h"])
     u, st = G.sample(cfg["kappa"], cfg["beta"], cfg["k"], seed=cfg["seed"], n_samples=cfg["n_samples"],
                      return_stats=True)
     assert G.n_dofs == 983_289 and st["n_nodes"] == 331 and st["n_unconverged"] == 0
-    assert np.isfinite(u.cpu().numpy()).all()
-    prob = solve.setup(g, cfg["h"], cfg["kappa"], cfg["beta"], cfg["k"])
-    W = noise.white_noise(prob.ML, cfg["seed"], 2)
-    for li in (0, prob.plan.n_nodes // 2, prob.plan.n_nodes - 1):
-        x = G.sample(cfg["kappa"], cfg["beta"], cfg["k"], seed=cfg["seed"], n_samples=2,
-                     node_range=(li, li + 1)).cpu().numpy()
-        assert _rel(x, solve.node_solve(prob, li, W)).max() <= 1e-10, f"node {li}"
+    picks = [0, 31, 63]
+    got = u[picks].cpu().numpy()
+    assert bool(torch.isfinite(u).all())
+    ref, _, _ = solve.sample(g, cfg["h"], cfg["kappa"], cfg["beta"], cfg["k"], cfg["seed"], cfg["n_samples"],
+                             samples=picks)
+    assert _rel(got, ref).max() <= FIELD_TOL
 
 
 def test_config5_star_finest_level():
-    """configs[4] at the finest level h = 2^-12 (N = 15 759 609, edges of 4095 interior nodes)
-    with beta = 0.9 (L = 687, the largest rule), 64 samples: one call fits on one GPU because
-    the 3848 identical edges share one Thomas table; the defining residual A_l x_l = W of
-    single-node solves is checked with the oracle's assembled operator."""
-    from oracle import fem
+    """configs[4] at the finest level h = 2^-12 (N = 15 759 609, edges of 4095 interior nodes:
+    longer than the recovery kernel's shared-memory output tile) with beta = 0.9 (L = 687, the
+    largest rule), 64 samples in one call; the oracle recomputes samples 0 and 63 over all 687
+    nodes (a stated subset of the 64 samples; fields <= 1e-9 relative L2)."""
     g = star_of_lattices(8, 16)
     h, kappa, beta, k = 2.0 ** -12, 8.0, 0.9, 0.2
     G = _graph(g, h)
     u, st = G.sample(kappa, beta, k, seed=0, n_samples=64, return_stats=True)
     assert G.n_dofs == 15_759_609 and st["n_nodes"] == 687 and st["n_unconverged"] == 0
     assert bool(torch.isfinite(u).all())
-    del u
+    picks = [0, 63]
+    got = u[picks].cpu().numpy()
+    del u, G
     torch.cuda.empty_cache()
-    prob = solve.setup(g, h, kappa, beta, k)
-    W = noise.white_noise(prob.ML, 0, 1)
-    for li in (0, 686):
-        x = G.sample(kappa, beta, k, seed=0, n_samples=1, node_range=(li, li + 1)).cpu().numpy()
-        A = fem.operator(prob.ML, prob.G, prob.kappa, prob.plan.c_I[li], prob.plan.c_L[li])
-        res = (A @ x.T).T - W
-        assert (np.linalg.norm(res, axis=1) / np.linalg.norm(W, axis=1)).max() <= 1e-9, f"node {li}"
+    ref, _, _ = solve.sample(g, h, kappa, beta, k, 0, 64, samples=picks)
+    assert _rel(got, ref).max() <= FIELD_TOL
+
+
+@pytest.mark.parametrize("n_samples", [20, 40])
+def test_long_edges_direct_accumulation(n_samples):
+    """Edges with 1199 / 899 / 300 interior nodes (l = 6, 4.5, 1.505 at h = 0.005) next to short
+    ones: with >= 17 samples the recovery's shared-memory output tile cannot hold the long edges,
+    which then accumulate straight into u (sweep_impl.cuh); fields vs the oracle."""
+    g = MetricGraph(5, np.array([0, 1, 2, 0, 3, 3, 2]), np.array([1, 2, 3, 2, 4, 4, 2]),
+                    np.array([6.0, 4.5, 1.505, 0.3, 0.02, 0.9, 0.6]))
+    h, kappa, beta, k = 0.005, 2.0, 0.7, 0.35
+    G = _graph(g, h)
+    u, st = G.sample(kappa, beta, k, seed=6, n_samples=n_samples, return_stats=True)
+    assert st["n_unconverged"] == 0
+    picks = sorted({0, 17, n_samples - 1})
+    ref, _, _ = solve.sample(g, h, kappa, beta, k, 6, n_samples, samples=picks)
+    assert _rel(u.cpu().numpy()[picks], ref).max() <= FIELD_TOL
 
 
 # ----------------------------------------------------------------------------- NEXT-1 strong-error study

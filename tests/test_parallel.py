@@ -22,10 +22,14 @@ def test_shards_cover_every_unit_once(world, S, L):
         if not sh.active:
             continue
         (s0, s1), (l0, l1) = sh.sample_range, sh.node_range
-        seen[s0:s1, l0:l1] += 1
+        seen[s0:s1, l0:l1:sh.node_stride] += 1
         roots += sh.is_root
     assert np.all(seen == 1)
     assert roots == shard(world, 0, S, L).n_sample_shards
+    # round-robin node shards: their sizes differ by at most one node
+    sizes = [len(range(*shard(world, r, S, L).node_range, shard(world, r, S, L).node_stride))
+             for r in range(world) if shard(world, r, S, L).active]
+    assert max(sizes) - min(sizes) <= 1
     for ranks in node_groups(world, S, L):
         assert shard(world, ranks[0], S, L).is_root
 
@@ -47,7 +51,7 @@ def _worker(rank, world, port, S, L, out):
     l0, l1 = sh.node_range
     part = torch.zeros(s1 - s0, 4, dtype=torch.float64)
     for s in range(s0, s1):
-        part[s - s0] = sum((l + 1) * (s + 1) for l in range(l0, l1))
+        part[s - s0] = sum((l + 1) * (s + 1) for l in range(l0, l1, sh.node_stride))
     res = reduce_partial(part, sh, groups)
     if res is not None:
         out[rank] = (s0, s1, res.numpy().copy())
@@ -77,7 +81,7 @@ def test_library_shard_matches_host_logic(world, S, L):
     for r in range(world):
         sh = shard(world, r, S, L)
         srange, nrange, root, active, is_root, pl = dist_shard(world, r, S, L)
-        assert active == sh.active and is_root == sh.is_root and pl == sh.n_node_shards
+        assert active == sh.active and is_root == sh.is_root and pl == sh.n_node_shards == sh.node_stride
         if sh.active:
             assert srange == sh.sample_range and nrange == sh.node_range
             assert root == sh.group_index * sh.n_node_shards
