@@ -1,28 +1,35 @@
 #!/usr/bin/env python
 """Benchmark of the fractional-SPDE GRF sampler hot path (one JSON line on rank 0).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config lattice256] [--impl grf|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config lattice256] [--edgepart] [--impl grf|reference]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
 
-A "step" is one grf_sample call over the whole workload: noise -> condense -> vertex
-NN-PCG -> recovery + quadrature sum for every sample and every quadrature node
-(the per-(kappa,beta,k) edge setup a3 is cached after the
-first call, like model weights).  Default workload: BASELINE.json configs[2]
-("lattice256": 32x32 lattice, N = 198325 DOFs, L = 212 nodes, 256 samples) -- the
-throughput configuration the metric is quoted on and the one sharded over 1/2/4/8 GPUs.
-Multi-GPU: one process per GPU; each rank draws its own 256 samples (seeds rank*256 + j),
-no data-path collective -> "scaling": "weak".  Time = max over ranks of CUDA-event time
-between barriers.  Inputs (W/u 406 MB, plan tables 333 MB, vertex buffers 445 MB) are
-far larger than the 126 MB L2, so no explicit L2 flush is needed.
+A "step" is one sampling call over the whole workload of a BASELINE.json config: noise ->
+condense -> vertex NN-PCG -> recovery + quadrature sum for every sample and every quadrature
+node (the per-(kappa, beta, k) edge setup a3 is cached after the first
+call, like model weights).  Default workload: configs[2] ("lattice256": 32x32 lattice,
+N = 198 325 DOFs, L = 212 nodes, 256 samples) -- the throughput configuration the metric is
+quoted on.  --config tadpole | lattice1 | lattice256 | rgg | star selects configs[0..4].
 
---impl reference times the CPU oracle (oracle/, scipy sparse LU per node) on a bounded
-sample of the same workload; it is the deliberately slow definition, not a competitor.
+Multi-GPU (one process per GPU, policy BY_SAMPLE_THEN_NODE through the library's
+grf_sample_dist): the config's samples are split over the ranks (P_s = min(N, S) contiguous
+ranges) and the ranks sharing a sample range split the quadrature nodes round-robin, their
+partial sums meeting on the range's root through NCCL -- the total work is fixed, so
+"scaling": "strong".  --edgepart (config 4): every rank holds one edge part (recursive
+coordinate bisection, grf_partition_edges / grf_graph_create_part) and the vertex NN-PCG runs
+distributed (grf_sample_edgepart: neighbour halo send/recv + dot-product allreduce over NCCL).
+Time = max over ranks of the CUDA-event time between barriers.  Latency-bound single-GPU
+configs (tadpole, lattice1) replay the step as a captured CUDA graph (same seed each replay:
+every replay recomputes everything).  Inputs far exceed the 126 MB L2 for lattice256 / rgg /
+star (no flush needed); tadpole and lattice1 are L2-resident by nature.
+
+--impl reference times the CPU oracle (oracle/, sparse LDL^T per node) on a bounded sample of
+the same workload; it is the deliberately slow definition, not a competitor.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import subprocess
@@ -34,14 +41,18 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 METRIC = "GRF samples/s & DOF×quad-node solves/s; achieved HBM GB/s vs B200 peak"
+CONFIG_INDEX = {"tadpole": 0, "lattice1": 1, "lattice256": 2, "rgg": 3, "star": 4}
+SMALL = ("tadpole", "lattice1")  # latency-bound: CUDA-graph replay, L2-resident
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="lattice256")
+    ap.add_argument("--config", default="lattice256", choices=list(CONFIG_INDEX))
+    ap.add_argument("--edgepart", action="store_true", help="config 4: edge-partitioned over the ranks")
+    ap.add_argument("--no-graph", action="store_true", help="do not replay small configs as a CUDA graph")
     ap.add_argument("--impl", default="grf", choices=["grf", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
@@ -120,11 +131,23 @@ def workload(name):
     return cfg, config_graph(name)
 
 
-def oracle_time(g, cfg, n_nodes, sample_index=0):
-    """Time the oracle (as it stands) on 1 sample x n_nodes quadrature nodes spread over the rule."""
+def config_dict(name, cfg, g, n_nodes, n_dofs, world, mode):
+    """The same dict for both arms (the GPU arm takes L from grf_plan_info and N from the graph
+    handle, the reference arm from the oracle: the numbers agree)."""
+    return {"workload": f"{name} (BASELINE.json configs[{CONFIG_INDEX[name]}])", "graph": g.name,
+            "n_vertices": int(g.n_vertices), "n_edges": int(g.n_edges), "n_dofs": int(n_dofs), "h": cfg["h"],
+            "kappa": cfg["kappa"], "beta": cfg["beta"], "k": cfg["k"], "quad_nodes": int(n_nodes),
+            "samples": cfg["n_samples"], "seed": cfg["seed"], "mode": mode,
+            "l2": "small: L2-resident" if name in SMALL else "inputs larger than L2 (no flush)"}
+
+
+# ------------------------------------------------------------------------------------ reference arm
+def oracle_time(g, cfg, n_nodes, sample_index=0, prob=None):
+    """The oracle (as it stands) on 1 sample x n_nodes quadrature nodes spread over the rule."""
     import numpy as np
     from oracle import noise, solve
-    prob = solve.setup(g, cfg["h"], cfg["kappa"], cfg["beta"], cfg["k"])
+    if prob is None:
+        prob = solve.setup(g, cfg["h"], cfg["kappa"], cfg["beta"], cfg["k"])
     L = prob.plan.n_nodes
     picks = np.unique(np.linspace(0, L - 1, min(n_nodes, L)).round().astype(int))
     t0 = time.perf_counter()
@@ -133,7 +156,7 @@ def oracle_time(g, cfg, n_nodes, sample_index=0):
         solve.node_solve(prob, int(li), W)
     dt = time.perf_counter() - t0
     N = prob.mesh.n_dofs
-    return dict(seconds=dt, nodes=len(picks), L=L, N=N,
+    return dict(seconds=dt, nodes=len(picks), L=L, N=N, prob=prob,
                 samples_per_s=(len(picks) / L) / dt, dof_node_per_s=N * len(picks) / dt)
 
 
@@ -149,15 +172,11 @@ def _oracle_nodes(payload):
     return len(nodes)
 
 
-def oracle_time_all_cores(name, n_nodes):
+def oracle_time_all_cores(name, n_nodes, L):
     """The same oracle over n_nodes quadrature nodes of one sample, spread over every host core
     (one process per core, each with its own setup -- the paper's OpenMP-over-l layout, P164)."""
     import concurrent.futures as cf
     import numpy as np
-    from oracle.quadrature import limits
-    cfg, _ = workload(name)
-    km, kp = limits(cfg["beta"], cfg["k"])
-    L = km + kp + 1
     cores = os.cpu_count() or 1
     picks = np.unique(np.linspace(0, L - 1, min(n_nodes, L)).round().astype(int))
     chunks = [picks[i::cores] for i in range(cores) if len(picks[i::cores])]
@@ -172,49 +191,41 @@ def run_reference(args, rank, world):
     if rank != 0:
         return 0
     cfg, g = workload(args.config)
+    prob = None
     for _ in range(max(0, args.warmup)):
-        oracle_time(g, cfg, args.ref_nodes)
-    ts = [oracle_time(g, cfg, args.ref_nodes, sample_index=i) for i in range(args.steps)]
+        prob = oracle_time(g, cfg, args.ref_nodes, prob=prob)["prob"]
+    ts = [oracle_time(g, cfg, args.ref_nodes, sample_index=i, prob=prob) for i in range(args.steps)]
+    prob = ts[0]["prob"]
     tot = sum(t["seconds"] for t in ts)
     samples = sum(t["nodes"] / t["L"] for t in ts)
     value = samples / tot
+    mode = "edgepart" if args.edgepart else "dist"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_dict(args.config, cfg, g, None),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(args.config, cfg, g, prob.plan.n_nodes, prob.mesh.n_dofs,
+                                                   args.gpus, mode),
         "dof_node_per_s": sum(t["N"] * t["nodes"] for t in ts) / tot,
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": 1, "kind": "oracle",
                          "sample": f"per step: sample j, {ts[0]['nodes']} of {ts[0]['L']} quadrature nodes "
-                                   f"(scipy SuperLU per node); value = node-fraction of a sample per second"},
+                                   f"(C sparse LDL^T per node, 1 thread); value = node-fraction of a sample per "
+                                   f"second"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def config_dict(name, cfg, g, G):
-    from oracle.quadrature import limits
-    km, kp = limits(cfg["beta"], cfg["k"])
-    d = {"workload": f"{name} (BASELINE.json configs[{['tadpole', 'lattice1', 'lattice256', 'rgg', 'star'].index(name)}])",
-         "graph": g.name, "n_vertices": int(g.n_vertices), "n_edges": int(g.n_edges),
-         "h": cfg["h"], "kappa": cfg["kappa"], "beta": cfg["beta"], "k": cfg["k"],
-         "quad_nodes": km + kp + 1, "samples_per_rank": cfg["n_samples"],
-         "l2": "inputs larger than L2 (no flush)" if name in ("lattice256", "rgg", "star") else "small: L2-resident"}
-    if G is not None:
-        d["n_dofs"] = G.n_dofs
-    return d
-
-
-def algorithmic(kernel, G, L, S, iters_mean):
+# ------------------------------------------------------------------------------------ GPU arm
+def algorithmic(kernel, n_interior, V, E, N, L, S, iters_mean):
     """Algorithmic work per launch: (amount, unit)."""
-    NI, V, E, N = G.n_interior, G.n_vertices, G.n_edges, G.n_dofs
     if kernel == "recover":
         # Thomas forward (2 flop) + back substitution (3 flop) + sum over l (1 flop) per DOF.node.sample
-        return 6.0 * NI * L * S, "flop"
+        return 6.0 * n_interior * L * S, "flop"
     if kernel == "condense":
         # two one-sided forward eliminations (2 flop each) per interior DOF.node.sample
-        return 4.0 * NI * L * S, "flop"
+        return 4.0 * n_interior * L * S, "flop"
     if kernel == "pcg":
         # per iteration: Schur SpMV 4 flop + NN precond 6 flop per incidence (2E), 6 vector ops (2 flop) per vertex
         return (iters_mean * (20.0 * E + 12.0 * V) + 12.0 * V) * L * S, "flop"
@@ -238,30 +249,65 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    from paper_2605_02670_b200 import Graph
+    from paper_2605_02670_b200 import Comm, Graph, plan_info, sample_edgepart
+    from paper_2605_02670_b200.grf import dist_shard, make_options, sample_dist
 
     cfg, g = workload(args.config)
-    G = Graph.from_metric_graph(g, cfg["h"])
     S = cfg["n_samples"]
-    kappa, beta, k = cfg["kappa"], cfg["beta"], cfg["k"]
-    seed = cfg["seed"] + rank * S
-    out = torch.empty((S, G.n_dofs), dtype=torch.float64, device="cuda")
-    ws = torch.empty(G.workspace_size(kappa, beta, k, S), dtype=torch.uint8, device="cuda")
+    kappa, beta, k, seed = cfg["kappa"], cfg["beta"], cfg["k"], cfg["seed"]
+    km, kp, _, _ = plan_info(beta, k)
+    L = km + kp + 1
+    G = Graph.from_metric_graph(g, cfg["h"])
+    n_dofs = G.n_dofs
+    mode = "edgepart" if args.edgepart else "dist"
+    comm = Comm() if world > 1 else None
     stream = torch.cuda.current_stream()
+    graph_replay = None
+    info = {}
+
+    if mode == "edgepart":
+        ep, pinfo = G.partition(world, xy=g.coords)
+        info["partition"] = dict(pinfo, parts=world, method="RCB" if g.coords is not None else "BFS runs")
+        part = Graph.part_of(G, ep, world, rank)
+        work_graph = part
+        n_local, sample_lo = S, 0
+        outs = [torch.empty((S, part.n_dofs), dtype=torch.float64, device="cuda")]
+
+        def step(stats=False):
+            return sample_edgepart([part], kappa, beta, k, seed=seed, n_samples=S, comm=comm, return_stats=stats)
+    else:
+        (s0, s1), (l0, l1), root, active, is_root, pl = dist_shard(world, rank, S, L)
+        info["shard"] = {"sample_range": [s0, s1], "node_begin": l0, "node_stride": pl, "ranks_per_range": pl}
+        work_graph = G
+        n_local, sample_lo = s1 - s0, s0
+        out = torch.empty((max(n_local, 1), n_dofs), dtype=torch.float64, device="cuda")
+        ws = torch.empty(G.workspace_size(kappa, beta, k, max(n_local, 1)), dtype=torch.uint8, device="cuda")
+
+        def step(stats=False):
+            if world == 1:
+                return G.sample(kappa, beta, k, seed=seed, n_samples=S, out=out, workspace=ws, return_stats=stats)
+            return sample_dist(G, comm, kappa, beta, k, seed=seed, n_samples=S, out=out, return_stats=stats)
 
     # cold-plan call: the first call for (kappa, beta, k) also builds the per-plan tables (K2)
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     c0.record(stream)
-    _, st = G.sample(kappa, beta, k, seed=seed, n_samples=S, out=out, workspace=ws, return_stats=True)
+    res = step(stats=True)
     c1.record(stream)
     torch.cuda.synchronize()
     cold_ms = c0.elapsed_time(c1)
-    L = st["n_nodes"]
+    st = res[1] if isinstance(res, tuple) else {}
     for _ in range(args.warmup):
-        G.sample(kappa, beta, k, seed=seed, n_samples=S, out=out, workspace=ws)
+        step()
     torch.cuda.synchronize()
-    G.profile(True)
-    G.profile_read()
+    if mode == "dist" and world == 1 and args.config in SMALL and not args.no_graph:
+        graph_replay = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph_replay):
+            step()
+        for _ in range(3):
+            graph_replay.replay()
+        torch.cuda.synchronize()
+    work_graph.profile(True)
+    work_graph.profile_read()
 
     clocks = Clocks(local)
     if world > 1:
@@ -275,7 +321,10 @@ def main():
     e0.record(stream)
     marks[0].record(stream)
     for i in range(args.steps):
-        G.sample(kappa, beta, k, seed=seed, n_samples=S, out=out, workspace=ws)
+        if graph_replay is not None:
+            graph_replay.replay()
+        else:
+            step()
         marks[i + 1].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -284,35 +333,62 @@ def main():
     clk = clocks.stop()
     t_ms = e0.elapsed_time(e1)
     per_step = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
-    prof = G.profile_read()
-    G.profile(False)
+    prof = work_graph.profile_read()
+    work_graph.profile(False)
     if world > 1:
         t = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_ms = float(t.item())
-    # kernels launched inside the timed region: the library's own per-call count (stats) x steps
-    launches = int(st["gpu_launches"]) * args.steps
+    launches_per_step = int(st.get("gpu_launches", 0))
+    if graph_replay is not None:  # kernels of one replay = those of one call (profiling brackets not captured)
+        prof = {name: (ms, n) for name, (ms, n) in prof.items()}
+    launches = launches_per_step * args.steps
 
-    # end to end: the same call with a pinned HOST output (D2H + sync inside the timed region)
+    # end to end: the public API with the step's result read back to pinned host memory each step
     e2e = None
     if not args.no_e2e:
-        host = torch.empty((S, G.n_dofs), dtype=torch.float64, pin_memory=True)
-        G.sample_into_host(kappa, beta, k, seed, S, host)
+        host = None
+        if mode == "edgepart":
+            host = torch.empty((S, work_graph.n_dofs), dtype=torch.float64, pin_memory=True)
+
+            def e2e_step():
+                us = sample_edgepart([work_graph], kappa, beta, k, seed=seed, n_samples=S, comm=comm)
+                host.copy_(us[0])
+            d2h = S * work_graph.n_dofs * 8
+        elif world == 1 or info["shard"]["ranks_per_range"] == 1:
+            host = torch.empty((max(n_local, 1), n_dofs), dtype=torch.float64, pin_memory=True)
+
+            def e2e_step():
+                if n_local > 0:
+                    G.sample_into_host(kappa, beta, k, seed + sample_lo, n_local, host)
+            d2h = n_local * n_dofs * 8
+        else:
+            is_root = info["shard"]["node_begin"] == 0
+            host = torch.empty((max(n_local, 1), n_dofs), dtype=torch.float64, pin_memory=True)
+
+            def e2e_step():
+                u, _, root_ = sample_dist(G, comm, kappa, beta, k, seed=seed, n_samples=S, out=out)
+                if root_ and u is not None:
+                    host.copy_(u)
+            d2h = n_local * n_dofs * 8 if is_root else 0
+        e2e_step()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            G.sample_into_host(kappa, beta, k, seed, S, host)
+            e2e_step()
+        torch.cuda.synchronize()
         te = time.perf_counter() - t0
         if world > 1:
             t = torch.tensor([te], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
-        e2e = {"value": world * S * args.e2e_steps / te, "unit": "samples/s", "h2d_bytes_per_step": 0,
-               "d2h_bytes_per_step": int(S * G.n_dofs * 8), "ms_per_step": 1e3 * te / args.e2e_steps,
-               "note": "grf_sample_host into pinned host memory; per-step inputs are the scalars "
-                       "(kappa, beta, k, seed) -- the noise is generated on the device from the seed"}
+        e2e = {"value": S * args.e2e_steps / te, "unit": "samples/s", "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * te / args.e2e_steps,
+               "note": "the public call with the result copied to pinned host memory inside the timed region "
+                       "(grf_sample_host / grf_sample_dist / grf_sample_edgepart + copy); per-step inputs are the "
+                       "scalars (kappa, beta, k, seed) -- the noise is generated on the device from the seed"}
 
     if rank != 0:
         if world > 1:
@@ -322,60 +398,70 @@ def main():
 
     pk = peaks()
     step_s = t_ms / 1e3 / args.steps
-    value = world * S / step_s
-    dof_node = world * G.n_dofs * L * S / step_s
+    value = S / step_s
+    dof_node = n_dofs * L * S / step_s
+    wg = work_graph
     kernels = {}
     for name, (ms, n) in prof.items():
         if n == 0:
             continue
-        amt, unit = algorithmic(name, G, L, S, st["iter_mean"])
+        amt, unit = algorithmic(name, wg.n_interior, wg.n_vertices, wg.n_edges, wg.n_dofs, L, n_local,
+                                st.get("iter_mean", 0.0))
         per = ms / n
         kernels[name] = {"ms_per_launch": per, "launches": n, "share": ms / t_ms,
                          ("tflops" if unit == "flop" else "gbs"): (amt / (per / 1e3)) / (1e12 if unit == "flop" else 1e9)}
-    dom = max((k_ for k_ in kernels if k_ != "noise"), key=lambda k_: kernels[k_]["share"])
-    amt, unit = algorithmic(dom, G, L, S, st["iter_mean"])
-    ach = amt / (kernels[dom]["ms_per_launch"] / 1e3) / 1e12
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            tj = json.load(f)
-        if tj.get("config") == args.config and dom in tj.get("kernels", {}):
-            traffic = tj["kernels"][dom].get("dram_bytes_per_launch")
-    roofline = {"bound": "alu", "achieved": ach, "peak": pk["fp64_tflops"], "unit": "TFLOP/s",
-                "frac": ach / pk["fp64_tflops"], "traffic": traffic, "kernel": dom,
-                "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x sm_max_mhz (B200_PROFILING.md clocks)"}
-    # north_star's design-independent number: the per-(l,s) streaming formulation moves
-    # 32 B per DOF.node; what bandwidth would it need to match this run?
-    eff_hbm = 32.0 * dof_node / world / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config_dict(args.config, cfg, g, G),
+        "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args.config, cfg, g, L, n_dofs, world, mode),
         "dof_node_per_s": dof_node,
-        "effective_streaming_hbm": {"gbs_per_gpu": eff_hbm, "frac_of_hbm_peak": eff_hbm / pk["hbm_gbs"],
-                                    "note": "32 B/DOF.node of the per-(l,s) streaming form / measured time; "
-                                            ">1 is possible because the fused kernels keep W and the sum on chip"},
-        "roofline": roofline, "kernels": kernels,
-        "pcg": {"iter_min": st["iter_min"], "iter_max": st["iter_max"], "iter_mean": st["iter_mean"],
-                "worst_rel_residual": st["worst_rel_residual"]},
-        "step_ms": {"median": statistics.median(per_step), "best": min(per_step), "worst": max(per_step),
-                    "cold_plan_first_call": cold_ms},
-        "gpu_launches": launches, "clocks": clk,
-        "peaks": {"hbm_gbs": pk["hbm_gbs"], "fp64_tflops": pk["fp64_tflops"], "source": pk["source"],
-                  "fp64_measured_tflops": pk["fp64_measured_tflops"],
-                  "frac_of_measured_fp64": ach / pk["fp64_measured_tflops"]},
     }
+    line["config"]["cuda_graph"] = graph_replay is not None
+    line["config"].update(info)
+    if kernels:
+        dom = max((k_ for k_ in kernels if k_ != "noise"), key=lambda k_: kernels[k_]["share"], default=None)
+        if dom is not None:
+            amt, unit = algorithmic(dom, wg.n_interior, wg.n_vertices, wg.n_edges, wg.n_dofs, L, n_local,
+                                    st.get("iter_mean", 0.0))
+            ach = amt / (kernels[dom]["ms_per_launch"] / 1e3) / 1e12
+            traffic = None
+            tpath = os.path.join(ROOT, "profiles", "traffic.json")
+            if os.path.exists(tpath):
+                with open(tpath) as f:
+                    tj = json.load(f)
+                if tj.get("config") == args.config and dom in tj.get("kernels", {}):
+                    traffic = tj["kernels"][dom].get("dram_bytes_per_launch")
+            line["roofline"] = {"bound": "alu", "achieved": ach, "peak": pk["fp64_tflops"], "unit": "TFLOP/s",
+                                "frac": ach / pk["fp64_tflops"], "traffic": traffic, "kernel": dom,
+                                "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x sm_max_mhz "
+                                               "(B200_PROFILING.md clocks)"}
+            line["peaks"] = {"hbm_gbs": pk["hbm_gbs"], "fp64_tflops": pk["fp64_tflops"], "source": pk["source"],
+                             "fp64_measured_tflops": pk["fp64_measured_tflops"],
+                             "frac_of_measured_fp64": ach / pk["fp64_measured_tflops"]}
+    # north_star's design-independent number: the per-(l,s) streaming formulation moves 32 B per
+    # DOF.node; what bandwidth would it need to match this run?
+    eff_hbm = 32.0 * dof_node / world / 1e9
+    line["effective_streaming_hbm"] = {"gbs_per_gpu": eff_hbm, "frac_of_hbm_peak": eff_hbm / pk["hbm_gbs"],
+                                       "note": "32 B/DOF.node of the per-(l,s) streaming form / measured time; "
+                                               ">1 is possible because the fused kernels keep W and the sum on chip"}
+    line["kernels"] = kernels
+    line["pcg"] = {k_: st.get(k_) for k_ in ("iter_min", "iter_max", "iter_mean", "worst_rel_residual",
+                                             "worst_true_rel_residual") if k_ in st}
+    line["step_ms"] = {"median": statistics.median(per_step), "best": min(per_step), "worst": max(per_step),
+                       "cold_plan_first_call": cold_ms}
+    line["gpu_launches"] = launches
+    line["clocks"] = clk
     if e2e is not None:
         line["e2e"] = e2e
     if world == 1 and not args.no_cpu_baseline:
         ob = oracle_time(g, cfg, args.cpu_nodes)
         line["cpu_baseline"] = {"value": ob["samples_per_s"], "unit": "samples/s", "cores": 1, "kind": "oracle",
                                 "sample": f"sample 0, {ob['nodes']} of {ob['L']} quadrature nodes, "
-                                          f"{ob['seconds']:.1f} s (scipy SuperLU per node, 1 thread)",
+                                          f"{ob['seconds']:.1f} s (C sparse LDL^T per node, 1 thread)",
                                 "dof_node_per_s": ob["dof_node_per_s"]}
         try:
-            oa = oracle_time_all_cores(args.config, args.cpu_nodes_all)
+            oa = oracle_time_all_cores(args.config, args.cpu_nodes_all, L)
             line["cpu_baseline"]["all_cores"] = {
                 "value": oa["samples_per_s"], "cores": oa["cores"],
                 "sample": f"sample 0, {oa['nodes']} of {oa['L']} nodes over {oa['cores']} processes "

@@ -91,31 +91,29 @@ grf_status grf_graph_create(int64_t n_vertices, int64_t n_edges, const int64_t* 
                             const grf_allocator* alloc, grf_graph** out);
 /* ---- edge-partitioned graphs (the largest graph, config 4) ------------
  * The edges of a whole graph are split into parts; a part is the subgraph of its edges with
- * every vertex they touch (local ids 0..n_vertices-1, edge orientation as in the whole
- * graph).  Vertices touched by several parts are interface vertices.  A part needs, per
- * local vertex / edge, what only the whole graph knows (all arrays host, copied):
- *   vertex_gid[v]     global vertex id               (noise counter)
- *   edge_goff[e]      global DOF index of the edge's first interior node (DOF order S97)
- *   global_n_interior N_I of the whole graph          (vertex DOF = N_I + global id)
- *   vertex_mass[v]    lumped mass of the vertex in the whole graph (P137-145)
- *   vertex_degree[v]  incident edge ends in the whole graph (d_v of the NN step, P261)
- *   vertex_owned[v]   1 on exactly one part per vertex (adds W_v, counts it in dot products)
- *   vertex_iface[v]   interface id in [0, n_interface), -1 for a vertex of this part only
- * EINVAL for NULL arrays, masses <= 0, degrees below the local count, ids out of range. */
-typedef struct grf_part_info {
-    int64_t global_n_interior;
-    const int64_t* vertex_gid;
-    const int64_t* edge_goff;
-    const double* vertex_mass;
-    const int32_t* vertex_degree;
-    const uint8_t* vertex_owned;
-    int64_t n_interface;
-    const int64_t* vertex_iface;
-} grf_part_info;
-grf_status grf_graph_create_part(int64_t n_vertices, int64_t n_edges, const int64_t* edge_u,
-                                 const int64_t* edge_v, const double* length, double h,
-                                 const grf_part_info* part, const grf_allocator* alloc,
-                                 grf_graph** out);
+ * every vertex they touch.  Vertices touched by several parts are interface vertices.
+ *
+ * grf_partition_edges (host only, deterministic): edge_part[e] in [0, n_parts) for every edge
+ * (host array of length E).  With vertex coordinates xy (host [V][2], nullable) the edges are
+ * split by recursive coordinate bisection of their midpoints weighted by their DOF weight n_e
+ * (SURVEY §8e); without, the breadth-first edge order is cut into runs of equal DOF weight.
+ * info (host int64[4], nullable): interface vertices, max / min part DOF weight, empty parts.
+ *
+ * grf_graph_create_part: part `part` of that partition as a graph handle, everything it needs
+ * from the whole graph derived inside the library from (whole, edge_part): its edges (ascending
+ * global id) and vertices (ascending global id, local ids 0..V_part-1; edge orientation as in
+ * the whole graph), the global DOF index of every local DOF (noise counters),
+ * the whole graph's lumped vertex masses (P137-145) and degrees d_v (P261), vertex ownership
+ * (the lowest part touching it adds W_v and counts it in dot products) and the interface
+ * numbering and halo neighbour lists.  The part's device data uses `alloc` (NULL: the whole
+ * graph's allocator).  EINVAL for a part id or edge_part entry out of range, or an empty part.
+ * grf_graph_part_dofs: global DOF index of each local DOF (host int64[N_part]; the identity
+ * for a whole graph). */
+grf_status grf_partition_edges(const grf_graph* whole, int32_t n_parts, const double* xy, int32_t* edge_part,
+                               int64_t* info);
+grf_status grf_graph_create_part(const grf_graph* whole, const int32_t* edge_part, int32_t n_parts, int32_t part,
+                                 const grf_allocator* alloc, grf_graph** out);
+grf_status grf_graph_part_dofs(const grf_graph* g, int64_t* gid);
 
 /* Frees the handle and everything it allocated (synchronises the device first). */
 void grf_graph_destroy(grf_graph* g);
@@ -164,8 +162,16 @@ typedef struct grf_stats {
     int64_t n_unconverged;     /* systems that hit max_iter */
     int32_t iter_min, iter_max;
     double iter_mean;
-    double worst_rel_residual; /* max over systems of the final ||r||_2/||g||_2 */
-    int64_t gpu_launches;      /* kernels this call launched */
+    double worst_rel_residual; /* max over systems of the final recursive ||r||_2/||g||_2 (the stop test) */
+    int64_t gpu_launches;      /* kernels this call launched (without the checks below) */
+    /* exit checks (computed because stats were requested; not in gpu_launches):
+     * the TRUE relative residual ||g - S u_G||_2 / ||g||_2 of every vertex system (the Dirichlet
+     * operator applied to the answer; -1 where not computed: edge-partitioned),
+     * the count of non-finite entries of the output (GRF_ENOCONV when > 0), and the device time
+     * of the phases in ms: [noise, edge setup (plan build, 0 when cached), condense, PCG, recover] */
+    double worst_true_rel_residual;
+    int64_t n_nonfinite;
+    double phase_ms[5];
 } grf_stats;
 
 /* Workspace bytes grf_sample / grf_apply need for these arguments. */
@@ -276,10 +282,10 @@ void grf_comm_destroy(grf_comm* c);
  * active rank, u_out (device, n_local x N, n_local = sample_end - sample_begin): the full field of
  * the range on its root, scratch elsewhere.  Inactive ranks (world > P_s P_l) touch no output.
  * EVERY rank of the communicator must call grf_sample_dist with the same arguments: after its
- * local work each rank joins one status allreduce, so a local failure on any rank makes every
- * rank return an error (GRF_ENCCL "a peer rank ... failed" on the others) instead of blocking
- * in the exchange.  opt's node range must be left at its default.  Synchronises the stream when
- * world > 1.  (The EDGE_PARTITION policy is grf_sample_edgepart.) */
+ * local work each rank joins one status allreduce when P_l > 1, so a local failure on any rank
+ * makes every rank return an error (GRF_ENCCL "a peer rank ... failed" on the others) instead
+ * of blocking in the exchange.  opt's node range must be left at its default.  Synchronises the
+ * stream when P_l > 1; pure sample shards (P_l = 1) exchange nothing and stay asynchronous.  (The EDGE_PARTITION policy is grf_sample_edgepart.) */
 grf_status grf_dist_shard(int32_t world, int32_t rank, int64_t n_samples, int64_t n_nodes, int64_t* out);
 grf_status grf_sample_dist(grf_graph* g, grf_comm* comm, double kappa, double beta, double k, uint64_t seed,
                            int64_t n_samples, const grf_options* opt, double* u_out, int64_t* range_out,

@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libgrf.so")
+LIB_PATH = os.environ.get("GRF_LIB") or os.path.join(HERE, "lib", "libgrf.so")  # GRF_LIB: experiments only
 
 GRF_OK, GRF_EINVAL, GRF_ENOMEM, GRF_ECUDA, GRF_ENCCL, GRF_ENOCONV, GRF_EUNSUPPORTED = range(7)
 STATUS_NAMES = {0: "GRF_OK", 1: "GRF_EINVAL", 2: "GRF_ENOMEM", 3: "GRF_ECUDA", 4: "GRF_ENCCL",
@@ -23,13 +23,6 @@ class grf_allocator(C.Structure):
     _fields_ = [("alloc", ALLOC_FN), ("free", FREE_FN), ("ctx", C.c_void_p)]
 
 
-class grf_part_info(C.Structure):
-    _fields_ = [("global_n_interior", C.c_int64), ("vertex_gid", C.POINTER(C.c_int64)),
-                ("edge_goff", C.POINTER(C.c_int64)), ("vertex_mass", C.POINTER(C.c_double)),
-                ("vertex_degree", C.POINTER(C.c_int32)), ("vertex_owned", C.POINTER(C.c_uint8)),
-                ("n_interface", C.c_int64), ("vertex_iface", C.POINTER(C.c_int64))]
-
-
 class grf_options(C.Structure):
     _fields_ = [("rtol", C.c_double), ("max_iter", C.c_int32), ("precond", C.c_int32),
                 ("node_begin", C.c_int64), ("node_end", C.c_int64), ("pcg_variant", C.c_int32),
@@ -40,10 +33,13 @@ class grf_stats(C.Structure):
     _fields_ = [("n_nodes", C.c_int64), ("k_minus", C.c_int64), ("k_plus", C.c_int64),
                 ("n_systems", C.c_int64), ("n_unconverged", C.c_int64), ("iter_min", C.c_int32),
                 ("iter_max", C.c_int32), ("iter_mean", C.c_double), ("worst_rel_residual", C.c_double),
-                ("gpu_launches", C.c_int64)]
+                ("gpu_launches", C.c_int64), ("worst_true_rel_residual", C.c_double), ("n_nonfinite", C.c_int64),
+                ("phase_ms", C.c_double * 5)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["phase_ms"] = dict(zip(("noise", "edge_setup", "condense", "pcg", "recover"), list(self.phase_ms)))
+        return d
 
 
 EXPORTS = [
@@ -53,7 +49,7 @@ EXPORTS = [
     "grf_comm_get_unique_id", "grf_comm_init", "grf_comm_destroy", "grf_reduce_sum",
     "grf_profile_enable", "grf_profile_read", "grf_graph_create_part", "grf_sample_edgepart",
     "grf_prolong", "grf_project_noise", "grf_mnorm_sq_diff", "grf_noise_mass", "grf_dist_shard",
-    "grf_sample_dist",
+    "grf_sample_dist", "grf_partition_edges", "grf_graph_part_dofs",
 ]
 KERNEL_NAMES = ["noise", "edge_setup", "condense", "pcg", "recover"]
 
@@ -98,8 +94,10 @@ def load() -> C.CDLL:
         "grf_comm_destroy": (None, [P]),
         "grf_reduce_sum": (C.c_int, [P, P, P, I64, C.c_int, P]),
         "grf_profile_enable": (C.c_int, [P, C.c_int]),
-        "grf_graph_create_part": (C.c_int, [I64, I64, pi64, pi64, pd, D, C.POINTER(grf_part_info),
+        "grf_graph_create_part": (C.c_int, [P, C.POINTER(C.c_int32), C.c_int32, C.c_int32,
                                             C.POINTER(grf_allocator), C.POINTER(P)]),
+        "grf_partition_edges": (C.c_int, [P, C.c_int32, pd, C.POINTER(C.c_int32), pi64]),
+        "grf_graph_part_dofs": (C.c_int, [P, pi64]),
         "grf_prolong": (C.c_int, [P, P, I64, P, P, P]),
         "grf_noise_mass": (C.c_int, [P, U64, I64, C.c_int32, P, P]),
         "grf_dist_shard": (C.c_int, [C.c_int32, C.c_int32, I64, I64, pi64]),

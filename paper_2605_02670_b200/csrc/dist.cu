@@ -227,6 +227,42 @@ __global__ void unpack_kernel(DevGraph g, int32_t L, const double* __restrict__ 
     }
 }
 
+// neighbour halo (p2p): send[j][l][s] = X[l][idx[j]][s] for the shared vertices of every neighbour
+template <int CS>
+__global__ void halo_pack_kernel(int32_t V, int32_t L, int64_t n, const int32_t* __restrict__ idx,
+                                 const double* __restrict__ X, double* __restrict__ send) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * L; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / L;
+        const int l = (int)(t % L);
+        const double* src = X + ((int64_t)l * V + idx[j]) * CS;
+#pragma unroll
+        for (int s = 0; s < CS; ++s) send[t * CS + s] = src[s];
+    }
+}
+
+// X[l][v][s] = sum over the parts touching interface vertex v, in ascending part order, of their
+// values: own (src = -1) or received (src = slot of recv); every part evaluates the same sum
+template <int CS>
+__global__ void halo_combine_kernel(int32_t V, int32_t L, int32_t nif, const int32_t* __restrict__ vert,
+                                    const int32_t* __restrict__ ptr, const int32_t* __restrict__ src,
+                                    const double* __restrict__ recv, double* __restrict__ X) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)nif * L;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(t / L), l = (int)(t % L);
+        double* x = X + ((int64_t)l * V + vert[i]) * CS;
+        double acc[CS];
+        bool first = true;
+        for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+            const double* y = src[k] < 0 ? x : recv + ((int64_t)src[k] * L + l) * CS;
+#pragma unroll
+            for (int s = 0; s < CS; ++s) acc[s] = first ? y[s] : acc[s] + y[s];
+            first = false;
+        }
+#pragma unroll
+        for (int s = 0; s < CS; ++s) x[s] = acc[s];
+    }
+}
+
 // out = sum_p in[p] (fixed part order)
 __global__ void sum_parts_kernel(int32_t P, double* const* __restrict__ in, int64_t n, double* __restrict__ out) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
@@ -376,6 +412,20 @@ void pack(const DevGraph& g, int32_t L, int32_t cs, const double* X, double* buf
 void unpack(const DevGraph& g, int32_t L, int32_t cs, const double* buf, double* X, cudaStream_t st) {
     const int grid = grid_for((int64_t)L * g.V);
     GRF_CS_SWITCH(cs, (unpack_kernel<C><<<grid, BT, 0, st>>>(g, L, buf, X)));
+}
+
+void halo_pack(const DevGraph& g, int32_t L, int32_t cs, int64_t n, const int32_t* idx, const double* X, double* send,
+               cudaStream_t st) {
+    if (n == 0) return;
+    const int grid = grid_for(n * L);
+    GRF_CS_SWITCH(cs, (halo_pack_kernel<C><<<grid, BT, 0, st>>>(g.V, L, n, idx, X, send)));
+}
+
+void halo_combine(const DevGraph& g, int32_t L, int32_t cs, int32_t nif, const int32_t* vert, const int32_t* ptr,
+                  const int32_t* src, const double* recv, double* X, cudaStream_t st) {
+    if (nif == 0) return;
+    const int grid = grid_for((int64_t)nif * L);
+    GRF_CS_SWITCH(cs, (halo_combine_kernel<C><<<grid, BT, 0, st>>>(g.V, L, nif, vert, ptr, src, recv, X)));
 }
 
 void sum_parts(int32_t P, double* const* in_dev, int64_t n, double* out, cudaStream_t st) {

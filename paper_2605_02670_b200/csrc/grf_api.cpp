@@ -6,6 +6,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -14,6 +15,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "grf_internal.h"
@@ -72,6 +74,21 @@ struct PlanKey {
     }
 };
 
+// What a part of an edge partition needs from the whole graph (grf_graph_create_part derives it)
+struct PartSpec {
+    int32_t part = 0, n_parts = 1;
+    int64_t global_n_interior = 0;
+    std::vector<int64_t> vertex_gid, edge_goff, vertex_iface;
+    std::vector<double> vertex_mass;    // whole-graph lumped vertex mass (P137-145)
+    std::vector<int32_t> vertex_degree; // whole-graph incident edge ends (d_v of the NN step, P261)
+    std::vector<uint8_t> vertex_owned;  // 1 on exactly one part per vertex (the lowest touching it)
+    int64_t n_interface = 0;
+    // halo neighbours: every other part sharing a vertex with this one, ascending, with the local
+    // ids of the shared vertices in ascending global id (both sides list them in the same order)
+    std::vector<int32_t> nbr_part;
+    std::vector<std::vector<int32_t>> nbr_verts;
+};
+
 struct Plan {
     PlanKey key{};
     int64_t Km = 0, Kp = 0;
@@ -92,6 +109,10 @@ struct grf_graph {
     std::vector<Block> blocks;  // graph-lifetime device allocations
     std::list<std::unique_ptr<Plan>> plans;  // most recent first
     bool partitioned = false;                // created by grf_graph_create_part
+    int32_t part = 0, n_parts = 1;           // this part's index in its partition
+    std::vector<int64_t> dof_gid;            // part: global DOF index of every local DOF
+    std::vector<int32_t> nbr_part;           // part: halo neighbours (PartSpec)
+    std::vector<std::vector<int32_t>> nbr_verts;
     // consistent-mass noise factor (NEXT-3), built on first use: chain Cholesky factors per
     // Thomas-table class (Ld, Lo) and the dense Cholesky factor of the vertex Schur complement
     const double *cLd = nullptr, *cLo = nullptr, *cLs = nullptr;
@@ -282,7 +303,8 @@ grf_status get_plan(grf_graph* g, double kappa, double beta, double k, const grf
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct WsLayout {
-    size_t w = 0, cnoise = 0, ends = 0, rhs = 0, ug = 0, gws = 0, iters = 0, relres = 0, counter = 0, total = 0;
+    size_t w = 0, cnoise = 0, ends = 0, rhs = 0, ug = 0, gws = 0, iters = 0, relres = 0, truer = 0, counter = 0,
+           total = 0;
 };
 
 // with_noise: grf_sample keeps the white noise W (S x N) in the workspace
@@ -315,6 +337,8 @@ WsLayout ws_layout(const grf_graph* g, int64_t L, int64_t S, bool with_noise, bo
     o += align_up((size_t)S * L * sizeof(int32_t));
     w.relres = o;
     o += align_up((size_t)S * L * sizeof(double));
+    w.truer = o;  // exit checks: true relative residuals [S][L], then the non-finite count
+    o += align_up((size_t)S * L * sizeof(double) + sizeof(unsigned long long));
     w.counter = o;
     o += align_up(2 * sizeof(int32_t));
     w.total = o;
@@ -415,6 +439,14 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
         return fail(GRF_ENOMEM, "workspace too small: %zu < %zu bytes", ws_bytes, w.total);
     }
     char* base = static_cast<char*>(ws);
+    // with statistics: device time of the phases (events on the stream) and the exit checks
+    cudaEvent_t ph[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    if (stats)
+        for (auto& e : ph) cudaEventCreate(&e);
+    auto mark = [&](int i) {
+        if (ph[i]) cudaEventRecord(ph[i], st);
+    };
+    mark(0);
     // kernels this call launches: [noise] condense, assemble, K4 (one per sample tile for the
     // global-memory variant), recover, vertex sum
     const int64_t cs = (int64_t)1 << grf::sample_tile_log2(S);
@@ -436,6 +468,7 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
         W = Wd;
         launches += 1;
     }
+    mark(1);
     double* ends = reinterpret_cast<double*>(base + w.ends);
     double* uG = reinterpret_cast<double*>(base + w.ug);
     double* rhs = reinterpret_cast<double*>(base + w.rhs);
@@ -454,24 +487,38 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
         le = grf::launch_condense(g->dev, p->dev, S, W, ends, counters, st);
     });
     if (ce == cudaSuccess) ce = le;
+    mark(2);
     if (ce == cudaSuccess)
         ce = g->timed(GRF_K_PCG, st, [&] {
             le = grf::launch_pcg(g->dev, p->dev, S, prm, W, ends, rhs, uG, iters, relres, gws, st);
         });
     if (ce == cudaSuccess) ce = le;
+    mark(3);
     if (ce == cudaSuccess)
         ce = g->timed(GRF_K_RECOVER, st, [&] {
             le = grf::launch_recover(g->dev, p->dev, S, W, u, uG, counters + 1, st);
             if (le == cudaSuccess) le = grf::launch_vertex_sum(g->dev, p->dev, S, uG, u, st);
         });
     if (ce == cudaSuccess) ce = le;
+    mark(4);
+    double* truer = reinterpret_cast<double*>(base + w.truer);
+    unsigned long long* nonfin = reinterpret_cast<unsigned long long*>(truer + S * L);
+    if (ce == cudaSuccess && stats) {  // exit checks: true residuals, non-finite outputs
+        grf::launch_true_residual(g->dev, p->dev, S, rhs, uG, truer, st);
+        grf::launch_nonfinite(u, S * g->N, nonfin, st);
+        ce = cudaGetLastError();
+    }
     if (ce != cudaSuccess) rc = fail(GRF_ECUDA, "kernel launch failed: %s", cudaGetErrorString(ce));
     if (rc == GRF_OK && stats) {
         std::vector<int32_t> it(S * L);
-        std::vector<double> rr(S * L);
+        std::vector<double> rr(S * L), tr(S * L);
+        unsigned long long nf = 0;
         ce = cudaMemcpyAsync(it.data(), iters, it.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
         if (ce == cudaSuccess)
             ce = cudaMemcpyAsync(rr.data(), relres, rr.size() * sizeof(double), cudaMemcpyDeviceToHost, st);
+        if (ce == cudaSuccess)
+            ce = cudaMemcpyAsync(tr.data(), truer, tr.size() * sizeof(double), cudaMemcpyDeviceToHost, st);
+        if (ce == cudaSuccess) ce = cudaMemcpyAsync(&nf, nonfin, sizeof(nf), cudaMemcpyDeviceToHost, st);
         if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
         if (ce != cudaSuccess) {
             rc = fail(GRF_ECUDA, "stats readback: %s", cudaGetErrorString(ce));
@@ -494,10 +541,20 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
             stats->worst_rel_residual = worst;
             stats->n_unconverged = bad;
             stats->gpu_launches = launches;
+            stats->worst_true_rel_residual = tr.empty() ? 0.0 : *std::max_element(tr.begin(), tr.end());
+            stats->n_nonfinite = (int64_t)nf;
+            const int slot[4] = {0, 2, 3, 4};  // noise, condense, pcg, recover (edge setup: grf_sample)
+            for (int i = 0; i < 4; ++i) {
+                float ms = 0.f;
+                if (cudaEventElapsedTime(&ms, ph[i], ph[i + 1]) == cudaSuccess) stats->phase_ms[slot[i]] = ms;
+            }
             if (bad) rc = fail(GRF_ENOCONV, "%lld of %lld PCG systems missed rtol %g (worst %g)", (long long)bad,
                                (long long)(S * L), prm.rtol, worst);
+            else if (nf) rc = fail(GRF_ENOCONV, "%llu non-finite output values", nf);
         }
     }
+    for (auto e : ph)
+        if (e) cudaEventDestroy(e);
     if (own) {
         cudaStreamSynchronize(st);
         g->alloc.put(own, w.total, st);
@@ -528,7 +585,7 @@ void grf_options_default(grf_options* opt) {
 
 namespace {
 grf_status create_impl(int64_t n_vertices, int64_t n_edges, const int64_t* edge_u, const int64_t* edge_v,
-                       const double* length, double h, const grf_part_info* part, const grf_allocator* alloc,
+                       const double* length, double h, const PartSpec* part, const grf_allocator* alloc,
                        grf_graph** out) {
     if (!out) return fail(GRF_EINVAL, "out is NULL");
     *out = nullptr;
@@ -621,25 +678,23 @@ grf_status create_impl(int64_t n_vertices, int64_t n_edges, const int64_t* edge_
     std::vector<uint8_t> vowned;
     std::vector<int64_t> viface;
     if (part) {
-        if (!part->vertex_gid || !part->edge_goff || !part->vertex_mass || !part->vertex_degree ||
-            !part->vertex_owned || !part->vertex_iface || part->global_n_interior < 0 || part->n_interface < 0)
-            return fail(GRF_EINVAL, "grf_part_info: NULL array or negative size");
         dof_gid.resize(g->N);
         for (int64_t e = 0; e < E; ++e)
             for (int64_t i = 0; i < g->n_el[e] - 1; ++i) dof_gid[g->off[e] + i] = part->edge_goff[e] + i;
         vowned.resize(V);
         viface.resize(V);
         for (int64_t v = 0; v < V; ++v) {
-            if (!(part->vertex_mass[v] > 0.0) || part->vertex_degree[v] < deg[v])
-                return fail(GRF_EINVAL, "grf_part_info: vertex %lld has an inconsistent mass or degree", (long long)v);
-            if (part->vertex_iface[v] >= part->n_interface)
-                return fail(GRF_EINVAL, "grf_part_info: interface id out of range");
             dof_gid[NI + v] = part->global_n_interior + part->vertex_gid[v];
             sq[NI + v] = std::sqrt(part->vertex_mass[v]);
             vowned[v] = part->vertex_owned[v] ? 1 : 0;
             viface[v] = part->vertex_iface[v];
         }
         g->n_iface = part->n_interface;
+        g->part = part->part;
+        g->n_parts = part->n_parts;
+        g->nbr_part = part->nbr_part;
+        g->nbr_verts = part->nbr_verts;
+        g->dof_gid = dof_gid;
     }
     // incidence CSR in (edge, end) order, owner = first incidence, 1/d_v
     std::vector<int32_t> ptr(V + 1, 0), inc(2 * E), other(2 * E), owner(V, -1);
@@ -713,6 +768,11 @@ grf_status create_impl(int64_t n_vertices, int64_t n_edges, const int64_t* edge_
     }
     grf_status st = GRF_OK;
     grf::DevGraph& d = g->dev;
+    {
+        int nsm = 0;
+        if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device) == cudaSuccess && nsm > 0)
+            d.n_sm = nsm;
+    }
     d.V = (int32_t)V;
     d.E = (int32_t)E;
     d.N = g->N;
@@ -775,11 +835,196 @@ grf_status grf_graph_create(int64_t n_vertices, int64_t n_edges, const int64_t* 
     return create_impl(n_vertices, n_edges, edge_u, edge_v, length, h, nullptr, alloc, out);
 }
 
-grf_status grf_graph_create_part(int64_t n_vertices, int64_t n_edges, const int64_t* edge_u, const int64_t* edge_v,
-                                 const double* length, double h, const grf_part_info* part,
+grf_status grf_graph_create_part(const grf_graph* whole, const int32_t* edge_part, int32_t n_parts, int32_t part,
                                  const grf_allocator* alloc, grf_graph** out) {
-    if (!part) return fail(GRF_EINVAL, "part is NULL");
-    return create_impl(n_vertices, n_edges, edge_u, edge_v, length, h, part, alloc, out);
+    if (out) *out = nullptr;
+    if (!whole || !edge_part || !out) return fail(GRF_EINVAL, "NULL argument");
+    if (whole->partitioned) return fail(GRF_EINVAL, "the whole graph is itself a part");
+    if (n_parts < 1 || part < 0 || part >= n_parts) return fail(GRF_EINVAL, "part %d of %d invalid", part, n_parts);
+    const int64_t V = whole->V, E = whole->E;
+    // parts touching each vertex (ascending, distinct)
+    std::vector<std::vector<int32_t>> touch(V);
+    auto add = [&](int64_t v, int32_t q) {
+        auto& t = touch[v];
+        auto it = std::lower_bound(t.begin(), t.end(), q);
+        if (it == t.end() || *it != q) t.insert(it, q);
+    };
+    for (int64_t e = 0; e < E; ++e) {
+        const int32_t q = edge_part[e];
+        if (q < 0 || q >= n_parts) return fail(GRF_EINVAL, "edge_part[%lld] = %d out of range", (long long)e, q);
+        add(whole->eu[e], q);
+        add(whole->ev[e], q);
+    }
+    PartSpec ps;
+    ps.part = part;
+    ps.n_parts = n_parts;
+    ps.global_n_interior = whole->NI;
+    std::vector<int64_t> iface_id(V, -1);
+    for (int64_t v = 0; v < V; ++v)
+        if (touch[v].size() > 1) iface_id[v] = ps.n_interface++;
+    // local edges (ascending global id) and vertices (ascending global id)
+    std::vector<int64_t> edges, loc(V, -1);
+    for (int64_t e = 0; e < E; ++e)
+        if (edge_part[e] == part) edges.push_back(e);
+    if (edges.empty()) return fail(GRF_EINVAL, "part %d has no edges", part);
+    for (int64_t e : edges) loc[whole->eu[e]] = loc[whole->ev[e]] = 0;
+    int64_t nv = 0;
+    for (int64_t v = 0; v < V; ++v)
+        if (loc[v] == 0) {
+            loc[v] = nv++;
+            ps.vertex_gid.push_back(v);
+        }
+    std::vector<int64_t> leu, lev;
+    std::vector<double> llen;
+    std::vector<int32_t> deg(V, 0);
+    for (int64_t e = 0; e < E; ++e) {
+        deg[whole->eu[e]]++;
+        deg[whole->ev[e]]++;
+    }
+    for (int64_t e : edges) {
+        leu.push_back(loc[whole->eu[e]]);
+        lev.push_back(loc[whole->ev[e]]);
+        llen.push_back(whole->len[e]);
+        ps.edge_goff.push_back(whole->off[e]);
+    }
+    std::map<int32_t, std::vector<int32_t>> nb;
+    for (int64_t i = 0; i < nv; ++i) {
+        const int64_t v = ps.vertex_gid[i];
+        ps.vertex_mass.push_back(whole->ml[whole->NI + v]);  // the whole graph's vertex mass (noise, P150)
+        ps.vertex_degree.push_back(deg[v]);
+        ps.vertex_owned.push_back(touch[v].front() == part ? 1 : 0);
+        ps.vertex_iface.push_back(iface_id[v]);
+        for (int32_t r : touch[v])
+            if (r != part) nb[r].push_back((int32_t)i);
+    }
+    for (auto& kv : nb) {
+        ps.nbr_part.push_back(kv.first);
+        ps.nbr_verts.push_back(kv.second);
+    }
+    return create_impl(nv, (int64_t)edges.size(), leu.data(), lev.data(), llen.data(), whole->h, &ps,
+                       alloc ? alloc : (whole->alloc.custom ? &whole->alloc.a : nullptr), out);
+}
+
+grf_status grf_partition_edges(const grf_graph* g, int32_t n_parts, const double* xy, int32_t* edge_part,
+                               int64_t* info) {
+    if (!g || !edge_part) return fail(GRF_EINVAL, "NULL argument");
+    if (g->partitioned) return fail(GRF_EINVAL, "partition the whole graph, not a part");
+    const int64_t E = g->E, V = g->V;
+    if (n_parts < 1 || n_parts > E) return fail(GRF_EINVAL, "n_parts must lie in [1, E]");
+    // DOF weight of an edge: its n_e elements (m_e interior DOFs + one for its end vertices, P123)
+    std::vector<double> w(E);
+    for (int64_t e = 0; e < E; ++e) w[e] = (double)g->n_el[e];
+    // cut `ids` (in order) into consecutive runs for parts [p0, p0 + np) at equal weight fractions
+    auto cut_runs = [&](const std::vector<int64_t>& ids, int32_t p0, int32_t np) {
+        double tot = 0.0;
+        for (int64_t e : ids) tot += w[e];
+        double acc = 0.0;
+        int32_t q = 0;
+        for (size_t i = 0; i < ids.size(); ++i) {
+            // the edge goes to the part whose weight interval holds its weight midpoint
+            const double mid = acc + 0.5 * w[ids[i]];
+            while (q + 1 < np && mid >= tot * (q + 1) / np) ++q;
+            edge_part[ids[i]] = p0 + q;
+            acc += w[ids[i]];
+        }
+    };
+    if (xy) {
+        // recursive coordinate bisection of the edge midpoints, weighted by n_e:
+        // split the longer extent at the weight fraction of the two halves' part counts
+        std::vector<double> mx(E), my(E);
+        for (int64_t e = 0; e < E; ++e) {
+            mx[e] = 0.5 * (xy[2 * g->eu[e]] + xy[2 * g->ev[e]]);
+            my[e] = 0.5 * (xy[2 * g->eu[e] + 1] + xy[2 * g->ev[e] + 1]);
+        }
+        std::vector<int64_t> all(E);
+        for (int64_t e = 0; e < E; ++e) all[e] = e;
+        std::vector<std::tuple<std::vector<int64_t>, int32_t, int32_t>> work;
+        work.emplace_back(std::move(all), 0, n_parts);
+        while (!work.empty()) {
+            auto [ids, p0, np] = std::move(work.back());
+            work.pop_back();
+            if (np == 1) {
+                for (int64_t e : ids) edge_part[e] = p0;
+                continue;
+            }
+            double x0 = 1e300, x1 = -1e300, y0 = 1e300, y1 = -1e300;
+            for (int64_t e : ids) {
+                x0 = std::min(x0, mx[e]);
+                x1 = std::max(x1, mx[e]);
+                y0 = std::min(y0, my[e]);
+                y1 = std::max(y1, my[e]);
+            }
+            const std::vector<double>& c = (x1 - x0 >= y1 - y0) ? mx : my;
+            std::stable_sort(ids.begin(), ids.end(), [&](int64_t a, int64_t b) { return c[a] < c[b]; });
+            const int32_t nl = np / 2;
+            double tot = 0.0;
+            for (int64_t e : ids) tot += w[e];
+            double acc = 0.0;
+            size_t k = 0;
+            while (k < ids.size() && acc + 0.5 * w[ids[k]] < tot * nl / np) acc += w[ids[k++]];
+            k = std::max<size_t>(1, std::min(k, ids.size() - 1));
+            std::vector<int64_t> left(ids.begin(), ids.begin() + k), right(ids.begin() + k, ids.end());
+            work.emplace_back(std::move(left), p0, nl);
+            work.emplace_back(std::move(right), p0 + nl, np - nl);
+        }
+    } else {
+        // breadth-first edge order (an edge takes the visit rank of its earlier-visited end; each
+        // component from its lowest vertex), cut into runs of equal DOF weight
+        std::vector<std::vector<int64_t>> adj(V);
+        for (int64_t e = 0; e < E; ++e) {
+            adj[g->eu[e]].push_back(g->ev[e]);
+            adj[g->ev[e]].push_back(g->eu[e]);
+        }
+        std::vector<int64_t> rank(V, -1), queue;
+        int64_t nxt = 0;
+        for (int64_t r = 0; r < V; ++r) {
+            if (rank[r] >= 0) continue;
+            rank[r] = nxt++;
+            queue.assign(1, r);
+            for (size_t i = 0; i < queue.size(); ++i)
+                for (int64_t b : adj[queue[i]])
+                    if (rank[b] < 0) {
+                        rank[b] = nxt++;
+                        queue.push_back(b);
+                    }
+        }
+        std::vector<int64_t> ids(E);
+        for (int64_t e = 0; e < E; ++e) ids[e] = e;
+        std::stable_sort(ids.begin(), ids.end(), [&](int64_t a, int64_t b) {
+            return std::min(rank[g->eu[a]], rank[g->ev[a]]) < std::min(rank[g->eu[b]], rank[g->ev[b]]);
+        });
+        cut_runs(ids, 0, n_parts);
+    }
+    if (info) {  // [0] interface vertices, [1] max part weight, [2] min part weight, [3] parts that got no edge
+        std::vector<int32_t> first(V, -1);
+        std::vector<uint8_t> multi(V, 0);
+        std::vector<double> pw(n_parts, 0.0);
+        for (int64_t e = 0; e < E; ++e) {
+            pw[edge_part[e]] += w[e];
+            for (int64_t v : {g->eu[e], g->ev[e]}) {
+                if (first[v] < 0) first[v] = edge_part[e];
+                else if (first[v] != edge_part[e]) multi[v] = 1;
+            }
+        }
+        int64_t ni = 0, empty_parts = 0;
+        for (int64_t v = 0; v < V; ++v) ni += multi[v];
+        for (double x : pw) empty_parts += x == 0.0;
+        info[0] = ni;
+        info[1] = (int64_t)*std::max_element(pw.begin(), pw.end());
+        info[2] = (int64_t)*std::min_element(pw.begin(), pw.end());
+        info[3] = empty_parts;
+    }
+    return GRF_OK;
+}
+
+grf_status grf_graph_part_dofs(const grf_graph* g, int64_t* gid) {
+    if (!g || !gid) return fail(GRF_EINVAL, "NULL argument");
+    if (!g->partitioned) {
+        for (int64_t i = 0; i < g->N; ++i) gid[i] = i;
+        return GRF_OK;
+    }
+    std::copy(g->dof_gid.begin(), g->dof_gid.end(), gid);
+    return GRF_OK;
 }
 
 void grf_graph_destroy(grf_graph* g) {
@@ -882,12 +1127,14 @@ grf_status grf_sample(grf_graph* g, double kappa, double beta, double k, uint64_
     st = check_kernel_limits(g);
     if (st) return st;
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t nplans = g->plans.size();
     Plan* p = nullptr;
-    st = get_plan(g, kappa, beta, k, opt, s, &p);
+    const auto t0 = std::chrono::steady_clock::now();
+    st = get_plan(g, kappa, beta, k, opt, s, &p);  // synchronises when it builds the tables (K2)
+    const double setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (st) return st;
-    (void)nplans;
-    return solve(g, p, n_samples, opt, nullptr, seed, u_out, workspace, ws_bytes, s, stats);
+    st = solve(g, p, n_samples, opt, nullptr, seed, u_out, workspace, ws_bytes, s, stats);
+    if (stats) stats->phase_ms[1] = setup_ms;
+    return st;
 }
 
 grf_status grf_apply(grf_graph* g, double kappa, double beta, double k, int64_t n_rhs, const double* rhs,
@@ -969,6 +1216,9 @@ grf_status grf_sample_host(grf_graph* g, double kappa, double beta, double k, ui
                 tot.iter_max = std::max(tot.iter_max, cst.iter_max);
                 tot.worst_rel_residual = std::max(tot.worst_rel_residual, cst.worst_rel_residual);
                 tot.gpu_launches += cst.gpu_launches;
+                tot.worst_true_rel_residual = std::max(tot.worst_true_rel_residual, cst.worst_true_rel_residual);
+                tot.n_nonfinite += cst.n_nonfinite;
+                for (int i = 0; i < 5; ++i) tot.phase_ms[i] += cst.phase_ms[i];
             }
             iter_sum += cst.iter_mean * (double)cst.n_systems;
         }
@@ -1127,6 +1377,8 @@ grf_status grf_reduce_sum(grf_comm* c, const double* send, double* recv, int64_t
 // ---------------------------------------------------------------- edge-partitioned sampling
 namespace {
 typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef int (*nccl_p2p_fn)(void*, size_t, int, int, void*, cudaStream_t);  // ncclSend / ncclRecv
+typedef int (*nccl_group_fn)();
 
 // sum of a device fp64 buffer over the ranks (in place); ncclDouble = 8, ncclSum = 0
 grf_status allreduce_sum(grf_comm* c, double* buf, int64_t n, cudaStream_t st) {
@@ -1147,11 +1399,24 @@ struct PartRun {
     int32_t* iters = nullptr;
     int32_t* counters = nullptr;
     grf::dist::Vecs v{};
-    double *dpart = nullptr, *dots = nullptr, *halo = nullptr;
+    double *dpart = nullptr, *dots = nullptr;
+    // neighbour halo: send / recv [n_shared][L][cs] (segments per neighbour, in grf_graph::nbr_part
+    // order), the local vertex of every send slot, and per local interface vertex the ordered
+    // sources of its sum (-1: own value, else a recv slot)
+    std::vector<int64_t> seg;  // [n_nbr + 1] slot offsets of the neighbour segments
+    double *send = nullptr, *recv = nullptr;
+    int32_t *pidx = nullptr, *cvert = nullptr, *cptr = nullptr, *csrc = nullptr;
+    int32_t n_if = 0;
     void* get(size_t bytes, cudaStream_t st) {
         void* p = g->alloc.get(bytes, st);
         if (p) mem.push_back({p, bytes});
         return p;
+    }
+    template <class T>
+    T* put_vec(const std::vector<T>& h, cudaStream_t st) {
+        T* d = (T*)get(std::max<size_t>(h.size(), 1) * sizeof(T), st);
+        if (d && !h.empty()) cudaMemcpyAsync(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st);
+        return d;
     }
     void release(cudaStream_t st) {
         cudaStreamSynchronize(st);
@@ -1159,6 +1424,34 @@ struct PartRun {
         mem.clear();
     }
 };
+
+// halo tables of one part from its neighbour lists (grf_graph_create_part): the sum at a shared
+// vertex runs over the parts touching it in ascending part order, own value at its own place
+void halo_tables(const grf_graph* g, std::vector<int64_t>& seg, std::vector<int32_t>& pidx, std::vector<int32_t>& cvert,
+                 std::vector<int32_t>& cptr, std::vector<int32_t>& csrc) {
+    const size_t nn = g->nbr_part.size();
+    seg.assign(nn + 1, 0);
+    for (size_t k = 0; k < nn; ++k) seg[k + 1] = seg[k] + (int64_t)g->nbr_verts[k].size();
+    pidx.clear();
+    std::map<int32_t, std::vector<std::pair<int32_t, int32_t>>> src;  // local vertex -> (part, recv slot)
+    for (size_t k = 0; k < nn; ++k)
+        for (size_t i = 0; i < g->nbr_verts[k].size(); ++i) {
+            const int32_t v = g->nbr_verts[k][i];
+            pidx.push_back(v);
+            src[v].push_back({g->nbr_part[k], (int32_t)(seg[k] + i)});
+        }
+    cvert.clear();
+    cptr.assign(1, 0);
+    csrc.clear();
+    for (auto& kv : src) {
+        auto list = kv.second;
+        list.push_back({g->part, -1});
+        std::sort(list.begin(), list.end());
+        cvert.push_back(kv.first);
+        for (auto& ps : list) csrc.push_back(ps.second);
+        cptr.push_back((int32_t)csrc.size());
+    }
+}
 }  // namespace
 
 extern "C" grf_status grf_sample_edgepart(grf_graph* const* parts, int32_t n_parts, grf_comm* comm, double kappa,
@@ -1170,14 +1463,17 @@ extern "C" grf_status grf_sample_edgepart(grf_graph* const* parts, int32_t n_par
     if (opt && opt->mass != GRF_MASS_LUMPED)
         return fail(GRF_EUNSUPPORTED, "edge-partitioned sampling uses the lumped mass (the paper's method)");
     cudaStream_t st = (cudaStream_t)stream;
-    const int64_t I = parts[0]->n_iface;
+    const int32_t P = comm ? comm->nranks : n_parts;  // parts of the partition
     for (int32_t q = 0; q < n_parts; ++q) {
         grf_status s = check_params(parts[q], kappa, beta, k, n_samples);
         if (s) return s;
         if (!u_out[q]) return fail(GRF_EINVAL, "u_out[%d] is NULL", q);
-        if (!parts[q]->partitioned && (n_parts > 1 || comm))
-            return fail(GRF_EINVAL, "part %d was not created by grf_graph_create_part", q);
-        if (parts[q]->n_iface != I) return fail(GRF_EINVAL, "parts disagree on the interface count");
+        const bool part_ok = parts[q]->partitioned ? parts[q]->n_parts == P : P == 1;
+        if (!part_ok) return fail(GRF_EINVAL, "part %d does not belong to a partition into %d parts", q, P);
+        if (!comm && parts[q]->partitioned && parts[q]->part != q)
+            return fail(GRF_EINVAL, "parts must be passed in part order (got part %d at %d)", parts[q]->part, q);
+        if (comm && parts[q]->partitioned && parts[q]->part != comm->rank)
+            return fail(GRF_EINVAL, "rank %d must pass part %d", comm->rank, comm->rank);
         s = check_kernel_limits(parts[q]);
         if (s) return s;
     }
@@ -1212,64 +1508,113 @@ extern "C" grf_status grf_sample_edgepart(grf_graph* const* parts, int32_t n_par
         for (auto p : vv) *p = (double*)r.get(vec, st);
         r.dpart = (double*)r.get(sizeof(double) * 2 * L * grf::dist::dot_blocks(r.g->dev) * cs, st);
         r.dots = (double*)r.get(sizeof(double) * 2 * L * cs, st);
-        r.halo = (double*)r.get(sizeof(double) * std::max<int64_t>(I, 1) * L * cs, st);
+        std::vector<int32_t> pidx, cvert, cptr, csrc;
+        halo_tables(r.g, r.seg, pidx, cvert, cptr, csrc);
+        const int64_t ns = r.seg.back();
+        r.n_if = (int32_t)cvert.size();
+        r.send = (double*)r.get(sizeof(double) * std::max<int64_t>(ns, 1) * L * cs, st);
+        r.recv = (double*)r.get(sizeof(double) * std::max<int64_t>(ns, 1) * L * cs, st);
+        r.pidx = r.put_vec(pidx, st);
+        r.cvert = r.put_vec(cvert, st);
+        r.cptr = r.put_vec(cptr, st);
+        r.csrc = r.put_vec(csrc, st);
         for (auto& b : r.mem)
             if (!b.p) rc = fail(GRF_ENOMEM, "edge-partitioned workspace could not be allocated");
         if (!r.W || !r.ends || !r.rhs || !r.uG || !r.iters || !r.relres || !r.counters || !r.v.x || !r.v.r0 ||
-            !r.v.r1 || !r.v.p0 || !r.v.p1 || !r.v.q || !r.v.z || !r.dpart || !r.dots || !r.halo)
+            !r.v.r1 || !r.v.p0 || !r.v.p1 || !r.v.q || !r.v.z || !r.dpart || !r.dots || !r.send || !r.recv ||
+            !r.pidx || !r.cvert || !r.cptr || !r.csrc)
             rc = fail(GRF_ENOMEM, "edge-partitioned workspace could not be allocated");
     }
-    // shared (all-part) state: summed halo / dots and the system scalars, on part 0's allocator
+    // shared (all-part) state: summed dots and the system scalars, on part 0's allocator
     PartRun& R0 = R[0];
     const int32_t nsys = L * cs;
-    double *hsum = nullptr, *dsum = nullptr;
+    double* dsum = nullptr;
     double** ptrs = nullptr;
+    int32_t* flag_host = nullptr;  // pinned: the device's count of unconverged systems, polled
     grf::dist::Scal sc{};
     if (!rc) {
-        hsum = (double*)R0.get(sizeof(double) * std::max<int64_t>(I, 1) * L * cs, st);
         dsum = (double*)R0.get(sizeof(double) * 2 * nsys, st);
-        ptrs = (double**)R0.get(sizeof(double*) * 2 * n_parts, st);
+        ptrs = (double**)R0.get(sizeof(double*) * n_parts, st);
         double** sd[5] = {&sc.alpha, &sc.beta, &sc.rz, &sc.gg, &sc.rr};
         for (auto p : sd) *p = (double*)R0.get(sizeof(double) * nsys, st);
         sc.done = (int32_t*)R0.get(sizeof(int32_t) * nsys, st);
         sc.its = (int32_t*)R0.get(sizeof(int32_t) * nsys, st);
         sc.active = (int32_t*)R0.get(sizeof(int32_t), st);
-        if (!hsum || !dsum || !ptrs || !sc.alpha || !sc.beta || !sc.rz || !sc.gg || !sc.rr || !sc.done || !sc.its ||
-            !sc.active)
+        if (cudaHostAlloc((void**)&flag_host, 2 * sizeof(int32_t), cudaHostAllocDefault) != cudaSuccess) flag_host = nullptr;
+        if (!dsum || !ptrs || !sc.alpha || !sc.beta || !sc.rz || !sc.gg || !sc.rr || !sc.done || !sc.its ||
+            !sc.active || !flag_host)
             rc = fail(GRF_ENOMEM, "edge-partitioned workspace could not be allocated");
     }
-    if (rc) {
+    cudaEvent_t polled[2] = {nullptr, nullptr};
+    for (auto& e : polled)
+        if (!rc && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+            rc = fail(GRF_ECUDA, "event creation failed");
+    auto finish_all = [&]() {
         cleanup();
+        for (auto e : polled)
+            if (e) cudaEventDestroy(e);
+        if (flag_host) cudaFreeHost(flag_host);
+    };
+    if (rc) {
+        finish_all();
         return rc;
     }
-    // device arrays of part pointers for the in-process sums: [halo_0..halo_P-1, dots_0..dots_P-1]
-    std::vector<double*> hp(2 * n_parts);
-    for (int32_t q = 0; q < n_parts; ++q) {
-        hp[q] = R[q].halo;
-        hp[n_parts + q] = R[q].dots;
+    {  // device array of the parts' dot buffers for the in-process sums
+        std::vector<double*> hp(n_parts);
+        for (int32_t q = 0; q < n_parts; ++q) hp[q] = R[q].dots;
+        cudaMemcpyAsync(ptrs, hp.data(), sizeof(double*) * hp.size(), cudaMemcpyHostToDevice, st);
+        cudaStreamSynchronize(st);  // the host vector dies here
     }
-    CUDA_TRY(cudaMemcpyAsync(ptrs, hp.data(), sizeof(double*) * hp.size(), cudaMemcpyHostToDevice, st));
     const int32_t pc = opt ? opt->precond : GRF_PRECOND_NN;
     const double rtol = opt ? opt->rtol : 1e-13;
     const int32_t max_iter = (opt && opt->max_iter > 0) ? opt->max_iter : (int32_t)(V_sum + 10);
-    const int64_t hn = I * L * cs;
+    static nccl_p2p_fn nsend = nullptr, nrecv = nullptr;
+    static nccl_group_fn gstart = nullptr, gend = nullptr;
+    if (comm && !nsend) {
+        nsend = (nccl_p2p_fn)dlsym(g_nccl.h, "ncclSend");
+        nrecv = (nccl_p2p_fn)dlsym(g_nccl.h, "ncclRecv");
+        gstart = (nccl_group_fn)dlsym(g_nccl.h, "ncclGroupStart");
+        gend = (nccl_group_fn)dlsym(g_nccl.h, "ncclGroupEnd");
+    }
+    if (comm && (!nsend || !nrecv || !gstart || !gend)) {
+        finish_all();
+        return fail(GRF_ENCCL, "ncclSend/ncclRecv/ncclGroup* not found");
+    }
 
-    // halo sum of vector X (per part pointer) over all parts: interface values become the totals
+    // halo of vector X (per part): every shared vertex gets the sum of the parts' values, in part
+    // order.  Each part packs the shared vertices per neighbour; the segments travel to the
+    // neighbours (NCCL send/recv pairs across ranks, device copies between in-process parts);
+    // each part then combines its own and the received values.
     auto halo = [&](auto getX) -> grf_status {
-        if (I == 0) return GRF_OK;
-        for (int32_t q = 0; q < n_parts; ++q) {
-            CUDA_TRY(cudaMemsetAsync(R[q].halo, 0, sizeof(double) * hn, st));
-            grf::dist::pack(R[q].g->dev, L, cs, getX(R[q]), R[q].halo, st);
-        }
-        double* total = R0.halo;
+        for (auto& r : R) grf::dist::halo_pack(r.g->dev, L, cs, r.seg.back(), r.pidx, getX(r), r.send, st);
+        const size_t row = sizeof(double) * (size_t)L * cs;
         if (comm) {
-            grf_status s = allreduce_sum(comm, R0.halo, hn, st);
-            if (s) return s;
+            PartRun& r = R0;
+            if (!r.g->nbr_part.empty()) {
+                int e = gstart();
+                for (size_t kk = 0; kk < r.g->nbr_part.size() && !e; ++kk) {
+                    const size_t cnt = (size_t)(r.seg[kk + 1] - r.seg[kk]) * L * cs;
+                    e = nsend(r.send + r.seg[kk] * L * cs, cnt, 8, r.g->nbr_part[kk], comm->comm, st);
+                    if (!e) e = nrecv(r.recv + r.seg[kk] * L * cs, cnt, 8, r.g->nbr_part[kk], comm->comm, st);
+                }
+                int e2 = gend();
+                if (e || e2) return fail(GRF_ENCCL, "halo send/recv: %s", g_nccl.err ? g_nccl.err(e ? e : e2) : "error");
+            }
         } else {
-            grf::dist::sum_parts(n_parts, ptrs, hn, hsum, st);
-            total = hsum;
+            for (int32_t q = 0; q < n_parts; ++q) {
+                const grf_graph* gq = R[q].g;
+                for (size_t kk = 0; kk < gq->nbr_part.size(); ++kk) {  // q's segment for r -> r's segment for q
+                    const int32_t rr = gq->nbr_part[kk];
+                    const grf_graph* gr = R[rr].g;
+                    const size_t back = std::find(gr->nbr_part.begin(), gr->nbr_part.end(), q) - gr->nbr_part.begin();
+                    CUDA_TRY(cudaMemcpyAsync(R[rr].recv + R[rr].seg[back] * L * cs, R[q].send + R[q].seg[kk] * L * cs,
+                                             (size_t)(R[q].seg[kk + 1] - R[q].seg[kk]) * row, cudaMemcpyDeviceToDevice,
+                                             st));
+                }
+            }
         }
-        for (int32_t q = 0; q < n_parts; ++q) grf::dist::unpack(R[q].g->dev, L, cs, total, getX(R[q]), st);
+        for (auto& r : R)
+            grf::dist::halo_combine(r.g->dev, L, cs, r.n_if, r.cvert, r.cptr, r.csrc, r.recv, getX(r), st);
         return GRF_OK;
     };
     // dot products (owned vertices) summed over parts into dsum [K][nsys]
@@ -1281,18 +1626,36 @@ extern "C" grf_status grf_sample_edgepart(grf_graph* const* parts, int32_t n_par
             if (s) return s;
             CUDA_TRY(cudaMemcpyAsync(dsum, R0.dots, sizeof(double) * K * nsys, cudaMemcpyDeviceToDevice, st));
         } else {
-            grf::dist::sum_parts(n_parts, ptrs + n_parts, (int64_t)K * nsys, dsum, st);
+            grf::dist::sum_parts(n_parts, ptrs, (int64_t)K * nsys, dsum, st);
         }
         return GRF_OK;
     };
 
+    // kernels launched (per-call count for grf_stats) and the profiling brackets (grf_profile_*)
+    int64_t nlaunch = 0;
+    grf_graph* gp = R0.g;  // the bracket events go to the first part's profile
+    cudaEvent_t pcg_a = nullptr;
     // stage 1 (per part, no communication): noise, condensation, partial condensed rhs
     for (auto& r : R) {
-        grf::launch_noise(r.g->dev, seed, n_samples, r.W, st);
-        CUDA_TRY(grf::launch_condense(r.g->dev, r.plan->dev, n_samples, r.W, r.ends, r.counters, st));
+        CUDA_TRY(gp->timed(GRF_K_NOISE, st, [&] { grf::launch_noise(r.g->dev, seed, n_samples, r.W, st); }));
+        cudaError_t le = cudaSuccess;
+        CUDA_TRY(gp->timed(GRF_K_CONDENSE, st, [&] {
+            le = grf::launch_condense(r.g->dev, r.plan->dev, n_samples, r.W, r.ends, r.counters, st);
+        }));
+        CUDA_TRY(le);
         grf::launch_assemble_rhs(r.g->dev, r.plan->dev, n_samples, r.W, r.ends, r.rhs, st);
+        nlaunch += 3;
     }
-    // stage 2: distributed NN-PCG per sample tile
+    if (gp->prof) {  // the whole distributed PCG (every tile, halos and collectives) as one record
+        pcg_a = gp->new_event();
+        cudaEventRecord(pcg_a, st);
+    }
+    // stage 2: distributed NN-PCG per sample tile.  The iterations are enqueued without host
+    // round trips: every POLL iterations the device's count of unconverged systems is copied to
+    // pinned memory and the copy of the PREVIOUS chunk is inspected, so the host never waits for
+    // the GPU to drain; iterations enqueued after convergence do no work (converged systems have
+    // alpha = beta = 0 and every system is masked once the count reaches 0).
+    constexpr int32_t POLL = 8;
     for (int64_t tile = 0; tile < tiles && !rc; ++tile) {
         for (auto& r : R) grf::dist::init(r.g->dev, L, n_samples, csl, tile, r.rhs, r.v, st);
         rc = halo([](PartRun& r) { return r.v.r0; });  // g = W_G + sum over ALL parts' edges
@@ -1306,11 +1669,10 @@ extern "C" grf_status grf_sample_edgepart(grf_graph* const* parts, int32_t n_par
         CUDA_TRY(cudaMemsetAsync(sc.active, 0, sizeof(int32_t), st));
         grf::dist::scal_init(nsys, cs, n_samples, tile, csl, dsum, sc, st);
         bool flip = false;  // which of the double-buffered p / r is current
+        int64_t chunk = 0;
+        int64_t ran = 0;  // iterations enqueued
         for (int32_t it = 0; it < max_iter; ++it) {
-            int32_t active = 0;
-            CUDA_TRY(cudaMemcpyAsync(&active, sc.active, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-            CUDA_TRY(cudaStreamSynchronize(st));
-            if (active == 0) break;
+            ran = it + 1;
             for (auto& r : R) {
                 double* po = flip ? r.v.p1 : r.v.p0;
                 double* pn = flip ? r.v.p0 : r.v.p1;
@@ -1338,15 +1700,37 @@ extern "C" grf_status grf_sample_edgepart(grf_graph* const* parts, int32_t n_par
             if (rc) break;
             grf::dist::scal_beta(nsys, rtol * rtol, dsum, sc, st);
             flip = !flip;
+            if ((it + 1) % POLL == 0) {
+                const int slot = (int)(chunk & 1);
+                if (chunk >= 1) {  // the previous chunk's count: the GPU is a chunk ahead of this check
+                    CUDA_TRY(cudaEventSynchronize(polled[slot ^ 1]));
+                    if (flag_host[slot ^ 1] == 0) break;
+                }
+                CUDA_TRY(cudaMemcpyAsync(&flag_host[slot], sc.active, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+                CUDA_TRY(cudaEventRecord(polled[slot], st));
+                ++chunk;
+            }
         }
         if (rc) break;
         for (auto& r : R) grf::dist::finish(r.g->dev, L, n_samples, csl, tile, r.v.x, sc, r.uG, r.iters, r.relres, st);
+        // per iteration and part: spmv, update, 2 x (halo pack + combine), 3 dot kernels x 2, plus 2 scalars
+        nlaunch += ran * (n_parts * 12 + 2) + n_parts * 9 + 2;
+    }
+    if (pcg_a) {
+        cudaEvent_t pcg_b = gp->new_event();
+        cudaEventRecord(pcg_b, st);
+        gp->recs.push_back({GRF_K_PCG, pcg_a, pcg_b});
     }
     // stage 3 (per part): recovery of the interiors and the vertex values
     for (int32_t q = 0; q < n_parts && !rc; ++q) {
         PartRun& r = R[q];
-        cudaError_t e = grf::launch_recover(r.g->dev, r.plan->dev, n_samples, r.W, u_out[q], r.uG, r.counters + 1, st);
-        if (e == cudaSuccess) e = grf::launch_vertex_sum(r.g->dev, r.plan->dev, n_samples, r.uG, u_out[q], st);
+        cudaError_t e = cudaSuccess;
+        cudaError_t te = gp->timed(GRF_K_RECOVER, st, [&] {
+            e = grf::launch_recover(r.g->dev, r.plan->dev, n_samples, r.W, u_out[q], r.uG, r.counters + 1, st);
+            if (e == cudaSuccess) e = grf::launch_vertex_sum(r.g->dev, r.plan->dev, n_samples, r.uG, u_out[q], st);
+        });
+        if (e == cudaSuccess) e = te;
+        nlaunch += 2;
         if (e != cudaSuccess) rc = fail(GRF_ECUDA, "edge-partitioned recovery: %s", cudaGetErrorString(e));
     }
     if (!rc) {
@@ -1376,9 +1760,11 @@ extern "C" grf_status grf_sample_edgepart(grf_graph* const* parts, int32_t n_par
         stats->iter_mean = sum / its.size();
         stats->worst_rel_residual = worst;
         stats->n_unconverged = bad;
+        stats->gpu_launches = nlaunch;
+        stats->worst_true_rel_residual = -1.0;  // not computed for edge-partitioned solves
         if (bad) rc = fail(GRF_ENOCONV, "%lld PCG systems missed rtol %g", (long long)bad, rtol);
     }
-    cleanup();
+    finish_all();
     return rc;
 }
 
@@ -1435,9 +1821,6 @@ extern "C" grf_status grf_mnorm_sq_diff(grf_graph* g, int64_t n, const double* a
 
 // ---------------------------------------------------------------- sample-then-node sharded sampling
 namespace {
-typedef int (*nccl_p2p_fn)(void*, size_t, int, int, void*, cudaStream_t);  // ncclSend / ncclRecv
-typedef int (*nccl_group_fn)();
-
 int64_t split_lo(int64_t n, int64_t parts, int64_t i) {
     const int64_t base = n / parts, extra = n % parts;
     return i * base + std::min(i, extra);
@@ -1478,10 +1861,11 @@ grf_status allreduce_max_i32(grf_comm* c, int32_t* dev_buf, int32_t* host_val, c
 extern "C" grf_status grf_sample_dist(grf_graph* g, grf_comm* comm, double kappa, double beta, double k,
                                       uint64_t seed, int64_t n_samples, const grf_options* opt, double* u_out,
                                       int64_t* range_out, void* stream, grf_stats* stats) {
-    // Every rank of the communicator -- active or not -- takes part in one status agreement (an
-    // int32 max allreduce) after its local work, so that a rank whose local call failed cannot
-    // leave its peers blocked in the partial-sum exchange: on any failure every rank returns
-    // (GRF_ENCCL "a peer failed" on the others) before a single partial is sent.
+    // With node shards (P_l > 1) every rank of the communicator -- active or not -- takes part in
+    // one status agreement (an int32 max allreduce) after its local work, so that a rank whose
+    // local call failed cannot leave its peers blocked in the partial-sum exchange: on any failure
+    // every rank returns (GRF_ENCCL "a peer failed" on the others) before a single partial is
+    // sent.  Pure sample shards (P_l = 1) exchange nothing and stay asynchronous.
     if (!g || !comm || !range_out) return fail(GRF_EINVAL, "NULL argument");
     grf_status st = check_params(g, kappa, beta, k, n_samples);
     if (st) return st;  // identical arguments on every rank: every rank fails here alike
@@ -1514,7 +1898,7 @@ extern "C" grf_status grf_sample_dist(grf_graph* g, grf_comm* comm, double kappa
         }
     }
     const std::string local_msg = g_err;
-    if (comm->nranks > 1) {
+    if (pl > 1) {  // only node shards exchange data; P_l is the same on every rank
         int32_t* flag = (int32_t*)g->alloc.get(sizeof(int32_t), s);
         if (!flag) return fail(GRF_ENOMEM, "status buffer");  // (a peer then blocks: allocation of 8 B failed)
         int32_t worst = (local == GRF_OK || local == GRF_ENOCONV) ? 0 : 1;

@@ -12,6 +12,7 @@ namespace grf {
 // Device view of a graph + mesh (grf_graph_create).  All arrays device-resident.
 struct DevGraph {
     int32_t V = 0, E = 0;
+    int32_t n_sm = 148;               // multiprocessors of the graph's device (persistent grids)
     int64_t N = 0, NI = 0;            // all DOFs / interior DOFs
     int32_t max_m = 0;                // max interior count over edges
     const int32_t* eu = nullptr;      // [E] edge_u
@@ -129,6 +130,11 @@ cudaError_t launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, c
 // K4a condensed rhs (pcg.cu): rhs [tile][l][cs][v] from W and the end values
 void launch_assemble_rhs(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W, const double* ends,
                          double* rhs, cudaStream_t st);
+// exit checks (pcg.cu), run when the caller asks for statistics: the true relative residual
+// ||g - S u_G|| / ||g|| of every vertex system (out [S][L]) and the count of non-finite outputs
+void launch_true_residual(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* rhs, const double* uG,
+                          double* out, cudaStream_t st);
+void launch_nonfinite(const double* u, int64_t n, unsigned long long* count, cudaStream_t st);
 // K4 global-memory variant (pcg_global.cu) and its workspace
 bool pcg_shared_ok(const DevGraph& g);
 void launch_pcg_tables_pos(const DevGraph& g, const DevPlan& p, cudaStream_t st);
@@ -170,6 +176,11 @@ void dots(const DevGraph& g, int32_t L, int32_t cs, int K, const double* a0, con
 void pack(const DevGraph& g, int32_t L, int32_t cs, const double* X, double* buf, cudaStream_t st);
 void unpack(const DevGraph& g, int32_t L, int32_t cs, const double* buf, double* X, cudaStream_t st);
 void sum_parts(int32_t P, double* const* in_dev, int64_t n, double* out, cudaStream_t st);
+// neighbour halo: pack the shared vertices per neighbour, combine own + received in part order
+void halo_pack(const DevGraph& g, int32_t L, int32_t cs, int64_t n, const int32_t* idx, const double* X, double* send,
+               cudaStream_t st);
+void halo_combine(const DevGraph& g, int32_t L, int32_t cs, int32_t nif, const int32_t* vert, const int32_t* ptr,
+                  const int32_t* src, const double* recv, double* X, cudaStream_t st);
 void scal_init(int32_t n, int32_t cs, int64_t S, int64_t tile, int32_t csl, const double* dots, const Scal& sc,
                cudaStream_t st);
 void scal_alpha(int32_t n, const double* pq, const Scal& sc, cudaStream_t st);

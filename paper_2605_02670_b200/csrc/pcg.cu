@@ -595,4 +595,75 @@ cudaError_t launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, c
     return cudaGetLastError();
 }
 
+namespace {
+// True residual of every vertex system at exit (SURVEY §8c Q10, P296 "J ~ 0"): per (node l,
+// sample s) ||g - S u_G||_2^2 and ||g||_2^2 with the plan's operator tables (the Dirichlet step
+// of P247-258 applied to the PCG's answer).  One block per (l, sample), threads over vertices,
+// fixed-order reduction.
+__global__ void true_residual_kernel(DevGraph g, int32_t L, const double* __restrict__ ops, int64_t S, int32_t csl,
+                                     const double* __restrict__ rhs, const double* __restrict__ uG,
+                                     double* __restrict__ out /* [S][L] relative residual */) {
+    __shared__ double red[2][8];
+    const int l = blockIdx.x % L;
+    const int64_t s = blockIdx.x / L;
+    const int V = g.V;
+    const int64_t ns = ops_nslots(g);
+    const double* tab = ops + l * ops_stride(g);
+    double rr = 0.0, gg = 0.0;
+    for (int v = threadIdx.x; v < V; v += blockDim.x) {
+        const double x = uG[ug_index(s, v, l, L, V, csl)];
+        double sx = tab[v] * x;
+        const int dg = g.inc_ptr[v + 1] - g.inc_ptr[v];
+        for (int j = 0; j < dg; ++j) {
+            const int64_t k = ops_slot(g, v, j);
+            sx = fma(tab[3 * (int64_t)V + k], uG[ug_index(s, ops_other(g, k), l, L, V, csl)], sx);
+        }
+        const double gv = rhs[rhs_index(s, l, v, L, V, csl)];
+        rr = fma(gv - sx, gv - sx, rr);
+        gg = fma(gv, gv, gg);
+    }
+    (void)ns;
+    for (int o = 16; o > 0; o >>= 1) {
+        rr += __shfl_xor_sync(0xffffffffu, rr, o);
+        gg += __shfl_xor_sync(0xffffffffu, gg, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = rr;
+        red[1][threadIdx.x >> 5] = gg;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            a += red[0][w];
+            b += red[1][w];
+        }
+        out[s * L + l] = b > 0.0 ? sqrt(a / b) : 0.0;
+    }
+}
+
+// count of non-finite entries of u (S x N), one partial per block, summed by the host
+__global__ void nonfinite_kernel(const double* __restrict__ u, int64_t n, unsigned long long* __restrict__ count) {
+    unsigned int c = 0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+        c += isfinite(u[t]) ? 0u : 1u;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, (unsigned long long)c);
+}
+}  // namespace
+
+void launch_true_residual(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* rhs, const double* uG,
+                          double* out, cudaStream_t st) {
+    true_residual_kernel<<<(unsigned)(p.L * n_samples), 256, 0, st>>>(g, p.L, p.ops, n_samples,
+                                                                       sample_tile_log2(n_samples), rhs, uG, out);
+}
+
+void launch_nonfinite(const double* u, int64_t n, unsigned long long* count, cudaStream_t st) {
+    cudaMemsetAsync(count, 0, sizeof(unsigned long long), st);
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks < 1) blocks = 1;
+    nonfinite_kernel<<<(unsigned)blocks, 256, 0, st>>>(u, n, count);
+}
+
 }  // namespace grf

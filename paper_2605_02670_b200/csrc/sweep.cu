@@ -1,20 +1,26 @@
 // K3 / K5 host-side dispatch: plan node tiling (Lp, TL, rounds) and the launch of the
 // sweep kernel instance for it (kernel and mapping: sweep_impl.cuh).
+#include <cstdlib>
+
 #include "grf_internal.h"
 #include "sweep_impl.cuh"
 
 namespace grf {
 namespace sweep {
 cudaError_t launch_c0(int tl, Args a, cudaStream_t st);
-cudaError_t launch_c1(int tl, Args a, cudaStream_t st);
-cudaError_t launch_c2(int tl, Args a, cudaStream_t st);
-cudaError_t launch_r0(int tl, Args a, cudaStream_t st);
-cudaError_t launch_r1(int tl, Args a, cudaStream_t st);
-cudaError_t launch_r2(int tl, Args a, cudaStream_t st);
+cudaError_t launch_r0k(int tl, Args a, cudaStream_t st);
+cudaError_t launch_r1k(int tl, Args a, cudaStream_t st);
+cudaError_t launch_r2k(int tl, Args a, cudaStream_t st);
 }  // namespace sweep
+namespace sweep2 {
+cudaError_t launch_c16(int tl, sweep::Args a, cudaStream_t st);
+cudaError_t launch_c32(int tl, sweep::Args a, cudaStream_t st);
+cudaError_t launch_r16(int tl, sweep::Args a, cudaStream_t st);
+cudaError_t launch_r32(int tl, sweep::Args a, cudaStream_t st);
+}  // namespace sweep2
 
 namespace {
-constexpr int TL_MAX = 10;
+constexpr int TL_MAX = 7;  // nodes per lane of the sweep kernels (register tile)
 
 sweep::Args make_args(const DevGraph& g, const DevPlan& p, int64_t S, const double* W, double* out,
                       const double* uG, int32_t* counter) {
@@ -34,7 +40,12 @@ sweep::Args make_args(const DevGraph& g, const DevPlan& p, int64_t S, const doub
     a.out = out;
     a.uG = uG;
     a.counter = counter;
-    a.nk = p.L < p.Lp ? 1 : 0;  // edge_setup.cu wrote the correction node at slot L
+    a.nk = 1;  // plan_tiling leaves slot L free: edge_setup.cu writes the correction node there
+    static const int ablate = [] {
+        const char* v = getenv("GRF_ABLATE");
+        return v ? atoi(v) : 0;
+    }();
+    a.ablate = ablate;
     return a;
 }
 }  // namespace
@@ -47,8 +58,9 @@ int32_t sample_tile_log2(int64_t S) {
     }
 }
 
+// L nodes plus the correction node (slot L) in rounds of 32 x TL nodes, TL <= TL_MAX
 void plan_tiling(int32_t L, int32_t* Lp, int32_t* tl, int32_t* rounds) {
-    const int q0 = (L + sweep::NLT - 1) / sweep::NLT;
+    const int q0 = (L + 1 + sweep::NLT - 1) / sweep::NLT;
     const int r = (q0 + TL_MAX - 1) / TL_MAX;
     const int t = (q0 + r - 1) / r;
     *rounds = r;
@@ -60,8 +72,8 @@ cudaError_t launch_condense(const DevGraph& g, const DevPlan& p, int64_t n_sampl
                             int32_t* counter, cudaStream_t st) {
     const sweep::Args a = make_args(g, p, n_samples, W, ends, nullptr, counter);
     switch (sweep::variant_for(n_samples)) {
-        case sweep::V2: return sweep::launch_c2(p.TL, a, st);
-        case sweep::V1: return sweep::launch_c1(p.TL, a, st);
+        case sweep::V2: return sweep2::launch_c32(p.TL, a, st);
+        case sweep::V1: return sweep2::launch_c16(p.TL, a, st);
         default: return sweep::launch_c0(p.TL, a, st);
     }
 }
@@ -70,9 +82,9 @@ cudaError_t launch_recover(const DevGraph& g, const DevPlan& p, int64_t n_sample
                            const double* uG, int32_t* counter, cudaStream_t st) {
     const sweep::Args a = make_args(g, p, n_samples, W, u, uG, counter);
     switch (sweep::variant_for(n_samples)) {
-        case sweep::V2: return sweep::launch_r2(p.TL, a, st);
-        case sweep::V1: return sweep::launch_r1(p.TL, a, st);
-        default: return sweep::launch_r0(p.TL, a, st);
+        case sweep::V2: return a.ablate & 8 ? sweep2::launch_r32(p.TL, a, st) : sweep::launch_r2k(p.TL, a, st);
+        case sweep::V1: return a.ablate & 8 ? sweep2::launch_r16(p.TL, a, st) : sweep::launch_r1k(p.TL, a, st);
+        default: return sweep::launch_r0k(p.TL, a, st);
     }
 }
 

@@ -1,4 +1,4 @@
-// Sweep kernel instances (sweep_impl.cuh): K3 condense, sample mapping V0, node tiles TL = 1..10.
+// Sweep kernel instances (sweep_impl.cuh): K3 condense, sample mapping V0, node tiles TL = 1..7.
 #include "sweep_impl.cuh"
 
 namespace grf {

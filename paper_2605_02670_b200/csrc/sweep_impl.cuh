@@ -71,6 +71,8 @@ struct Args {
     int32_t n_items;        // E * chunks
     int32_t tile_ms;        // recover: max (m | 1) the shared-memory output tile holds (0: none)
     int32_t nk;             // recover: 1 if slot L is the correction node (edge_setup.cu; L < Lp)
+    int32_t ablate;         // design studies only (env GRF_ABLATE, default 0): sweep2 bits 1 no output
+                            // reduction, 2 no u_G loads, 4 no data waits -- wrong results by construction
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -716,7 +718,7 @@ cudaError_t launch(Args a, cudaStream_t st) {
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_kernel<TL, TS, LW, NWS, REC, NK>, C::NT, smem);
     if (per_sm < 1) per_sm = 1;
-    int blocks = 148 * per_sm;
+    int blocks = (a.g.n_sm > 0 ? a.g.n_sm : 148) * per_sm;
     if (blocks > a.n_items) blocks = a.n_items;
     sweep_kernel<TL, TS, LW, NWS, REC, NK><<<blocks, C::NT, smem, st>>>(a);
     return cudaGetLastError();
@@ -744,9 +746,6 @@ cudaError_t launch_v(int tl, Args a, cudaStream_t st) {
         case 5: return launch<5, TS, LW, NWS, REC, NK>(a, st);
         case 6: return launch<6, TS, LW, NWS, REC, NK>(a, st);
         case 7: return launch<7, TS, LW, NWS, REC, NK>(a, st);
-        case 8: return launch<8, TS, LW, NWS, REC, NK>(a, st);
-        case 9: return launch<9, TS, LW, NWS, REC, NK>(a, st);
-        case 10: return launch<10, TS, LW, NWS, REC, NK>(a, st);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -1,5 +1,5 @@
 // Sweep kernel instances (sweep_impl.cuh): K5 recover with the correction-node interior steps,
-// sample mapping V0, node tiles TL = 1..10.
+// sample mapping V0, node tiles TL = 1..7.
 #include "sweep_impl.cuh"
 
 namespace grf {

@@ -18,7 +18,7 @@ from typing import Optional, Tuple
 import numpy as np
 
 from ._lib import (ALLOC_FN, FREE_FN, GRF_ENOCONV, GRF_OK, GrfError, check, grf_allocator, grf_options,
-                   grf_part_info, grf_stats, load)
+                   grf_stats, load)
 
 PRECOND = {"nn": 0, "neumann-neumann": 0, "jacobi": 1, "none": 2}
 
@@ -76,16 +76,11 @@ def make_options(rtol=1e-13, max_iter=0, precond="nn", node_range=None, pcg="aut
 class Graph:
     """A metric graph + its P1 mesh, resident on the current CUDA device."""
 
-    def __init__(self, n_vertices, edge_u, edge_v, length, h, use_torch_allocator: bool = True, part=None):
+    def __init__(self, n_vertices, edge_u, edge_v, length, h, use_torch_allocator: bool = True, _part=None):
         torch = _torch()
         lib = load()
         self._lib = lib
         self.device = torch.cuda.current_device()
-        eu = np.ascontiguousarray(edge_u, dtype=np.int64)
-        ev = np.ascontiguousarray(edge_v, dtype=np.int64)
-        ln = np.ascontiguousarray(length, dtype=np.float64)
-        self.n_vertices = int(n_vertices)
-        self.n_edges = int(len(eu))
         self.h = float(h)
         self._alloc = None
         if use_torch_allocator:
@@ -110,40 +105,63 @@ class Graph:
         h_ = C.c_void_p()
         pi64 = C.POINTER(C.c_int64)
         alloc = C.byref(self._alloc) if self._alloc is not None else None
-        self.part = part
-        if part is None:
+        self.part = None
+        if _part is None:
+            eu = np.ascontiguousarray(edge_u, dtype=np.int64)
+            ev = np.ascontiguousarray(edge_v, dtype=np.int64)
+            ln = np.ascontiguousarray(length, dtype=np.float64)
+            self.n_vertices = int(n_vertices)
+            self.n_edges = int(len(eu))
             check(lib.grf_graph_create(self.n_vertices, self.n_edges, eu.ctypes.data_as(pi64),
                                        ev.ctypes.data_as(pi64), ln.ctypes.data_as(C.POINTER(C.c_double)), self.h,
                                        alloc, C.byref(h_)))
-        else:  # edge-partitioned part (edgepart.Part): grf_graph_create_part
-            keep = [np.ascontiguousarray(part.vertices, dtype=np.int64),
-                    np.ascontiguousarray(part.edge_goff, dtype=np.int64),
-                    np.ascontiguousarray(part.vertex_mass, dtype=np.float64),
-                    np.ascontiguousarray(part.vertex_degree, dtype=np.int32),
-                    np.ascontiguousarray(part.vertex_owned, dtype=np.uint8),
-                    np.ascontiguousarray(part.vertex_iface, dtype=np.int64)]
-            info = grf_part_info(part.global_n_interior, keep[0].ctypes.data_as(pi64), keep[1].ctypes.data_as(pi64),
-                                 keep[2].ctypes.data_as(C.POINTER(C.c_double)),
-                                 keep[3].ctypes.data_as(C.POINTER(C.c_int32)),
-                                 keep[4].ctypes.data_as(C.POINTER(C.c_uint8)), part.n_interface,
-                                 keep[5].ctypes.data_as(pi64))
-            check(lib.grf_graph_create_part(self.n_vertices, self.n_edges, eu.ctypes.data_as(pi64),
-                                            ev.ctypes.data_as(pi64), ln.ctypes.data_as(C.POINTER(C.c_double)),
-                                            self.h, C.byref(info), alloc, C.byref(h_)))
+        else:  # part q of an edge partition of a whole graph: grf_graph_create_part
+            whole, edge_part, n_parts, q = _part
+            ep = np.ascontiguousarray(edge_part, dtype=np.int32)
+            if ep.shape != (whole.n_edges,):
+                raise ValueError("edge_part needs one entry per edge of the whole graph")
+            check(lib.grf_graph_create_part(whole._h, ep.ctypes.data_as(C.POINTER(C.c_int32)), int(n_parts), int(q),
+                                            alloc, C.byref(h_)))
+            self.part = (int(q), int(n_parts))
+            self._whole = whole  # the part borrows nothing, but keep creation order for teardown
         self._h = h_
         n, ni = C.c_int64(), C.c_int64()
         check(lib.grf_graph_num_dofs(self._h, C.byref(n), C.byref(ni)))
         self.n_dofs = n.value
         self.n_interior = ni.value
+        if _part is not None:
+            self.n_edges = int(np.count_nonzero(ep == q))
+            self.n_vertices = self.n_dofs - self.n_interior
 
     @classmethod
     def from_metric_graph(cls, g, h, **kw):
         return cls(g.n_vertices, g.edge_u, g.edge_v, g.length, h, **kw)
 
     @classmethod
-    def from_part(cls, part, h, **kw):
-        """A part of an edge-partitioned graph (edgepart.Part) -> grf_graph_create_part."""
-        return cls(part.n_vertices, part.edge_u, part.edge_v, part.length, h, part=part, **kw)
+    def part_of(cls, whole: "Graph", edge_part, n_parts: int, q: int, **kw):
+        """Part q of an edge partition of `whole` (grf_graph_create_part: the library derives the
+        local mesh, global DOF ids, whole-graph vertex masses / degrees, ownership and halo lists)."""
+        return cls(0, None, None, None, whole.h, _part=(whole, edge_part, n_parts, q), **kw)
+
+    def partition(self, n_parts: int, xy=None):
+        """grf_partition_edges: (edge_part [E] int32, info dict).  xy: vertex coordinates [V, 2] for
+        recursive coordinate bisection, else breadth-first runs of equal DOF weight."""
+        ep = np.empty(self.n_edges, dtype=np.int32)
+        info = np.zeros(4, dtype=np.int64)
+        pxy = None
+        if xy is not None:
+            xy = np.ascontiguousarray(xy, dtype=np.float64)
+            pxy = xy.ctypes.data_as(C.POINTER(C.c_double))
+        check(self._lib.grf_partition_edges(self._h, int(n_parts), pxy, ep.ctypes.data_as(C.POINTER(C.c_int32)),
+                                            info.ctypes.data_as(C.POINTER(C.c_int64))))
+        return ep, {"n_interface": int(info[0]), "max_part_weight": int(info[1]), "min_part_weight": int(info[2]),
+                    "empty_parts": int(info[3])}
+
+    def part_dofs(self) -> np.ndarray:
+        """Global DOF index of every local DOF (grf_graph_part_dofs; the identity for a whole graph)."""
+        out = np.empty(self.n_dofs, dtype=np.int64)
+        check(self._lib.grf_graph_part_dofs(self._h, out.ctypes.data_as(C.POINTER(C.c_int64))))
+        return out
 
     # ------------------------------------------------------------------ queries
     def edge_layout(self):
@@ -356,17 +374,25 @@ def dist_shard(world: int, rank: int, n_samples: int, n_nodes: int):
     return (out[0], out[1]), (out[2], out[3]), out[4], bool(f & 1), bool(f & 2), f >> 2
 
 
-def sample_dist(graph: "Graph", comm: "Comm", kappa, beta, k, seed=0, n_samples=1, stream=None, **opts):
+def sample_dist(graph: "Graph", comm: "Comm", kappa, beta, k, seed=0, n_samples=1, stream=None, out=None,
+                return_stats=False, **opts):
     """grf_sample_dist (sample-then-node sharding in the library, NCCL reduce of node shards):
-    returns (u or None, sample_range, is_root); u is the rank's [n_local, N] result."""
+    returns (u or None, sample_range, is_root[, stats]); u is the rank's [n_local, N] result (the
+    full field of its sample range on the range's root).  Every rank of the communicator calls it."""
     torch = _torch()
     o = make_options(**opts)
     km, kp, _, _ = plan_info(beta, k)
     (s0, s1), _, _, active, is_root, _ = dist_shard(comm.world, comm.rank, n_samples, km + kp + 1)
-    if not active:
-        return None, (0, 0), False
-    u = torch.empty((s1 - s0, graph.n_dofs), dtype=torch.float64, device=f"cuda:{graph.device}")
+    u = None
+    if active:
+        u = out if out is not None else torch.empty((s1 - s0, graph.n_dofs), dtype=torch.float64,
+                                                    device=f"cuda:{graph.device}")
+        graph._check_out(u, s1 - s0)
     rng = (C.c_int64 * 6)()
-    check(load().grf_sample_dist(graph._h, comm.handle, kappa, beta, k, C.c_uint64(seed & (2 ** 64 - 1)), n_samples,
-                                 C.byref(o), C.c_void_p(u.data_ptr()), rng, C.c_void_p(_stream_ptr(stream)), None))
-    return u, (s0, s1), is_root
+    st = grf_stats() if return_stats else None
+    rc = load().grf_sample_dist(graph._h, comm.handle, kappa, beta, k, C.c_uint64(seed & (2 ** 64 - 1)), n_samples,
+                                C.byref(o), C.c_void_p(u.data_ptr() if u is not None else 0), rng,
+                                C.c_void_p(_stream_ptr(stream)), C.byref(st) if st is not None else None)
+    check(rc)
+    res = (u if active else None, (s0, s1) if active else (0, 0), bool(is_root and active))
+    return res + (st.as_dict(),) if return_stats else res

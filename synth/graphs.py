@@ -36,6 +36,7 @@ class MetricGraph:
     edge_v: np.ndarray  # int64 [E]
     length: np.ndarray  # float64 [E]
     name: str = "graph"
+    coords: object = None  # optional float64 [V, 2] vertex positions (geometric graphs: partitioning)
 
     @property
     def n_edges(self) -> int:
@@ -182,7 +183,7 @@ def rgg_knn(n: int = 100_000, k: int = 3, scale: float = 300.0, seed: int = 0) -
     eu = np.concatenate([eu, np.asarray(bu, dtype=np.int64)])
     ev = np.concatenate([ev, np.asarray(bv, dtype=np.int64)])
     lengths = np.hypot(*(pts[eu] - pts[ev]).T)
-    return MetricGraph(n, eu, ev, lengths, f"rgg{n}_knn{k}_seed{seed}")
+    return MetricGraph(n, eu, ev, lengths, f"rgg{n}_knn{k}_seed{seed}", coords=pts)
 
 
 # --------------------------------------------------------------------------

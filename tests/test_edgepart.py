@@ -12,7 +12,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import dd, fem, solve
-from paper_2605_02670_b200.edgepart import element_counts, gather, partition
+from _edgepart_ref import element_counts, gather, partition
 from synth import lattice, star_of_lattices, tadpole
 
 

@@ -10,8 +10,8 @@ pytestmark = pytest.mark.gpu
 
 from oracle import solve  # noqa: E402
 from paper_2605_02670_b200 import Graph, sample_edgepart  # noqa: E402
-from paper_2605_02670_b200.edgepart import gather, partition  # noqa: E402
-from synth import CONFIGS, config_graph, lattice, star_of_lattices  # noqa: E402
+from paper_2605_02670_b200.edgepart import gather, make_parts, partition  # noqa: E402
+from synth import CONFIGS, config_graph, lattice, star_of_lattices, tadpole  # noqa: E402
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -25,12 +25,45 @@ def _rel(a, b):
     return np.linalg.norm(a - b, axis=-1) / np.linalg.norm(b, axis=-1)
 
 
-def _run_parts(g, h, P, kappa, beta, k, seed, S, **opts):
-    parts = partition(g, h, P)
-    gs = [Graph.from_part(p, h) for p in parts]
+def _run_parts(g, h, P, kappa, beta, k, seed, S, xy=None, **opts):
+    G = Graph.from_metric_graph(g, h)
+    ep, _ = partition(G, P, xy=xy)
+    gs = make_parts(G, ep, P)
     us, st = sample_edgepart(gs, kappa, beta, k, seed=seed, n_samples=S, return_stats=True, **opts)
-    N = int(sum(np.maximum(1, np.ceil(g.length / h)) - 1)) + g.n_vertices
-    return gather(parts, [u.cpu().numpy() for u in us], h, N), st, parts, gs
+    return gather(gs, [u.cpu().numpy() for u in us], G.n_dofs), st, ep, gs
+
+
+@pytest.mark.parametrize("gname,h,P,geo", [("lattice5", 0.05, 2, False), ("lattice5", 0.05, 3, True),
+                                           ("star", 0.25, 4, False), ("tadpole", 0.1, 2, False),
+                                           ("rgg", 0.05, 5, True), ("lattice5", 0.05, 1, False)])
+def test_library_partition_structure(gname, h, P, geo):
+    """grf_partition_edges + grf_graph_create_part: every edge in exactly one non-empty part; each
+    vertex owned once; the parts' global DOF maps (grf_graph_part_dofs) cover the whole graph with
+    interiors exactly once; part noise = whole-graph noise at the part's DOFs (so the whole-graph
+    vertex masses and global counters are used); balanced DOF weights."""
+    from synth import rgg_knn
+    g = {"lattice5": lattice(5, seed=1), "star": star_of_lattices(3, 3), "tadpole": tadpole(),
+         "rgg": rgg_knn(600, k=3, scale=300.0 * (600 / 100_000) ** 0.5, seed=2)}[gname]
+    G = Graph.from_metric_graph(g, h)
+    ep, info = partition(G, P, xy=g.coords if geo else None)
+    assert ep.shape == (g.n_edges,) and ep.min() >= 0 and ep.max() < P and info["empty_parts"] == 0
+    gs = make_parts(G, ep, P)
+    seen = np.zeros(G.n_dofs, int)
+    for q, Gq in enumerate(gs):
+        assert Gq.n_edges == int((ep == q).sum())
+        d = Gq.part_dofs()
+        seen[d] += 1
+        Wq = Gq.noise(7, 2).cpu().numpy()
+        assert np.array_equal(Wq.view(np.uint64), G.noise(7, 2).cpu().numpy()[:, d].view(np.uint64))
+    NI = G.n_interior
+    assert np.all(seen[:NI] == 1) and np.all(seen[NI:] >= 1)
+    touched = np.zeros(g.n_vertices, int)
+    for q in range(P):
+        vs = np.unique(np.concatenate([g.edge_u[ep == q], g.edge_v[ep == q]]))
+        touched[vs] += 1
+    assert info["n_interface"] == int((touched > 1).sum())
+    w = np.bincount(ep, weights=np.maximum(1, np.ceil(g.length / h)), minlength=P)
+    assert info["max_part_weight"] == int(w.max()) and w.max() <= 2.0 * w.mean() + np.ceil(g.length / h).max()
 
 
 @pytest.mark.parametrize("P,S", [(1, 2), (2, 1), (2, 3), (3, 16), (4, 20)])
@@ -50,21 +83,24 @@ def test_edgepart_noise_and_interfaces_consistent():
     whole graph's noise (global Philox counters, whole-graph vertex masses)."""
     g = star_of_lattices(3, 4)
     h = 0.125
-    parts = partition(g, h, 3)
-    gs = [Graph.from_part(p, h) for p in parts]
     whole = Graph.from_metric_graph(g, h)
+    ep, _ = partition(whole, 3)
+    gs = make_parts(whole, ep, 3)
     Wall = whole.noise(7, 2).cpu().numpy()
-    for p, G in zip(parts, gs):
-        assert np.array_equal(G.noise(7, 2).cpu().numpy().view(np.uint64), Wall[:, p.dof_gid(h)].view(np.uint64))
+    for G in gs:
+        assert np.array_equal(G.noise(7, 2).cpu().numpy().view(np.uint64), Wall[:, G.part_dofs()].view(np.uint64))
     us = sample_edgepart(gs, 3.0, 0.6, 0.35, seed=7, n_samples=2)
     vals = {}
-    for p, u in zip(parts, us):
+    NI = whole.n_interior
+    for G, u in zip(gs, us):
         uu = u.cpu().numpy()
-        for i, v in enumerate(p.vertices):
-            x = uu[:, u.shape[1] - p.n_vertices + i]
-            if v in vals:
-                assert np.allclose(vals[v], x, rtol=1e-12, atol=1e-14)
-            vals[v] = x
+        for i, d in enumerate(G.part_dofs()):
+            if d < NI:
+                continue
+            x = uu[:, i]
+            if d in vals:
+                assert np.allclose(vals[d], x, rtol=1e-12, atol=1e-14)
+            vals[d] = x
 
 
 def test_edgepart_equals_whole_graph_rgg():
@@ -72,8 +108,8 @@ def test_edgepart_equals_whole_graph_rgg():
     g = rgg_knn(5000, k=3, scale=300.0 * (5000 / 100_000) ** 0.5, seed=1)
     h, kappa, beta, k = 0.02, 2.0, 0.55, 0.6
     whole = Graph.from_metric_graph(g, h).sample(kappa, beta, k, seed=4, n_samples=16).cpu().numpy()
-    for P in (2, 5):
-        u, st, _, _ = _run_parts(g, h, P, kappa, beta, k, seed=4, S=16)
+    for P, geo in ((2, False), (5, True)):
+        u, st, _, _ = _run_parts(g, h, P, kappa, beta, k, seed=4, S=16, xy=g.coords if geo else None)
         assert _rel(u, whole).max() <= 1e-10, f"P={P}"
 
 
@@ -94,11 +130,12 @@ def test_edgepart_nccl_one_rank():
         comm = Comm()
         g = lattice(4, seed=3)
         h = 0.05
-        part = partition(g, h, 1)[0]
-        G = Graph.from_part(part, h)
+        W = Graph.from_metric_graph(g, h)
+        ep, _ = partition(W, 1)
+        G = make_parts(W, ep, 1)[0]
         u = sample_edgepart([G], 3.0, 0.7, 0.4, seed=1, n_samples=4, comm=comm)[0].cpu().numpy()
-        ref = Graph.from_metric_graph(g, h).sample(3.0, 0.7, 0.4, seed=1, n_samples=4).cpu().numpy()
-        assert _rel(gather([part], [u], h, ref.shape[1]), ref).max() <= 1e-11
+        ref = W.sample(3.0, 0.7, 0.4, seed=1, n_samples=4).cpu().numpy()
+        assert _rel(gather([G], [u], ref.shape[1]), ref).max() <= 1e-11
         comm.close()
     finally:
         dist.destroy_process_group()
@@ -115,7 +152,7 @@ def test_config4_edge_partitioned_two_parts():
     del G
     gc.collect()
     torch.cuda.empty_cache()
-    u, st, _, _ = _run_parts(g, cfg["h"], 2, cfg["kappa"], cfg["beta"], cfg["k"], seed=0, S=16)
+    u, st, _, _ = _run_parts(g, cfg["h"], 2, cfg["kappa"], cfg["beta"], cfg["k"], seed=0, S=16, xy=g.coords)
     assert st["n_unconverged"] == 0
     assert _rel(u[[0, 15]], whole).max() <= 1e-10
 

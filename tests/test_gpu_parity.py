@@ -131,7 +131,7 @@ def test_small_graph_all_preconditioners(precond):
     u, st = G.sample(kappa, beta, k, seed=1, n_samples=5, precond=precond, return_stats=True)
     ref, _, _ = solve.sample(g, h, kappa, beta, k, 1, 5)
     assert _rel(u.cpu().numpy(), ref).max() <= FIELD_TOL
-    assert st["n_unconverged"] == 0
+    assert st["n_unconverged"] == 0 and st["worst_true_rel_residual"] <= 1e-11
 
 
 def test_ragged_and_degenerate_edges():
@@ -217,6 +217,17 @@ def test_host_output_matches_device(n_samples):
     assert st["worst_rel_residual"] <= 1e-13
 
 
+def test_nonfinite_output_is_reported():
+    """An infinite right-hand side (grf_apply) gives non-finite fields: the exit check reports them
+    (GRF_ENOCONV with statistics) instead of returning silently."""
+    from paper_2605_02670_b200 import GrfError
+    G = _graph(lattice(3, seed=2), 0.1)
+    rhs = torch.zeros((2, G.n_dofs), dtype=torch.float64, device="cuda")
+    rhs[1, 3] = float("inf")
+    with pytest.raises(GrfError):
+        G.apply(2.0, 0.6, 0.3, rhs, return_stats=True)
+
+
 def test_invalid_arguments():
     from paper_2605_02670_b200 import GrfError
     G = _graph(single_edge(1.0), 0.1)
@@ -249,6 +260,10 @@ def test_config3_lattice_256_samples_sampled():
     u, st = G.sample(cfg["kappa"], cfg["beta"], cfg["k"], seed=cfg["seed"], n_samples=cfg["n_samples"],
                      return_stats=True)
     assert st["n_nodes"] == 212 and st["n_unconverged"] == 0
+    # exit checks: the TRUE residual of every vertex system, no non-finite output,
+    # and the per-phase device times
+    assert 0.0 < st["worst_true_rel_residual"] <= 1e-11 and st["n_nonfinite"] == 0
+    assert all(st["phase_ms"][k] > 0.0 for k in ("noise", "condense", "pcg", "recover"))
     picks = [0, 101, 255]
     ref, _, _ = solve.sample(g, cfg["h"], cfg["kappa"], cfg["beta"], cfg["k"], cfg["seed"], cfg["n_samples"],
                              samples=picks)
@@ -314,6 +329,7 @@ def test_config4_rgg_full_size():
                      return_stats=True)
     assert G.n_dofs == 28_032_313
     assert st["n_nodes"] == 112 and st["n_unconverged"] == 0 and st["worst_rel_residual"] <= 1e-13
+    assert st["worst_true_rel_residual"] <= 1e-11 and st["n_nonfinite"] == 0
     picks = [0, 15]
     got = u[picks].cpu().numpy()
     del u
