@@ -31,6 +31,7 @@ namespace grf {
 namespace {
 
 constexpr int GT = 256;  // threads per CTA = vertices per item
+constexpr int NB = 4;    // neighbours gathered per batch (loads issued together)
 
 struct GArgs {
     DevGraph g;
@@ -164,7 +165,7 @@ __device__ void node_reduce(const GArgs& A, int l, int nvb, double* red, Finish&
 }
 
 template <int CS>
-__global__ void __launch_bounds__(GT, 6) pcg_global_kernel(GArgs A) {
+__global__ void __launch_bounds__(GT, 4) pcg_global_kernel(GArgs A) {
     cg::grid_group grid = cg::this_grid();
     constexpr int VBK = GT / CS;  // vertices per sub-chunk
     constexpr int RED = (GT + 2 * CS) > ((GT / 32) * 2 * CS) ? (GT + 2 * CS) : ((GT / 32) * 2 * CS);
@@ -295,9 +296,25 @@ __global__ void __launch_bounds__(GT, 6) pcg_global_kernel(GArgs A) {
                 const int e = v * CS + s;  // offset within node l's [V][CS] slab (32-bit)
                 const double pv = fma(bt, po_l[e], z_l[e]);
                 double qv = tab[v] * pv;
-                for (int k = g.gp_ptr[v]; k < g.gp_ptr[v + 1]; ++k) {
-                    const int ob = g.gp_other[k] * CS + s;
-                    qv = fma(tab[3 * (int64_t)V + k], fma(bt, po_l[ob], z_l[ob]), qv);
+                // neighbours in chunks of NB: indices and coefficients first, then every vector load,
+                // then the FMAs (many loads in flight per thread; padding slots read the own row)
+                const int kb = g.gp_ptr[v], ke = g.gp_ptr[v + 1];
+                for (int k0 = kb; k0 < ke; k0 += NB) {
+                    int ob[NB];
+                    double cf[NB], a[NB], b[NB];
+#pragma unroll
+                    for (int j = 0; j < NB; ++j) {
+                        const bool ok = k0 + j < ke;
+                        ob[j] = (ok ? g.gp_other[k0 + j] : v) * CS + s;
+                        cf[j] = ok ? tab[3 * (int64_t)V + k0 + j] : 0.0;
+                    }
+#pragma unroll
+                    for (int j = 0; j < NB; ++j) {
+                        a[j] = po_l[ob[j]];
+                        b[j] = z_l[ob[j]];
+                    }
+#pragma unroll
+                    for (int j = 0; j < NB; ++j) qv = fma(cf[j], fma(bt, a[j], b[j]), qv);
                 }
                 __stcs(pn_l + e, pv);  // streaming stores: keep L2 for the neighbour gathers
                 __stcs(q_l + e, qv);
@@ -342,9 +359,23 @@ __global__ void __launch_bounds__(GT, 6) pcg_global_kernel(GArgs A) {
                 double zv;
                 if (A.prm.precond == 0) {
                     zv = tab[V + v] * rv;
-                    for (int k = g.gp_ptr[v]; k < g.gp_ptr[v + 1]; ++k) {
-                        const int ob = g.gp_other[k] * CS + s;
-                        zv = fma(tab[3 * (int64_t)V + E2 + k], fma(-al, q_l[ob], ro_l[ob]), zv);
+                    const int kb = g.gp_ptr[v], ke = g.gp_ptr[v + 1];
+                    for (int k0 = kb; k0 < ke; k0 += NB) {
+                        int ob[NB];
+                        double cf[NB], a[NB], b[NB];
+#pragma unroll
+                        for (int j = 0; j < NB; ++j) {
+                            const bool ok = k0 + j < ke;
+                            ob[j] = (ok ? g.gp_other[k0 + j] : v) * CS + s;
+                            cf[j] = ok ? tab[3 * (int64_t)V + E2 + k0 + j] : 0.0;
+                        }
+#pragma unroll
+                        for (int j = 0; j < NB; ++j) {
+                            a[j] = q_l[ob[j]];
+                            b[j] = ro_l[ob[j]];
+                        }
+#pragma unroll
+                        for (int j = 0; j < NB; ++j) zv = fma(cf[j], fma(-al, a[j], b[j]), zv);
                     }
                 } else {
                     zv = (A.prm.precond == 1 ? tab[2 * V + v] : 1.0) * rv;

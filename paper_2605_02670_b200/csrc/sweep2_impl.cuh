@@ -51,6 +51,14 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void cpasync_arrive_noinc(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// The item a stage belongs to, written by the producer (which loads the edge's metadata anyway)
+// so that consumers start an item from shared memory instead of a chain of dependent global loads.
+struct ItemDesc {
+    int32_t it, e, m, vu, vv, pad;
+    int64_t off, toff;
+    double h;
+};
+
 // Output accesses of the writer lanes (generic addresses: the shared output tile, or u itself for
 // edges too long for it), predicated and branch-free so the scheduler can interleave them with
 // the next step's FMAs.  Volatile asm WITHOUT a memory clobber: they stay in program order among
@@ -88,12 +96,13 @@ struct Cfg {
     static constexpr int WROW = CS + 4;             // a staged noise row (skewed: the (side, copy) rows read
                                                     // together fall into different shared-memory banks)
     static constexpr int WEL = IBK * 2 * NC * WROW; // staged noise doubles per stage
-    static constexpr size_t HDR = 256;              // mbarriers, stage headers
+    static constexpr size_t HDR = 512;              // mbarriers, stage headers (item descriptors)
     static constexpr size_t COEF = (size_t)NST * NTAB * IBK * RN * sizeof(double);
     static constexpr size_t WB = (size_t)NST * WEL * sizeof(double);
     static constexpr size_t FIXED = HDR + COEF + WB;
     static_assert(TS == 2 || TS == 4, "2 or 4 samples per lane");
-    static_assert(NST * (8 + 8 + 4) <= (int)HDR, "header room");
+    static_assert(NST * (8 + 8 + 48) + 16 <= (int)HDR, "header room");
+    static_assert(2 * NC * CS <= 128, "one noise row per producer thread");
 };
 
 template <int TL, int TS, bool REC>
@@ -110,7 +119,7 @@ __global__ void __launch_bounds__(Cfg<TL, TS, REC>::NT, 1) sweep2_kernel(Args A)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);         // [NST]
     uint64_t* empty = full + NST;                                    // [NST]
-    int* header = reinterpret_cast<int*>(empty + NST);               // [NST] item of the stage (-1: end)
+    ItemDesc* header = reinterpret_cast<ItemDesc*>(empty + NST);    // [NST] item of the stage (it = -1: end)
     double* coef = reinterpret_cast<double*>(smem_raw + C::HDR);     // [NST][NTAB][IBK][RN]
     double* wbuf = coef + NST * NTAB * IBK * RN;                     // [NST][IBK][2 side][NC][WROW]
     double* cLs = wbuf + NST * C::WEL;                               // [Lp] c_L (REC)
@@ -118,7 +127,7 @@ __global__ void __launch_bounds__(Cfg<TL, TS, REC>::NT, 1) sweep2_kernel(Args A)
 
     if (tid == 0) {
         for (int s = 0; s < NST; ++s) {
-            mbar_init(&full[s], 33);    // producer lane 0's expect_tx arrive + 32 cp.async arrivals
+            mbar_init(&full[s], 129);   // the expect_tx arrive + the 128 producer threads' cp.async arrivals
             mbar_init(&empty[s], NCW);  // one release per consumer warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -128,48 +137,54 @@ __global__ void __launch_bounds__(Cfg<TL, TS, REC>::NT, 1) sweep2_kernel(Args A)
     __syncthreads();
 
     // ------------------------------------------------------------------------------------ producer
+    // All four warps of the producer warpgroup (one per SM sub-partition, so the copy issue
+    // load is spread evenly over the schedulers) walk the same stage sequence: warp NCW takes the
+    // queue and broadcasts the item through shared memory (named barrier 1 over the warpgroup);
+    // every producer thread owns one (sample, copy, side) noise row per stage and its lane 0 in
+    // warp NCW issues the coefficient bulk copies.
     if (warp >= NCW) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
-        if (warp != NCW) return;
+        const int ptid = tid - NCW * 32;  // 0..127
+        volatile int* qbox = reinterpret_cast<volatile int*>(header + NST);  // queue broadcast slot
+        auto pbar = []() { asm volatile("bar.sync 1, 128;" ::: "memory"); };
         int stage = 0;
         uint32_t use = 0;  // bit s: parity of stage s's current use
+        ItemDesc cur{};
+        constexpr int NROW = 2 * NC * CS;  // noise rows per stage (<= 128)
         auto produce = [&](int item_hdr, int64_t c0, int m, int64_t off, int64_t toff, int rd, int t0, int nb) {
             mbar_wait(&empty[stage], ((use >> stage) & 1u) ^ 1u);
-            if (lane == 0) {
-                header[stage] = item_hdr;
+            if (ptid == 0) {
+                header[stage] = cur;
+                header[stage].it = item_hdr;
                 fence_proxy_async();
                 mbar_expect_tx(&full[stage], (uint32_t)(NTAB * nb * RN * sizeof(double)));
             }
-            __syncwarp();
+            pbar();  // the expect_tx arrive precedes every copy's completion
             if (nb > 0) {
                 double* cdst = coef + stage * NTAB * IBK * RN;
                 if (A.rounds == 1) {  // rows are contiguous: one copy per table
-                    if (lane < NTAB)
-                        bulk_g2s(cdst + lane * IBK * RN, (lane == 0 ? A.mu : A.gam) + (toff + t0) * (int64_t)Lp,
+                    if (ptid < NTAB)
+                        bulk_g2s(cdst + ptid * IBK * RN, (ptid == 0 ? A.mu : A.gam) + (toff + t0) * (int64_t)Lp,
                                  (uint32_t)(nb * RN * sizeof(double)), &full[stage]);
                 } else {
-                    for (int x = lane; x < NTAB * nb; x += 32) {
+                    for (int x = ptid; x < NTAB * nb; x += 128) {
                         const int tb = x / nb, tt = x % nb;
                         bulk_g2s(cdst + (tb * IBK + tt) * RN,
                                  (tb == 0 ? A.mu : A.gam) + (toff + t0 + tt) * (int64_t)Lp + rd * RN,
                                  (uint32_t)(RN * sizeof(double)), &full[stage]);
                     }
                 }
-                // noise at the left positions t0+tt and the right positions m-1-t0-tt; consecutive
-                // lanes take consecutive steps of one (sample, copy, side) run (copy 1: samples
-                // pair-swapped, sample s ^ 1 at index s)
-                double* wb = wbuf + stage * C::WEL;
+                // noise row (side, copy, sample) of this thread: the nb positions t0+tt (left) or
+                // m-1-t0-tt (right); copy 1 holds the samples pair-swapped (sample s ^ 1 at index s)
+                if (ptid < NROW) {
+                    const int side = ptid & 1, c = (ptid >> 1) % NC, s = (ptid >> 1) / NC;
+                    int64_t sg = c0 + (c ? (s ^ 1) : s);
+                    if (sg >= A.S) sg = A.S - 1;
+                    const double* src = A.W + sg * N + off + (side ? (m - 1 - t0) : t0);
+                    const int dstep = side ? -1 : 1;
+                    double* dst = wbuf + stage * C::WEL + (side * NC + c) * C::WROW + s;
 #pragma unroll 4
-                for (int x = lane; x < IBK * 2 * NC * CS; x += 32) {
-                    const int tt = x % IBK, r = x / IBK;
-                    const int side = r & 1, r2 = r >> 1;
-                    const int c = r2 % NC, s = r2 / NC;
-                    if (tt < nb) {
-                        int64_t sg = c0 + (c ? (s ^ 1) : s);
-                        if (sg >= A.S) sg = A.S - 1;
-                        const int pos = side ? (m - 1 - t0 - tt) : (t0 + tt);
-                        cp_async8(wb + ((tt * 2 + side) * NC + c) * C::WROW + s, A.W + sg * N + off + pos);
-                    }
+                    for (int tt = 0; tt < nb; ++tt) cp_async8(dst + tt * 2 * NC * C::WROW, src + dstep * tt);
                 }
             }
             cpasync_arrive_noinc(&full[stage]);
@@ -177,9 +192,10 @@ __global__ void __launch_bounds__(Cfg<TL, TS, REC>::NT, 1) sweep2_kernel(Args A)
             stage = stage + 1 == NST ? 0 : stage + 1;
         };
         for (;;) {
-            int it = 0;
-            if (lane == 0) it = atomicAdd(A.counter, 1);
-            it = __shfl_sync(0xffffffffu, it, 0);
+            if (ptid == 0) *qbox = atomicAdd(A.counter, 1);
+            pbar();
+            const int it = *qbox;
+            pbar();  // everyone has read the slot before it is rewritten
             if (it >= A.n_items) {
                 produce(-1, 0, 0, 0, 0, 0, 0, 0);
                 break;
@@ -189,6 +205,19 @@ __global__ void __launch_bounds__(Cfg<TL, TS, REC>::NT, 1) sweep2_kernel(Args A)
             if (REC && m == 0) continue;  // nothing to recover: the vertex values come from vertex_sum
             const int64_t c0 = (int64_t)(it % A.chunks) * CS;
             const int64_t off = g.off[e], toff = g.toff[e];
+            cur.it = it;
+            cur.e = e;
+            cur.m = m;
+            cur.vu = g.eu[e];
+            cur.vv = g.ev[e];
+            cur.off = off;
+            cur.toff = toff;
+            cur.h = g.h[e];
+            if (REC && ptid < 2) {  // the consumers' round-start u_G rows of this item: into L2 now
+                const int v = ptid ? cur.vv : cur.vu;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.uG + (((it % A.chunks) * g.V + v) * (int64_t)L << CSL)),
+                             "r"((uint32_t)(L * CS * sizeof(double))) : "memory");
+            }
             if (m == 0) {  // condense: one empty stage, the consumers write zero end values
                 produce(it, c0, m, off, toff, 0, 0, 0);
                 continue;
@@ -225,17 +254,18 @@ __global__ void __launch_bounds__(Cfg<TL, TS, REC>::NT, 1) sweep2_kernel(Args A)
 
     for (;;) {
         acquire();
-        const int it = header[stage];
+        const ItemDesc d = header[stage];
+        const int it = d.it;
         if (it < 0) break;
-        const int e = g.edge_order[it / A.chunks];
+        const int e = d.e;
         const int64_t tile = it % A.chunks;
         const int64_t c0 = tile * CS;
-        const int m = g.m[e];
-        const int64_t off = g.off[e];
-        const int64_t toff = g.toff[e];
-        const double h = g.h[e];
+        const int m = d.m;
+        const int64_t off = d.off;
+        const int64_t toff = d.toff;
+        const double h = d.h;
         const double inv_h = 1.0 / h;
-        const int vu = g.eu[e], vv = g.ev[e];
+        const int vu = d.vu, vv = d.vv;
         if (!REC && m == 0) {  // no interior: zero end values (ends [tile][l][code][CS])
             for (int x = lane; x < L * 2 * TS; x += 32) {
                 const int l = x / (2 * TS), r = x % (2 * TS);
@@ -286,7 +316,10 @@ __global__ void __launch_bounds__(Cfg<TL, TS, REC>::NT, 1) sweep2_kernel(Args A)
 #pragma unroll
                 for (int n = 0; n < TL; ++n) {
                     const int l = rb + slot(n);
-                    g0[n] = l < L ? A.gam[toff * (int64_t)Lp + l] : 0.0;  // g_0 = g_{m-1} for the end values
+                    // g_0 = g_{m-1} for the end values, loaded now (volatile: not sunk to the round's end)
+                    double gv = 0.0;
+                    if (l < L) asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(gv) : "l"(A.gam + toff * (int64_t)Lp + l));
+                    g0[n] = gv;
 #pragma unroll
                     for (int j = 0; j < TS; ++j) X[n][j] = Q[n][j] = 0.0;
                 }
