@@ -26,7 +26,10 @@
  * base seed sigma uses Philox4x32-10 key (lo32(sigma+j), hi32(sigma+j)) and for
  * DOF i the counter (lo32(i), hi32(i), 0, 0); Box-Muller with the fixed ln / cos
  * operation sequences of DESIGN.md; W_i = sqrt(M_L,ii) z_i.  Hence
- * grf_sample(seed=s0, n=1) reproduces sample s0 of grf_sample(seed=0, n > s0).
+ * grf_sample(seed=s0, n=1) reproduces sample s0 of grf_sample(seed=0, n > s0) -- and, the flip
+ * side, calls with base seeds sigma and sigma + 1 share all but one sample (shifted by one):
+ * independent calls must use base seeds at least n_samples apart (the chunked host path and the
+ * sample-sharded path rely on the shift to draw sample ranges).
  *
  * Conventions for every call:
  *   - status codes, never exceptions / aborts across the ABI; grf_last_error()

@@ -237,6 +237,11 @@ class Graph:
 
     def sample_into_host(self, kappa, beta, k, seed, n_samples, host_out, stream=None, **opts):
         """grf_sample_host into a caller (e.g. pinned) host buffer; returns host_out."""
+        torch = _torch()
+        if (host_out.is_cuda or host_out.dtype != torch.float64 or not host_out.is_contiguous()
+                or host_out.numel() != n_samples * self.n_dofs):
+            raise ValueError(f"host_out must be a contiguous CPU float64 tensor with {n_samples}x{self.n_dofs} "
+                             "elements (pinned memory lets the copies overlap)")
         o = make_options(**opts)
         check(self._lib.grf_sample_host(self._h, kappa, beta, k, C.c_uint64(seed & (2 ** 64 - 1)), n_samples,
                                         C.byref(o), C.c_void_p(host_out.data_ptr()), C.c_void_p(_stream_ptr(stream)),

@@ -228,6 +228,20 @@ def test_nonfinite_output_is_reported():
         G.apply(2.0, 0.6, 0.3, rhs, return_stats=True)
 
 
+def test_sample_into_host_checks_its_buffer():
+    """grf_sample_host writes n x N doubles into the caller's buffer: a wrong size, dtype or device
+    is rejected before the call (no out-of-bounds host write)."""
+    G = _graph(lattice(3, seed=2), 0.1)
+    for bad in (torch.empty((2, G.n_dofs - 1), dtype=torch.float64),
+                torch.empty((2, G.n_dofs), dtype=torch.float32),
+                torch.empty((2, G.n_dofs), dtype=torch.float64, device="cuda")):
+        with pytest.raises(ValueError):
+            G.sample_into_host(2.0, 0.6, 0.3, 0, 2, bad)
+    ok = torch.empty((2, G.n_dofs), dtype=torch.float64)
+    G.sample_into_host(2.0, 0.6, 0.3, 0, 2, ok)
+    assert torch.equal(ok, G.sample(2.0, 0.6, 0.3, seed=0, n_samples=2).cpu())
+
+
 def test_invalid_arguments():
     from paper_2605_02670_b200 import GrfError
     G = _graph(single_edge(1.0), 0.1)

@@ -22,6 +22,10 @@ def short(name):
     m = re.search(r"sweep_kernel<\s*\d+,\s*\d+,\s*\d+,\s*\d+,\s*(\d)", name)  # the REC argument
     if m:
         return "condense" if m.group(1) == "0" else "recover"
+    m = re.search(r"sweep2_kernel<([^>]*)>", name)  # warp-specialised sweep: <TL, TS, REC>
+    if m:
+        rec = m.group(1).split(",")[-1].strip().replace("(bool)", "")
+        return "condense" if rec in ("0", "false") else "recover"
     for k, v in (("noise_kernel", "noise"), ("edge_setup_kernel", "edge_setup"), ("pcg_tables_pos_kernel", "pcg_tables_pos"),
                  ("pcg_tables_kernel", "pcg_tables"),
                  ("assemble_rhs_kernel", "assemble"), ("vertex_sum_kernel", "vertex_sum"),
@@ -71,7 +75,7 @@ raw = subprocess.run(["ncu", "-i", os.path.join(G, f"{R}_full.ncu-rep"), "--page
                      capture_output=True, text=True).stdout.splitlines()
 r = list(csv.reader(raw))
 hdr = r[0]
-keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sector_hit_rate.pct",
         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "launch__registers_per_thread", "launch__block_size", "launch__grid_size", "smsp__inst_executed.sum",
