@@ -26,5 +26,5 @@ for P in (2, 4, 8):
         out["partitions"].append(dict(parts=P, method=method, edges_per_part=counts, **info,
                                       weight_imbalance=info["max_part_weight"] * P / total))
         print(P, method, info, flush=True)
-os.makedirs("profiles", exist_ok=True)
-json.dump(out, open(f"profiles/{tag}_partition.json", "w"), indent=1)
+os.makedirs("gpurun_out", exist_ok=True)  # copied into profiles/ by hand (gpurun returns gpurun_out/ only)
+json.dump(out, open(f"gpurun_out/{tag}_partition.json", "w"), indent=1)
