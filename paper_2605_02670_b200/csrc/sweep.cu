@@ -18,6 +18,9 @@ cudaError_t launch_c32(int tl, sweep::Args a, cudaStream_t st);
 cudaError_t launch_r16(int tl, sweep::Args a, cudaStream_t st);
 cudaError_t launch_r32(int tl, sweep::Args a, cudaStream_t st);
 }  // namespace sweep2
+namespace sweep3 {
+cudaError_t launch_r32(int tl, sweep::Args a, cudaStream_t st);
+}  // namespace sweep3
 
 namespace {
 constexpr int TL_MAX = 7;  // nodes per lane of the sweep kernels (register tile)
@@ -82,7 +85,12 @@ cudaError_t launch_recover(const DevGraph& g, const DevPlan& p, int64_t n_sample
                            const double* uG, int32_t* counter, cudaStream_t st) {
     const sweep::Args a = make_args(g, p, n_samples, W, u, uG, counter);
     switch (sweep::variant_for(n_samples)) {
-        case sweep::V2: return a.ablate & 8 ? sweep2::launch_r32(p.TL, a, st) : sweep::launch_r2k(p.TL, a, st);
+        case sweep::V2:
+            // sweep3 (warp-specialised around the sweep_impl register tile) is the default; the
+            // earlier designs stay selectable for design studies (GRF_ABLATE bits 8, 16)
+            if (a.ablate & 8) return sweep2::launch_r32(p.TL, a, st);
+            if (a.ablate & 16) return sweep::launch_r2k(p.TL, a, st);
+            return sweep3::launch_r32(p.TL, a, st);
         case sweep::V1: return a.ablate & 8 ? sweep2::launch_r16(p.TL, a, st) : sweep::launch_r1k(p.TL, a, st);
         default: return sweep::launch_r0k(p.TL, a, st);
     }

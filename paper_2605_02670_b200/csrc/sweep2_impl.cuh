@@ -39,6 +39,7 @@ using sweep::fence_proxy_async;
 using sweep::mbar_expect_tx;
 using sweep::mbar_init;
 using sweep::mbar_wait;
+using sweep::mbar_wait_sleep;
 using sweep::smem_u32;
 
 constexpr int NCW = 8;  // consumer warps
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(Cfg<TL, TS, REC>::NT, 1) sweep2_kernel(Args A)
         ItemDesc cur{};
         constexpr int NROW = 2 * NC * CS;  // noise rows per stage (<= 128)
         auto produce = [&](int item_hdr, int64_t c0, int m, int64_t off, int64_t toff, int rd, int t0, int nb) {
-            mbar_wait(&empty[stage], ((use >> stage) & 1u) ^ 1u);
+            mbar_wait_sleep(&empty[stage], ((use >> stage) & 1u) ^ 1u);
             if (ptid == 0) {
                 header[stage] = cur;
                 header[stage].it = item_hdr;
