@@ -321,7 +321,8 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
                 const double bt = beta_of(l);
 #pragma unroll
                 for (int j = 0; j < TS; ++j) {
-                    const double ul = ok ? uGu[j][l << CSL] : 0.0, ur = ok ? uGv[j][l << CSL] : 0.0;
+                    const bool ld = ok && !(A.ablate & 64);
+                    const double ul = ld ? uGu[j][l << CSL] : 0.0, ur = ld ? uGv[j][l << CSL] : 0.0;
                     Y[n][j] = bt * (m == 1 ? ul + ur : ul);
                     Z[n][j] = bt * (m == 1 ? ul + ur : ur);
                 }
@@ -369,30 +370,46 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
                     const double* rga = cga + tt * RN;
 #pragma unroll
                     for (int j = 0; j < TS; ++j) aL[j] = aR[j] = 0.0;
+                    // all chain updates first, then the accumulations (each uses a chain value computed
+                    // >= TL*TS*2 FMAs earlier: no back-to-back DFMA dependencies)
+                    double2 g2s[NP > 0 ? NP : 1];
 #pragma unroll
                     for (int q = 0; q < NP; ++q) {
                         const double2 m2 = *reinterpret_cast<const double2*>(rmu + 2 * lt + 64 * q);
-                        const double2 g2 = *reinterpret_cast<const double2*>(rga + 2 * lt + 64 * q);
+                        g2s[q] = *reinterpret_cast<const double2*>(rga + 2 * lt + 64 * q);
 #pragma unroll
                         for (int j = 0; j < TS; ++j) {
                             Y[2 * q][j] = fma(-m2.x, Y[2 * q][j], wl[j]);
-                            aL[j] = fma(g2.x, Y[2 * q][j], aL[j]);
                             Z[2 * q][j] = fma(-m2.x, Z[2 * q][j], wr[j]);
-                            aR[j] = fma(g2.x, Z[2 * q][j], aR[j]);
                             Y[2 * q + 1][j] = fma(-m2.y, Y[2 * q + 1][j], wl[j]);
-                            aL[j] = fma(g2.y, Y[2 * q + 1][j], aL[j]);
                             Z[2 * q + 1][j] = fma(-m2.y, Z[2 * q + 1][j], wr[j]);
-                            aR[j] = fma(g2.y, Z[2 * q + 1][j], aR[j]);
                         }
                     }
+                    double go = 0.0;
                     if (ODD) {
-                        const double mu = rmu[64 * NP + lt], gg = rga[64 * NP + lt];
+                        const double mu = rmu[64 * NP + lt];
+                        go = rga[64 * NP + lt];
 #pragma unroll
                         for (int j = 0; j < TS; ++j) {
                             Y[TL - 1][j] = fma(-mu, Y[TL - 1][j], wl[j]);
-                            aL[j] = fma(gg, Y[TL - 1][j], aL[j]);
                             Z[TL - 1][j] = fma(-mu, Z[TL - 1][j], wr[j]);
-                            aR[j] = fma(gg, Z[TL - 1][j], aR[j]);
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < NP; ++q) {
+#pragma unroll
+                        for (int j = 0; j < TS; ++j) {
+                            aL[j] = fma(g2s[q].x, Y[2 * q][j], aL[j]);
+                            aR[j] = fma(g2s[q].x, Z[2 * q][j], aR[j]);
+                            aL[j] = fma(g2s[q].y, Y[2 * q + 1][j], aL[j]);
+                            aR[j] = fma(g2s[q].y, Z[2 * q + 1][j], aR[j]);
+                        }
+                    }
+                    if (ODD) {
+#pragma unroll
+                        for (int j = 0; j < TS; ++j) {
+                            aL[j] = fma(go, Y[TL - 1][j], aL[j]);
+                            aR[j] = fma(go, Z[TL - 1][j], aR[j]);
                         }
                     }
                 };
@@ -451,8 +468,10 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
                     aR[1] += __shfl_xor_sync(0xffffffffu, aR[3], 1);
                     aL[0] += __shfl_xor_sync(0xffffffffu, aL[1], 2);
                     aR[0] += __shfl_xor_sync(0xffffffffu, aR[1], 2);
-                    pb[tt * NWL * 2 * CS] = aL[0];
-                    pb[tt * NWL * 2 * CS + CS] = aR[0];
+                    if (!(A.ablate & 32)) {
+                        pb[tt * NWL * 2 * CS] = aL[0];
+                        pb[tt * NWL * 2 * CS + CS] = aR[0];
+                    }
                 };
                 const bool last_here = (t0 + nb == m) && (m > 1);
                 if (last_here && nb > 1) {  // the last step re-reads both vertices' u_G: pull it into L1
