@@ -30,7 +30,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", INCLUDE
           "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 PER_FILE = {"noise.cu": ["--fmad=false"]}
 SOURCES = ["noise.cu", "edge_setup.cu", "sweep.cu", "sweep_c0.cu", "sweep_r0k.cu", "sweep_r1k.cu", "sweep_r2k.cu", "sweep2_c16.cu", "sweep2_c32.cu",
-           "sweep2_r16.cu", "sweep2_r32.cu", "sweep3_r32.cu", "pcg.cu", "pcg_warp.cu", "pcg_global.cu", "dist.cu", "refine.cu", "grf_api.cpp"]
+           "sweep2_r16.cu", "sweep2_r32.cu", "sweep3_r32.cu", "sweep3_c32.cu", "pcg.cu", "pcg_warp.cu", "pcg_global.cu", "dist.cu", "refine.cu", "grf_api.cpp"]
 HEADERS = ["grf_internal.h", "thomas.cuh", "sweep_impl.cuh", "sweep2_impl.cuh", "sweep3_impl.cuh"]
 
 

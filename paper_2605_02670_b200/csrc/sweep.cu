@@ -20,6 +20,7 @@ cudaError_t launch_r32(int tl, sweep::Args a, cudaStream_t st);
 }  // namespace sweep2
 namespace sweep3 {
 cudaError_t launch_r32(int tl, sweep::Args a, cudaStream_t st);
+cudaError_t launch_c32(int tl, sweep::Args a, cudaStream_t st);
 }  // namespace sweep3
 
 namespace {
@@ -75,7 +76,8 @@ cudaError_t launch_condense(const DevGraph& g, const DevPlan& p, int64_t n_sampl
                             int32_t* counter, cudaStream_t st) {
     const sweep::Args a = make_args(g, p, n_samples, W, ends, nullptr, counter);
     switch (sweep::variant_for(n_samples)) {
-        case sweep::V2: return sweep2::launch_c32(p.TL, a, st);
+        case sweep::V2:  // sweep3's condense is the default; sweep2's stays selectable (GRF_ABLATE bit 128)
+            return a.ablate & 128 ? sweep2::launch_c32(p.TL, a, st) : sweep3::launch_c32(p.TL, a, st);
         case sweep::V1: return sweep2::launch_c16(p.TL, a, st);
         default: return sweep::launch_c0(p.TL, a, st);
     }

@@ -41,8 +41,8 @@ constexpr int CS = SLW * TS;  // 32 samples per item
 constexpr int CSL = 5;
 constexpr int NT = (NCW + 4) * 32;
 constexpr int IBK = 8;       // steps per stage
-constexpr int NST = 3;       // data ring depth
-constexpr int NPS = 2;       // partial ring depth
+constexpr int NST = 3;       // data ring depth (max; A.nst in use, see launch)
+constexpr int NPS = 2;       // partial ring depth (max; A.nps in use: 1 when that lets the output tile fit)
 constexpr int NC = 2;        // noise copies: natural, pair-swapped
 constexpr int WROW = CS + 4; // skewed noise row
 constexpr int WEL = IBK * 2 * NC * WROW;
@@ -58,13 +58,11 @@ struct BlockDesc {
 template <int TL>
 struct Cfg {
     static constexpr int RN = 32 * TL;
-    static constexpr size_t COEF = (size_t)NST * 2 * IBK * RN * sizeof(double);
-    static constexpr size_t WB = (size_t)NST * WEL * sizeof(double);
-    static constexpr size_t PART = (size_t)NPS * PEL * sizeof(double);
-    static constexpr size_t FIXED = HDR + COEF + WB + PART;
+    static constexpr size_t STAGE1 = (size_t)(2 * IBK * RN + WEL) * sizeof(double);  // one data stage
+    static constexpr size_t PART1 = (size_t)PEL * sizeof(double);                     // one partial stage
 };
 
-template <int TL>
+template <int TL, int NSTT>
 __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
     using C = Cfg<TL>;
     constexpr int RN = C::RN;
@@ -82,10 +80,12 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
     uint64_t* pempty = pfull + NPS;                              // [NPS]
     ItemDesc* header = reinterpret_cast<ItemDesc*>(pempty + NPS);  // [NST]
     BlockDesc* phdr = reinterpret_cast<BlockDesc*>(header + NST);  // [NPS]
-    double* coef = reinterpret_cast<double*>(smem_raw + HDR);   // [NST][2][IBK][RN]
-    double* wbuf = coef + NST * 2 * IBK * RN;                    // [NST][IBK][2 side][NC][WROW]
-    double* part = wbuf + NST * WEL;                             // [NPS][IBK][NWL][2][CS]
-    double* cLs = part + NPS * PEL;                              // [Lp] c_L
+    constexpr int nst = NSTT;
+    const int nps = A.nps;
+    double* coef = reinterpret_cast<double*>(smem_raw + HDR);   // [nst][2][IBK][RN]
+    double* wbuf = coef + nst * 2 * IBK * RN;                    // [nst][IBK][2 side][NC][WROW]
+    double* part = wbuf + nst * WEL;                             // [nps][IBK][NWL][2][CS]
+    double* cLs = part + nps * PEL;                              // [Lp] c_L
     double* otile = cLs + Lp;                                    // [CS][tile_ms]
 
     if (tid == 0) {
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
                 }
                 cpasync_arrive_noinc(&full[stage]);
                 use ^= 1u << stage;
-                stage = stage + 1 == NST ? 0 : stage + 1;
+                stage = stage + 1 == nst ? 0 : stage + 1;
             };
             for (;;) {
                 int it = 0;
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
             fbar();
             if (lane == 0) mbar_arrive(&pempty[ps]);  // the partials are consumed (the tile is ours)
             puse ^= 1u << ps;
-            ps = ps + 1 == NPS ? 0 : ps + 1;
+            ps = ps + 1 == nps ? 0 : ps + 1;
             if (bd.last && in_tile) {  // the item's output tile -> u (coalesced), then reusable
                 for (int x = ftid; x < CS * m; x += NFW * 32) {
                     const int s = x / m, p = x - s * m;
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
         use ^= 1u << stage;
-        stage = stage + 1 == NST ? 0 : stage + 1;
+        stage = stage + 1 == nst ? 0 : stage + 1;
     };
     auto slot = [&](int n) -> int { return (n < 2 * NP) ? (2 * lt + 64 * (n >> 1) + (n & 1)) : (64 * NP + lt); };
 
@@ -536,46 +536,302 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&pfull[ps]);
                 puse ^= 1u << ps;
-                ps = ps + 1 == NPS ? 0 : ps + 1;
+                ps = ps + 1 == nps ? 0 : ps + 1;
                 release();
             }
         }
     }
 }
 
+// ------------------------------------------------------------------------------------------------
+// K3 condense (P197-239) with the same decomposition: the register tile and thread mapping of
+// sweep_impl.cuh's condense V2 instance (4 l-warps of 8 l-lanes x 4 s-lanes, 2 s-warps: the 8
+// l-lanes of a warp share each staged coefficient pair, so a coefficient load is one shared-memory
+// wavefront), chains only; the producer warpgroup streams the stages as in sweep2_impl.cuh (its
+// four warps split the noise rows); no fold, no barriers: every consumer thread writes its own end
+// values w_1 = g_0 Z, w_m = g_0 Y after a round's last block.
+namespace cond {
+constexpr int LWc = 8, SLWc = 4, NWLc = 4, NWSc = 2;
+constexpr int IBKc = 16, NSTc = 4;
+constexpr int WROWc = CS + 4;
+constexpr int WELc = IBKc * 2 * WROWc;  // [IBK][2 side][WROW]
+constexpr size_t HDRc = 512;
+}  // namespace cond
+
 template <int TL>
-cudaError_t launch(Args a, cudaStream_t st) {
-    using C = Cfg<TL>;
+__global__ void __launch_bounds__(NT, 1) sweep3c_kernel(Args A) {
+    using namespace cond;
+    constexpr int RN = 32 * TL;
+    constexpr int NP = TL / 2;
+    constexpr bool ODD = (TL & 1) != 0;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const DevGraph& g = A.g;
+    const int64_t N = g.N;
+    const int L = A.L, Lp = A.Lp;
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);         // [NSTc]
+    uint64_t* empty = full + NSTc;                                   // [NSTc]
+    ItemDesc* header = reinterpret_cast<ItemDesc*>(empty + NSTc);   // [NSTc]
+    double* coef = reinterpret_cast<double*>(smem_raw + HDRc);       // [NSTc][IBKc][RN] (mu)
+    double* wbuf = coef + NSTc * IBKc * RN;                          // [NSTc][IBKc][2][WROWc]
+
+    if (tid == 0) {
+        for (int s = 0; s < NSTc; ++s) {
+            mbar_init(&full[s], 129);  // the expect_tx arrive + the 128 producer threads' cp.async arrivals
+            mbar_init(&empty[s], NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp >= NCW) {  // ------------------------------------------------------------ producer warpgroup
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+        const int ptid = tid - NCW * 32;
+        volatile int* qbox = reinterpret_cast<volatile int*>(header + NSTc);
+        auto pbar = []() { asm volatile("bar.sync 1, 128;" ::: "memory"); };
+        int stage = 0;
+        uint32_t use = 0;
+        ItemDesc cur{};
+        auto produce = [&](int item_hdr, int64_t c0, int m, int64_t off, int64_t toff, int rd, int t0, int nb) {
+            sweep::mbar_wait_sleep(&empty[stage], ((use >> stage) & 1u) ^ 1u);
+            if (ptid == 0) {
+                header[stage] = cur;
+                header[stage].it = item_hdr;
+                fence_proxy_async();
+                mbar_expect_tx(&full[stage], (uint32_t)(nb * RN * sizeof(double)));
+            }
+            pbar();
+            if (nb > 0) {
+                double* cdst = coef + stage * IBKc * RN;
+                if (A.rounds == 1) {
+                    if (ptid == 0)
+                        bulk_g2s(cdst, A.mu + (toff + t0) * (int64_t)Lp, (uint32_t)(nb * RN * sizeof(double)),
+                                 &full[stage]);
+                } else {
+                    for (int tt = ptid; tt < nb; tt += 128)
+                        bulk_g2s(cdst + tt * RN, A.mu + (toff + t0 + tt) * (int64_t)Lp + rd * RN,
+                                 (uint32_t)(RN * sizeof(double)), &full[stage]);
+                }
+                if (ptid < 2 * CS) {  // noise row (side, sample) of this thread
+                    const int side = ptid & 1, s = ptid >> 1;
+                    int64_t sg = c0 + s;
+                    if (sg >= A.S) sg = A.S - 1;
+                    const double* src = A.W + sg * N + off + (side ? (m - 1 - t0) : t0);
+                    const int dstep = side ? -1 : 1;
+                    double* dst = wbuf + stage * WELc + side * WROWc + s;
+#pragma unroll 4
+                    for (int tt = 0; tt < nb; ++tt) cp_async8(dst + tt * 2 * WROWc, src + dstep * tt);
+                }
+            }
+            cpasync_arrive_noinc(&full[stage]);
+            use ^= 1u << stage;
+            stage = stage + 1 == NSTc ? 0 : stage + 1;
+        };
+        for (;;) {
+            if (ptid == 0) *qbox = atomicAdd(A.counter, 1);
+            pbar();
+            const int it = *qbox;
+            pbar();
+            if (it >= A.n_items) {
+                produce(-1, 0, 0, 0, 0, 0, 0, 0);
+                break;
+            }
+            const int e = g.edge_order[it / A.chunks];
+            const int m = g.m[e];
+            const int64_t c0 = (int64_t)(it % A.chunks) * CS;
+            const int64_t off = g.off[e], toff = g.toff[e];
+            cur.it = it;
+            cur.e = e;
+            cur.m = m;
+            cur.vu = g.eu[e];
+            cur.vv = g.ev[e];
+            cur.off = off;
+            cur.toff = toff;
+            cur.h = g.h[e];
+            if (m == 0) {  // one empty stage: the consumers write zero end values
+                produce(it, c0, m, off, toff, 0, 0, 0);
+                continue;
+            }
+            for (int rd = 0; rd < A.rounds; ++rd)
+                for (int t0 = 0; t0 < m; t0 += IBKc) produce(it, c0, m, off, toff, rd, t0, min(IBKc, m - t0));
+        }
+        return;
+    }
+
+    // ---------------------------------------------------------------------------------- consumers
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
+    const int ll = lane % LWc, sl = lane / LWc;
+    const int lw = warp % NWLc, sw = warp / NWLc;
+    const int lt = lw * LWc + ll;             // l-thread 0..31
+    const int st0 = (sw * SLWc + sl) * TS;   // first sample (within the item) of this thread
+    int stage = 0;
+    uint32_t use = 0;
+    auto acquire = [&]() { mbar_wait(&full[stage], (use >> stage) & 1u); };
+    auto release = [&]() {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        use ^= 1u << stage;
+        stage = stage + 1 == NSTc ? 0 : stage + 1;
+    };
+    auto slot = [&](int n) -> int { return (n < 2 * NP) ? (2 * lt + 64 * (n >> 1) + (n & 1)) : (64 * NP + lt); };
+    for (;;) {
+        acquire();
+        const ItemDesc d = header[stage];
+        const int it = d.it;
+        if (it < 0) break;
+        const int e = d.e;
+        const int64_t tile = it % A.chunks;
+        const int m = d.m;
+        const int64_t toff = d.toff;
+        if (m == 0) {  // no interior: zero end values (ends [tile][l][code][CS])
+#pragma unroll
+            for (int n = 0; n < TL; ++n) {
+                const int l = slot(n);
+                for (int rb = 0; rb < A.rounds * RN; rb += RN) {
+                    if (rb + l < L) {
+                        double* o = A.out + ((tile * L + rb + l) * 2 * (int64_t)g.E + 2 * e) * CS + st0;
+                        *reinterpret_cast<double2*>(o) = make_double2(0.0, 0.0);
+                        *reinterpret_cast<double2*>(o + 2) = make_double2(0.0, 0.0);
+                        *reinterpret_cast<double2*>(o + CS) = make_double2(0.0, 0.0);
+                        *reinterpret_cast<double2*>(o + CS + 2) = make_double2(0.0, 0.0);
+                    }
+                }
+            }
+            release();
+            continue;
+        }
+        const int nblk = (m + IBKc - 1) / IBKc;
+        for (int rd = 0; rd < A.rounds; ++rd) {
+            const int rb = rd * RN;
+            if (rd > 0) acquire();
+            double Y[TL][TS], Z[TL][TS], g0[TL];
+#pragma unroll
+            for (int n = 0; n < TL; ++n) {
+                const int l = rb + slot(n);
+                // g_0 = g_{m-1} for the end values, loaded now (volatile: not sunk to the round's end)
+                double gv = 0.0;
+                if (l < L) asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(gv) : "l"(A.gam + toff * (int64_t)Lp + l));
+                g0[n] = gv;
+#pragma unroll
+                for (int j = 0; j < TS; ++j) Y[n][j] = Z[n][j] = 0.0;
+            }
+            for (int b = 0; b < nblk; ++b) {
+                if (b > 0) acquire();
+                const int nb = min(IBKc, m - b * IBKc);
+                const double* cmu = coef + stage * IBKc * RN;
+                const double* wb = wbuf + stage * WELc;
+                auto step = [&](int tt) {
+                    const double2 wl01 = *reinterpret_cast<const double2*>(wb + (tt * 2 + 0) * WROWc + st0);
+                    const double2 wl23 = *reinterpret_cast<const double2*>(wb + (tt * 2 + 0) * WROWc + st0 + 2);
+                    const double2 wr01 = *reinterpret_cast<const double2*>(wb + (tt * 2 + 1) * WROWc + st0);
+                    const double2 wr23 = *reinterpret_cast<const double2*>(wb + (tt * 2 + 1) * WROWc + st0 + 2);
+                    const double wl[TS] = {wl01.x, wl01.y, wl23.x, wl23.y};
+                    const double wr[TS] = {wr01.x, wr01.y, wr23.x, wr23.y};
+                    const double* rmu = cmu + tt * RN;
+#pragma unroll
+                    for (int q = 0; q < NP; ++q) {
+                        const double2 m2 = *reinterpret_cast<const double2*>(rmu + 2 * lt + 64 * q);
+#pragma unroll
+                        for (int j = 0; j < TS; ++j) {
+                            Y[2 * q][j] = fma(-m2.x, Y[2 * q][j], wl[j]);
+                            Z[2 * q][j] = fma(-m2.x, Z[2 * q][j], wr[j]);
+                            Y[2 * q + 1][j] = fma(-m2.y, Y[2 * q + 1][j], wl[j]);
+                            Z[2 * q + 1][j] = fma(-m2.y, Z[2 * q + 1][j], wr[j]);
+                        }
+                    }
+                    if (ODD) {
+                        const double mu = rmu[64 * NP + lt];
+#pragma unroll
+                        for (int j = 0; j < TS; ++j) {
+                            Y[TL - 1][j] = fma(-mu, Y[TL - 1][j], wl[j]);
+                            Z[TL - 1][j] = fma(-mu, Z[TL - 1][j], wr[j]);
+                        }
+                    }
+                };
+                if (nb == IBKc) {
+#pragma unroll
+                    for (int tt = 0; tt < IBKc; ++tt) step(tt);
+                } else {
+                    for (int tt = 0; tt < nb; ++tt) step(tt);
+                }
+                release();
+            }
+            // w_1 = g_0 Z (right sweep end, position 0), w_m = g_0 Y (left sweep end); g_0 = g_{m-1}
+#pragma unroll
+            for (int n = 0; n < TL; ++n) {
+                const int l = rb + slot(n);
+                if (l < L) {
+                    double* o = A.out + ((tile * L + l) * 2 * (int64_t)g.E + 2 * e) * CS + st0;
+                    *reinterpret_cast<double2*>(o) = make_double2(g0[n] * Z[n][0], g0[n] * Z[n][1]);
+                    *reinterpret_cast<double2*>(o + 2) = make_double2(g0[n] * Z[n][2], g0[n] * Z[n][3]);
+                    *reinterpret_cast<double2*>(o + CS) = make_double2(g0[n] * Y[n][0], g0[n] * Y[n][1]);
+                    *reinterpret_cast<double2*>(o + CS + 2) = make_double2(g0[n] * Y[n][2], g0[n] * Y[n][3]);
+                }
+            }
+        }
+    }
+}
+
+template <int TL>
+cudaError_t launch_c(Args a, cudaStream_t st) {
+    using namespace cond;
     a.chunks = (int32_t)((a.S + CS - 1) / CS);
     a.n_items = a.g.E * a.chunks;
-    size_t smem = C::FIXED + (size_t)a.Lp * sizeof(double);
-    // the output tile holds edges with (m | 1) <= tile_ms; sized for the longest edge if it fits
-    const int want = a.g.max_m | 1;
-    const size_t room = sweep::SMEM_MAX > smem ? sweep::SMEM_MAX - smem : 0;
-    const int fit = (int)(room / ((size_t)CS * sizeof(double)));
-    a.tile_ms = want <= fit ? want : (fit >= 1 ? ((fit - 1) | 1) : 0);
-    smem += (size_t)CS * a.tile_ms * sizeof(double);
-    cudaError_t e = cudaFuncSetAttribute(sweep3_kernel<TL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = HDRc + (size_t)NSTc * IBKc * 32 * TL * sizeof(double) + (size_t)NSTc * WELc * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(sweep3c_kernel<TL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(a.counter, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return e;
     int blocks = a.g.n_sm > 0 ? a.g.n_sm : 148;
     if (blocks > a.n_items) blocks = a.n_items;
-    sweep3_kernel<TL><<<blocks, NT, smem, st>>>(a);
+    sweep3c_kernel<TL><<<blocks, NT, smem, st>>>(a);
     return cudaGetLastError();
 }
 
-inline cudaError_t launch_tl(int tl, Args a, cudaStream_t st) {
-    switch (tl) {
-        case 1: return launch<1>(a, st);
-        case 2: return launch<2>(a, st);
-        case 3: return launch<3>(a, st);
-        case 4: return launch<4>(a, st);
-        case 5: return launch<5>(a, st);
-        case 6: return launch<6>(a, st);
-        case 7: return launch<7>(a, st);
-        default: return cudaErrorInvalidValue;
+
+template <int TL>
+cudaError_t launch(Args a, cudaStream_t st) {
+    using C = Cfg<TL>;
+    a.chunks = (int32_t)((a.S + CS - 1) / CS);
+    a.n_items = a.g.E * a.chunks;
+    // the output tile holds edges with (m | 1) <= tile_ms, sized for the longest edge if it fits; the
+    // ring depths (data nst, partials nps) give way to it: edges past the tile are folded into u in
+    // global memory, a read-modify-write per visit, far slower than a shallower ring.  Preference:
+    // (3, 2), (2, 2), (3, 1), (2, 1).
+    const int want = a.g.max_m | 1;
+    auto base_for = [&](int nst, int nps) {
+        return HDR + nst * C::STAGE1 + nps * C::PART1 + (size_t)a.Lp * sizeof(double);
+    };
+    auto fit_for = [&](int nst, int nps) {
+        const size_t b = base_for(nst, nps);
+        const size_t room = sweep::SMEM_MAX > b ? sweep::SMEM_MAX - b : 0;
+        return (int)(room / ((size_t)CS * sizeof(double)));
+    };
+    static const int depth[4][2] = {{NST, NPS}, {2, NPS}, {NST, 1}, {2, 1}};
+    a.nst = NST;
+    a.nps = NPS;
+    for (const auto& d : depth) {
+        if (fit_for(d[0], d[1]) >= want) {
+            a.nst = d[0];
+            a.nps = d[1];
+            break;
+        }
     }
+    size_t smem = base_for(a.nst, a.nps);
+    const int fit = fit_for(a.nst, a.nps);
+    a.tile_ms = want <= fit ? want : (fit >= 1 ? ((fit - 1) | 1) : 0);
+    smem += (size_t)CS * a.tile_ms * sizeof(double);
+    // the ring depth is a template constant (the stage offsets fold into the addressing)
+    auto kern = a.nst == NST ? sweep3_kernel<TL, NST> : sweep3_kernel<TL, 2>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(a.counter, 0, sizeof(int32_t), st);
+    if (e != cudaSuccess) return e;
+    int blocks = a.g.n_sm > 0 ? a.g.n_sm : 148;
+    if (blocks > a.n_items) blocks = a.n_items;
+    kern<<<blocks, NT, smem, st>>>(a);
+    return cudaGetLastError();
 }
 
 }  // namespace sweep3

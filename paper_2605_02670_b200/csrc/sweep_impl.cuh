@@ -71,9 +71,10 @@ struct Args {
     int32_t n_items;        // E * chunks
     int32_t tile_ms;        // recover: max (m | 1) the shared-memory output tile holds (0: none)
     int32_t nk;             // recover: 1 if slot L is the correction node (edge_setup.cu; L < Lp)
+    int32_t nst, nps;       // sweep3 recover: data / partial ring depths in use (set by its launch)
     int32_t ablate;         // design studies only (env GRF_ABLATE, default 0), wrong results by construction:
                             // sweep2 bits 1 no output reduction, 2 no u_G loads, 4 no data waits; sweep3
-                            // bits 32 no partial stores, 64 no u_G loads; kernel choice bits 8, 16 (sweep.cu)
+                            // bits 32 no partial stores, 64 no u_G loads; kernel choice bits 8, 16, 128 (sweep.cu)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
