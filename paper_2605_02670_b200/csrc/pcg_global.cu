@@ -51,6 +51,7 @@ struct GArgs {
     int32_t* its;                           // [L][CS]
     int32_t* node_active;                   // [L]
     int32_t* n_active;                      // [1]
+    int32_t* fin;                           // [L] iteration at which the node converged (-1: none)
     double* part;                           // [L][nvb][2][CS]
     int32_t* cnt;                           // [L] arrival counters (zero between phases)
     int32_t group;                          // nodes solved together (their work vectors stay L2-resident)
@@ -58,37 +59,82 @@ struct GArgs {
 };
 
 
-// Threads: one per (vertex, sample) -- thread t of a CTA owns sample s = t % CS of vertex
-// sub-row t / CS; an item = (node l, block of VPI vertices) walked in sub-chunks of GT / CS
-// vertices, so a thread keeps only scalars (small register footprint, many resident warps
-// for the latency of the neighbour gathers), and the CS threads of a vertex read one
-// contiguous CS-double run of each vector and share the vertex's operator coefficients.
+// Threads: SP samples of one vertex each (SP = 2 for sample tiles of 16 or 32: double2
+// accesses) -- thread t of a CTA owns samples s = SP * (t % TPV) .. + SP - 1 of vertex sub-row
+// t / TPV (TPV = CS / SP threads per vertex); an item = (node l, block of VPI vertices) walked in
+// sub-chunks of GT / TPV vertices, so a thread keeps only a few values (small register footprint,
+// many resident warps for the latency of the neighbour gathers), and the TPV threads of a vertex
+// read one contiguous CS-double run of each vector and share the vertex's operator coefficients.
 constexpr int VPI_MAX = 256;  // vertices per item (at most): per-node partials have ceil(V / vpi) rows
 
-// Reduce K per-thread values over the CTA's vertices into part[l][vb][k][s]; the last CTA of
-// node l to arrive reduces the node's rows (columns in parallel, each in fixed order) and runs
-// finish(l, totals) with totals[k * CS + s] in shared memory (all threads of that CTA).
-template <int CS, int K, class Finish>
-__device__ void block_partials(const GArgs& A, int l, int vb, int nvb, const double (&v)[K], double* red,
-                               Finish&& finish) {
+template <int CS>
+struct Lanes {
+    static constexpr int SP = CS >= 2 ? 2 : 1;  // samples per thread
+    static constexpr int TPV = CS / SP;         // threads per vertex
+    static constexpr int VBK = GT / TPV;        // vertices per sub-chunk
+};
+
+template <int SP>
+struct Vec {
+    double v[SP];
+};
+template <int SP>
+__device__ __forceinline__ Vec<SP> ldv(const double* p) {
+    Vec<SP> r;
+    if constexpr (SP == 2) {
+        const double2 t = *reinterpret_cast<const double2*>(p);
+        r.v[0] = t.x;
+        r.v[1] = t.y;
+    } else {
+        r.v[0] = *p;
+    }
+    return r;
+}
+template <int SP>
+__device__ __forceinline__ void stv(double* p, const Vec<SP>& a) {  // streaming store: keep L2 for the gathers
+    if constexpr (SP == 2) {
+        __stcs(reinterpret_cast<double2*>(p), make_double2(a.v[0], a.v[1]));
+    } else {
+        __stcs(p, a.v[0]);
+    }
+}
+
+// Sum K x SP per-thread values over the CTA's vertices into red as [warp][k][s] rows summed over
+// warps: tot(k, s) for this CTA, written to part[l][vb][k][s] by threads tid < K * CS.
+template <int CS, int K>
+__device__ __forceinline__ void cta_partials(const double (&v)[K][Lanes<CS>::SP], double* red, double* dst) {
+    using LN = Lanes<CS>;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    __shared__ int last;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        double t = v[k];
 #pragma unroll
-        for (int o = 16; o >= CS && o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);  // over vertex lanes
-        if (lane < (CS < 32 ? CS : 32)) red[(warp * K + k) * CS + lane % CS] = t;
+        for (int j = 0; j < LN::SP; ++j) {
+            double t = v[k][j];
+#pragma unroll
+            for (int o = 16; o >= LN::TPV && o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);  // over vertex lanes
+            if (lane < (LN::TPV < 32 ? LN::TPV : 32)) red[(warp * K + k) * CS + (lane % LN::TPV) * LN::SP + j] = t;
+        }
     }
     __syncthreads();
-    double* pb = A.part + ((int64_t)l * nvb + vb) * 2 * CS;
     if (tid < K * CS) {
         const int k = tid / CS, s = tid % CS;
         double t = 0.0;
         for (int w = 0; w < GT / 32; ++w) t += red[(w * K + k) * CS + s];
-        pb[tid] = t;
-        __threadfence();
+        dst[tid] = t;
     }
+}
+
+// Reduce the per-thread values into part[l][vb][k][s]; the last CTA of node l to arrive reduces the
+// node's rows (columns in parallel, each in fixed order) and runs finish(l, totals) with
+// totals[k * CS + s] in shared memory (all threads of that CTA).
+template <int CS, int K, class Finish>
+__device__ void block_partials(const GArgs& A, int l, int vb, int nvb, const double (&v)[K][Lanes<CS>::SP],
+                               double* red, Finish&& finish) {
+    const int tid = threadIdx.x;
+    __shared__ int last;
+    double* pb = A.part + ((int64_t)l * nvb + vb) * 2 * CS;
+    cta_partials<CS, K>(v, red, pb);
+    if (tid < K * CS) __threadfence();
     __syncthreads();
     if (tid == 0) last = (atomicAdd(&A.cnt[l], 1) == nvb - 1);
     __syncthreads();
@@ -122,22 +168,9 @@ __device__ void block_partials(const GArgs& A, int l, int vb, int nvb, const dou
 // barrier one CTA per active node reduces the node's rows in the same fixed order as the
 // last-arriving CTA of block_partials does and runs finish(l, totals).
 template <int CS, int K>
-__device__ void item_partials(const GArgs& A, int l, int vb, int nvb, const double (&v)[K], double* red) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        double t = v[k];
-#pragma unroll
-        for (int o = 16; o >= CS && o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);  // over vertex lanes
-        if (lane < (CS < 32 ? CS : 32)) red[(warp * K + k) * CS + lane % CS] = t;
-    }
-    __syncthreads();
-    if (tid < K * CS) {
-        const int k = tid / CS, s = tid % CS;
-        double t = 0.0;
-        for (int w = 0; w < GT / 32; ++w) t += red[(w * K + k) * CS + s];
-        A.part[((int64_t)l * nvb + vb) * 2 * CS + tid] = t;
-    }
+__device__ void item_partials(const GArgs& A, int l, int vb, int nvb, const double (&v)[K][Lanes<CS>::SP],
+                              double* red) {
+    cta_partials<CS, K>(v, red, A.part + ((int64_t)l * nvb + vb) * 2 * CS);
     __syncthreads();  // red is reused by the next item
 }
 
@@ -164,10 +197,15 @@ __device__ void node_reduce(const GArgs& A, int l, int nvb, double* red, Finish&
     __syncthreads();
 }
 
+// p_k of iteration k lives in p1 for even k, p0 for odd k (po / pn swap after every iteration)
+__device__ __forceinline__ bool p_in_p1(int k) { return (k & 1) == 0; }
+
 template <int CS>
 __global__ void __launch_bounds__(GT, 4) pcg_global_kernel(GArgs A) {
+    using LN = Lanes<CS>;
+    constexpr int SP = LN::SP, VBK = LN::VBK;
+    using VS = Vec<SP>;
     cg::grid_group grid = cg::this_grid();
-    constexpr int VBK = GT / CS;  // vertices per sub-chunk
     constexpr int RED = (GT + 2 * CS) > ((GT / 32) * 2 * CS) ? (GT + 2 * CS) : ((GT / 32) * 2 * CS);
     __shared__ double red[RED];
     const DevGraph& g = A.g;
@@ -175,14 +213,20 @@ __global__ void __launch_bounds__(GT, 4) pcg_global_kernel(GArgs A) {
     const int64_t E2 = 2 * (int64_t)g.E;
     const int VPI = A.vpi;
     const int nvb = (V + VPI - 1) / VPI;
-    const int tid = threadIdx.x, s = tid % CS, vl = tid / CS;
+    const int tid = threadIdx.x, s = (tid % LN::TPV) * SP, vl = tid / LN::TPV;
     const int64_t stride = 3 * (int64_t)V + 2 * E2;  // position table per node
     const int64_t s0 = A.tile << A.csl;
     double *po, *pn, *ro, *rn;
     const double tol2c = A.prm.rtol * A.prm.rtol;
 
-    // the vertex of sub-chunk c of item vb for this thread (or V: none)
+    // the vertex of sub-chunk c of item vb for this thread (or -1: none)
     auto vert = [&](int vb, int c) { const int v = vb * VPI + c * VBK + vl; return v < V ? v : -1; };
+    auto vzero = [] {
+        VS r;
+#pragma unroll
+        for (int j = 0; j < SP; ++j) r.v[j] = 0.0;
+        return r;
+    };
 
     // Node groups are solved one after the other (the launcher currently uses one group of all
     // nodes: per-group barriers outweighed the L2 residency they buy on config 4).
@@ -198,25 +242,21 @@ __global__ void __launch_bounds__(GT, 4) pcg_global_kernel(GArgs A) {
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
         const int l = l0 + (int)(it / nvb), vb = (int)(it % nvb);
         const int64_t lb = (int64_t)l * V * CS;  // node l's [V][CS] slab
-        double* const ro_l = ro + lb;
-        double* const po_l = po + lb;
-        double* const pn_l = pn + lb;
-        double* const rn_l = rn + lb;
-        double* const x_l = A.x + lb;
-        double* const z_l = A.z + lb;
-        double* const q_l = A.q + lb;
-        (void)ro_l; (void)po_l; (void)pn_l; (void)rn_l; (void)x_l; (void)z_l; (void)q_l;
-        double acc[1] = {0.0};
+        double acc[1][SP] = {};
         for (int c = 0; c < VPI / VBK; ++c) {
             const int v = vert(vb, c);
             if (v < 0) continue;
             const int e = v * CS + s;  // offset within node l's [V][CS] slab (32-bit)
-            const int64_t sg = s0 + s;
-            const double gv = sg < A.S ? A.rhs[rhs_index(sg, l, g.vorder[v], L, V, A.csl)] : 0.0;
-            ro_l[e] = gv;
-            x_l[e] = 0.0;
-            po_l[e] = 0.0;
-            acc[0] = fma(gv, gv, acc[0]);
+            VS gv;
+#pragma unroll
+            for (int j = 0; j < SP; ++j) {
+                const int64_t sg = s0 + s + j;
+                gv.v[j] = sg < A.S ? A.rhs[rhs_index(sg, l, g.vorder[v], L, V, A.csl)] : 0.0;
+                acc[0][j] = fma(gv.v[j], gv.v[j], acc[0][j]);
+            }
+            stv(ro + lb + e, gv);
+            stv(A.x + lb + e, vzero());
+            stv(po + lb + e, vzero());
         }
         block_partials<CS, 1>(A, l, vb, nvb, acc, red, [&](int ln, const double* tot) {
             if (tid < CS) {
@@ -226,7 +266,9 @@ __global__ void __launch_bounds__(GT, 4) pcg_global_kernel(GArgs A) {
                 A.done[ln * CS + tid] = !(t > 0.0) || (s0 + tid >= A.S);
                 A.its[ln * CS + tid] = 0;
                 A.beta[ln * CS + tid] = 0.0;
+                A.alpha[ln * CS + tid] = 0.0;  // phase 1 of iteration 0 adds alpha p_{-1} = 0 to x
             }
+            if (tid == 0) A.fin[ln] = -1;
         });
     }
     grid.sync();
@@ -234,31 +276,33 @@ __global__ void __launch_bounds__(GT, 4) pcg_global_kernel(GArgs A) {
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
         const int l = l0 + (int)(it / nvb), vb = (int)(it % nvb);
         const int64_t lb = (int64_t)l * V * CS;  // node l's [V][CS] slab
-        double* const ro_l = ro + lb;
-        double* const po_l = po + lb;
-        double* const pn_l = pn + lb;
-        double* const rn_l = rn + lb;
-        double* const x_l = A.x + lb;
-        double* const z_l = A.z + lb;
-        double* const q_l = A.q + lb;
-        (void)ro_l; (void)po_l; (void)pn_l; (void)rn_l; (void)x_l; (void)z_l; (void)q_l;
+        const double* const ro_l = ro + lb;
         const double* tab = A.ops + l * stride;
-        double acc[1] = {0.0};
+        double acc[1][SP] = {};
         for (int c = 0; c < VPI / VBK; ++c) {
             const int v = vert(vb, c);
             if (v < 0) continue;
             const int e = v * CS + s;  // offset within node l's [V][CS] slab (32-bit)
-            const double rv = ro_l[e];
-            double zv;
+            const VS rv = ldv<SP>(ro_l + e);
+            VS zv;
             if (A.prm.precond == 0) {
-                zv = tab[V + v] * rv;
-                for (int k = g.gp_ptr[v]; k < g.gp_ptr[v + 1]; ++k)
-                    zv = fma(tab[3 * (int64_t)V + E2 + k], ro_l[g.gp_other[k] * CS + s], zv);
+                const double d = tab[V + v];
+#pragma unroll
+                for (int j = 0; j < SP; ++j) zv.v[j] = d * rv.v[j];
+                for (int k = g.gp_ptr[v]; k < g.gp_ptr[v + 1]; ++k) {
+                    const double cf = tab[3 * (int64_t)V + E2 + k];
+                    const VS ro_o = ldv<SP>(ro_l + g.gp_other[k] * CS + s);
+#pragma unroll
+                    for (int j = 0; j < SP; ++j) zv.v[j] = fma(cf, ro_o.v[j], zv.v[j]);
+                }
             } else {
-                zv = (A.prm.precond == 1 ? tab[2 * V + v] : 1.0) * rv;
+                const double d = A.prm.precond == 1 ? tab[2 * V + v] : 1.0;
+#pragma unroll
+                for (int j = 0; j < SP; ++j) zv.v[j] = d * rv.v[j];
             }
-            z_l[e] = zv;
-            acc[0] = fma(rv, zv, acc[0]);
+            stv(A.z + lb + e, zv);
+#pragma unroll
+            for (int j = 0; j < SP; ++j) acc[0][j] = fma(rv.v[j], zv.v[j], acc[0][j]);
         }
         block_partials<CS, 1>(A, l, vb, nvb, acc, red, [&](int ln, const double* tot) {
             if (tid < CS) A.rz[ln * CS + tid] = tot[tid];
@@ -272,36 +316,45 @@ __global__ void __launch_bounds__(GT, 4) pcg_global_kernel(GArgs A) {
     }
     grid.sync();
 
+    int iters_run = 0;
     for (int iter = 0; iter < A.prm.max_iter; ++iter) {
         if (*(volatile int32_t*)A.n_active == 0) break;
-        // ---- phase 1: p' = z + beta p, q = S p', p'.q -> alpha
+        iters_run = iter + 1;
+        // ---- phase 1: x += alpha_{k-1} p_{k-1};  p' = z + beta p, q = S p', p'.q -> alpha
         for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
             const int l = l0 + (int)(it / nvb), vb = (int)(it % nvb);
-            const int64_t lb = (int64_t)l * V * CS;  // node l's [V][CS] slab
-            double* const ro_l = ro + lb;
-            double* const po_l = po + lb;
-            double* const pn_l = pn + lb;
-            double* const rn_l = rn + lb;
-            double* const x_l = A.x + lb;
-            double* const z_l = A.z + lb;
-            double* const q_l = A.q + lb;
-            (void)ro_l; (void)po_l; (void)pn_l; (void)rn_l; (void)x_l; (void)z_l; (void)q_l;
             if (!A.node_active[l]) continue;  // block-uniform
+            const int64_t lb = (int64_t)l * V * CS;  // node l's [V][CS] slab
+            const double* const po_l = po + lb;
+            const double* const z_l = A.z + lb;
             const double* tab = A.ops + l * stride;
-            const double bt = A.beta[l * CS + s];
-            double acc[1] = {0.0};
+            double bt[SP], alo[SP];
+#pragma unroll
+            for (int j = 0; j < SP; ++j) {
+                bt[j] = A.beta[l * CS + s + j];
+                alo[j] = A.alpha[l * CS + s + j];
+            }
+            double acc[1][SP] = {};
             for (int c = 0; c < VPI / VBK; ++c) {
                 const int v = vert(vb, c);
                 if (v < 0) continue;
                 const int e = v * CS + s;  // offset within node l's [V][CS] slab (32-bit)
-                const double pv = fma(bt, po_l[e], z_l[e]);
-                double qv = tab[v] * pv;
+                const VS p_old = ldv<SP>(po_l + e), z_own = ldv<SP>(z_l + e), x_old = ldv<SP>(A.x + lb + e);
+                const double dS = tab[v];
+                VS pv, qv, xv;
+#pragma unroll
+                for (int j = 0; j < SP; ++j) {
+                    pv.v[j] = fma(bt[j], p_old.v[j], z_own.v[j]);
+                    qv.v[j] = dS * pv.v[j];
+                    xv.v[j] = fma(alo[j], p_old.v[j], x_old.v[j]);
+                }
                 // neighbours in chunks of NB: indices and coefficients first, then every vector load,
                 // then the FMAs (many loads in flight per thread; padding slots read the own row)
                 const int kb = g.gp_ptr[v], ke = g.gp_ptr[v + 1];
                 for (int k0 = kb; k0 < ke; k0 += NB) {
                     int ob[NB];
-                    double cf[NB], a[NB], b[NB];
+                    double cf[NB];
+                    VS a[NB], b[NB];
 #pragma unroll
                     for (int j = 0; j < NB; ++j) {
                         const bool ok = k0 + j < ke;
@@ -310,15 +363,20 @@ __global__ void __launch_bounds__(GT, 4) pcg_global_kernel(GArgs A) {
                     }
 #pragma unroll
                     for (int j = 0; j < NB; ++j) {
-                        a[j] = po_l[ob[j]];
-                        b[j] = z_l[ob[j]];
+                        a[j] = ldv<SP>(po_l + ob[j]);
+                        b[j] = ldv<SP>(z_l + ob[j]);
                     }
 #pragma unroll
-                    for (int j = 0; j < NB; ++j) qv = fma(cf[j], fma(bt, a[j], b[j]), qv);
+                    for (int j = 0; j < NB; ++j) {
+#pragma unroll
+                        for (int i = 0; i < SP; ++i) qv.v[i] = fma(cf[j], fma(bt[i], a[j].v[i], b[j].v[i]), qv.v[i]);
+                    }
                 }
-                __stcs(pn_l + e, pv);  // streaming stores: keep L2 for the neighbour gathers
-                __stcs(q_l + e, qv);
-                acc[0] = fma(pv, qv, acc[0]);
+                stv(pn + lb + e, pv);
+                stv(A.q + lb + e, qv);
+                stv(A.x + lb + e, xv);
+#pragma unroll
+                for (int j = 0; j < SP; ++j) acc[0][j] = fma(pv.v[j], qv.v[j], acc[0][j]);
             }
             item_partials<CS, 1>(A, l, vb, nvb, acc, red);
         }
@@ -334,35 +392,36 @@ __global__ void __launch_bounds__(GT, 4) pcg_global_kernel(GArgs A) {
             });
         }
         grid.sync();
-        // ---- phase 2: r' = r - alpha q, x += alpha p', z = M^{-1} r', r'.r', r'.z -> beta, convergence
+        // ---- phase 2: r' = r - alpha q, z = M^{-1} r', r'.r', r'.z -> beta, convergence
+        //      (x takes alpha p' in the next phase 1, or in the write-out)
         for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
             const int l = l0 + (int)(it / nvb), vb = (int)(it % nvb);
-            const int64_t lb = (int64_t)l * V * CS;  // node l's [V][CS] slab
-            double* const ro_l = ro + lb;
-            double* const po_l = po + lb;
-            double* const pn_l = pn + lb;
-            double* const rn_l = rn + lb;
-            double* const x_l = A.x + lb;
-            double* const z_l = A.z + lb;
-            double* const q_l = A.q + lb;
-            (void)ro_l; (void)po_l; (void)pn_l; (void)rn_l; (void)x_l; (void)z_l; (void)q_l;
             if (!A.node_active[l]) continue;
+            const int64_t lb = (int64_t)l * V * CS;  // node l's [V][CS] slab
+            const double* const ro_l = ro + lb;
+            const double* const q_l = A.q + lb;
             const double* tab = A.ops + l * stride;
-            const double al = A.alpha[l * CS + s];
-            double acc[2] = {0.0, 0.0};
+            double al[SP];
+#pragma unroll
+            for (int j = 0; j < SP; ++j) al[j] = A.alpha[l * CS + s + j];
+            double acc[2][SP] = {};
             for (int c = 0; c < VPI / VBK; ++c) {
                 const int v = vert(vb, c);
                 if (v < 0) continue;
                 const int e = v * CS + s;  // offset within node l's [V][CS] slab (32-bit)
-                const double rv = fma(-al, q_l[e], ro_l[e]);
-                __stcs(x_l + e, fma(al, pn_l[e], x_l[e]));
-                double zv;
+                const VS q_own = ldv<SP>(q_l + e), r_own = ldv<SP>(ro_l + e);
+                VS rv, zv;
+#pragma unroll
+                for (int j = 0; j < SP; ++j) rv.v[j] = fma(-al[j], q_own.v[j], r_own.v[j]);
                 if (A.prm.precond == 0) {
-                    zv = tab[V + v] * rv;
+                    const double d = tab[V + v];
+#pragma unroll
+                    for (int j = 0; j < SP; ++j) zv.v[j] = d * rv.v[j];
                     const int kb = g.gp_ptr[v], ke = g.gp_ptr[v + 1];
                     for (int k0 = kb; k0 < ke; k0 += NB) {
                         int ob[NB];
-                        double cf[NB], a[NB], b[NB];
+                        double cf[NB];
+                        VS a[NB], b[NB];
 #pragma unroll
                         for (int j = 0; j < NB; ++j) {
                             const bool ok = k0 + j < ke;
@@ -371,19 +430,27 @@ __global__ void __launch_bounds__(GT, 4) pcg_global_kernel(GArgs A) {
                         }
 #pragma unroll
                         for (int j = 0; j < NB; ++j) {
-                            a[j] = q_l[ob[j]];
-                            b[j] = ro_l[ob[j]];
+                            a[j] = ldv<SP>(q_l + ob[j]);
+                            b[j] = ldv<SP>(ro_l + ob[j]);
                         }
 #pragma unroll
-                        for (int j = 0; j < NB; ++j) zv = fma(cf[j], fma(-al, a[j], b[j]), zv);
+                        for (int j = 0; j < NB; ++j) {
+#pragma unroll
+                            for (int i = 0; i < SP; ++i) zv.v[i] = fma(cf[j], fma(-al[i], a[j].v[i], b[j].v[i]), zv.v[i]);
+                        }
                     }
                 } else {
-                    zv = (A.prm.precond == 1 ? tab[2 * V + v] : 1.0) * rv;
+                    const double d = A.prm.precond == 1 ? tab[2 * V + v] : 1.0;
+#pragma unroll
+                    for (int j = 0; j < SP; ++j) zv.v[j] = d * rv.v[j];
                 }
-                __stcs(rn_l + e, rv);
-                __stcs(z_l + e, zv);
-                acc[0] = fma(rv, rv, acc[0]);
-                acc[1] = fma(rv, zv, acc[1]);
+                stv(rn + lb + e, rv);
+                stv(A.z + lb + e, zv);
+#pragma unroll
+                for (int j = 0; j < SP; ++j) {
+                    acc[0][j] = fma(rv.v[j], rv.v[j], acc[0][j]);
+                    acc[1][j] = fma(rv.v[j], zv.v[j], acc[1][j]);
+                }
             }
             item_partials<CS, 2>(A, l, vb, nvb, acc, red);
         }
@@ -410,6 +477,7 @@ __global__ void __launch_bounds__(GT, 4) pcg_global_kernel(GArgs A) {
                     for (int q = 0; q < CS; ++q) act |= !A.done[ln * CS + q];
                     if (!act) {
                         A.node_active[ln] = 0;
+                        A.fin[ln] = iter;  // p' of this iteration: its last alpha p' goes to x at the write-out
                         atomicSub(A.n_active, 1);
                     }
                 }
@@ -423,14 +491,26 @@ __global__ void __launch_bounds__(GT, 4) pcg_global_kernel(GArgs A) {
         ro = rn;
         rn = t;
     }
-    // ---- write u_G, iteration counts and final relative residuals
+    // ---- write u_G = x + alpha_last p_last, iteration counts and final relative residuals
     for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
         const int l = l0 + (int)(it / nvb), vb = (int)(it % nvb);
-        const int64_t sg = s0 + s;
+        const int kl = A.node_active[l] ? iters_run - 1 : A.fin[l];  // the node's last iteration (-1: none)
+        const double* pl = (kl < 0 ? A.p0 : (p_in_p1(kl) ? A.p1 : A.p0)) + (int64_t)l * V * CS;
+        double al[SP];
+#pragma unroll
+        for (int j = 0; j < SP; ++j) al[j] = kl < 0 ? 0.0 : A.alpha[l * CS + s + j];
         for (int c = 0; c < VPI / VBK; ++c) {
             const int v = vert(vb, c);
-            if (v < 0 || sg >= A.S) continue;
-            A.uG[ug_index(sg, g.vorder[v], l, L, V, A.csl)] = A.x[((int64_t)l * V) * CS + v * CS + s];
+            if (v < 0) continue;
+            const int e = v * CS + s;
+            const VS xv = ldv<SP>(A.x + (int64_t)l * V * CS + e);
+#pragma unroll
+            for (int j = 0; j < SP; ++j) {
+                const int64_t sg = s0 + s + j;
+                if (sg >= A.S) continue;
+                const double xo = al[j] != 0.0 ? fma(al[j], pl[e + j], xv.v[j]) : xv.v[j];
+                A.uG[ug_index(sg, g.vorder[v], l, L, V, A.csl)] = xo;
+            }
         }
         if (vb == 0 && tid < CS && s0 + tid < A.S) {
             const int sy = l * CS + tid;
@@ -456,7 +536,7 @@ cudaError_t launch_cs(GArgs a, int64_t n_tiles, cudaStream_t st) {
     // on config 4: the per-group grid barriers cost more than the HBM traffic they save.)
     a.group = a.L;
     // vertices per item: enough items per phase for about two per CTA
-    const int vbk = GT / CS;
+    const int vbk = Lanes<CS>::VBK;
     a.vpi = VPI_MAX;
     while (a.vpi > vbk && (int64_t)a.group * ((a.g.V + a.vpi - 1) / a.vpi) < 2 * (int64_t)blocks) a.vpi /= 2;
     if (a.vpi < vbk) a.vpi = vbk;
@@ -502,6 +582,9 @@ __global__ void pcg_tables_pos_kernel(DevGraph g, int32_t L, const double4* __re
     }
 }
 
+// vertices per sub-chunk = the smallest item (Lanes<CS>::VBK)
+int vbk_min(int64_t cs) { return cs == 1 ? Lanes<1>::VBK : (cs == 16 ? Lanes<16>::VBK : Lanes<32>::VBK); }
+
 }  // namespace
 
 void launch_pcg_tables_pos(const DevGraph& g, const DevPlan& p, cudaStream_t st) {
@@ -514,13 +597,13 @@ void launch_pcg_tables_pos(const DevGraph& g, const DevPlan& p, cudaStream_t st)
 
 size_t pcg_global_ws_bytes(const DevGraph& g, int32_t L, int64_t n_samples) {
     const int64_t cs = (int64_t)1 << sample_tile_log2(n_samples);
-    const int64_t nvb = (g.V + (GT / cs) - 1) / (GT / cs);  // rows for the smallest item size
+    const int64_t nvb = (g.V + vbk_min(cs) - 1) / vbk_min(cs);  // rows for the smallest item size
     size_t b = 7 * sizeof(double) * (size_t)L * g.V * cs;      // x, r0, r1, p0, p1, q, z
     b += 5 * sizeof(double) * (size_t)L * cs;                  // alpha, beta, rz, gg, rr
     b += 2 * sizeof(int32_t) * (size_t)L * cs;                 // done, its
     b += sizeof(int32_t) * (size_t)(L + 1);                    // node_active, n_active
     b += sizeof(double) * (size_t)L * nvb * 2 * cs;            // partials
-    b += sizeof(int32_t) * (size_t)L;                          // counters
+    b += 2 * sizeof(int32_t) * (size_t)L;                      // counters, fin
     return b + 16 * 256;
 }
 
@@ -530,7 +613,7 @@ cudaError_t launch_pcg_global(const DevGraph& g, const DevPlan& p, int64_t n_sam
     const int32_t csl = sample_tile_log2(n_samples);
     const int64_t cs = (int64_t)1 << csl;
     const int64_t L = p.L;
-    const int64_t nvb = (g.V + (GT / cs) - 1) / (GT / cs);
+    const int64_t nvb = (g.V + vbk_min(cs) - 1) / vbk_min(cs);
     char* b = static_cast<char*>(ws);
     auto take = [&](size_t bytes) {
         char* r = b;
@@ -568,6 +651,7 @@ cudaError_t launch_pcg_global(const DevGraph& g, const DevPlan& p, int64_t n_sam
     a.n_active = (int32_t*)take(sizeof(int32_t));
     a.part = (double*)take(sizeof(double) * (size_t)L * nvb * 2 * cs);
     a.cnt = (int32_t*)take(sizeof(int32_t) * L);
+    a.fin = (int32_t*)take(sizeof(int32_t) * L);
     const int64_t n_tiles = (n_samples + cs - 1) / cs;
     switch (cs) {
         case 1: return launch_cs<1>(a, n_tiles, st);
