@@ -1,5 +1,7 @@
 // K4 warp-per-system variant of the batched NN-PCG (pcg.cu has the operator definitions,
 // the table layout and the thread-group variant for larger vertex sets).
+#include <cstdlib>
+
 #include "grf_internal.h"
 
 namespace grf {
@@ -10,13 +12,16 @@ constexpr size_t SMEM_LIMIT = 227 * 1024;
 __host__ __device__ inline int64_t table_stride(int V, int W) { return 3 * (int64_t)V + 3 * (int64_t)W * V; }
 
 // ---------------------------------------------------------------------------------------
-// Warp-per-system variant (V <= 1024).  CTA = 8 warps = node l x one octet of consecutive
-// samples per pass (the CTA walks `octs` octets); each warp solves one (l, s) system alone:
-// r and p in shared memory (neighbour access of the two operators), x, q = S p and
-// z = M^{-1} r in registers (VPL vertices v = lane + 32 k per lane), dot products by
-// 5-level xor shuffles (fixed order), __syncwarp between the phases -- no block barriers
-// after the optional staging of node l's operator tables and ELL neighbour indices.
-constexpr int WARP_NW = 8;
+// Warp-group-per-system variant (V <= 1024).  CTA = node l x one octet of consecutive samples
+// per pass (the CTA walks `octs` octets); a group of WPS warps solves one (l, s) system: r and p
+// in shared memory (neighbour access of the two operators), x, q = S p and z = M^{-1} r in
+// registers (VPL vertices v = 32 (WPS k + wi) + lane per lane of group warp wi), dot products by
+// 5-level xor shuffles then a fixed-order sum over the group's warps through shared memory,
+// group barriers (bar.sync, one id per system) between the phases -- no block barriers after the
+// optional staging of node l's operator tables and ELL neighbour indices.  WPS = 1 is the
+// warp-per-system form (__syncwarp only); WPS = 2 halves the registers per thread, so twice the
+// warps are resident for the same shared memory (latency hiding of the neighbour loads).
+constexpr int WARP_NW = 8;  // systems per CTA (an octet)
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -24,15 +29,34 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-template <int VPL, int W, bool STAGE>
-__global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int32_t L, const double* __restrict__ ops,
+template <int VPL, int W, bool STAGE, int WPS>
+__global__ void __launch_bounds__(WARP_NW * WPS * 32) pcg_warp_kernel(DevGraph g, int32_t L, const double* __restrict__ ops,
                                                                 PcgParams prm, int64_t S, int32_t octs, int32_t csl,
                                                                 const double* __restrict__ rhs, double* __restrict__ uG,
                                                                 int32_t* __restrict__ iters, double* __restrict__ relres) {
     extern __shared__ double sm[];
     const int V = g.V;
     const int l = blockIdx.x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NT = WARP_NW * WPS * 32;
+    const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) / WPS, wi = (threadIdx.x >> 5) % WPS;
+    __shared__ double xch[WARP_NW][4][WPS];  // group dot-product exchange: [system][slot][warp]
+    // barrier over the system's warp group (id 1 + system: id 0 is __syncthreads)
+    auto gsync = [&]() {
+        if (WPS == 1)
+            __syncwarp();
+        else
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + warp), "r"(WPS * 32) : "memory");
+    };
+    // fixed-order group sum of a warp-reduced value (every warp of the group gets the same total)
+    auto gsum = [&](double v, int slot) {
+        if (WPS == 1) return v;
+        if (lane == 0) xch[warp][slot][wi] = v;
+        gsync();
+        double t = xch[warp][slot][0];
+#pragma unroll
+        for (int q = 1; q < WPS; ++q) t += xch[warp][slot][q];
+        return t;
+    };
     const int64_t stride = table_stride(V, W);
     const double* tab = ops + l * stride;
     const double* DS = tab;
@@ -55,8 +79,8 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
             double* sD = st;                                          // DS [V], DM [V]
             double2* sO = reinterpret_cast<double2*>(st + 2 * V);     // OS01, OS23, OM01, OM23: [V] each
             ushort4* sN = reinterpret_cast<ushort4*>(sO + 4 * V);     // neighbours [V]
-            for (int i = threadIdx.x; i < 2 * V; i += WARP_NW * 32) sD[i] = tab[i];
-            for (int v = threadIdx.x; v < V; v += WARP_NW * 32) {
+            for (int i = threadIdx.x; i < 2 * V; i += NT) sD[i] = tab[i];
+            for (int v = threadIdx.x; v < V; v += NT) {
                 const double* oS = OS + v;
                 const double* oM = OM + v;
                 sO[v] = make_double2(oS[0], oS[V]);
@@ -76,9 +100,9 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
             nb4 = sN;
         } else {
             int* so = reinterpret_cast<int*>(st + (size_t)(2 + 2 * W) * V);
-            for (int i = threadIdx.x; i < 2 * V; i += WARP_NW * 32) st[i] = tab[i];                      // DS, DM
-            for (int i = threadIdx.x; i < 2 * W * V; i += WARP_NW * 32) st[2 * V + i] = tab[3 * V + i];  // OS, OM
-            for (int i = threadIdx.x; i < W * V; i += WARP_NW * 32) so[i] = eo[i];
+            for (int i = threadIdx.x; i < 2 * V; i += NT) st[i] = tab[i];                      // DS, DM
+            for (int i = threadIdx.x; i < 2 * W * V; i += NT) st[2 * V + i] = tab[3 * V + i];  // OS, OM
+            for (int i = threadIdx.x; i < W * V; i += NT) so[i] = eo[i];
             __syncthreads();
             DS = st;
             DM = st + V;
@@ -94,7 +118,7 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
                      double (&y)[VPL], int mode, double& d1, double& d2) {
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
-            const int v = lane + 32 * k;
+            const int v = lane + 32 * (WPS * k + wi);
             if (v < V) {
                 const double xv = xs[v];
                 double a = D[v] * xv;
@@ -124,7 +148,7 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
         } else {
 #pragma unroll
             for (int k = 0; k < VPL; ++k) {
-                const int v = lane + 32 * k;
+                const int v = lane + 32 * (WPS * k + wi);
                 if (v < V) {
                     const double rv = r[v];
                     z[k] = (prm.precond == 1 ? DJ[v] : 1.0) * rv;
@@ -152,7 +176,7 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
             const double* gs = rhs + rhs_index(s, l, 0, L, V, csl);
     #pragma unroll
             for (int k = 0; k < VPL; ++k) {
-                const int v = lane + 32 * k;
+                const int v = lane + 32 * (WPS * k + wi);
                 x[k] = 0.0;
                 if (v < V) {
                     const double gv = gs[v];
@@ -160,17 +184,23 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
                     gg = fma(gv, gv, gg);
                 }
             }
-            gg = warp_sum(gg);
+            gg = gsum(warp_sum(gg), 0);
             double sup = 1.0;
             if (gg > 0.0 && (gg < 0x1p-900 || gg > 0x1p900)) {  // rare: rescale by a power of two (exact)
                 double gmax = 0.0;
     #pragma unroll
                 for (int k = 0; k < VPL; ++k) {
-                    const int v = lane + 32 * k;
+                    const int v = lane + 32 * (WPS * k + wi);
                     if (v < V) gmax = fmax(gmax, fabs(r[v]));
                 }
     #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+                if (WPS > 1) {
+                    if (lane == 0) xch[warp][1][wi] = gmax;
+                    gsync();
+#pragma unroll
+                    for (int q = 0; q < WPS; ++q) gmax = fmax(gmax, xch[warp][1][q]);
+                }
                 int e = 0;
                 frexp(gmax, &e);
                 e = e < -1000 ? -1000 : (e > 1000 ? 1000 : e);
@@ -179,29 +209,29 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
                 gg = 0.0;
     #pragma unroll
                 for (int k = 0; k < VPL; ++k) {
-                    const int v = lane + 32 * k;
+                    const int v = lane + 32 * (WPS * k + wi);
                     if (v < V) {
                         const double gv = r[v] * sdown;
                         r[v] = gv;
                         gg = fma(gv, gv, gg);
                     }
                 }
-                gg = warp_sum(gg);
+                gg = gsum(warp_sum(gg), 2);
             }
-            __syncwarp();
+            gsync();  // r complete
             double d0a = 0.0, d0b = 0.0;
             precond(t, 0, d0a, d0b);
             double rz = 0.0;
     #pragma unroll
             for (int k = 0; k < VPL; ++k) {
-                const int v = lane + 32 * k;
+                const int v = lane + 32 * (WPS * k + wi);
                 if (v < V) {
                     p[v] = t[k];
                     rz = fma(r[v], t[k], rz);
                 }
             }
-            rz = warp_sum(rz);
-            __syncwarp();
+            rz = gsum(warp_sum(rz), 3);
+            gsync();  // p complete
             const double tol2 = prm.rtol * prm.rtol * gg;
             bool done = !(gg > 0.0);
             double rr = gg;
@@ -210,40 +240,54 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
                 ++it;
                 double pq = 0.0, unused = 0.0;
                 apply(DS, OS, os01, os23, p, t, 1, pq, unused);  // Dirichlet step (P247-258): t = q, pq = p.q
-                pq = warp_sum(pq);
+                pq = gsum(warp_sum(pq), 0);
                 if (!(pq > 0.0)) break;  // p = 0 (e.g. an underflowed rhs): nothing left to reduce
                 const double alpha = rz / pq;
     #pragma unroll
                 for (int k = 0; k < VPL; ++k) {
-                    const int v = lane + 32 * k;
+                    const int v = lane + 32 * (WPS * k + wi);
                     if (v < V) {
                         x[k] = fma(alpha, p[v], x[k]);
                         r[v] = fma(-alpha, t[k], r[v]);
                     }
                 }
-                __syncwarp();
+                gsync();  // r complete
                 double t_rr = 0.0, t_rz = 0.0;
                 precond(t, 2, t_rr, t_rz);  // Neumann step (P260-298): t = z, with r.r and r.z
                 t_rr = warp_sum(t_rr);
                 t_rz = warp_sum(t_rz);
+                if (WPS > 1) {  // both totals through one exchange (slots 1, 2)
+                    if (lane == 0) {
+                        xch[warp][1][wi] = t_rr;
+                        xch[warp][2][wi] = t_rz;
+                    }
+                    gsync();
+                    t_rr = xch[warp][1][0];
+                    t_rz = xch[warp][2][0];
+#pragma unroll
+                    for (int q = 1; q < WPS; ++q) {
+                        t_rr += xch[warp][1][q];
+                        t_rz += xch[warp][2][q];
+                    }
+                }
                 rr = t_rr;
                 if (t_rr <= tol2) break;
                 const double beta = t_rz / rz;
                 rz = t_rz;
     #pragma unroll
                 for (int k = 0; k < VPL; ++k) {
-                    const int v = lane + 32 * k;
+                    const int v = lane + 32 * (WPS * k + wi);
                     if (v < V) p[v] = fma(beta, p[v], t[k]);
                 }
-                __syncwarp();
+                gsync();  // p complete
             }
-            __syncwarp();
+            gsync();
     #pragma unroll
             for (int k = 0; k < VPL; ++k) {  // u_G of this system parked in r (free now)
-                const int v = lane + 32 * k;
+                const int v = lane + 32 * (WPS * k + wi);
                 if (v < V) r[v] = x[k] * sup;
             }
-            if (lane == 0) {
+            if (lane == 0 && wi == 0) {
                 iters[s * L + l] = it;
                 relres[s * L + l] = gg > 0.0 ? sqrt(rr / gg) : 0.0;
             }
@@ -251,7 +295,7 @@ __global__ void __launch_bounds__(WARP_NW * 32) pcg_warp_kernel(DevGraph g, int3
         __syncthreads();
         // the octet's 8 samples are consecutive slots of one sample tile: write u_G [tile][v][l][cs]
         // as 64-byte runs (vertex-major, sample fastest) instead of 8-byte scatters
-        for (int i = threadIdx.x; i < V * WARP_NW; i += WARP_NW * 32) {
+        for (int i = threadIdx.x; i < V * WARP_NW; i += NT) {
             const int v = i / WARP_NW, w = i % WARP_NW;
             if (s0 + w < S) uG[ug_index(s0 + w, v, l, L, V, csl)] = sm[(size_t)w * 2 * V + v];
         }
@@ -265,9 +309,10 @@ size_t warp_smem_bytes(const DevGraph& g, int W, bool stage) {
     return b;
 }
 
-template <int VPL, int W>
+template <int VPL, int W, int WPS>
 bool launch_warp_t(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* rhs,
                    double* uG, int32_t* iters, double* relres, cudaStream_t st) {
+    constexpr int NT = WARP_NW * WPS * 32;
     const bool stage = warp_smem_bytes(g, W, true) <= SMEM_LIMIT;
     const size_t smem = warp_smem_bytes(g, W, stage);
     if (smem > SMEM_LIMIT) return false;
@@ -275,11 +320,11 @@ bool launch_warp_t(const DevGraph& g, const DevPlan& p, int64_t n_samples, const
     // octets per CTA: the CTAs run in waves of (resident CTAs per SM) x 148 and a wave lasts about
     // `octs` octet solves, so pick the power of two minimising waves x octs (the partial last wave
     // included); ties go to the larger octs (fewer table stagings).  Config 3: 2 (23 waves).
-    auto* kern = stage ? pcg_warp_kernel<VPL, W, true> : pcg_warp_kernel<VPL, W, false>;
+    auto* kern = stage ? pcg_warp_kernel<VPL, W, true, WPS> : pcg_warp_kernel<VPL, W, false, WPS>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WARP_NW * 32, smem);
-    const int64_t slots = 148 * (int64_t)(per_sm > 0 ? per_sm : 1);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
+    const int64_t slots = (int64_t)g.n_sm * (per_sm > 0 ? per_sm : 1);
     int64_t octs = 1, best = -1;
     for (int64_t o = 1; o <= n_oct; o *= 2) {
         const int64_t ctas = p.L * ((n_oct + o - 1) / o);
@@ -291,15 +336,7 @@ bool launch_warp_t(const DevGraph& g, const DevPlan& p, int64_t n_samples, const
     }
     const dim3 grid(p.L, (unsigned)((n_oct + octs - 1) / octs));
     const int32_t csl = sample_tile_log2(n_samples);
-    if (stage) {
-        cudaFuncSetAttribute(pcg_warp_kernel<VPL, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        pcg_warp_kernel<VPL, W, true><<<grid, WARP_NW * 32, smem, st>>>(g, p.L, p.ops, prm, n_samples, (int32_t)octs, csl,
-                                                                      rhs, uG, iters, relres);
-    } else {
-        cudaFuncSetAttribute(pcg_warp_kernel<VPL, W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        pcg_warp_kernel<VPL, W, false><<<grid, WARP_NW * 32, smem, st>>>(g, p.L, p.ops, prm, n_samples, (int32_t)octs,
-                                                                       csl, rhs, uG, iters, relres);
-    }
+    kern<<<grid, NT, smem, st>>>(g, p.L, p.ops, prm, n_samples, (int32_t)octs, csl, rhs, uG, iters, relres);
     return true;
 }
 
@@ -307,8 +344,19 @@ template <int W>
 bool launch_warp(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* rhs,
                  double* uG, int32_t* iters, double* relres, cudaStream_t st) {
     const int vpl = (g.V + 31) / 32;
-#define GRF_PW(N) \
-    if (vpl <= N) return launch_warp_t<N, W>(g, p, n_samples, prm, rhs, uG, iters, relres, st);
+    // warps per system: 2 once a lane holds 16+ vertices (the register file, not the shared memory,
+    // bounds the resident systems there); design study override: env GRF_PCG_WPS
+    static const int wps_env = [] {
+        const char* e = getenv("GRF_PCG_WPS");
+        return e ? atoi(e) : 0;
+    }();
+    const int wps = wps_env > 0 ? wps_env : (vpl > 8 ? 2 : 1);
+#define GRF_PW(N)                                                                                      \
+    if (vpl <= N) {                                                                                    \
+        if (wps >= 4 && N >= 4) return launch_warp_t<(N >= 4 ? N / 4 : 1), W, 4>(g, p, n_samples, prm, rhs, uG, iters, relres, st); \
+        if (wps >= 2 && N >= 2) return launch_warp_t<(N >= 2 ? N / 2 : 1), W, 2>(g, p, n_samples, prm, rhs, uG, iters, relres, st); \
+        return launch_warp_t<N, W, 1>(g, p, n_samples, prm, rhs, uG, iters, relres, st);               \
+    }
     GRF_PW(1) GRF_PW(2) GRF_PW(4) GRF_PW(8) GRF_PW(16) GRF_PW(32)
 #undef GRF_PW
     return false;

@@ -26,6 +26,10 @@ def short(name):
     if m:
         rec = m.group(1).split(",")[-1].strip().replace("(bool)", "")
         return "condense" if rec in ("0", "false") else "recover"
+    if "sweep3c_kernel" in name:  # warp-specialised condense (sweep3_impl.cuh)
+        return "condense"
+    if "sweep3_kernel" in name:  # warp-specialised recover (sweep3_impl.cuh)
+        return "recover"
     for k, v in (("noise_kernel", "noise"), ("edge_setup_kernel", "edge_setup"), ("pcg_tables_pos_kernel", "pcg_tables_pos"),
                  ("pcg_tables_kernel", "pcg_tables"),
                  ("assemble_rhs_kernel", "assemble"), ("vertex_sum_kernel", "vertex_sum"),
