@@ -62,7 +62,7 @@ struct Cfg {
     static constexpr size_t PART1 = (size_t)PEL * sizeof(double);                     // one partial stage
 };
 
-template <int TL, int NSTT>
+template <int TL, int NSTT, int CL>
 __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
     using C = Cfg<TL>;
     constexpr int RN = C::RN;
@@ -255,11 +255,17 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
 
     // ------------------------------------------------------------------------------------ consumers
     asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
-    const int ll = lane % LW, sl = lane / LW;
+    // consumer mapping: CL l-lanes x (32 / CL) s-lanes per warp, TSC = CL samples and TLT nodes per
+    // thread (CL = 4: the sweep_impl.cuh V2 tile; CL = 2: twice the nodes per thread, one
+    // reduce-scatter level instead of two)
+    constexpr int LWC = CL, TSC = CL, NLT = NWL * CL, TLT = RN / NLT, NPT = TLT / 2;
+    constexpr bool ODDT = (TLT & 1) != 0;
+    static_assert(TLT * NLT == RN, "node slots");
+    const int ll = lane % LWC, sl = lane / LWC;
     const int lw = warp;                    // l-warp
-    const int lt = lw * LW + ll;            // l-thread 0..31
-    const int st0 = sl * TS;                // first sample (within the item) of this thread
-    const int sig = ((ll & 1) << 1) | ((ll >> 1) & 1);  // sample slot j holds sample j ^ sig
+    const int lt = lw * LWC + ll;           // l-thread 0..NLT-1
+    const int st0 = sl * TSC;                // first sample (within the item) of this thread
+    const int sig = CL == 4 ? (((ll & 1) << 1) | ((ll >> 1) & 1)) : ll;  // sample slot j holds sample j ^ sig
     int stage = 0, ps = 0;
     uint32_t use = 0, puse = 0;
     auto acquire = [&]() { mbar_wait(&full[stage], (use >> stage) & 1u); };
@@ -269,7 +275,7 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
         use ^= 1u << stage;
         stage = stage + 1 == nst ? 0 : stage + 1;
     };
-    auto slot = [&](int n) -> int { return (n < 2 * NP) ? (2 * lt + 64 * (n >> 1) + (n & 1)) : (64 * NP + lt); };
+    auto slot = [&](int n) -> int { return (n < 2 * NPT) ? (2 * lt + 2 * NLT * (n >> 1) + (n & 1)) : (2 * NLT * NPT + lt); };
 
     for (;;) {
         acquire();
@@ -295,16 +301,16 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
             if (l >= L) return 0.0;
             return A.mass ? edge_coef(A.cI[l], A.cL[l], A.kappa2, h, 1).beta : cLs[l] * inv_h;
         };
-        int64_t sidx[TS];  // sample of slot j (clamped for loads)
+        int64_t sidx[TSC];  // sample of slot j (clamped for loads)
 #pragma unroll
-        for (int j = 0; j < TS; ++j) {
+        for (int j = 0; j < TSC; ++j) {
             const int64_t s = c0 + st0 + (j ^ sig);
             sidx[j] = s < A.S ? s : A.S - 1;
         }
-        const double* uGu[TS];
-        const double* uGv[TS];
+        const double* uGu[TSC];
+        const double* uGv[TSC];
 #pragma unroll
-        for (int j = 0; j < TS; ++j) {
+        for (int j = 0; j < TSC; ++j) {
             uGu[j] = A.uG + ug_index(sidx[j], vu, 0, L, g.V, CSL);
             uGv[j] = A.uG + ug_index(sidx[j], vv, 0, L, g.V, CSL);
         }
@@ -312,15 +318,15 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
         for (int rd = 0; rd < A.rounds; ++rd) {
             const int rb = rd * RN;
             if (rd > 0) acquire();
-            double Y[TL][TS], Z[TL][TS];
+            double Y[TLT][TSC], Z[TLT][TSC];
             // boundary rows (P310): Y = beta u_left, Z = beta u_right enter at step 0 (mu_0 = 0)
 #pragma unroll
-            for (int n = 0; n < TL; ++n) {
+            for (int n = 0; n < TLT; ++n) {
                 const int l = rb + slot(n);
                 const bool ok = l < L;
                 const double bt = beta_of(l);
 #pragma unroll
-                for (int j = 0; j < TS; ++j) {
+                for (int j = 0; j < TSC; ++j) {
                     const bool ld = ok && !(A.ablate & 64);
                     const double ul = ld ? uGu[j][l << CSL] : 0.0, ur = ld ? uGv[j][l << CSL] : 0.0;
                     Y[n][j] = bt * (m == 1 ? ul + ur : ul);
@@ -349,10 +355,10 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
                     bd.c0 = c0;
                     phdr[ps] = bd;
                 }
-                auto load_w = [&](int tt, double (&wl)[TS], double (&wr)[TS]) {
+                auto load_w = [&](int tt, double (&wl)[TSC], double (&wr)[TSC]) {
                     const int cp = sig & 1, px = sig >> 1;
 #pragma unroll
-                    for (int q = 0; q < TS / 2; ++q) {
+                    for (int q = 0; q < TSC / 2; ++q) {
                         const int o = st0 + 2 * (q ^ px);
                         const double2 a = *reinterpret_cast<const double2*>(wb + ((tt * 2 + 0) * NC + cp) * WROW + o);
                         const double2 c = *reinterpret_cast<const double2*>(wb + ((tt * 2 + 1) * NC + cp) * WROW + o);
@@ -363,22 +369,22 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
                     }
                 };
                 // interior step: correction-node form (both chains contribute g X_t)
-                auto body_mid = [&](int tt, double (&aL)[TS], double (&aR)[TS]) {
-                    double wl[TS], wr[TS];
+                auto body_mid = [&](int tt, double (&aL)[TSC], double (&aR)[TSC]) {
+                    double wl[TSC], wr[TSC];
                     load_w(tt, wl, wr);
                     const double* rmu = cmu + tt * RN;
                     const double* rga = cga + tt * RN;
 #pragma unroll
-                    for (int j = 0; j < TS; ++j) aL[j] = aR[j] = 0.0;
+                    for (int j = 0; j < TSC; ++j) aL[j] = aR[j] = 0.0;
                     // all chain updates first, then the accumulations (each uses a chain value computed
-                    // >= TL*TS*2 FMAs earlier: no back-to-back DFMA dependencies)
-                    double2 g2s[NP > 0 ? NP : 1];
+                    // >= TLT*TSC*2 FMAs earlier: no back-to-back DFMA dependencies)
+                    double2 g2s[NPT > 0 ? NPT : 1];
 #pragma unroll
-                    for (int q = 0; q < NP; ++q) {
-                        const double2 m2 = *reinterpret_cast<const double2*>(rmu + 2 * lt + 64 * q);
-                        g2s[q] = *reinterpret_cast<const double2*>(rga + 2 * lt + 64 * q);
+                    for (int q = 0; q < NPT; ++q) {
+                        const double2 m2 = *reinterpret_cast<const double2*>(rmu + 2 * lt + 2 * NLT * q);
+                        g2s[q] = *reinterpret_cast<const double2*>(rga + 2 * lt + 2 * NLT * q);
 #pragma unroll
-                        for (int j = 0; j < TS; ++j) {
+                        for (int j = 0; j < TSC; ++j) {
                             Y[2 * q][j] = fma(-m2.x, Y[2 * q][j], wl[j]);
                             Z[2 * q][j] = fma(-m2.x, Z[2 * q][j], wr[j]);
                             Y[2 * q + 1][j] = fma(-m2.y, Y[2 * q + 1][j], wl[j]);
@@ -386,44 +392,44 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
                         }
                     }
                     double go = 0.0;
-                    if (ODD) {
-                        const double mu = rmu[64 * NP + lt];
-                        go = rga[64 * NP + lt];
+                    if (ODDT) {
+                        const double mu = rmu[2 * NLT * NPT + lt];
+                        go = rga[2 * NLT * NPT + lt];
 #pragma unroll
-                        for (int j = 0; j < TS; ++j) {
-                            Y[TL - 1][j] = fma(-mu, Y[TL - 1][j], wl[j]);
-                            Z[TL - 1][j] = fma(-mu, Z[TL - 1][j], wr[j]);
+                        for (int j = 0; j < TSC; ++j) {
+                            Y[TLT - 1][j] = fma(-mu, Y[TLT - 1][j], wl[j]);
+                            Z[TLT - 1][j] = fma(-mu, Z[TLT - 1][j], wr[j]);
                         }
                     }
 #pragma unroll
-                    for (int q = 0; q < NP; ++q) {
+                    for (int q = 0; q < NPT; ++q) {
 #pragma unroll
-                        for (int j = 0; j < TS; ++j) {
+                        for (int j = 0; j < TSC; ++j) {
                             aL[j] = fma(g2s[q].x, Y[2 * q][j], aL[j]);
                             aR[j] = fma(g2s[q].x, Z[2 * q][j], aR[j]);
                             aL[j] = fma(g2s[q].y, Y[2 * q + 1][j], aL[j]);
                             aR[j] = fma(g2s[q].y, Z[2 * q + 1][j], aR[j]);
                         }
                     }
-                    if (ODD) {
+                    if (ODDT) {
 #pragma unroll
-                        for (int j = 0; j < TS; ++j) {
-                            aL[j] = fma(go, Y[TL - 1][j], aL[j]);
-                            aR[j] = fma(go, Z[TL - 1][j], aR[j]);
+                        for (int j = 0; j < TSC; ++j) {
+                            aL[j] = fma(go, Y[TLT - 1][j], aL[j]);
+                            aR[j] = fma(go, Z[TLT - 1][j], aR[j]);
                         }
                     }
                 };
                 // step 0: mu_0 = 0, Y_0 = f_0 (W + the preloaded boundary term), no left contribution
-                auto body_first = [&](double (&aL)[TS], double (&aR)[TS]) {
-                    double wl[TS], wr[TS];
+                auto body_first = [&](double (&aL)[TSC], double (&aR)[TSC]) {
+                    double wl[TSC], wr[TSC];
                     load_w(0, wl, wr);
 #pragma unroll
-                    for (int j = 0; j < TS; ++j) aL[j] = aR[j] = 0.0;
+                    for (int j = 0; j < TSC; ++j) aL[j] = aR[j] = 0.0;
 #pragma unroll
-                    for (int n = 0; n < TL; ++n) {
+                    for (int n = 0; n < TLT; ++n) {
                         const double gg = cga[slot(n)];
 #pragma unroll
-                        for (int j = 0; j < TS; ++j) {
+                        for (int j = 0; j < TSC; ++j) {
                             Y[n][j] += wl[j];
                             Z[n][j] += wr[j];
                             aR[j] = fma(gg, Z[n][j], aR[j]);
@@ -432,15 +438,15 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
                 };
                 // step m-1 (m >= 2): the left chain reaches position m-1 (f += beta u_right), the right
                 // chain position 0 (f += beta u_left)
-                auto body_last = [&](int tt, double (&aL)[TS], double (&aR)[TS]) {
-                    double wl[TS], wr[TS];
+                auto body_last = [&](int tt, double (&aL)[TSC], double (&aR)[TSC]) {
+                    double wl[TSC], wr[TSC];
                     load_w(tt, wl, wr);
                     const double* rmu = cmu + tt * RN;
                     const double* rga = cga + tt * RN;
 #pragma unroll
-                    for (int j = 0; j < TS; ++j) aL[j] = aR[j] = 0.0;
+                    for (int j = 0; j < TSC; ++j) aL[j] = aR[j] = 0.0;
 #pragma unroll
-                    for (int n = 0; n < TL; ++n) {
+                    for (int n = 0; n < TLT; ++n) {
                         const int sn = slot(n);
                         const int l = rb + sn;
                         const bool ok = l < L;
@@ -448,7 +454,7 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
                         const double mu = rmu[sn], gg = rga[sn];
                         const double nk = gg * mu;
 #pragma unroll
-                        for (int j = 0; j < TS; ++j) {
+                        for (int j = 0; j < TSC; ++j) {
                             const double ul = ok ? uGu[j][l << CSL] : 0.0;
                             const double ur = ok ? uGv[j][l << CSL] : 0.0;
                             aL[j] = fma(-nk, Y[n][j], aL[j]);
@@ -459,15 +465,20 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
                     }
                 };
                 double* pb = pbase + lw * 2 * CS + st0 + sig;
-                // sum the step's partials over the warp's 4 l-lanes (select-free reduce-scatter: slot j
+                // sum the step's partials over the warp's CL l-lanes (select-free reduce-scatter: slot j
                 // holds sample j ^ sig) and store them for the fold warps
-                auto reduce_store = [&](double (&aL)[TS], double (&aR)[TS], int tt) {
-                    aL[0] += __shfl_xor_sync(0xffffffffu, aL[2], 1);
-                    aL[1] += __shfl_xor_sync(0xffffffffu, aL[3], 1);
-                    aR[0] += __shfl_xor_sync(0xffffffffu, aR[2], 1);
-                    aR[1] += __shfl_xor_sync(0xffffffffu, aR[3], 1);
-                    aL[0] += __shfl_xor_sync(0xffffffffu, aL[1], 2);
-                    aR[0] += __shfl_xor_sync(0xffffffffu, aR[1], 2);
+                auto reduce_store = [&](double (&aL)[TSC], double (&aR)[TSC], int tt) {
+                    if constexpr (CL == 4) {
+                        aL[0] += __shfl_xor_sync(0xffffffffu, aL[2], 1);
+                        aL[1] += __shfl_xor_sync(0xffffffffu, aL[3], 1);
+                        aR[0] += __shfl_xor_sync(0xffffffffu, aR[2], 1);
+                        aR[1] += __shfl_xor_sync(0xffffffffu, aR[3], 1);
+                        aL[0] += __shfl_xor_sync(0xffffffffu, aL[1], 2);
+                        aR[0] += __shfl_xor_sync(0xffffffffu, aR[1], 2);
+                    } else {
+                        aL[0] += __shfl_xor_sync(0xffffffffu, aL[1], 1);
+                        aR[0] += __shfl_xor_sync(0xffffffffu, aR[1], 1);
+                    }
                     if (!(A.ablate & 32)) {
                         pb[tt * NWL * 2 * CS] = aL[0];
                         pb[tt * NWL * 2 * CS + CS] = aR[0];
@@ -476,11 +487,11 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
                 const bool last_here = (t0 + nb == m) && (m > 1);
                 if (last_here && nb > 1) {  // the last step re-reads both vertices' u_G: pull it into L1
 #pragma unroll
-                    for (int n = 0; n < TL; ++n) {
+                    for (int n = 0; n < TLT; ++n) {
                         const int l = rb + slot(n);
                         if (l < L) {
 #pragma unroll
-                            for (int j = 0; j < TS; ++j) {
+                            for (int j = 0; j < TSC; ++j) {
                                 asm volatile("prefetch.global.L1 [%0];" ::"l"(uGu[j] + (l << CSL)));
                                 asm volatile("prefetch.global.L1 [%0];" ::"l"(uGv[j] + (l << CSL)));
                             }
@@ -488,7 +499,7 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
                     }
                 }
                 const int tend = last_here ? nb - 1 : nb;
-                double pL[TS], pR[TS];
+                double pL[TSC], pR[TSC];
                 bool pend = false;
                 int tt = 0;
                 if (t0 == 0) {
@@ -503,29 +514,29 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
                 // steps in pairs with alternating partial registers (no register copies); the
                 // reduction of step tt-1 is issued under step tt's FMAs
                 for (; tt + 1 < tend; tt += 2) {
-                    double aL[TS], aR[TS];
+                    double aL[TSC], aR[TSC];
                     body_mid(tt, aL, aR);
                     reduce_store(pL, pR, tt - 1);
                     body_mid(tt + 1, pL, pR);
                     reduce_store(aL, aR, tt);
                 }
                 if (tt < tend) {
-                    double aL[TS], aR[TS];
+                    double aL[TSC], aR[TSC];
                     body_mid(tt, aL, aR);
                     reduce_store(pL, pR, tt - 1);
 #pragma unroll
-                    for (int j = 0; j < TS; ++j) {
+                    for (int j = 0; j < TSC; ++j) {
                         pL[j] = aL[j];
                         pR[j] = aR[j];
                     }
                     ++tt;
                 }
                 if (last_here) {
-                    double aL[TS], aR[TS];
+                    double aL[TSC], aR[TSC];
                     body_last(nb - 1, aL, aR);
                     if (pend) reduce_store(pL, pR, nb - 2);
 #pragma unroll
-                    for (int j = 0; j < TS; ++j) {
+                    for (int j = 0; j < TSC; ++j) {
                         pL[j] = aL[j];
                         pR[j] = aR[j];
                     }
@@ -823,7 +834,10 @@ cudaError_t launch(Args a, cudaStream_t st) {
     a.tile_ms = want <= fit ? want : (fit >= 1 ? ((fit - 1) | 1) : 0);
     smem += (size_t)CS * a.tile_ms * sizeof(double);
     // the ring depth is a template constant (the stage offsets fold into the addressing)
-    auto kern = a.nst == NST ? sweep3_kernel<TL, NST> : sweep3_kernel<TL, 2>;
+    // consumer mapping CL = 2 l-lanes per warp (one reduce-scatter level) unless GRF_ABLATE bit 256
+    const bool cl4 = (a.ablate & 256) != 0;
+    auto kern = a.nst == NST ? (cl4 ? sweep3_kernel<TL, NST, 4> : sweep3_kernel<TL, NST, 2>)
+                             : (cl4 ? sweep3_kernel<TL, 2, 4> : sweep3_kernel<TL, 2, 2>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(a.counter, 0, sizeof(int32_t), st);
