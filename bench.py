@@ -334,15 +334,20 @@ def main():
     t_ms = e0.elapsed_time(e1)
     per_step = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
     prof = work_graph.profile_read()
+    if graph_replay is not None:
+        # the replays carry no profiling brackets (not captured): the per-kernel times for
+        # `kernels` / `roofline` come from as many eager calls after the timed region
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize()
+        prof = work_graph.profile_read()
     work_graph.profile(False)
     if world > 1:
         t = torch.tensor([t_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_ms = float(t.item())
     launches_per_step = int(st.get("gpu_launches", 0))
-    if graph_replay is not None:  # kernels of one replay = those of one call (profiling brackets not captured)
-        prof = {name: (ms, n) for name, (ms, n) in prof.items()}
-    launches = launches_per_step * args.steps
+    launches = launches_per_step * args.steps  # a replay launches the kernels of one call
 
     # end to end: the public API with the step's result read back to pinned host memory each step
     e2e = None
@@ -418,6 +423,9 @@ def main():
         "dof_node_per_s": dof_node,
     }
     line["config"]["cuda_graph"] = graph_replay is not None
+    if graph_replay is not None:
+        line["kernels_timed"] = ("per-kernel times (kernels, roofline) from as many eager calls right after the "
+                                 "timed graph replays; share = their time / the replays' time")
     line["config"].update(info)
     if kernels:
         dom = max((k_ for k_ in kernels if k_ != "noise"), key=lambda k_: kernels[k_]["share"], default=None)

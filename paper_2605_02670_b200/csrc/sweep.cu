@@ -102,8 +102,8 @@ cudaError_t launch_recover(const DevGraph& g, const DevPlan& p, int64_t n_sample
 
 namespace grf {
 namespace {
-// vertex values of the sample (P313-324): u_v = sum_l u_G^{(l)}(v); one warp per (s, v),
-// lanes stride over l, fixed-order shuffle sum
+// vertex values of the sample (P313-324): u_v = sum_l u_G^{(l)}(v); one thread per (s, v),
+// a sequential sum over l in node order
 __global__ void vertex_sum_kernel(int64_t S, int32_t V, int64_t N, int64_t NI, int32_t L, int32_t csl,
                                   const double* __restrict__ uG, double* __restrict__ u) {
     // thread per (tile, v, sample-in-tile): consecutive threads read consecutive samples
