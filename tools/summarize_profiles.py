@@ -108,6 +108,26 @@ with open(os.path.join(P, f"{R}_ncu_full.md"), "w") as fh:
             return v * scale
         traffic[k] = {"dram_bytes_per_launch": tobytes("dram__bytes_read.sum") + tobytes("dram__bytes_write.sum"),
                       "duration_ms": float(d["gpu__time_duration.sum"]) * (1e-6 if u["gpu__time_duration.sum"] == "ns" else 1e-3 if u["gpu__time_duration.sum"] == "us" else 1)}
+# ---- config 4's global PCG (one launch), if captured
+rgg = os.path.join(G, f"{R}_rgg_pcg.ncu-rep")
+if os.path.exists(rgg):
+    raw = subprocess.run(["ncu", "-i", rgg, "--page", "raw", "--csv"], capture_output=True, text=True).stdout.splitlines()
+    rr = list(csv.reader(raw))
+    if len(rr) > 2:
+        d = dict(zip(rr[0], rr[2]))
+        u = dict(zip(rr[0], rr[1]))
+        with open(os.path.join(P, f"{R}_ncu_rgg_pcg.md"), "w") as fh:
+            fh.write(f"# {R} ncu --set full of config 4's global PCG (rgg, one launch, --clock-control none)\n\n"
+                     f"`{d['Kernel Name'][:120]}`\n\n| metric | value | unit |\n|---|---|---|\n")
+            for key in keys + ["lts__t_sectors_srcunit_tex_op_read.sum", "l1tex__t_sector_hit_rate.pct"]:
+                if key in d:
+                    fh.write(f"| {key} | {d[key]} | {u.get(key, '')} |\n")
+            st = [(float(d[x]), x) for x in rr[0] if x.startswith("smsp__pcsamp_warps_issue_stalled")
+                  and not x.endswith("not_issued") and d[x] not in ("", "n/a")]
+            s_tot = sum(v for v, _ in st) or 1
+            fh.write("\nTop stall reasons (PC sampling): " + ", ".join(
+                f"{x.replace('smsp__pcsamp_warps_issue_stalled_', '')} {100 * v / s_tot:.0f}%"
+                for v, x in sorted(st, reverse=True)[:6]) + "\n")
 json.dump({"round": R, "config": CONFIG, "kernels": traffic}, open(os.path.join(P, "traffic.json"), "w"), indent=1)
 print(open(os.path.join(P, f"{R}_launches.md")).read())
 print(json.dumps(traffic, indent=1))
