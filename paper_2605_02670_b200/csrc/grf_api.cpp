@@ -1159,26 +1159,61 @@ grf_status grf_sample_host(grf_graph* g, double kappa, double beta, double k, ui
     if (st) return st;
     if (!u_host) return fail(GRF_EINVAL, "u_host is NULL");
     cudaStream_t s = (cudaStream_t)stream;
-    // Sample chunks of a multiple of 32 (about eight per call; the last one also takes the
-    // remainder, so every chunk runs the same kernel variants as the whole call and the field is
-    // bitwise the one-call field): chunk c's device->host copy runs on a second stream while chunk
-    // c+1 is computed; two device staging buffers alternate.  Chunk c draws samples [c0, c0 + n_c)
-    // with seed + c0, so its noise is that of the same samples in one call (key = seed + sample
-    // index, noise.cu).
-    const int64_t chunk = n_samples >= 64 ? std::max<int64_t>(32, ((n_samples / 8 + 31) / 32) * 32) : n_samples;
-    const int64_t n_chunks = n_samples / chunk;
-    const int64_t max_chunk = n_samples - (n_chunks - 1) * chunk;
+    // Sample chunks, chunk c's device->host copy running on a second stream while chunk c+1 is
+    // computed (three device staging buffers in turn).  The copy of the LAST chunk cannot be
+    // hidden, and a chunk of fewer samples runs the kernels less efficiently, so the call is cut
+    // into chunks of B = max(64, ~n/6) samples followed by a tail of two 32-sample chunks (every
+    // chunk >= 17 samples: the same kernel variants as the whole call, so the field is bitwise the
+    // one-call field; per-sample arithmetic does not depend on the chunking).  Config 3 (256
+    // samples): 64, 64, 64, 32, 32.  Chunk c draws samples [c0, c0 + n_c) with seed + c0, so its
+    // noise is that of the same samples in one call (key = seed + sample index, noise.cu).
+    std::vector<int64_t> sizes;
+    if (n_samples < 64) {
+        sizes.push_back(n_samples);
+    } else {
+        const int64_t B = std::max<int64_t>(64, ((n_samples / 6 + 31) / 32) * 32);
+        int64_t rem = n_samples;
+        while (rem > B + 64) {
+            sizes.push_back(B);
+            rem -= B;
+        }
+        if (rem - 64 >= 32) {
+            sizes.push_back(rem - 64);
+            sizes.push_back(32);
+            sizes.push_back(32);
+        } else if (rem - 32 >= 32) {
+            sizes.push_back(rem - 32);
+            sizes.push_back(32);
+        } else {
+            sizes.push_back(rem);
+        }
+    }
+    const int64_t n_chunks = (int64_t)sizes.size();
+    const int64_t max_chunk = *std::max_element(sizes.begin(), sizes.end());
     const size_t cbytes = (size_t)max_chunk * g->N * sizeof(double);
-    void* du[2] = {g->alloc.get(cbytes, s), n_chunks > 1 ? g->alloc.get(cbytes, s) : nullptr};
-    if (!du[0] || (n_chunks > 1 && !du[1])) {
-        if (du[0]) g->alloc.put(du[0], cbytes, s);
-        if (du[1]) g->alloc.put(du[1], cbytes, s);
-        return fail(GRF_ENOMEM, "staging buffers of 2 x %zu bytes could not be allocated", cbytes);
+    // one workspace for every chunk (stream-ordered reuse): a call that allocates its own
+    // workspace synchronises before returning it, which would stall the host between chunks
+    size_t wbytes = 0;
+    st = grf_workspace_size(g, kappa, beta, k, max_chunk, opt, &wbytes);
+    if (st) return st;
+    // NB staging buffers: a chunk never waits for the copy-out of the chunk before last
+    constexpr int NB = 3;
+    const int nbuf = (int)std::min<int64_t>(NB, n_chunks);
+    void* du[NB] = {nullptr, nullptr, nullptr};
+    bool ok = true;
+    for (int b = 0; b < nbuf; ++b) ok = ok && (du[b] = g->alloc.get(cbytes, s)) != nullptr;
+    void* wsp = ok ? g->alloc.get(wbytes, s) : nullptr;
+    if (!ok || !wsp) {
+        for (int b = 0; b < nbuf; ++b)
+            if (du[b]) g->alloc.put(du[b], cbytes, s);
+        if (wsp) g->alloc.put(wsp, wbytes, s);
+        return fail(GRF_ENOMEM, "staging buffers of %d x %zu bytes + a %zu-byte workspace could not be allocated",
+                    nbuf, cbytes, wbytes);
     }
     cudaStream_t cs = nullptr;
-    cudaEvent_t done[2] = {nullptr, nullptr}, copied[2] = {nullptr, nullptr};
+    cudaEvent_t done[NB] = {nullptr, nullptr, nullptr}, copied[NB] = {nullptr, nullptr, nullptr};
     cudaError_t ce = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
-    for (int b = 0; b < 2 && ce == cudaSuccess; ++b) {
+    for (int b = 0; b < nbuf && ce == cudaSuccess; ++b) {
         ce = cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming);
         if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming);
     }
@@ -1186,12 +1221,13 @@ grf_status grf_sample_host(grf_graph* g, double kappa, double beta, double k, ui
     double iter_sum = 0.0;
     bool enoconv = false;
     if (ce != cudaSuccess) st = fail(GRF_ECUDA, "copy stream / events: %s", cudaGetErrorString(ce));
-    for (int64_t c = 0; c < n_chunks && st == GRF_OK; ++c) {
-        const int b = (int)(c & 1);
-        const int64_t c0 = c * chunk, nc = c + 1 < n_chunks ? chunk : n_samples - c0;
-        if (c >= 2) cudaStreamWaitEvent(s, copied[b], 0);  // staging buffer b has been copied out
+    int64_t c0 = 0;
+    for (int64_t c = 0; c < n_chunks && st == GRF_OK; c0 += sizes[c], ++c) {
+        const int b = (int)(c % nbuf);
+        const int64_t nc = sizes[c];
+        if (c >= nbuf) cudaStreamWaitEvent(s, copied[b], 0);  // staging buffer b has been copied out
         grf_stats cst{};
-        grf_status sc = grf_sample(g, kappa, beta, k, seed + (uint64_t)c0, nc, opt, (double*)du[b], nullptr, 0, s,
+        grf_status sc = grf_sample(g, kappa, beta, k, seed + (uint64_t)c0, nc, opt, (double*)du[b], wsp, wbytes, s,
                                    stats ? &cst : nullptr);
         if (sc == GRF_ENOCONV) {
             enoconv = true;
@@ -1228,11 +1264,12 @@ grf_status grf_sample_host(grf_graph* g, double kappa, double beta, double k, ui
         if (ce != cudaSuccess && st == GRF_OK) st = fail(GRF_ECUDA, "device->host copy: %s", cudaGetErrorString(ce));
     }
     cudaStreamSynchronize(s);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < nbuf; ++b) {
         if (done[b]) cudaEventDestroy(done[b]);
         if (copied[b]) cudaEventDestroy(copied[b]);
         if (du[b]) g->alloc.put(du[b], cbytes, s);
     }
+    g->alloc.put(wsp, wbytes, s);
     if (cs) cudaStreamDestroy(cs);
     if (stats && st == GRF_OK) {
         tot.iter_mean = tot.n_systems > 0 ? iter_sum / (double)tot.n_systems : 0.0;
