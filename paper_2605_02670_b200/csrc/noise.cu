@@ -162,7 +162,7 @@ void launch_noise(const DevGraph& g, uint64_t seed, int64_t n_samples, double* W
     const int64_t total = n_samples * g.N;
     if (total == 0) return;
     int64_t blocks = (total + 255) / 256;
-    const int64_t cap = 148 * 16;
+    const int64_t cap = (int64_t)g.n_sm * 16;
     if (blocks > cap) blocks = cap;
     noise_kernel<<<(unsigned)blocks, 256, 0, st>>>(g.sqrt_ml, g.dof_gid, g.N, total, seed, W);
 }
@@ -171,7 +171,7 @@ void launch_noise_consistent(const DevGraph& g, const double* Ld, const double* 
                              int64_t S, double* W, double* evec, double* vtmp, cudaStream_t st) {
     const int64_t total = S * g.N;
     int64_t blocks = (total + 255) / 256;
-    if (blocks > 148 * 64) blocks = 148 * 64;
+    if (blocks > (int64_t)g.n_sm * 64) blocks = (int64_t)g.n_sm * 64;
     noise_kernel<<<(unsigned)blocks, 256, 0, st>>>(nullptr, g.dof_gid, g.N, total, seed, W);
     cnoise_edge_kernel<<<(unsigned)((S * g.E + 127) / 128), 128, 0, st>>>(g, Ld, Lo, S, W, evec);
     cnoise_vertex_kernel<<<(unsigned)((S * g.V + 127) / 128), 128, 0, st>>>(g, Ls, S, W, evec, vtmp);

@@ -443,7 +443,7 @@ bool launch_t(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgP
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, PCG_THREADS, smem);
-    const int64_t slots = 148 * (int64_t)(per_sm > 0 ? per_sm : 1);
+    const int64_t slots = (int64_t)(g.n_sm > 0 ? g.n_sm : 148) * (per_sm > 0 ? per_sm : 1);
     int64_t groups = 1, best = -1;
     for (int64_t gc = 1; gc <= maxg; gc *= 2) {
         const int64_t per_group = (batches + gc * NG - 1) / (gc * NG);
@@ -569,7 +569,7 @@ bool pcg_supported(const DevGraph& g) {
 void launch_pcg_tables(const DevGraph& g, const DevPlan& p, cudaStream_t st) {
     const int64_t n = (int64_t)p.L * g.V;
     int blocks = (int)((n + 255) / 256);
-    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks > g.n_sm * 8) blocks = g.n_sm * 8;
     pcg_tables_kernel<<<blocks, 256, 0, st>>>(g, p.L, p.cI, p.cL, p.kappa * p.kappa, p.mass, reinterpret_cast<const double4*>(p.sig), p.ops);
 }
 
@@ -577,7 +577,8 @@ void launch_assemble_rhs(const DevGraph& g, const DevPlan& p, int64_t n_samples,
                          double* rhs, cudaStream_t st) {
     const int32_t csl = sample_tile_log2(n_samples);
     const int64_t work = (int64_t)p.L * ((g.V + ASM_VB - 1) / ASM_VB);
-    int blocks = (int)(work < 148 * 8 ? work : 148 * 8);
+    const int64_t cap = (int64_t)g.n_sm * 8;
+    int blocks = (int)(work < cap ? work : cap);
     assemble_rhs_kernel<<<blocks, 256, 0, st>>>(g, p.L, p.ops, n_samples, csl, W, ends, rhs);
 }
 

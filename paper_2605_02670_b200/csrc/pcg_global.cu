@@ -591,7 +591,7 @@ void launch_pcg_tables_pos(const DevGraph& g, const DevPlan& p, cudaStream_t st)
     const int64_t n = (int64_t)p.L * g.V;
     if (n == 0) return;
     int blocks = (int)((n + 255) / 256);
-    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks > g.n_sm * 8) blocks = g.n_sm * 8;
     pcg_tables_pos_kernel<<<blocks, 256, 0, st>>>(g, p.L, reinterpret_cast<const double4*>(p.sig), p.ops_pos);
 }
 
