@@ -563,15 +563,15 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
 // values w_1 = g_0 Z, w_m = g_0 Y after a round's last block.
 namespace cond {
 constexpr int LWc = 8, SLWc = 4, NWLc = 4, NWSc = 2;
-constexpr int IBKc = 16, NSTc = 4;
+constexpr int IBKd = 28, NSTd = 3;  // steps per stage x ring depth (config 3: 16 x 4 2.04 ms, 24 x 3 2.00, 28 x 3 2.00)
 constexpr int WROWc = CS + 4;
-constexpr int WELc = IBKc * 2 * WROWc;  // [IBK][2 side][WROW]
 constexpr size_t HDRc = 512;
 }  // namespace cond
 
-template <int TL>
+template <int TL, int IBKc, int NSTc>
 __global__ void __launch_bounds__(NT, 1) sweep3c_kernel(Args A) {
     using namespace cond;
+    constexpr int WELc = IBKc * 2 * WROWc;  // [IBK][2 side][WROW]
     constexpr int RN = 32 * TL;
     constexpr int NP = TL / 2;
     constexpr bool ODD = (TL & 1) != 0;
@@ -784,20 +784,27 @@ __global__ void __launch_bounds__(NT, 1) sweep3c_kernel(Args A) {
     }
 }
 
-template <int TL>
-cudaError_t launch_c(Args a, cudaStream_t st) {
+template <int TL, int IBKc, int NSTc>
+cudaError_t launch_c_k(Args a, cudaStream_t st) {
     using namespace cond;
-    a.chunks = (int32_t)((a.S + CS - 1) / CS);
-    a.n_items = a.g.E * a.chunks;
+    constexpr int WELc = IBKc * 2 * WROWc;
     const size_t smem = HDRc + (size_t)NSTc * IBKc * 32 * TL * sizeof(double) + (size_t)NSTc * WELc * sizeof(double);
-    cudaError_t e = cudaFuncSetAttribute(sweep3c_kernel<TL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(sweep3c_kernel<TL, IBKc, NSTc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(a.counter, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return e;
     int blocks = a.g.n_sm > 0 ? a.g.n_sm : 148;
     if (blocks > a.n_items) blocks = a.n_items;
-    sweep3c_kernel<TL><<<blocks, NT, smem, st>>>(a);
+    sweep3c_kernel<TL, IBKc, NSTc><<<blocks, NT, smem, st>>>(a);
     return cudaGetLastError();
+}
+
+template <int TL>
+cudaError_t launch_c(Args a, cudaStream_t st) {
+    using namespace cond;
+    a.chunks = (int32_t)((a.S + CS - 1) / CS);
+    a.n_items = a.g.E * a.chunks;
+    return launch_c_k<TL, IBKd, NSTd>(a, st);
 }
 
 
