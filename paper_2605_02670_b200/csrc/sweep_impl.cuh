@@ -138,7 +138,8 @@ struct Cfg {
     static constexpr int CSL = CS == 32 ? 5 : (CS == 16 ? 4 : (CS == 8 ? 3 : (CS == 4 ? 2 : (CS == 2 ? 1 : 0))));
     static constexpr int NTAB = REC ? 2 : 1;        // staged tables: mu (, g)
     static constexpr int RN = NLT * TL;             // nodes per round
-    static constexpr int IBK = REC ? 8 : 32;        // steps per staging block
+    // steps per staging block; the 1-warp (1-sample) instances stage less so more CTAs fit an SM
+    static constexpr int IBK = TS == 1 ? (REC ? 8 : 16) : (REC ? 8 : 32);
     // recover with TS = 4: sample slot j of a thread is sample (j ^ sig(lane)); this makes
     // the reduce-scatter over the 8 l-lanes select-free (see reduce_store)
     static constexpr bool PERM = REC && TS == 4;
