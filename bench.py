@@ -447,6 +447,22 @@ def main():
             line["peaks"] = {"hbm_gbs": pk["hbm_gbs"], "fp64_tflops": pk["fp64_tflops"], "source": pk["source"],
                              "fp64_measured_tflops": pk["fp64_measured_tflops"],
                              "frac_of_measured_fp64": ach / pk["fp64_measured_tflops"]}
+            if n_local <= 8 and dom in ("recover", "condense"):
+                # 1-sample items: each item streams its edge's Thomas tables for all
+                # Lp nodes (mu for K3, mu and g for K5) and no other item shares them -- the sweep is
+                # bound by that HBM traffic, not by fp64
+                q0 = (L + 1 + 31) // 32
+                r_ = (q0 + 6) // 7
+                Lp = 32 * ((q0 + r_ - 1) // r_) * r_
+                ntab = 2 if dom == "recover" else 1
+                byts = (ntab * 8.0 * Lp * wg.n_interior + 16.0 * wg.n_dofs) * n_local
+                gbs = byts / (kernels[dom]["ms_per_launch"] / 1e3) / 1e9
+                line["roofline_alu"] = line["roofline"]
+                line["roofline"] = {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                                    "frac": gbs / pk["hbm_gbs"], "traffic": traffic, "kernel": dom,
+                                    "algorithmic_bytes": byts,
+                                    "note": "Thomas-table rows (8 B x Lp per interior DOF and table) + W read + u "
+                                            "write per sample; peak = MEASURED_PEAKS.json copy bandwidth"}
     # north_star's design-independent number: the per-(l,s) streaming formulation moves 32 B per
     # DOF.node; what bandwidth would it need to match this run?
     eff_hbm = 32.0 * dof_node / world / 1e9
