@@ -202,11 +202,13 @@ grf_status grf_sample(grf_graph* g, double kappa, double beta, double k, uint64_
 
 /* Same as grf_sample with HOST output u_host (n_samples x N): device staging,
  * device->host copy and a stream synchronisation happen inside the call.  For n_samples >= 64
- * the samples are computed in chunks (multiples of 32, about eight per call, the last one taking
- * the remainder) whose device->host copies overlap the next chunk's computation on an internal
- * stream; the field is bitwise the one-call field (chunk c uses seed + its first sample index,
- * the noise stream's per-sample key, and the same kernel variants).  Page-locked u_host lets the
- * copies run asynchronously. */
+ * the samples are computed in chunks -- B = max(64, ~n/6) samples each, then a tail of two
+ * 32-sample chunks (256 samples: 64 64 64 32 32), every chunk >= 17 samples -- whose
+ * device->host copies overlap the following chunks' computation on an internal stream (three
+ * device staging buffers, one shared workspace); the field is bitwise the one-call field (chunk
+ * c uses seed + its first sample index, the noise stream's per-sample key, and the same kernel
+ * variants).  Page-locked u_host lets the copies run asynchronously.  ENOMEM if the staging
+ * buffers or the workspace cannot be allocated. */
 grf_status grf_sample_host(grf_graph* g, double kappa, double beta, double k, uint64_t seed,
                            int64_t n_samples, const grf_options* opt, double* u_host,
                            void* stream, grf_stats* stats);

@@ -204,10 +204,11 @@ def test_node_range_partial_sums_add_up():
     assert _rel(parts, full).max() <= 1e-13
 
 
-@pytest.mark.parametrize("n_samples", [2, 100, 256])
+@pytest.mark.parametrize("n_samples", [2, 70, 100, 256, 257, 1000])
 def test_host_output_matches_device(n_samples):
-    # n_samples >= 64 runs grf_sample_host in overlapped chunks (32 / 32 / 36 and 8 x 32):
-    # every chunk reseeds with seed + its first sample, so the field is bitwise the one-call field
+    # n_samples >= 64 runs grf_sample_host in overlapped chunks (70: 38 / 32; 100: 36 / 32 / 32;
+    # 256: 64 x 3 / 32 / 32; 257: 64 x 3 / 33 / 32; 1000: 192 x 4 / 168 / 32 / 32): every chunk
+    # reseeds with seed + its first sample, so the field is bitwise the one-call field
     g = lattice(3, seed=8)
     G = _graph(g, 0.05)
     a = G.sample(2.0, 0.6, 0.3, seed=7, n_samples=n_samples).cpu().numpy()
