@@ -1,19 +1,22 @@
-// K5 recover + quadrature sum (PAPER.md P300-324) for sample tiles of 32 samples, warp-specialised
-// around the register tile of sweep_impl.cuh.  The arithmetic and the thread mapping of the
-// consumer warps are those of sweep_impl.cuh's recover V2 instance (8 l-warps of 4 l-lanes x 8
-// s-lanes, TL nodes x TS = 4 samples x 2 chains per thread, the correction-node interior steps, a
-// select-free 2-level shuffle reduce-scatter over the warp's l-lanes); what changes is who does
-// the rest and how they synchronise:
+// K5 recover + quadrature sum (PAPER.md P300-324) and K3 condense (P197-239) for sample tiles of
+// 32 samples, warp-specialised.  Recover (sweep3_kernel):
+//   * consumers (warps 0-7, 232 registers): 8 l-warps of CL l-lanes x 32/CL s-lanes; a thread
+//     carries TLT = 4 TL / CL nodes x CL samples x 2 chains (56 chains at TL = 7) through the
+//     correction-node interior steps; per step the partial sums over its nodes are reduced over
+//     the warp's CL l-lanes by a select-free shuffle reduce-scatter (sample slot j of a lane holds
+//     sample j ^ sig(lane): one level for CL = 2, the default; two for CL = 4, the mapping of
+//     sweep_impl.cuh's V2 instance, GRF_ABLATE bit 256) and stored per l-warp into an NPS-deep
+//     ring of partial buffers (pfull / pempty mbarriers);
 //   * warp 8 (producer) streams the coefficient rows (bulk copies) and the noise (cp.async) into
 //     an NST-deep ring of stages (full / empty mbarriers), as in sweep2_impl.cuh;
-//   * warps 0-7 (consumers, 232 registers) only run the chains and store each step's per-l-warp
-//     partial sums into an NPS-deep ring of partial buffers (pfull / pempty mbarriers);
 //   * warps 9-11 (fold warps) add the 8 l-warp partials of every block in fixed order into the
 //     item's output tile [CS][m|1] (or into u for edges too long for it) and write the tile out
-//     at the item's end.
+//     at the item's end; the ring depths give way to the tile (launch).
 // No block-wide barrier anywhere after the prologue: the consumers wait only for staged data
 // and for a free partial buffer, the fold warps for complete partials.  Results are bitwise
-// those of the sweep_impl.cuh instance (same per-thread arithmetic, same fold order).
+// reproducible (fixed shuffle and fold orders).  Condense (sweep3c_kernel, further below):
+// chains only, the producer warpgroup streams the stages, every consumer writes its own end
+// values.
 #pragma once
 
 #include "sweep2_impl.cuh"
