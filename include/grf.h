@@ -207,7 +207,11 @@ grf_status grf_sample(grf_graph* g, double kappa, double beta, double k, uint64_
  * device->host copies overlap the following chunks' computation on an internal stream (three
  * device staging buffers, one shared workspace); the field is bitwise the one-call field (chunk
  * c uses seed + its first sample index, the noise stream's per-sample key, and the same kernel
- * variants).  Page-locked u_host lets the copies run asynchronously.  ENOMEM if the staging
+ * variants).  Page-locked u_host lets the copies run asynchronously; when it is also mapped into
+ * the device (cudaHostAlloc / pinned memory under unified addressing) and the call has one or two
+ * chunks, the last chunk's kernels write their result straight into u_host over PCIe (no staging,
+ * no copy after them) -- unless an edge is too long for the recovery's output tile, whose values
+ * are accumulated in u by read-modify-write and so stay on the device.  ENOMEM if the staging
  * buffers or the workspace cannot be allocated. */
 grf_status grf_sample_host(grf_graph* g, double kappa, double beta, double k, uint64_t seed,
                            int64_t n_samples, const grf_options* opt, double* u_host,

@@ -1191,6 +1191,32 @@ grf_status grf_sample_host(grf_graph* g, double kappa, double beta, double k, ui
     const int64_t n_chunks = (int64_t)sizes.size();
     const int64_t max_chunk = *std::max_element(sizes.begin(), sizes.end());
     const size_t cbytes = (size_t)max_chunk * g->N * sizeof(double);
+    // The last chunk writes straight into u_host when that is page-locked memory mapped into the
+    // device (cudaHostAlloc / torch pin_memory under unified addressing) and its recovery writes
+    // every output value exactly once by plain stores: its kernels then stream the result over
+    // PCIe while they run, instead of a device->host copy after them (the copy nothing can hide).
+    // Only for calls of one or two chunks: with more, the copy of the chunk before still holds the
+    // link while the last chunk's kernels store over it (measured: config 5, two chunks, 24.6 ->
+    // 20.6 ms; config 4, one chunk, 605 -> 554 ms; config 3, five chunks, 12.37 -> 12.49 ms).
+    // Design-study switch: env GRF_HOST_ZC (0 off, 2 for any chunk count).
+    double* u_mapped = nullptr;
+    {
+        static const int zc_env = [] {
+            const char* e = getenv("GRF_HOST_ZC");
+            return e ? atoi(e) : 1;
+        }();
+        cudaPointerAttributes pa{};
+        if (zc_env && (n_chunks <= 2 || zc_env == 2) && cudaPointerGetAttributes(&pa, u_host) == cudaSuccess &&
+            pa.type == cudaMemoryTypeHost &&
+            pa.devicePointer != nullptr) {
+            Plan* pl = nullptr;
+            if (get_plan(g, kappa, beta, k, opt, s, &pl) == GRF_OK &&
+                grf::recover_out_write_only(g->dev, pl->dev, sizes.back()))
+                u_mapped = static_cast<double*>(pa.devicePointer);
+        }
+        cudaGetLastError();  // clear the (non-sticky) error a pointer query may leave behind
+    }
+    const int64_t n_copied = n_chunks - (u_mapped ? 1 : 0);  // chunks that go through staging
     // one workspace for every chunk (stream-ordered reuse): a call that allocates its own
     // workspace synchronises before returning it, which would stall the host between chunks
     size_t wbytes = 0;
@@ -1198,7 +1224,7 @@ grf_status grf_sample_host(grf_graph* g, double kappa, double beta, double k, ui
     if (st) return st;
     // NB staging buffers: a chunk never waits for the copy-out of the chunk before last
     constexpr int NB = 3;
-    const int nbuf = (int)std::min<int64_t>(NB, n_chunks);
+    const int nbuf = (int)std::min<int64_t>(NB, n_copied);
     void* du[NB] = {nullptr, nullptr, nullptr};
     bool ok = true;
     for (int b = 0; b < nbuf; ++b) ok = ok && (du[b] = g->alloc.get(cbytes, s)) != nullptr;
@@ -1223,11 +1249,13 @@ grf_status grf_sample_host(grf_graph* g, double kappa, double beta, double k, ui
     if (ce != cudaSuccess) st = fail(GRF_ECUDA, "copy stream / events: %s", cudaGetErrorString(ce));
     int64_t c0 = 0;
     for (int64_t c = 0; c < n_chunks && st == GRF_OK; c0 += sizes[c], ++c) {
-        const int b = (int)(c % nbuf);
+        const bool direct = u_mapped != nullptr && c == n_chunks - 1;  // written in place, no copy
+        const int b = direct ? 0 : (int)(c % nbuf);
         const int64_t nc = sizes[c];
-        if (c >= nbuf) cudaStreamWaitEvent(s, copied[b], 0);  // staging buffer b has been copied out
+        if (!direct && c >= nbuf) cudaStreamWaitEvent(s, copied[b], 0);  // staging buffer b has been copied out
         grf_stats cst{};
-        grf_status sc = grf_sample(g, kappa, beta, k, seed + (uint64_t)c0, nc, opt, (double*)du[b], wsp, wbytes, s,
+        grf_status sc = grf_sample(g, kappa, beta, k, seed + (uint64_t)c0, nc, opt,
+                                   direct ? u_mapped + c0 * g->N : (double*)du[b], wsp, wbytes, s,
                                    stats ? &cst : nullptr);
         if (sc == GRF_ENOCONV) {
             enoconv = true;
@@ -1235,12 +1263,14 @@ grf_status grf_sample_host(grf_graph* g, double kappa, double beta, double k, ui
             st = sc;
             break;
         }
-        ce = cudaEventRecord(done[b], s);
-        if (ce == cudaSuccess) ce = cudaStreamWaitEvent(cs, done[b], 0);
-        if (ce == cudaSuccess)
-            ce = cudaMemcpyAsync(u_host + c0 * g->N, du[b], (size_t)nc * g->N * sizeof(double), cudaMemcpyDeviceToHost,
-                                 cs);
-        if (ce == cudaSuccess) ce = cudaEventRecord(copied[b], cs);
+        if (!direct) {
+            ce = cudaEventRecord(done[b], s);
+            if (ce == cudaSuccess) ce = cudaStreamWaitEvent(cs, done[b], 0);
+            if (ce == cudaSuccess)
+                ce = cudaMemcpyAsync(u_host + c0 * g->N, du[b], (size_t)nc * g->N * sizeof(double),
+                                     cudaMemcpyDeviceToHost, cs);
+            if (ce == cudaSuccess) ce = cudaEventRecord(copied[b], cs);
+        }
         if (ce != cudaSuccess) st = fail(GRF_ECUDA, "device->host copy: %s", cudaGetErrorString(ce));
         if (stats) {
             if (c == 0) {

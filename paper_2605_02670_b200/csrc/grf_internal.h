@@ -145,6 +145,10 @@ size_t pcg_global_ws_bytes(const DevGraph& g, int32_t L, int64_t n_samples);
 // K5  Thomas recovery + accumulation over nodes (sweep.cu): u[s*N + dof] from W and u_G
 cudaError_t launch_recover(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W, double* u,
                            const double* uG, int32_t* counter, cudaStream_t st);
+// true when K5 + K5b write every output value exactly once by plain stores (no read-modify-write
+// of u: every edge fits the recovery's shared-memory output tile), so u may be page-locked host
+// memory mapped into the device (grf_sample_host's last chunk)
+bool recover_out_write_only(const DevGraph& g, const DevPlan& p, int64_t n_samples);
 // K5b vertex values u_v = sum_l u_G^{(l)}(v) (sweep.cu)
 cudaError_t launch_vertex_sum(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* uG, double* u,
                               cudaStream_t st);

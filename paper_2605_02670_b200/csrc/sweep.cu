@@ -83,6 +83,20 @@ cudaError_t launch_condense(const DevGraph& g, const DevPlan& p, int64_t n_sampl
     }
 }
 
+bool recover_out_write_only(const DevGraph& g, const DevPlan& p, int64_t n_samples) {
+    sweep::Args a = make_args(g, p, n_samples, nullptr, nullptr, nullptr, nullptr);
+    if (a.ablate) return false;
+    int32_t fits = 0;
+    a.fits_out = &fits;
+    cudaError_t e = cudaSuccess;
+    switch (sweep::variant_for(n_samples)) {
+        case sweep::V2: e = sweep3::launch_r32(p.TL, a, nullptr); break;
+        case sweep::V1: e = sweep::launch_r1k(p.TL, a, nullptr); break;
+        default: e = sweep::launch_r0k(p.TL, a, nullptr); break;
+    }
+    return e == cudaSuccess && fits != 0;
+}
+
 cudaError_t launch_recover(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W, double* u,
                            const double* uG, int32_t* counter, cudaStream_t st) {
     const sweep::Args a = make_args(g, p, n_samples, W, u, uG, counter);

@@ -843,6 +843,10 @@ cudaError_t launch(Args a, cudaStream_t st) {
     const int fit = fit_for(a.nst, a.nps);
     a.tile_ms = want <= fit ? want : (fit >= 1 ? ((fit - 1) | 1) : 0);
     smem += (size_t)CS * a.tile_ms * sizeof(double);
+    if (a.fits_out) {  // query only (no launch): every edge's output leaves by plain tile stores
+        *a.fits_out = a.tile_ms >= want;
+        return cudaSuccess;
+    }
     // the ring depth is a template constant (the stage offsets fold into the addressing)
     // consumer mapping CL = 2 l-lanes per warp (one reduce-scatter level) unless GRF_ABLATE bit 256
     const bool cl4 = (a.ablate & 256) != 0;

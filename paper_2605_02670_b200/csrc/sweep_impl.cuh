@@ -72,6 +72,7 @@ struct Args {
     int32_t tile_ms;        // recover: max (m | 1) the shared-memory output tile holds (0: none)
     int32_t nk;             // recover: 1 if slot L is the correction node (edge_setup.cu; L < Lp)
     int32_t nst, nps;       // sweep3 recover: data / partial ring depths in use (set by its launch)
+    int32_t* fits_out;      // recover, host-side query (no launch): 1 if every edge fits the output tile
     int32_t ablate;         // design studies only (env GRF_ABLATE, default 0), wrong results by construction:
                             // sweep2 bits 1 no output reduction, 2 no u_G loads, 4 no data waits; sweep3
                             // bits 32 no partial stores, 64 no u_G loads; kernel choice bits 8, 16, 128 (sweep.cu)
@@ -727,6 +728,10 @@ cudaError_t launch(Args a, cudaStream_t st) {
         const int fit = (int)(room / ((size_t)C::CS * sizeof(double)));
         a.tile_ms = want <= fit ? want : (fit >= 1 ? ((fit - 1) | 1) : 0);
         smem += (size_t)C::CS * a.tile_ms * sizeof(double);
+        if (a.fits_out) {  // query only: does the output leave the kernel by plain tile stores?
+            *a.fits_out = a.tile_ms >= want;
+            return cudaSuccess;
+        }
     }
     cudaError_t e = cudaFuncSetAttribute(sweep_kernel<TL, TS, LW, NWS, REC, NK>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

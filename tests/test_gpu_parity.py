@@ -218,6 +218,32 @@ def test_host_output_matches_device(n_samples):
     assert st["worst_rel_residual"] <= 1e-13
 
 
+@pytest.mark.parametrize("n_samples", [2, 70, 256])
+def test_pinned_host_output_matches_device(n_samples):
+    # a page-locked buffer is mapped into the device: grf_sample_host's last chunk (all of it below
+    # 64 samples) is written by the recovery kernels straight into it, the earlier chunks through
+    # the staged copies -- bitwise the one-call device field either way
+    g = lattice(3, seed=8)
+    G = _graph(g, 0.05)
+    a = G.sample(2.0, 0.6, 0.3, seed=7, n_samples=n_samples).cpu().numpy()
+    host = torch.full((n_samples, G.n_dofs), float("nan"), dtype=torch.float64, pin_memory=True)
+    G.sample_into_host(2.0, 0.6, 0.3, 7, n_samples, host)
+    assert np.array_equal(_bits(a), _bits(host.numpy()))
+
+
+@pytest.mark.parametrize("n_samples", [20, 70])
+def test_pinned_host_output_long_edges(n_samples):
+    # edges longer than the recovery's output tile are folded into u by read-modify-write, which
+    # must not run over PCIe: such a last chunk goes through the staged copy (same field)
+    g = MetricGraph(5, np.array([0, 1, 2, 0, 3, 3, 2]), np.array([1, 2, 3, 2, 4, 4, 2]),
+                    np.array([6.0, 4.5, 1.505, 0.3, 0.02, 0.9, 0.6]))
+    G = _graph(g, 0.005)
+    a = G.sample(2.0, 0.7, 0.35, seed=6, n_samples=n_samples).cpu().numpy()
+    host = torch.full((n_samples, G.n_dofs), float("nan"), dtype=torch.float64, pin_memory=True)
+    G.sample_into_host(2.0, 0.7, 0.35, 6, n_samples, host)
+    assert np.array_equal(_bits(a), _bits(host.numpy()))
+
+
 def test_nonfinite_output_is_reported():
     """An infinite right-hand side (grf_apply) gives non-finite fields: the exit check reports them
     (GRF_ENOCONV with statistics) instead of returning silently."""
