@@ -1188,6 +1188,23 @@ grf_status grf_sample_host(grf_graph* g, double kappa, double beta, double k, ui
             sizes.push_back(rem);
         }
     }
+    {  // design study: env GRF_HOST_CHUNKS = comma-separated chunk sizes summing to n_samples
+        const char* e = getenv("GRF_HOST_CHUNKS");
+        if (e && *e) {
+            std::vector<int64_t> v;
+            int64_t sum = 0;
+            for (const char* q = e; *q;) {
+                char* end = nullptr;
+                const long long x = strtoll(q, &end, 10);
+                if (end == q || x <= 0) break;
+                v.push_back(x);
+                sum += x;
+                q = *end == ',' ? end + 1 : end;
+                if (*end != ',') break;
+            }
+            if (sum == n_samples) sizes = v;
+        }
+    }
     const int64_t n_chunks = (int64_t)sizes.size();
     const int64_t max_chunk = *std::max_element(sizes.begin(), sizes.end());
     const size_t cbytes = (size_t)max_chunk * g->N * sizeof(double);
