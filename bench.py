@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--edgepart", action="store_true", help="config 4: edge-partitioned over the ranks")
     ap.add_argument("--no-graph", action="store_true", help="do not replay small configs as a CUDA graph")
     ap.add_argument("--impl", default="grf", choices=["grf", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-nodes", type=int, default=12, help="oracle sample: quadrature nodes of 1 sample")
@@ -381,16 +381,21 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
+        marks = []
         for _ in range(args.e2e_steps):
-            e2e_step()
+            e2e_step()  # returns after the result is in host memory (the call synchronises)
+            marks.append(time.perf_counter())
         torch.cuda.synchronize()
         te = time.perf_counter() - t0
+        per_step = [1e3 * (b - a) for a, b in zip([t0] + marks[:-1], marks)]
         if world > 1:
             t = torch.tensor([te], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
         e2e = {"value": S * args.e2e_steps / te, "unit": "samples/s", "h2d_bytes_per_step": 0,
                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * te / args.e2e_steps,
+               "step_ms": {"min": min(per_step), "median": sorted(per_step)[len(per_step) // 2],
+                           "max": max(per_step)},
                "note": "the public call with the result copied to pinned host memory inside the timed region "
                        "(grf_sample_host / grf_sample_dist / grf_sample_edgepart + copy); per-step inputs are the "
                        "scalars (kappa, beta, k, seed) -- the noise is generated on the device from the seed"}
