@@ -427,11 +427,13 @@ def main():
         "config": config_dict(args.config, cfg, g, L, n_dofs, world, mode),
         "dof_node_per_s": dof_node,
     }
-    line["config"]["cuda_graph"] = graph_replay is not None
+    # how the step ran (kept out of `config`, which names the workload only and is the same dict
+    # in the reference arm's line)
+    line["run"] = {"cuda_graph": graph_replay is not None}
     if graph_replay is not None:
         line["kernels_timed"] = ("per-kernel times (kernels, roofline) from as many eager calls right after the "
                                  "timed graph replays; share = their time / the replays' time")
-    line["config"].update(info)
+    line["run"].update(info)
     if kernels:
         dom = max((k_ for k_ in kernels if k_ != "noise"), key=lambda k_: kernels[k_]["share"], default=None)
         if dom is not None:
