@@ -22,6 +22,10 @@ __host__ __device__ inline int64_t table_stride(int V, int W) { return 3 * (int6
 // warp-per-system form (__syncwarp only); WPS = 2 halves the registers per thread, so twice the
 // warps are resident for the same shared memory (latency hiding of the neighbour loads).
 constexpr int WARP_NW = 8;  // systems per CTA (an octet)
+// shared-memory stride of one system's r, p: 2V + 1 doubles (odd), so the octet's 8 values of a
+// vertex lie in 8 different banks when u_G is written out sample-fastest (an even stride put
+// them all in one bank: an 8-way conflict, 6 % of the kernel's shared-memory wavefronts)
+__host__ __device__ inline int sys_stride(int V) { return 2 * V + 1; }
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -65,7 +69,7 @@ __global__ void __launch_bounds__(WARP_NW * WPS * 32) pcg_warp_kernel(DevGraph g
     const double* OS = DJ + V;
     const double* OM = OS + (size_t)W * V;
     const int* eo = g.ell_other;
-    double* r = sm + (size_t)warp * 2 * V;
+    double* r = sm + (size_t)warp * sys_stride(V);
     double* p = r + V;
     // packed staging (W = 4): per vertex the 4 neighbour indices as one ushort4 (V <= 1024) and
     // the 4 slot coefficients of each operator as two double2: a vertex's operator row is one
@@ -74,7 +78,7 @@ __global__ void __launch_bounds__(WARP_NW * WPS * 32) pcg_warp_kernel(DevGraph g
     const ushort4* nb4 = nullptr;
     const double2 *os01 = nullptr, *os23 = nullptr, *om01 = nullptr, *om23 = nullptr;
     if (STAGE) {  // DS, DM, OS, OM and the neighbour indices of node l, once per CTA
-        double* st = sm + (size_t)WARP_NW * 2 * V;
+        double* st = sm + (size_t)((WARP_NW * sys_stride(V) + 1) & ~1);  // 16-byte aligned
         if (PACK) {
             double* sD = st;                                          // DS [V], DM [V]
             double2* sO = reinterpret_cast<double2*>(st + 2 * V);     // OS01, OS23, OM01, OM23: [V] each
@@ -297,14 +301,14 @@ __global__ void __launch_bounds__(WARP_NW * WPS * 32) pcg_warp_kernel(DevGraph g
         // as 64-byte runs (vertex-major, sample fastest) instead of 8-byte scatters
         for (int i = threadIdx.x; i < V * WARP_NW; i += NT) {
             const int v = i / WARP_NW, w = i % WARP_NW;
-            if (s0 + w < S) uG[ug_index(s0 + w, v, l, L, V, csl)] = sm[(size_t)w * 2 * V + v];
+            if (s0 + w < S) uG[ug_index(s0 + w, v, l, L, V, csl)] = sm[(size_t)w * sys_stride(V) + v];
         }
         __syncthreads();  // r / p are rewritten by the next octet
     }
 }
 
 size_t warp_smem_bytes(const DevGraph& g, int W, bool stage) {
-    size_t b = sizeof(double) * (size_t)WARP_NW * 2 * g.V;
+    size_t b = sizeof(double) * (size_t)((WARP_NW * sys_stride(g.V) + 1) & ~1);
     if (stage) b += sizeof(double) * (size_t)(2 + 2 * W) * g.V + sizeof(int) * (size_t)W * g.V;
     return b;
 }
