@@ -771,16 +771,27 @@ __global__ void __launch_bounds__(NT, 1) sweep3c_kernel(Args A) {
                 }
                 release();
             }
-            // w_1 = g_0 Z (right sweep end, position 0), w_m = g_0 Y (left sweep end); g_0 = g_{m-1}
+            // w_1 = g_0 Z (right sweep end, position 0), w_m = g_0 Y (left sweep end); g_0 = g_{m-1}.
+            // The products go into the (now dead) chain registers and are stored from there: fresh
+            // product registers were allocated over the sources of the previous node's stores, and
+            // every product then waited for those stores to release them
+#pragma unroll
+            for (int n = 0; n < TL; ++n) {
+#pragma unroll
+                for (int j = 0; j < TS; ++j) {
+                    Z[n][j] *= g0[n];
+                    Y[n][j] *= g0[n];
+                }
+            }
 #pragma unroll
             for (int n = 0; n < TL; ++n) {
                 const int l = rb + slot(n);
                 if (l < L) {
                     double* o = A.out + ((tile * L + l) * 2 * (int64_t)g.E + 2 * e) * CS + st0;
-                    *reinterpret_cast<double2*>(o) = make_double2(g0[n] * Z[n][0], g0[n] * Z[n][1]);
-                    *reinterpret_cast<double2*>(o + 2) = make_double2(g0[n] * Z[n][2], g0[n] * Z[n][3]);
-                    *reinterpret_cast<double2*>(o + CS) = make_double2(g0[n] * Y[n][0], g0[n] * Y[n][1]);
-                    *reinterpret_cast<double2*>(o + CS + 2) = make_double2(g0[n] * Y[n][2], g0[n] * Y[n][3]);
+                    *reinterpret_cast<double2*>(o) = make_double2(Z[n][0], Z[n][1]);
+                    *reinterpret_cast<double2*>(o + 2) = make_double2(Z[n][2], Z[n][3]);
+                    *reinterpret_cast<double2*>(o + CS) = make_double2(Y[n][0], Y[n][1]);
+                    *reinterpret_cast<double2*>(o + CS + 2) = make_double2(Y[n][2], Y[n][3]);
                 }
             }
         }
