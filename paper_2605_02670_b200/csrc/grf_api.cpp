@@ -18,6 +18,8 @@
 #include <tuple>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "grf_internal.h"
 
 namespace {
@@ -138,6 +140,13 @@ struct grf_graph {
     // run `launch` (enqueues one kernel on st), bracketed by events when profiling
     template <class F>
     cudaError_t timed(int kind, cudaStream_t st, F&& launch) {
+        // NVTX range per phase (header-only NVTX v3: a no-op unless a tool such as nsys is attached)
+        static const char* const names[GRF_K_COUNT] = {"grf:noise", "grf:edge_setup", "grf:condense", "grf:pcg",
+                                                       "grf:recover"};
+        struct Range {
+            explicit Range(const char* n) { nvtxRangePushA(n); }
+            ~Range() { nvtxRangePop(); }
+        } range(kind >= 0 && kind < GRF_K_COUNT ? names[kind] : "grf");
         if (!prof) {
             launch();
             return cudaGetLastError();
