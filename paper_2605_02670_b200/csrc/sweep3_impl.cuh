@@ -503,6 +503,31 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
                 }
                 const int tend = last_here ? nb - 1 : nb;
                 double pL[TSC], pR[TSC];
+                if (TL <= 6 && t0 > 0 && !last_here && nb == IBK) {
+                    // a full interior block (most blocks): the same step sequence as below, written
+                    // straight-line so the next step's shared-memory loads can be scheduled under
+                    // the current step's FMAs.  Only for TL <= 6: with the TL = 7 register tile the
+                    // longer live ranges cost more than they hide (measured: config 5, TL = 6, K5
+                    // 11.6 -> 11.0 ms; config 3, TL = 7, 5.69 -> 6.14 ms)
+                    double aL[TSC], aR[TSC];
+                    body_mid(0, pL, pR);
+#pragma unroll
+                    for (int u = 1; u + 1 < IBK; u += 2) {
+                        body_mid(u, aL, aR);
+                        reduce_store(pL, pR, u - 1);
+                        body_mid(u + 1, pL, pR);
+                        reduce_store(aL, aR, u);
+                    }
+                    body_mid(IBK - 1, aL, aR);
+                    reduce_store(pL, pR, IBK - 2);
+                    reduce_store(aL, aR, IBK - 1);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&pfull[ps]);
+                    puse ^= 1u << ps;
+                    ps = ps + 1 == nps ? 0 : ps + 1;
+                    release();
+                    continue;
+                }
                 bool pend = false;
                 int tt = 0;
                 if (t0 == 0) {
