@@ -116,16 +116,16 @@ def test_edgepart_equals_whole_graph_rgg():
 def test_edgepart_nccl_one_rank():
     """The NCCL code path (grf_comm) with a one-rank communicator."""
     import os
-    import socket
+    import tempfile
 
     import torch.distributed as dist
 
     from paper_2605_02670_b200 import Comm
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        port = s.getsockname()[1]
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=0, world_size=1)
+    # a file rendezvous: no TCP port to collide with the previous test's store (EADDRINUSE)
+    fd, path = tempfile.mkstemp(prefix="grf_pg_")
+    os.close(fd)
+    os.unlink(path)
+    dist.init_process_group("gloo", init_method=f"file://{path}", rank=0, world_size=1)
     try:
         comm = Comm()
         g = lattice(4, seed=3)
@@ -160,17 +160,17 @@ def test_config4_edge_partitioned_two_parts():
 def test_sample_dist_one_rank():
     """grf_sample_dist (sample-then-node sharding in the library) with a one-rank communicator."""
     import os
-    import socket
+    import tempfile
 
     import torch.distributed as dist
 
     from paper_2605_02670_b200 import Comm
     from paper_2605_02670_b200.grf import sample_dist
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        port = s.getsockname()[1]
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=0, world_size=1)
+    # a file rendezvous: no TCP port to collide with the previous test's store (EADDRINUSE)
+    fd, path = tempfile.mkstemp(prefix="grf_pg_")
+    os.close(fd)
+    os.unlink(path)
+    dist.init_process_group("gloo", init_method=f"file://{path}", rank=0, world_size=1)
     try:
         comm = Comm()
         G = Graph.from_metric_graph(lattice(4, seed=3), 0.05)
