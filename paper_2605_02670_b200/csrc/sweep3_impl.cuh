@@ -45,6 +45,8 @@ constexpr int CSL = 5;
 constexpr int NT = (NCW + 4) * 32;
 constexpr int IBK = 8;       // steps per stage
 constexpr int NST = 3;       // data ring depth (max; A.nst in use, see launch)
+constexpr bool K5_GLATE = true;   // g rows loaded after the chain updates (config 3 K5 5.69 -> 5.66 ms)
+constexpr int K5_SLMAX = 6;       // straight-line full blocks for TL <= K5_SLMAX
 constexpr int NPS = 2;       // partial ring depth (max; A.nps in use: 1 when that lets the output tile fit)
 constexpr int NC = 2;        // noise copies: natural, pair-swapped
 constexpr int WROW = CS + 4; // skewed noise row
@@ -385,7 +387,7 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
 #pragma unroll
                     for (int q = 0; q < NPT; ++q) {
                         const double2 m2 = *reinterpret_cast<const double2*>(rmu + 2 * lt + 2 * NLT * q);
-                        g2s[q] = *reinterpret_cast<const double2*>(rga + 2 * lt + 2 * NLT * q);
+                        if (!K5_GLATE) g2s[q] = *reinterpret_cast<const double2*>(rga + 2 * lt + 2 * NLT * q);
 #pragma unroll
                         for (int j = 0; j < TSC; ++j) {
                             Y[2 * q][j] = fma(-m2.x, Y[2 * q][j], wl[j]);
@@ -393,6 +395,10 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
                             Y[2 * q + 1][j] = fma(-m2.y, Y[2 * q + 1][j], wl[j]);
                             Z[2 * q + 1][j] = fma(-m2.y, Z[2 * q + 1][j], wr[j]);
                         }
+                    }
+                    if (K5_GLATE) {
+#pragma unroll
+                        for (int q = 0; q < NPT; ++q) g2s[q] = *reinterpret_cast<const double2*>(rga + 2 * lt + 2 * NLT * q);
                     }
                     double go = 0.0;
                     if (ODDT) {
@@ -503,7 +509,7 @@ __global__ void __launch_bounds__(NT, 1) sweep3_kernel(Args A) {
                 }
                 const int tend = last_here ? nb - 1 : nb;
                 double pL[TSC], pR[TSC];
-                if (TL <= 6 && t0 > 0 && !last_here && nb == IBK) {
+                if (TL <= K5_SLMAX && t0 > 0 && !last_here && nb == IBK) {
                     // a full interior block (most blocks): the same step sequence as below, written
                     // straight-line so the next step's shared-memory loads can be scheduled under
                     // the current step's FMAs.  Only for TL <= 6: with the TL = 7 register tile the
