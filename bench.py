@@ -451,6 +451,17 @@ def main():
                                 "frac": ach / pk["fp64_tflops"], "traffic": traffic, "kernel": dom,
                                 "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x sm_max_mhz "
                                                "(B200_PROFILING.md clocks)"}
+            if dom in ("recover", "condense"):
+                # what the fp64 pipe actually executes: 4 (K5) / 2 (K3) FMA per interior DOF, node slot
+                # and sample over the padded node rows Lp (the correction node and the padding slots
+                # included) -- the pipe efficiency, beside the algorithmic-work fraction above
+                q0 = (L + 1 + 31) // 32
+                r_ = (q0 + 6) // 7
+                Lp = 32 * ((q0 + r_ - 1) // r_) * r_
+                fma_per = 4.0 if dom == "recover" else 2.0
+                ex = 2.0 * fma_per * wg.n_interior * Lp * n_local / (kernels[dom]["ms_per_launch"] / 1e3) / 1e12
+                line["roofline"]["executed"] = {"tflops": ex, "frac": ex / pk["fp64_tflops"], "node_rows": Lp,
+                                                "flop_per_dof_node_sample": 2.0 * fma_per}
             line["peaks"] = {"hbm_gbs": pk["hbm_gbs"], "fp64_tflops": pk["fp64_tflops"], "source": pk["source"],
                              "fp64_measured_tflops": pk["fp64_measured_tflops"],
                              "frac_of_measured_fp64": ach / pk["fp64_measured_tflops"]}
