@@ -59,7 +59,10 @@ __device__ __forceinline__ double ln_fixed(double x) {
 
 // cos(2 pi u), u in [0,1) a multiple of 2^-53: t = 4u, q = floor(t + 1/2), f = t - q (exact),
 // theta = f pi/2 in [-pi/4, pi/4]; cos/sin by Taylor (10 Horner steps, constants 1.0/(n(n-1))).
-__device__ __forceinline__ double cos2pi_fixed(double u) {
+// Horner constants of the two series, k[odd][j - 1] = 1/((2j+1) 2j) (sine) or 1/(2j (2j-1)) (cosine),
+// as a per-CTA shared table: a lane reads its quadrant's constant with one load instead of
+// materialising both 64-bit immediates and selecting (the same constant values, so the same bits)
+__device__ __forceinline__ double cos2pi_fixed(double u, const double (*ktab)[10]) {
     const double HALF_PI = 1.5707963267948966;
     const double t = __dmul_rn(4.0, u);
     const double q = floor(__dadd_rn(t, 0.5));
@@ -71,9 +74,10 @@ __device__ __forceinline__ double cos2pi_fixed(double u) {
     const int qi = ((int)q) & 3;
     const bool odd = qi & 1;
     double p = 1.0;
+    const double* kq = ktab[odd ? 1 : 0];
 #pragma unroll
     for (int j = 10; j >= 1; --j) {
-        const double k = odd ? 1.0 / (double)((2 * j + 1) * (2 * j)) : 1.0 / (double)((2 * j) * (2 * j - 1));
+        const double k = kq[j - 1];
         p = __dsub_rn(1.0, __dmul_rn(__dmul_rn(th2, k), p));
     }
     const double v = odd ? __dmul_rn(th, p) : p;
@@ -83,6 +87,12 @@ __device__ __forceinline__ double cos2pi_fixed(double u) {
 __global__ void __launch_bounds__(256) noise_kernel(const double* __restrict__ sqrt_ml,
                                                     const int64_t* __restrict__ dof_gid, int64_t N,
                                                     int64_t total, uint64_t seed, double* __restrict__ W) {
+    __shared__ double ktab[2][10];
+    if (threadIdx.x < 20) {
+        const int odd = threadIdx.x / 10, j = threadIdx.x % 10 + 1;
+        ktab[odd][j - 1] = odd ? 1.0 / (double)((2 * j + 1) * (2 * j)) : 1.0 / (double)((2 * j) * (2 * j - 1));
+    }
+    __syncthreads();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int64_t s = t / N, i = t - s * N;  // (sample, dof) of t, advanced without a 64-bit division
@@ -97,7 +107,7 @@ __global__ void __launch_bounds__(256) noise_kernel(const double* __restrict__ s
         const double u1 = __dmul_rn((double)(A + 1ull), 0x1.0p-53);
         const double u2 = __dmul_rn((double)B, 0x1.0p-53);
         const double r = __dsqrt_rn(__dmul_rn(-2.0, ln_fixed(u1)));
-        const double z = __dmul_rn(r, cos2pi_fixed(u2));
+        const double z = __dmul_rn(r, cos2pi_fixed(u2, ktab));
         W[t] = sqrt_ml ? __dmul_rn(sqrt_ml[i], z) : z;  // sqrt_ml == nullptr: the raw normals xi
         s += ds;
         i += di;
