@@ -41,8 +41,11 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
 __device__ __forceinline__ double ln_fixed(double x) {
     const double LN2 = 0.6931471805599453;
     const double SQRT_HALF = 0.7071067811865476;
-    int e;
-    double m = frexp(x, &e);
+    // frexp for the normal x this sees (u1 >= 2^-53): the exponent field and the mantissa with
+    // exponent -1, exactly frexp's (m in [1/2, 1)) without its zero / subnormal / inf checks
+    const unsigned long long xb = (unsigned long long)__double_as_longlong(x);
+    int e = (int)((xb >> 52) & 0x7ffu) - 1022;
+    double m = __longlong_as_double((long long)((xb & 0x800fffffffffffffull) | 0x3fe0000000000000ull));
     if (m < SQRT_HALF) {
         m = __dmul_rn(m, 2.0);
         e -= 1;
