@@ -456,10 +456,8 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
         if (ph[i]) cudaEventRecord(ph[i], st);
     };
     mark(0);
-    // kernels this call launches: [noise] condense, assemble, K4 (one per sample tile for the
-    // global-memory variant), recover, vertex sum
-    const int64_t cs = (int64_t)1 << grf::sample_tile_log2(S);
-    int64_t launches = 5 + (use_global_pcg(g, opt) ? (S + cs - 1) / cs - 1 : 0);
+    // kernels this call launches: [noise] condense, K4 (+ assemble, see launch_pcg), recover, vertex sum
+    int64_t launches = 3;
     if (gen) {
         double* Wd = reinterpret_cast<double*>(base + w.w);
         cudaError_t ne = g->timed(GRF_K_NOISE, st, [&] {
@@ -499,7 +497,8 @@ grf_status solve(grf_graph* g, Plan* p, int64_t S, const grf_options* opt, const
     mark(2);
     if (ce == cudaSuccess)
         ce = g->timed(GRF_K_PCG, st, [&] {
-            le = grf::launch_pcg(g->dev, p->dev, S, prm, W, ends, rhs, uG, iters, relres, gws, st);
+            le = grf::launch_pcg(g->dev, p->dev, S, prm, W, ends, rhs, uG, iters, relres, gws, st, stats != nullptr,
+                                 &launches);
         });
     if (ce == cudaSuccess) ce = le;
     mark(3);

@@ -122,11 +122,12 @@ void launch_edge_setup(const DevGraph& g, DevPlan& p, cudaStream_t st);
 cudaError_t launch_condense(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W,
                             double* ends, int32_t* counter, cudaStream_t st);
 // K4  batched NN-PCG on the vertex Schur systems (pcg.cu): g from (W, ends), u_G -> uG[(s*V + v)*L + l]
-// (K4a first assembles g = W_G + sum (c_L/h_e) w_end from the end values into rhs)
+// (K4a first assembles g = W_G + sum (c_L/h_e) w_end from the end values into rhs; the warp
+// kernel does that itself and writes rhs only if need_rhs, i.e. for the exit checks)
 // (gws: workspace of the global-memory variant, pcg_global_ws_bytes; used when V > 4096)
 cudaError_t launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* W,
                        const double* ends, double* rhs, double* uG, int32_t* iters, double* relres, void* gws,
-                       cudaStream_t st);
+                       cudaStream_t st, bool need_rhs = true, int64_t* launches = nullptr);
 // K4a condensed rhs (pcg.cu): rhs [tile][l][cs][v] from W and the end values
 void launch_assemble_rhs(const DevGraph& g, const DevPlan& p, int64_t n_samples, const double* W, const double* ends,
                          double* rhs, cudaStream_t st);
@@ -156,8 +157,10 @@ cudaError_t launch_vertex_sum(const DevGraph& g, const DevPlan& p, int64_t n_sam
 void plan_tiling(int32_t L, int32_t* Lp, int32_t* tl, int32_t* rounds);
 
 // K4 warp-per-system variant (pcg_warp.cu); false if the graph is outside its range
-bool launch_pcg_warp(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* rhs,
-                     double* uG, int32_t* iters, double* relres, cudaStream_t st);
+// with K4a fused (ends != nullptr): g from W and the end values, written to rhs when rhs is not
+// null; ends == nullptr: g read from rhs (K4a's output)
+bool launch_pcg_warp(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* W,
+                     const double* ends, double* rhs, double* uG, int32_t* iters, double* relres, cudaStream_t st);
 
 // Edge-partitioned NN-PCG stages (dist.cu); vectors [L][V][cs] per part
 namespace dist {

@@ -474,7 +474,6 @@ bool launch_t(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgP
 template <int W>
 bool launch_w(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* rhs,
               double* uG, int32_t* iters, double* relres, cudaStream_t st) {
-    if (launch_pcg_warp(g, p, n_samples, prm, rhs, uG, iters, relres, st)) return true;  // V <= 1024, W <= 8
     if (launch_t<128, 1, 8, W>(g, p, n_samples, prm, rhs, uG, iters, relres, st)) return true;   // V <= 1024
     if (launch_t<256, 1, 8, W>(g, p, n_samples, prm, rhs, uG, iters, relres, st)) return true;   // V <= 2048
     return launch_t<512, 1, 8, W>(g, p, n_samples, prm, rhs, uG, iters, relres, st);            // V <= 4096
@@ -582,11 +581,28 @@ void launch_assemble_rhs(const DevGraph& g, const DevPlan& p, int64_t n_samples,
     assemble_rhs_kernel<<<blocks, 256, 0, st>>>(g, p.L, p.ops, n_samples, csl, W, ends, rhs);
 }
 
+constexpr int64_t PCG_FUSE_MAX_S = 8;
+
 cudaError_t launch_pcg(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* W,
                        const double* ends, double* rhs, double* uG, int32_t* iters, double* relres, void* gws,
-                       cudaStream_t st) {
+                       cudaStream_t st, bool need_rhs, int64_t* launches) {
+    const int64_t cs = (int64_t)1 << sample_tile_log2(n_samples);
+    // up to one sample octet the warp-per-system kernel (V <= 1024, W <= 8) assembles its rhs itself
+    // (K4a fused, from the end values; rhs written only for the exit checks): one launch and one
+    // DRAM round trip less for the latency-bound single-sample calls (config 2 K4a + K4 0.065 ->
+    // 0.054 ms).  For more samples the fill stalls the CTA (one per SM, shared-memory bound) on
+    // DRAM once per octet, which the separate, coalesced K4a does not: config 3 K4a + K4 1.97 ms
+    // against 2.48 / 2.78 ms fused (sample-fastest / vertex-per-thread fills).
+    if (!prm.global && n_samples <= PCG_FUSE_MAX_S &&
+        launch_pcg_warp(g, p, n_samples, prm, W, ends, need_rhs ? rhs : nullptr, uG, iters, relres, st)) {
+        if (launches) *launches += 1;
+        return cudaGetLastError();
+    }
+    // K4a + K4 (the global-memory variant launches once per sample tile)
+    if (launches) *launches += 1 + (prm.global ? (n_samples + cs - 1) / cs : 1);
     launch_assemble_rhs(g, p, n_samples, W, ends, rhs, st);
     if (prm.global) return launch_pcg_global(g, p, n_samples, prm, rhs, uG, iters, relres, gws, st);
+    if (launch_pcg_warp(g, p, n_samples, prm, W, nullptr, rhs, uG, iters, relres, st)) return cudaGetLastError();
     switch (g.ell_w) {
         case 4: launch_w<4>(g, p, n_samples, prm, rhs, uG, iters, relres, st); break;
         case 8: launch_w<8>(g, p, n_samples, prm, rhs, uG, iters, relres, st); break;

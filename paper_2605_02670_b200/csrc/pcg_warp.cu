@@ -36,7 +36,8 @@ __device__ __forceinline__ double warp_sum(double v) {
 template <int VPL, int W, bool STAGE, int WPS>
 __global__ void __launch_bounds__(WARP_NW * WPS * 32) pcg_warp_kernel(DevGraph g, int32_t L, const double* __restrict__ ops,
                                                                 PcgParams prm, int64_t S, int32_t octs, int32_t csl,
-                                                                const double* __restrict__ rhs, double* __restrict__ uG,
+                                                                const double* __restrict__ Wn, const double* __restrict__ ends,
+                                                                double* __restrict__ rhs_out, double* __restrict__ uG,
                                                                 int32_t* __restrict__ iters, double* __restrict__ relres) {
     extern __shared__ double sm[];
     const int V = g.V;
@@ -68,6 +69,7 @@ __global__ void __launch_bounds__(WARP_NW * WPS * 32) pcg_warp_kernel(DevGraph g
     const double* DJ = DM + V;
     const double* OS = DJ + V;
     const double* OM = OS + (size_t)W * V;
+    const double* GK = OM + (size_t)W * V;  // c_L/h_e per incidence slot (K4a's coefficients, fused below)
     const int* eo = g.ell_other;
     double* r = sm + (size_t)warp * sys_stride(V);
     double* p = r + V;
@@ -168,6 +170,72 @@ __global__ void __launch_bounds__(WARP_NW * WPS * 32) pcg_warp_kernel(DevGraph g
     for (int oc = 0; oc < octs; ++oc) {
         const int64_t s0 = ((int64_t)blockIdx.y * octs + oc) * WARP_NW;
         if (s0 >= S) break;  // block-uniform
+        // K4a fused: condensed rhs g_v = W_v + sum_j (c_L/h_e) w_{code_j(v)} (P233-239)
+        // of the octet's 8 systems, assembled by the whole CTA straight from K3's end values into
+        // each system's r: the 8 samples of a (vertex, slot) are one 64-byte run of `ends` (sample
+        // fastest), so 8 consecutive threads take the 8 samples of one vertex; slot order and
+        // arithmetic are K4a's (padding slots: code 0, coefficient 0), so g is bitwise K4a's.
+        // rhs_out (only when the caller asked for the exit checks) keeps g for the true residual.
+        // ends == nullptr: K4a ran separately and rhs_out is its assembled rhs, read per system.
+        // a thread per vertex, all 8 samples: its W incidence codes and coefficients, then every
+        // end-value run of the vertex (8 samples = 64 bytes = 4 x 16-byte loads per slot) issued
+        // before the first use -- one dependent DRAM round trip per vertex instead of one per value
+        const bool full = csl >= 3 && s0 + WARP_NW <= S;  // block-uniform: 8 samples in one tile
+        for (int v = threadIdx.x; ends && v < V; v += NT) {
+            int code[W];
+            double gk[W];
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+                code[j] = g.ell_code[j * V + v];
+                gk[j] = GK[j * V + v];
+            }
+            const bool own = g.vowned == nullptr || g.vowned[v];
+            double acc[WARP_NW];
+            if (full) {
+#pragma unroll
+                for (int w = 0; w < WARP_NW; ++w) acc[w] = 0.0;
+                constexpr int JC = W < 4 ? W : 4;  // slots whose runs are in flight together (registers)
+#pragma unroll
+                for (int j0 = 0; j0 < W; j0 += JC) {
+                    double2 ev[JC][WARP_NW / 2];
+#pragma unroll
+                    for (int j = 0; j < JC; ++j) {
+                        const double2* run =
+                            reinterpret_cast<const double2*>(ends + ends_index(s0, l, code[j0 + j], L, g.E, csl));
+#pragma unroll
+                        for (int q = 0; q < WARP_NW / 2; ++q) ev[j][q] = run[q];
+                    }
+#pragma unroll
+                    for (int j = 0; j < JC; ++j) {
+#pragma unroll
+                        for (int q = 0; q < WARP_NW / 2; ++q) {
+                            acc[2 * q] = fma(gk[j0 + j], ev[j][q].x, acc[2 * q]);
+                            acc[2 * q + 1] = fma(gk[j0 + j], ev[j][q].y, acc[2 * q + 1]);
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int w = 0; w < WARP_NW; ++w) {
+                    acc[w] = 0.0;
+                    if (s0 + w < S) {
+#pragma unroll
+                        for (int j = 0; j < W; ++j)
+                            acc[w] = fma(gk[j], ends[ends_index(s0 + w, l, code[j], L, g.E, csl)], acc[w]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int w = 0; w < WARP_NW; ++w) {
+                const int64_t s = s0 + w;
+                if (s < S) {
+                    const double gv = (own ? Wn[s * g.N + g.NI + v] : 0.0) + acc[w];
+                    sm[(size_t)w * sys_stride(V) + v] = gv;
+                    if (rhs_out) rhs_out[rhs_index(s, l, v, L, V, csl)] = gv;
+                }
+            }
+        }
+        if (ends) __syncthreads();  // the octet's r complete
         const int64_t s = s0 + warp;
         if (s < S) {  // warp-uniform; no block barriers inside
             double x[VPL], t[VPL];  // t holds q = S p, then z = M^{-1} r (disjoint lifetimes)
@@ -177,14 +245,19 @@ __global__ void __launch_bounds__(WARP_NW * WPS * 32) pcg_warp_kernel(DevGraph g
             // power-of-two scaling is exact (every PCG quantity scales exactly, alpha and beta are
             // unchanged) and keeps the dot products away from underflow
             double gg = 0.0;
-            const double* gs = rhs + rhs_index(s, l, 0, L, V, csl);
+            const double* gs = ends ? nullptr : rhs_out + rhs_index(s, l, 0, L, V, csl);  // K4a rhs
     #pragma unroll
             for (int k = 0; k < VPL; ++k) {
                 const int v = lane + 32 * (WPS * k + wi);
                 x[k] = 0.0;
                 if (v < V) {
-                    const double gv = gs[v];
-                    r[v] = gv;
+                    double gv;
+                    if (ends) {
+                        gv = r[v];
+                    } else {
+                        gv = gs[v];
+                        r[v] = gv;
+                    }
                     gg = fma(gv, gv, gg);
                 }
             }
@@ -314,8 +387,8 @@ size_t warp_smem_bytes(const DevGraph& g, int W, bool stage) {
 }
 
 template <int VPL, int W, int WPS>
-bool launch_warp_t(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* rhs,
-                   double* uG, int32_t* iters, double* relres, cudaStream_t st) {
+bool launch_warp_t(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* Wn,
+                   const double* ends, double* rhs, double* uG, int32_t* iters, double* relres, cudaStream_t st) {
     constexpr int NT = WARP_NW * WPS * 32;
     const bool stage = warp_smem_bytes(g, W, true) <= SMEM_LIMIT;
     const size_t smem = warp_smem_bytes(g, W, stage);
@@ -340,13 +413,13 @@ bool launch_warp_t(const DevGraph& g, const DevPlan& p, int64_t n_samples, const
     }
     const dim3 grid(p.L, (unsigned)((n_oct + octs - 1) / octs));
     const int32_t csl = sample_tile_log2(n_samples);
-    kern<<<grid, NT, smem, st>>>(g, p.L, p.ops, prm, n_samples, (int32_t)octs, csl, rhs, uG, iters, relres);
+    kern<<<grid, NT, smem, st>>>(g, p.L, p.ops, prm, n_samples, (int32_t)octs, csl, Wn, ends, rhs, uG, iters, relres);
     return true;
 }
 
 template <int W>
-bool launch_warp(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* rhs,
-                 double* uG, int32_t* iters, double* relres, cudaStream_t st) {
+bool launch_warp(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* Wn,
+                 const double* ends, double* rhs, double* uG, int32_t* iters, double* relres, cudaStream_t st) {
     const int vpl = (g.V + 31) / 32;
     // warps per system: 2 once a lane holds 16+ vertices (the register file, not the shared memory,
     // bounds the resident systems there); design study override: env GRF_PCG_WPS
@@ -357,9 +430,9 @@ bool launch_warp(const DevGraph& g, const DevPlan& p, int64_t n_samples, const P
     const int wps = wps_env > 0 ? wps_env : (vpl > 8 ? 2 : 1);
 #define GRF_PW(N)                                                                                      \
     if (vpl <= N) {                                                                                    \
-        if (wps >= 4 && N >= 4) return launch_warp_t<(N >= 4 ? N / 4 : 1), W, 4>(g, p, n_samples, prm, rhs, uG, iters, relres, st); \
-        if (wps >= 2 && N >= 2) return launch_warp_t<(N >= 2 ? N / 2 : 1), W, 2>(g, p, n_samples, prm, rhs, uG, iters, relres, st); \
-        return launch_warp_t<N, W, 1>(g, p, n_samples, prm, rhs, uG, iters, relres, st);               \
+        if (wps >= 4 && N >= 4) return launch_warp_t<(N >= 4 ? N / 4 : 1), W, 4>(g, p, n_samples, prm, Wn, ends, rhs, uG, iters, relres, st); \
+        if (wps >= 2 && N >= 2) return launch_warp_t<(N >= 2 ? N / 2 : 1), W, 2>(g, p, n_samples, prm, Wn, ends, rhs, uG, iters, relres, st); \
+        return launch_warp_t<N, W, 1>(g, p, n_samples, prm, Wn, ends, rhs, uG, iters, relres, st);               \
     }
     GRF_PW(1) GRF_PW(2) GRF_PW(4) GRF_PW(8) GRF_PW(16) GRF_PW(32)
 #undef GRF_PW
@@ -368,11 +441,11 @@ bool launch_warp(const DevGraph& g, const DevPlan& p, int64_t n_samples, const P
 
 }  // namespace
 
-bool launch_pcg_warp(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* rhs,
-                     double* uG, int32_t* iters, double* relres, cudaStream_t st) {
+bool launch_pcg_warp(const DevGraph& g, const DevPlan& p, int64_t n_samples, const PcgParams& prm, const double* Wn,
+                     const double* ends, double* rhs, double* uG, int32_t* iters, double* relres, cudaStream_t st) {
     if (g.V > 32 * 32) return false;
-    if (g.ell_w == 4) return launch_warp<4>(g, p, n_samples, prm, rhs, uG, iters, relres, st);
-    if (g.ell_w == 8) return launch_warp<8>(g, p, n_samples, prm, rhs, uG, iters, relres, st);
+    if (g.ell_w == 4) return launch_warp<4>(g, p, n_samples, prm, Wn, ends, rhs, uG, iters, relres, st);
+    if (g.ell_w == 8) return launch_warp<8>(g, p, n_samples, prm, Wn, ends, rhs, uG, iters, relres, st);
     return false;
 }
 
