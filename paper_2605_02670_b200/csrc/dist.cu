@@ -345,7 +345,8 @@ __global__ void finish_kernel(DevGraph g, int32_t L, int64_t S, int32_t csl, int
 
 int grid_for(int64_t n) {
     int64_t b = (n + BT - 1) / BT;
-    return (int)(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
+    const int64_t cap = (int64_t)device_sms() * 16;
+    return (int)(b < cap ? (b < 1 ? 1 : b) : cap);
 }
 
 }  // namespace

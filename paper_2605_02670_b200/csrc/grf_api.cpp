@@ -1901,7 +1901,7 @@ extern "C" grf_status grf_mnorm_sq_diff(grf_graph* g, int64_t n, const double* a
                                         void* stream) {
     if (!g || n < 1 || !a || !b || !out) return fail(GRF_EINVAL, "bad arguments");
     cudaStream_t st = (cudaStream_t)stream;
-    const size_t bytes = sizeof(double) * (size_t)n * 148;
+    const size_t bytes = sizeof(double) * (size_t)n * grf::MNORM_PARTS;
     void* part = g->alloc.get(bytes, st);
     if (!part) return fail(GRF_ENOMEM, "partial buffer");
     grf::launch_mnorm_sq_diff(g->dev, n, a, b, (double*)part, out, st);

@@ -107,6 +107,12 @@ __host__ __device__ inline int64_t ug_index(int64_t s, int32_t v, int32_t l, int
 __host__ __device__ inline int64_t rhs_index(int64_t s, int32_t l, int32_t v, int32_t L, int32_t V, int32_t cs_log2) {
     return (((((s >> cs_log2) * L + l) << cs_log2) + (s & ((1 << cs_log2) - 1))) * (int64_t)V) + v;
 }
+// SM count of the current device (queried once per device, cached): grid caps of the
+// grid-stride kernels (sweep.cu)
+int device_sms();
+// fixed split of grf_mnorm_sq_diff's reduction (a partition of the DOFs, not an SM count: the same
+// summation order on every device)
+constexpr int MNORM_PARTS = 148;
 // log2 of the sample tile for S samples (sweep.cu)
 int32_t sample_tile_log2(int64_t S);
 

@@ -678,7 +678,7 @@ void launch_true_residual(const DevGraph& g, const DevPlan& p, int64_t n_samples
 void launch_nonfinite(const double* u, int64_t n, unsigned long long* count, cudaStream_t st) {
     cudaMemsetAsync(count, 0, sizeof(unsigned long long), st);
     int64_t blocks = (n + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > (int64_t)device_sms() * 16) blocks = (int64_t)device_sms() * 16;
     if (blocks < 1) blocks = 1;
     nonfinite_kernel<<<(unsigned)blocks, 256, 0, st>>>(u, n, count);
 }

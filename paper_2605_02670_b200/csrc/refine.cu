@@ -121,27 +121,27 @@ __global__ void add_kernel(double* __restrict__ y, const double* __restrict__ x,
 }  // namespace
 
 void launch_add(double* y, const double* x, int64_t n, cudaStream_t st) {
-    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)device_sms() * 16);
     add_kernel<<<blocks, 256, 0, st>>>(y, x, n);
 }
 
 void launch_prolong(const DevGraph& gc, const DevGraph& gf, const int32_t* fedge, int64_t S, const double* uc,
                     double* uf, cudaStream_t st) {
     const int64_t n = S * gf.N;
-    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 32);
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)device_sms() * 32);
     prolong_kernel<<<blocks, 256, 0, st>>>(gc, gf, fedge, S, uc, uf);
 }
 
 void launch_project(const DevGraph& gc, const DevGraph& gf, const int32_t* cedge, int64_t S, const double* wf,
                     double* wc, cudaStream_t st) {
     const int64_t n = S * gc.N;
-    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 32);
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)device_sms() * 32);
     project_kernel<<<blocks, 256, 0, st>>>(gc, gf, cedge, S, wf, wc);
 }
 
 void launch_mnorm_sq_diff(const DevGraph& g, int64_t S, const double* a, const double* b, double* part, double* out,
                           cudaStream_t st) {
-    const int nblk = 148;
+    const int nblk = MNORM_PARTS;
     mnorm_partial_kernel<<<dim3(nblk, (unsigned)S), 256, 0, st>>>(g.N, g.ml, a, b, part, nblk);
     mnorm_final_kernel<<<(unsigned)((S + 127) / 128), 128, 0, st>>>(S, nblk, part, out);
 }

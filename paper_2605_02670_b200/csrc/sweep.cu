@@ -54,6 +54,19 @@ sweep::Args make_args(const DevGraph& g, const DevPlan& p, int64_t S, const doub
 }
 }  // namespace
 
+int device_sms() {
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (cache[dev] <= 0) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = n > 0 ? n : 148;
+    }
+    return cache[dev];
+}
+
 int32_t sample_tile_log2(int64_t S) {
     switch (sweep::variant_for(S)) {
         case sweep::V2: return 5;
