@@ -134,6 +134,26 @@ def test_small_graph_all_preconditioners(precond):
     assert st["n_unconverged"] == 0 and st["worst_true_rel_residual"] <= 1e-11
 
 
+@pytest.mark.parametrize("n_samples", [5, 8])
+def test_fused_rhs_assembly_small_calls(n_samples):
+    """Calls of <= 8 samples: the warp PCG assembles its rhs from the end values itself (K4a fused,
+    pcg.cu launch_pcg; 8 = one full octet, the 16-byte run loads; 5 = a partial octet).  Fields vs
+    the oracle; the call without statistics (rhs never written) equals the call with them bitwise;
+    the same samples from a 9-sample call (separate K4a) agree to rounding."""
+    g = lattice(6, seed=2)
+    h, kappa, beta, k = 0.04, 3.0, 0.7, 0.3
+    G = _graph(g, h)
+    u, st = G.sample(kappa, beta, k, seed=3, n_samples=n_samples, return_stats=True)
+    u = u.cpu().numpy()
+    ref, _, _ = solve.sample(g, h, kappa, beta, k, 3, n_samples)
+    assert _rel(u, ref).max() <= FIELD_TOL
+    assert st["n_unconverged"] == 0 and st["worst_true_rel_residual"] <= 1e-11
+    plain = G.sample(kappa, beta, k, seed=3, n_samples=n_samples).cpu().numpy()
+    assert np.array_equal(_bits(u), _bits(plain))
+    nine = G.sample(kappa, beta, k, seed=3, n_samples=9).cpu().numpy()
+    assert _rel(nine[:n_samples], u).max() <= 1e-12
+
+
 def test_ragged_and_degenerate_edges():
     """Edges with 0, 1, 2 interior nodes, a loop with n_e = 1, multi-edges; odd sample count."""
     g = MetricGraph(4, np.array([0, 0, 1, 1, 2, 3, 2, 0]), np.array([1, 1, 2, 1, 3, 3, 0, 3]),
