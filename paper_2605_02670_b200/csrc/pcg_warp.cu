@@ -33,7 +33,7 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-template <int VPL, int W, bool STAGE, int WPS>
+template <int VPL, int W, bool STAGE, int WPS, bool FUSE>
 __global__ void __launch_bounds__(WARP_NW * WPS * 32) pcg_warp_kernel(DevGraph g, int32_t L, const double* __restrict__ ops,
                                                                 PcgParams prm, int64_t S, int32_t octs, int32_t csl,
                                                                 const double* __restrict__ Wn, const double* __restrict__ ends,
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(WARP_NW * WPS * 32) pcg_warp_kernel(DevGraph g
         // end-value run of the vertex (8 samples = 64 bytes = 4 x 16-byte loads per slot) issued
         // before the first use -- one dependent DRAM round trip per vertex instead of one per value
         const bool full = csl >= 3 && s0 + WARP_NW <= S;  // block-uniform: 8 samples in one tile
-        for (int v = threadIdx.x; ends && v < V; v += NT) {
+        for (int v = threadIdx.x; FUSE && v < V; v += NT) {
             int code[W];
             double gk[W];
 #pragma unroll
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(WARP_NW * WPS * 32) pcg_warp_kernel(DevGraph g
                 }
             }
         }
-        if (ends) __syncthreads();  // the octet's r complete
+        if (FUSE) __syncthreads();  // the octet's r complete
         const int64_t s = s0 + warp;
         if (s < S) {  // warp-uniform; no block barriers inside
             double x[VPL], t[VPL];  // t holds q = S p, then z = M^{-1} r (disjoint lifetimes)
@@ -245,14 +245,14 @@ __global__ void __launch_bounds__(WARP_NW * WPS * 32) pcg_warp_kernel(DevGraph g
             // power-of-two scaling is exact (every PCG quantity scales exactly, alpha and beta are
             // unchanged) and keeps the dot products away from underflow
             double gg = 0.0;
-            const double* gs = ends ? nullptr : rhs_out + rhs_index(s, l, 0, L, V, csl);  // K4a rhs
+            const double* gs = FUSE ? nullptr : rhs_out + rhs_index(s, l, 0, L, V, csl);  // K4a rhs
     #pragma unroll
             for (int k = 0; k < VPL; ++k) {
                 const int v = lane + 32 * (WPS * k + wi);
                 x[k] = 0.0;
                 if (v < V) {
                     double gv;
-                    if (ends) {
+                    if (FUSE) {
                         gv = r[v];
                     } else {
                         gv = gs[v];
@@ -397,7 +397,9 @@ bool launch_warp_t(const DevGraph& g, const DevPlan& p, int64_t n_samples, const
     // octets per CTA: the CTAs run in waves of (resident CTAs per SM) x 148 and a wave lasts about
     // `octs` octet solves, so pick the power of two minimising waves x octs (the partial last wave
     // included); ties go to the larger octs (fewer table stagings).  Config 3: 2 (23 waves).
-    auto* kern = stage ? pcg_warp_kernel<VPL, W, true, WPS> : pcg_warp_kernel<VPL, W, false, WPS>;
+    // FUSE (template, no per-octet branch in the K4a-separate form): ends != nullptr
+    auto* kern = ends ? (stage ? pcg_warp_kernel<VPL, W, true, WPS, true> : pcg_warp_kernel<VPL, W, false, WPS, true>)
+                      : (stage ? pcg_warp_kernel<VPL, W, true, WPS, false> : pcg_warp_kernel<VPL, W, false, WPS, false>);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
