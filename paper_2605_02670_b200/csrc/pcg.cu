@@ -576,8 +576,9 @@ void launch_assemble_rhs(const DevGraph& g, const DevPlan& p, int64_t n_samples,
                          double* rhs, cudaStream_t st) {
     const int32_t csl = sample_tile_log2(n_samples);
     const int64_t work = (int64_t)p.L * ((g.V + ASM_VB - 1) / ASM_VB);
-    const int64_t cap = (int64_t)g.n_sm * 8;
-    int blocks = (int)(work < cap ? work : cap);
+    // one CTA per work unit (the hardware scheduler balances the tail): config 3 K4a 0.415 ->
+    // 0.395 ms (ncu) against a grid-stride cap of 8 CTAs per SM (4: 0.60 ms, 16: 0.41 ms)
+    const int blocks = (int)(work < INT32_MAX ? work : INT32_MAX);
     assemble_rhs_kernel<<<blocks, 256, 0, st>>>(g, p.L, p.ops, n_samples, csl, W, ends, rhs);
 }
 
